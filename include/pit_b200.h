@@ -1,0 +1,136 @@
+/*
+ * pit_b200.h — C ABI of the B200-native PIT hot path (libpit_b200.so).
+ *
+ * Drop-in boundary for the reference `pittile` operator API (pkg/src/pittile/__init__.py:9-76).
+ * Every entry point is extern "C", takes plain device pointers / sizes, is stream-ordered on the
+ * caller's cudaStream_t (passed as void*), never allocates, and returns a pit_status; the message of
+ * the last failure on the calling thread is available from pit_last_error().
+ *
+ * Index layout on the device (replaces MicroTileIndex, index.py:32-50):
+ *   counts  int32 [n_groups]                live coordinates per group
+ *   slots   int32 [n_groups * pit_grid]     group g's coordinates at slots[g*pit_grid + 0 .. counts[g])
+ *                                           in ascending order (== reference workers=1 order)
+ *   occ     uint32 [n_groups * words]       group-major occupancy bitmap, words = ceil(pit_grid/32),
+ *                                           bit b of word w of group g <=> coordinate 32w+b is live
+ * Groups run along the non-PIT micro grid; pit_dim 0 ("m"/"p") or 1 ("k"/"l") (index.py:25).
+ */
+#ifndef PIT_B200_H
+#define PIT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define PIT_API __attribute__((visibility("default")))
+#else
+#define PIT_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PIT_OK = 0,
+  PIT_ERR_ARG = 1,         /* maps to ValueError subclasses (ExecError / IndexBuildError) */
+  PIT_ERR_SHAPE = 2,       /* "shape mismatch" */
+  PIT_ERR_LAYOUT = 3,      /* LayoutError */
+  PIT_ERR_RANGE = 4,       /* "out of range" */
+  PIT_ERR_CUDA = 5,        /* CUDA runtime / driver failure */
+  PIT_ERR_UNSUPPORTED = 6  /* combination not implemented on this path */
+} pit_status;
+
+typedef enum { PIT_F32 = 0, PIT_F64 = 1, PIT_BF16 = 2, PIT_F16 = 3, PIT_U8 = 4 } pit_dtype;
+
+typedef enum { PIT_PLAN_DENSE = 0, PIT_PLAN_PIT_M = 1, PIT_PLAN_PIT_K = 2 } pit_plan;
+
+/* Last error message of the calling thread (static storage, never NULL). */
+PIT_API const char* pit_last_error(void);
+
+/* ABI version (major*100 + minor). */
+PIT_API int pit_abi_version(void);
+
+/* Micro-grid geometry of a (s0 x s1) operand under micro-tile (t0,t1) and PIT dim. */
+PIT_API int pit_index_geometry(int64_t s0, int64_t s1, int t0, int t1, int pit_dim, int64_t* n_groups, int64_t* pit_grid,
+                       int64_t* words_per_group);
+
+/*
+ * Online detection from raw values: an element is live iff value != 0.0 (sign bit ignored, so -0.0 is
+ * dead; NaN / inf / denormals live). Replaces build_index_from_tensor (index.py:164-173).
+ * values(i,j) lives at values + (i*stride0 + j*stride1) * sizeof(dtype); stride1 == 1 (row-major) or
+ * stride0 == 1 (column-major) are accepted.
+ */
+PIT_API int pit_build_index_from_tensor(const void* values, int dtype, int64_t s0, int64_t s1, int64_t stride0,
+                                int64_t stride1, int t0, int t1, int pit_dim, uint32_t* occ, int32_t* counts,
+                                int32_t* slots, void* stream);
+
+/*
+ * Detection from a block annotation: packed = np.packbits of the row-major block grid (MSB first),
+ * granularity (g0,g1). Replaces build_index (index.py:102-161) over a SparsityAnnotation
+ * (sparsity.py:27-65).
+ */
+PIT_API int pit_build_index(const uint8_t* packed, int64_t s0, int64_t s1, int g0, int g1, int t0, int t1, int pit_dim,
+                    uint32_t* occ, int32_t* counts, int32_t* slots, void* stream);
+
+/* Occupancy bitmap from an arbitrary (e.g. reordered) index; *bad set to 1 on a coordinate out of
+ * range (sread's "micro-tile coordinate out of range", executor.py:192-193). occ is overwritten. */
+PIT_API int pit_index_occupancy(const int32_t* counts, const int32_t* slots, int64_t n_groups, int64_t pit_grid,
+                        uint32_t* occ, int32_t* bad, void* stream);
+
+/* Union of live coordinates over all groups, ascending: rows[0..*n_rows). union_ws: words uint32. */
+PIT_API int pit_index_union(const uint32_t* occ, int64_t n_groups, int64_t pit_grid, uint32_t* union_ws, int32_t* rows,
+                    int32_t* n_rows, void* stream);
+
+/*
+ * SRead (executor.py:170-208): gather coords[0..n_coords) of one group into tile (row-major
+ * [tile_rows, tile_cols], contiguous). tensor is row-major [s0, s1] with pitch ld (stride1 == 1) or
+ * column-major (ld = pitch of a column, pass col_major = 1). zero_fill clears unfilled tile slots.
+ */
+PIT_API int pit_sread(const void* tensor, int dtype, int64_t s0, int64_t s1, int64_t ld, int col_major, void* tile,
+              int64_t tile_rows, int64_t tile_cols, int t0, int t1, int pit_dim, int64_t group,
+              const int32_t* coords, int64_t n_coords, int zero_fill, void* stream);
+
+/* SWrite (executor.py:211-264): mirror scatter; accumulate != 0 adds instead of assigning. */
+PIT_API int pit_swrite(const void* tile, void* tensor, int dtype, int64_t s0, int64_t s1, int64_t ld, int col_major,
+               int64_t tile_rows, int64_t tile_cols, int t0, int t1, int pit_dim, int64_t group,
+               const int32_t* coords, int64_t n_coords, int accumulate, void* stream);
+
+/* Sparse matmul against a prebuilt device index (run_matmul_with_index, executor.py:464-516). */
+typedef struct {
+  int plan;  /* pit_plan */
+  int dtype; /* pit_dtype of A, B and C */
+  int64_t M, N, K;
+  const void* A; /* element (m,k) at A + m*sam + k*sak; pit:k needs sam == 1, pit:m/dense sak == 1 */
+  int64_t sam, sak;
+  const void* B; /* row-major [K,N], pitch ldb */
+  int64_t ldb;
+  void* C; /* row-major [M,N], pitch ldc; every element is written */
+  int64_t ldc;
+  int t0, t1; /* plan micro-tile */
+  const int32_t* counts;
+  const int32_t* slots;
+  int64_t slot_stride; /* = pit_grid */
+  int64_t n_groups;
+  const uint32_t* occ; /* pit:m: group-major occupancy */
+  int64_t words_per_group;
+  const int32_t* rows;   /* pit:m: union rows (pit_index_union) */
+  const int32_t* n_rows; /* pit:m: device scalar */
+  int64_t n_rows_bound;  /* pit:m: host upper bound on *n_rows (M is always safe) */
+  int force_simt;        /* 1: CUDA-core path even for bf16/fp16 */
+} pit_spmm_args;
+
+PIT_API int pit_spmm(const pit_spmm_args* args, void* stream);
+
+/* 1 if the tcgen05 tensor-core path covers these arguments, else 0 (CUDA-core path). */
+PIT_API int pit_spmm_uses_tensor_cores(const pit_spmm_args* args);
+
+/* f64 verification oracle: C = A @ B with multiply-then-add in ascending k (no FMA), bit-identical to
+ * the reference's run_dense_reference (executor.py:267-283). A(i,k) at A + i*s0 + k*s1. */
+PIT_API int pit_dense_reference_f64(const double* A, int64_t s0, int64_t s1, const double* B, int64_t ldb, double* C,
+                            int64_t M, int64_t N, int64_t K, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PIT_B200_H */

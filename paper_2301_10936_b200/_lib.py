@@ -1,0 +1,127 @@
+"""ctypes binding of libpit_b200.so (the C ABI in include/pit_b200.h).
+
+There is no CPU fallback: if the library is missing or CUDA is unavailable, every device
+operation raises. ``load()`` builds the library in-tree on first use when nvcc is present.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+_LIB_PATH = Path(__file__).resolve().parent / "libpit_b200.so"
+_lock = threading.Lock()
+_lib = None
+
+# status codes (pit_status)
+PIT_OK = 0
+PIT_ERR_ARG = 1
+PIT_ERR_SHAPE = 2
+PIT_ERR_LAYOUT = 3
+PIT_ERR_RANGE = 4
+PIT_ERR_CUDA = 5
+PIT_ERR_UNSUPPORTED = 6
+
+# dtype codes (pit_dtype)
+PIT_F32, PIT_F64, PIT_BF16, PIT_F16, PIT_U8 = 0, 1, 2, 3, 4
+
+# plans (pit_plan)
+PIT_PLAN_DENSE, PIT_PLAN_PIT_M, PIT_PLAN_PIT_K = 0, 1, 2
+
+EXPORTS = (
+    "pit_last_error",
+    "pit_abi_version",
+    "pit_index_geometry",
+    "pit_build_index_from_tensor",
+    "pit_build_index",
+    "pit_index_occupancy",
+    "pit_index_union",
+    "pit_sread",
+    "pit_swrite",
+    "pit_spmm",
+    "pit_spmm_uses_tensor_cores",
+    "pit_dense_reference_f64",
+)
+
+
+class SpmmArgs(C.Structure):
+    """Mirror of ``pit_spmm_args``."""
+
+    _fields_ = [
+        ("plan", C.c_int),
+        ("dtype", C.c_int),
+        ("M", C.c_int64),
+        ("N", C.c_int64),
+        ("K", C.c_int64),
+        ("A", C.c_void_p),
+        ("sam", C.c_int64),
+        ("sak", C.c_int64),
+        ("B", C.c_void_p),
+        ("ldb", C.c_int64),
+        ("C", C.c_void_p),
+        ("ldc", C.c_int64),
+        ("t0", C.c_int),
+        ("t1", C.c_int),
+        ("counts", C.c_void_p),
+        ("slots", C.c_void_p),
+        ("slot_stride", C.c_int64),
+        ("n_groups", C.c_int64),
+        ("occ", C.c_void_p),
+        ("words_per_group", C.c_int64),
+        ("rows", C.c_void_p),
+        ("n_rows", C.c_void_p),
+        ("n_rows_bound", C.c_int64),
+        ("force_simt", C.c_int),
+    ]
+
+
+def _declare(lib) -> None:
+    i64, i32, vp = C.c_int64, C.c_int, C.c_void_p
+    lib.pit_last_error.restype = C.c_char_p
+    lib.pit_last_error.argtypes = []
+    lib.pit_abi_version.restype = i32
+    lib.pit_index_geometry.argtypes = [i64, i64, i32, i32, i32, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]
+    lib.pit_build_index_from_tensor.argtypes = [vp, i32, i64, i64, i64, i64, i32, i32, i32, vp, vp, vp, vp]
+    lib.pit_build_index.argtypes = [vp, i64, i64, i32, i32, i32, i32, i32, vp, vp, vp, vp]
+    lib.pit_index_occupancy.argtypes = [vp, vp, i64, i64, vp, vp, vp]
+    lib.pit_index_union.argtypes = [vp, i64, i64, vp, vp, vp, vp]
+    lib.pit_sread.argtypes = [vp, i32, i64, i64, i64, i32, vp, i64, i64, i32, i32, i32, i64, vp, i64, i32, vp]
+    lib.pit_swrite.argtypes = [vp, vp, i32, i64, i64, i64, i32, i64, i64, i32, i32, i32, i64, vp, i64, i32, vp]
+    lib.pit_spmm.argtypes = [C.POINTER(SpmmArgs), vp]
+    lib.pit_spmm_uses_tensor_cores.argtypes = [C.POINTER(SpmmArgs)]
+    lib.pit_dense_reference_f64.argtypes = [vp, i64, i64, vp, i64, vp, i64, i64, i64, vp]
+    for name in EXPORTS:
+        if name not in ("pit_last_error", "pit_abi_version"):
+            getattr(lib, name).restype = i32
+
+
+def library_path() -> Path:
+    return _LIB_PATH
+
+
+def load(build_if_missing: bool = True):
+    """Load (building if needed) the CUDA library. Raises if it cannot be loaded."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not _LIB_PATH.exists() and build_if_missing:
+            from . import _build
+
+            _build.build()
+        if not _LIB_PATH.exists():
+            raise RuntimeError(
+                f"{_LIB_PATH} is missing: build it with `python -m paper_2301_10936_b200._build` "
+                "(the PIT hot path has no CPU fallback)"
+            )
+        lib = C.CDLL(str(_LIB_PATH))
+        _declare(lib)
+        _lib = lib
+        return lib
+
+
+def last_error() -> str:
+    return load().pit_last_error().decode(errors="replace")

@@ -1,0 +1,294 @@
+// C-ABI layer: argument validation, physical-layout mapping and dispatch to the launchers.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "pit_b200.h"
+#include "pit_internal.h"
+
+namespace pit {
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn g_encode = nullptr;
+std::once_flag g_encode_once;
+
+bool dtype_ok(int dt) { return dt >= kDtypeF32 && dt <= kDtypeU8; }
+}  // namespace
+
+int cuda_status() {
+  const cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) return kOk;
+  return fail(kErrCuda, "CUDA error: %s", cudaGetErrorString(e));
+}
+
+CUresult encode_tensor_map_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner,
+                              uint64_t outer, uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_outer,
+                              CUtensorMapSwizzle swizzle) {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<EncodeFn>(fn);
+  });
+  if (!g_encode) {
+    fail(kErrCuda, "cuTensorMapEncodeTiled unavailable");
+    return CUDA_ERROR_NOT_FOUND;
+  }
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {row_pitch_bytes};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = g_encode(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    fail(kErrCuda, "cuTensorMapEncodeTiled failed (%d): dims %llu x %llu pitch %llu box %u x %u", static_cast<int>(r),
+         static_cast<unsigned long long>(inner), static_cast<unsigned long long>(outer),
+         static_cast<unsigned long long>(row_pitch_bytes), box_inner, box_outer);
+  return r;
+}
+
+}  // namespace pit
+
+using namespace pit;
+
+namespace {
+
+int geometry(int64_t s0, int64_t s1, int t0, int t1, int pit_dim, int64_t* ng, int64_t* pg, int64_t* wg) {
+  if (s0 < 0 || s1 < 0) return fail(kErrShape, "shape must be non-negative, got (%lld,%lld)", (long long)s0, (long long)s1);
+  if (t0 <= 0 || t1 <= 0) return fail(kErrArg, "micro-tile edges must be positive, got (%d,%d)", t0, t1);
+  if (pit_dim != 0 && pit_dim != 1) return fail(kErrArg, "pit dimension must be 0 or 1, got %d", pit_dim);
+  const int64_t G0 = ceil_div(s0, t0), G1 = ceil_div(s1, t1);
+  *ng = pit_dim == 0 ? G1 : G0;
+  *pg = pit_dim == 0 ? G0 : G1;
+  *wg = ceil_div(*pg, 32);
+  if (*pg >= (1ll << 31)) return fail(kErrShape, "PIT grid extent %lld exceeds int32", (long long)*pg);
+  return kOk;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pit_last_error(void) { return g_err.c_str(); }
+
+int pit_abi_version(void) { return 100; }
+
+int pit_index_geometry(int64_t s0, int64_t s1, int t0, int t1, int pit_dim, int64_t* n_groups, int64_t* pit_grid,
+                       int64_t* words_per_group) {
+  if (!n_groups || !pit_grid || !words_per_group) return fail(kErrArg, "null output pointer");
+  return geometry(s0, s1, t0, t1, pit_dim, n_groups, pit_grid, words_per_group);
+}
+
+int pit_build_index_from_tensor(const void* values, int dtype, int64_t s0, int64_t s1, int64_t stride0,
+                                int64_t stride1, int t0, int t1, int pit_dim, uint32_t* occ, int32_t* counts,
+                                int32_t* slots, void* stream) {
+  int64_t ng, pg, wg;
+  if (int st = geometry(s0, s1, t0, t1, pit_dim, &ng, &pg, &wg)) return st;
+  if (!dtype_ok(dtype)) return fail(kErrArg, "unsupported dtype code %d", dtype);
+  if (ng == 0 || pg == 0) return kOk;
+  if (!values || !occ || !counts || !slots) return fail(kErrArg, "null device pointer");
+  DetectValuesArgs a{};
+  a.x = values;
+  a.dtype = dtype;
+  a.occ = occ;
+  if (stride1 == 1 && (stride0 >= s1 || s0 == 1)) {  // row-major
+    a.R = s0;
+    a.C = s1;
+    a.ld = s0 == 1 ? s1 : stride0;
+    a.tr = t0;
+    a.tc = t1;
+    a.pit_phys = pit_dim;
+  } else if (stride0 == 1 && (stride1 >= s0 || s1 == 1)) {  // column-major: physical = transpose
+    a.R = s1;
+    a.C = s0;
+    a.ld = s1 == 1 ? s0 : stride1;
+    a.tr = t1;
+    a.tc = t0;
+    a.pit_phys = 1 - pit_dim;
+  } else {
+    return fail(kErrLayout, "values must be row-major or column-major, got strides (%lld,%lld)", (long long)stride0,
+                (long long)stride1);
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (int st = launch_detect_values(a, s)) return st == kErrShape ? fail(st, "tensor too large for detection grid") : st;
+  return launch_compact(occ, ng, wg, counts, slots, pg, s);
+}
+
+int pit_build_index(const uint8_t* packed, int64_t s0, int64_t s1, int g0, int g1, int t0, int t1, int pit_dim,
+                    uint32_t* occ, int32_t* counts, int32_t* slots, void* stream) {
+  int64_t ng, pg, wg;
+  if (int st = geometry(s0, s1, t0, t1, pit_dim, &ng, &pg, &wg)) return st;
+  if (g0 <= 0 || g1 <= 0) return fail(kErrArg, "granularity must be positive, got (%d,%d)", g0, g1);
+  if (ng == 0 || pg == 0) return kOk;
+  if (!packed || !occ || !counts || !slots) return fail(kErrArg, "null device pointer");
+  DetectBitsArgs a{packed, s0, s1, g0, g1, t0, t1, pit_dim, occ};
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (int st = launch_detect_bits(a, s)) return st;
+  return launch_compact(occ, ng, wg, counts, slots, pg, s);
+}
+
+int pit_index_occupancy(const int32_t* counts, const int32_t* slots, int64_t n_groups, int64_t pit_grid, uint32_t* occ,
+                        int32_t* bad, void* stream) {
+  if (n_groups < 0 || pit_grid < 0) return fail(kErrShape, "negative index geometry");
+  if (n_groups == 0) return kOk;
+  if (!counts || !slots || !occ || !bad) return fail(kErrArg, "null device pointer");
+  return launch_slots_to_occ(counts, slots, pit_grid, n_groups, ceil_div(pit_grid, 32), pit_grid, occ, bad,
+                             static_cast<cudaStream_t>(stream));
+}
+
+int pit_index_union(const uint32_t* occ, int64_t n_groups, int64_t pit_grid, uint32_t* union_ws, int32_t* rows,
+                    int32_t* n_rows, void* stream) {
+  if (!occ || !union_ws || !rows || !n_rows) return fail(kErrArg, "null device pointer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t wg = ceil_div(pit_grid, 32);
+  if (wg == 0 || n_groups == 0) {
+    cudaMemsetAsync(n_rows, 0, sizeof(int32_t), s);
+    return cuda_status();
+  }
+  if (int st = launch_union(occ, n_groups, wg, union_ws, s)) return st;
+  return launch_compact(union_ws, 1, wg, n_rows, rows, pit_grid, s);
+}
+
+static int gather_args(GatherArgs& a, void* tensor, int dtype, int64_t s0, int64_t s1, int64_t ld, int col_major,
+                       void* tile, int64_t tile_rows, int64_t tile_cols, int t0, int t1, int pit_dim, int64_t group,
+                       const int32_t* coords, int64_t n_coords) {
+  if (!dtype_ok(dtype) || dtype == kDtypeU8) return fail(kErrArg, "unsupported dtype code %d", dtype);
+  if (t0 <= 0 || t1 <= 0) return fail(kErrArg, "micro-tile edges must be positive");
+  if (pit_dim != 0 && pit_dim != 1) return fail(kErrArg, "pit dimension must be 0 or 1");
+  a = GatherArgs{};
+  a.dtype = dtype;
+  a.tile = tile;
+  a.TR = tile_rows;
+  a.TC = tile_cols;
+  a.coords = coords;
+  a.n_coords = n_coords;
+  a.src_or_dst = tensor;
+  const int t_d = pit_dim == 0 ? t0 : t1, t_o = pit_dim == 0 ? t1 : t0;
+  a.t_d = t_d;
+  a.t_o = t_o;
+  a.off_o = group * t_o;
+  a.R = s0;
+  a.C = s1;
+  a.st0 = col_major ? 1 : ld;
+  a.st1 = col_major ? ld : 1;
+  a.d = pit_dim;
+  return kOk;
+}
+
+int pit_sread(const void* tensor, int dtype, int64_t s0, int64_t s1, int64_t ld, int col_major, void* tile,
+              int64_t tile_rows, int64_t tile_cols, int t0, int t1, int pit_dim, int64_t group, const int32_t* coords,
+              int64_t n_coords, int zero_fill, void* stream) {
+  GatherArgs a;
+  if (int st = gather_args(a, const_cast<void*>(tensor), dtype, s0, s1, ld, col_major, tile, tile_rows, tile_cols, t0,
+                           t1, pit_dim, group, coords, n_coords))
+    return st;
+  a.zero_fill = zero_fill;
+  return launch_sread(a, static_cast<cudaStream_t>(stream));
+}
+
+int pit_swrite(const void* tile, void* tensor, int dtype, int64_t s0, int64_t s1, int64_t ld, int col_major,
+               int64_t tile_rows, int64_t tile_cols, int t0, int t1, int pit_dim, int64_t group, const int32_t* coords,
+               int64_t n_coords, int accumulate, void* stream) {
+  GatherArgs a;
+  if (int st = gather_args(a, tensor, dtype, s0, s1, ld, col_major, const_cast<void*>(tile), tile_rows, tile_cols, t0,
+                           t1, pit_dim, group, coords, n_coords))
+    return st;
+  a.accumulate = accumulate;
+  return launch_swrite(a, static_cast<cudaStream_t>(stream));
+}
+
+static SpmmArgs to_internal(const pit_spmm_args* p) {
+  SpmmArgs a{};
+  a.plan = p->plan;
+  a.dtype = p->dtype;
+  a.M = p->M;
+  a.N = p->N;
+  a.K = p->K;
+  a.A = p->A;
+  a.sam = p->sam;
+  a.sak = p->sak;
+  a.B = p->B;
+  a.ldb = p->ldb;
+  a.C = p->C;
+  a.ldc = p->ldc;
+  a.t0 = p->t0;
+  a.t1 = p->t1;
+  a.counts = p->counts;
+  a.slots = p->slots;
+  a.slot_stride = p->slot_stride;
+  a.n_groups = p->n_groups;
+  a.occ = p->occ;
+  a.WG = p->words_per_group;
+  a.rows = p->rows;
+  a.n_rows = p->n_rows;
+  a.n_rows_host = p->n_rows_bound;
+  return a;
+}
+
+int pit_spmm_uses_tensor_cores(const pit_spmm_args* p) {
+  if (!p || p->force_simt) return 0;
+  return spmm_tc_supported(to_internal(p)) ? 1 : 0;
+}
+
+int pit_spmm(const pit_spmm_args* p, void* stream) {
+  if (!p) return fail(kErrArg, "null args");
+  if (p->plan < kPlanDense || p->plan > kPlanPitK) return fail(kErrArg, "unknown plan %d", p->plan);
+  if (p->dtype == kDtypeU8 || !dtype_ok(p->dtype)) return fail(kErrArg, "unsupported dtype code %d", p->dtype);
+  if (p->M < 0 || p->N < 0 || p->K < 0) return fail(kErrShape, "shape mismatch: negative extent");
+  if (p->M == 0 || p->N == 0) return kOk;
+  if (!p->A || !p->B || !p->C) return fail(kErrArg, "null operand pointer");
+  if (p->plan == kPlanPitK) {
+    if (p->sam != 1 && p->M > 1)
+      return fail(kErrLayout, "plan requires the sparse operand in col_major; use convert_layout first");
+    if (!p->counts || !p->slots) return fail(kErrArg, "sparse plan needs a micro-tile index");
+    if (p->t1 != 1) return fail(kErrArg, "pit:k micro-tile must be (t0,1)");
+    if (p->n_groups != ceil_div(p->M, p->t0)) return fail(kErrShape, "index groups do not match M");
+  } else if (p->plan == kPlanPitM) {
+    if (p->sak != 1 && p->K > 1)
+      return fail(kErrLayout, "plan requires the sparse operand in row_major; use convert_layout first");
+    if (!p->occ || !p->rows || !p->n_rows) return fail(kErrArg, "sparse plan needs a micro-tile index");
+    if (p->t0 != 1) return fail(kErrArg, "pit:m micro-tile must be (1,t1)");
+    if (p->n_groups != ceil_div(p->K, p->t1)) return fail(kErrShape, "index groups do not match K");
+  }
+  SpmmArgs a = to_internal(p);
+  if (a.K == 0) {  // empty contraction: C = 0
+    const int eb = dtype_bytes(a.dtype);
+    cudaMemset2DAsync(a.C, a.ldc * eb, 0, a.N * eb, a.M, static_cast<cudaStream_t>(stream));
+    return cuda_status();
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!p->force_simt && spmm_tc_supported(a)) return launch_spmm_tc(a, s);
+  return launch_spmm_simt(a, s);
+}
+
+int pit_dense_reference_f64(const double* A, int64_t s0, int64_t s1, const double* B, int64_t ldb, double* C, int64_t M,
+                            int64_t N, int64_t K, void* stream) {
+  if (M < 0 || N < 0 || K < 0) return fail(kErrShape, "shape mismatch: negative extent");
+  if (M * N && (!A || !B || !C)) return fail(kErrArg, "null operand pointer");
+  return launch_dense_ref_f64(A, s0, s1, B, ldb, C, M, N, K, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

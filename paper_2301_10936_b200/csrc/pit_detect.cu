@@ -1,0 +1,352 @@
+// K1 — online sparsity detection and micro-tile index construction.
+//
+// Semantics follow pittile.index (reference pkg/src/pittile/index.py):
+//   * micro grid anchored at multiples of the micro-tile, ceil extents, tails are zero
+//     (index.py:64-65, :96-98);
+//   * value route: an element is live iff `v != 0.0` -> implemented as a bit test that ignores
+//     the sign bit, so -0.0 is dead and NaN / inf / denormals are live (index.py:164-173);
+//   * annotation route: a micro-tile is live iff any in-extent element maps to a set block bit
+//     (index.py:68-99, sparsity.py:43-48 MSB-first packing);
+//   * per group, coordinates along the PIT axis, ascending (== reference workers=1 order,
+//     index.py:131-140), counts[g] live entries.
+//
+// Pipeline: pass 1 writes an occupancy bitmap in group-major orientation
+// (occ[g][w] bit b <=> coordinate 32w+b live in group g); pass 2 compacts each group's bits into
+// ascending int32 slots with a warp popc/scan. Pass 1 is the HBM-bound scan; pass 2 reads only
+// the bitmap (>= 16x smaller than the input).
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "pit_internal.h"
+
+namespace pit {
+
+namespace {
+
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// Per-word "value bits" mask: drops the sign bit so that -0.0 tests as zero.
+struct LiveMask {
+  uint32_t even, odd;  // applied to 32-bit words at even / odd positions of a 16-byte vector
+};
+
+__host__ __device__ inline LiveMask live_mask_for(int dtype) {
+  switch (dtype) {
+    case kDtypeF16:
+    case kDtypeBF16:
+      return {0x7fff7fffu, 0x7fff7fffu};
+    case kDtypeF32:
+      return {0x7fffffffu, 0x7fffffffu};
+    case kDtypeF64:
+      return {0xffffffffu, 0x7fffffffu};  // little endian: high word carries the sign
+    default:
+      return {0xffffffffu, 0xffffffffu};  // u8 / bool masks: any non-zero byte
+  }
+}
+
+// Element-wise liveness of one element (generic path).
+__device__ __forceinline__ bool elem_live(const uint8_t* p, int dtype) {
+  switch (dtype) {
+    case kDtypeF16:
+    case kDtypeBF16:
+      return (__ldg(reinterpret_cast<const uint16_t*>(p)) & 0x7fffu) != 0;
+    case kDtypeF32:
+      return (__ldg(reinterpret_cast<const uint32_t*>(p)) & 0x7fffffffu) != 0;
+    case kDtypeF64: {
+      unsigned long long v = __ldg(reinterpret_cast<const unsigned long long*>(p));
+      return (v & 0x7fffffffffffffffull) != 0;
+    }
+    default:
+      return __ldg(p) != 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Pass 1, fast path: coordinates along physical rows (groups = micro-columns),
+// micro-column width a power-of-two number V of 16-byte vectors (V <= 32).
+// Block = 8 warps; each warp owns a 512-byte column segment and 32 micro-row bands.
+// The lane at the start of a micro-column accumulates the 32 band bits in a register
+// and writes one bitmap word: no atomics, no shared memory.
+// ---------------------------------------------------------------------------
+constexpr int kRaWarps = 8;
+
+__global__ void __launch_bounds__(kRaWarps * 32) detect_rows_vec_kernel(const uint8_t* __restrict__ x, int64_t R,
+                                                                          int64_t row_bytes, int64_t ld_bytes, int tr,
+                                                                          int V, int64_t GR, int64_t GC,
+                                                                          LiveMask mk, uint32_t* __restrict__ occ,
+                                                                          int64_t WG) {
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int64_t seg = static_cast<int64_t>(blockIdx.x) * kRaWarps + warp;  // 512-byte segment
+  const int64_t vec = seg * 32 + lane;                                     // 16-byte vector index in a row
+  const bool col_ok = vec * 16 < row_bytes;
+  const int64_t i0 = static_cast<int64_t>(blockIdx.y) * 32;  // first micro-row band of the block
+  const int64_t r0 = i0 * tr;
+  const int64_t r1 = min(R, (i0 + 32) * tr);
+  const uint8_t* base = x + vec * 16;
+
+  const bool is_start = (lane % V) == 0;
+  const uint32_t vmask = V >= 32 ? 0xffffffffu : ((1u << V) - 1u);
+  uint32_t bits = 0;
+  uint4 acc = make_uint4(0, 0, 0, 0);
+  int band_left = tr;
+  int band = 0;
+  for (int64_t r = r0; r < r1; r += 8) {
+    uint4 buf[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t rr = r + u;
+      buf[u] = (rr < r1 && col_ok) ? ldg_stream(base + rr * ld_bytes) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (r + u >= r1) break;  // warp-uniform
+      acc.x |= buf[u].x & mk.even;
+      acc.y |= buf[u].y & mk.odd;
+      acc.z |= buf[u].z & mk.even;
+      acc.w |= buf[u].w & mk.odd;
+      if (--band_left == 0 || r + u + 1 == r1) {
+        const bool live = (acc.x | acc.y | acc.z | acc.w) != 0;
+        const uint32_t b = __ballot_sync(0xffffffffu, live);
+        if (is_start) {
+          const uint32_t f = V >= 32 ? b : ((b >> lane) & vmask);
+          bits |= (f != 0 ? 1u : 0u) << band;
+        }
+        acc = make_uint4(0, 0, 0, 0);
+        band_left = tr;
+        ++band;
+      }
+    }
+  }
+  if (is_start && col_ok) {
+    const int64_t j = vec / V;
+    if (j < GC) occ[j * WG + (i0 >> 5)] = bits;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Pass 1, generic path: any micro-tile, any alignment, element loads.
+// Block covers 32 micro-row bands x TJ micro-columns; shared-memory bitmap tile in the
+// output's group-major orientation, then plain stores of whole words.
+// ---------------------------------------------------------------------------
+constexpr int kGenThreads = 256;
+
+__global__ void __launch_bounds__(kGenThreads) detect_generic_kernel(const uint8_t* __restrict__ x, int dtype, int eb,
+                                                                       int64_t R, int64_t C, int64_t ld, int tr,
+                                                                       int tc, int64_t GR, int64_t GC, int pit_phys,
+                                                                       int TJ, uint32_t* __restrict__ occ,
+                                                                       int64_t WG) {
+  extern __shared__ uint32_t tile[];  // pit_phys==0: [TJ] words (bits over bands); ==1: [32][TJ/32]
+  const int nwords = pit_phys == 0 ? TJ : 32 * (TJ / 32);
+  for (int i = threadIdx.x; i < nwords; i += blockDim.x) tile[i] = 0;
+  __syncthreads();
+
+  const int64_t i0 = static_cast<int64_t>(blockIdx.y) * 32;
+  const int64_t j0 = static_cast<int64_t>(blockIdx.x) * TJ;
+  const int64_t c_lo = j0 * tc;
+  const int64_t c_hi = min(C, (j0 + TJ) * tc);
+  const int64_t nb = (GR - i0 < 32 ? GR - i0 : int64_t(32));
+  for (int64_t c = c_lo + threadIdx.x; c < c_hi; c += blockDim.x) {
+    const int jl = static_cast<int>(c / tc - j0);
+    for (int64_t bi = 0; bi < nb; ++bi) {
+      const int64_t ra = (i0 + bi) * tr;
+      const int64_t rb = min(R, ra + tr);
+      bool live = false;
+      for (int64_t r = ra; r < rb && !live; ++r) live = elem_live(x + (r * ld + c) * eb, dtype);
+      if (live) {
+        if (pit_phys == 0)
+          atomicOr(&tile[jl], 1u << bi);
+        else
+          atomicOr(&tile[bi * (TJ / 32) + (jl >> 5)], 1u << (jl & 31));
+      }
+    }
+  }
+  __syncthreads();
+  if (pit_phys == 0) {
+    for (int jl = threadIdx.x; jl < TJ; jl += blockDim.x) {
+      const int64_t j = j0 + jl;
+      if (j < GC) occ[j * WG + (i0 >> 5)] = tile[jl];
+    }
+  } else {
+    const int wpr = TJ / 32;
+    for (int t = threadIdx.x; t < 32 * wpr; t += blockDim.x) {
+      const int bi = t / wpr, wl = t % wpr;
+      const int64_t i = i0 + bi;
+      const int64_t w = (j0 >> 5) + wl;
+      if (i < GR && w < WG) occ[i * WG + w] = tile[t];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Pass 1, annotation route: packed MSB-first block bits. One warp per (group, word).
+// ---------------------------------------------------------------------------
+__global__ void detect_bits_kernel(const uint8_t* __restrict__ packed, int64_t s0, int64_t s1, int g0, int g1,
+                                   int t0, int t1, int pit_dim, int64_t n_groups, int64_t pit_grid, int64_t WG,
+                                   uint32_t* __restrict__ occ) {
+  const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= n_groups * WG) return;
+  const int64_t g = gw / WG, w = gw % WG;
+  const int64_t coord = w * 32 + lane;
+  bool live = false;
+  if (coord < pit_grid) {
+    const int64_t i = pit_dim == 0 ? coord : g;
+    const int64_t j = pit_dim == 0 ? g : coord;
+    const int64_t bg1 = (s1 + g1 - 1) / g1;
+    const int64_t b0 = (i * t0) / g0, b1 = (min((i + 1) * t0, s0) + g0 - 1) / g0;
+    const int64_t c0 = (j * t1) / g1, c1 = (min((j + 1) * t1, s1) + g1 - 1) / g1;
+    for (int64_t bi = b0; bi < b1 && !live; ++bi) {
+      for (int64_t bj = c0; bj < c1; ++bj) {
+        const int64_t f = bi * bg1 + bj;
+        if ((__ldg(packed + (f >> 3)) >> (7 - (f & 7))) & 1) {
+          live = true;
+          break;
+        }
+      }
+    }
+  }
+  const uint32_t word = __ballot_sync(0xffffffffu, live);
+  if (lane == 0) occ[g * WG + w] = word;
+}
+
+// ---------------------------------------------------------------------------
+// Pass 2: per-group ordered compaction. One warp per group.
+// ---------------------------------------------------------------------------
+__global__ void compact_kernel(const uint32_t* __restrict__ occ, int64_t n_groups, int64_t WG,
+                               int32_t* __restrict__ counts, int32_t* __restrict__ slots, int64_t slot_stride) {
+  const int64_t g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (g >= n_groups) return;
+  const uint32_t* row = occ + g * WG;
+  int32_t* out = slots + g * slot_stride;
+  int base = 0;
+  for (int64_t w0 = 0; w0 < WG; w0 += 32) {
+    const int64_t w = w0 + lane;
+    uint32_t word = w < WG ? row[w] : 0u;
+    const int c = __popc(word);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    int pos = base + incl - c;
+    while (word) {
+      const int b = __ffs(word) - 1;
+      word &= word - 1;
+      out[pos++] = static_cast<int32_t>(w * 32 + b);
+    }
+    base += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (lane == 0) counts[g] = base;
+}
+
+// OR of all group rows: the union of live coordinates (used by pit:m union-row tiles).
+__global__ void union_kernel(const uint32_t* __restrict__ occ, int64_t n_groups, int64_t WG,
+                             uint32_t* __restrict__ uni) {
+  const int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (w >= WG) return;
+  uint32_t acc = 0;
+  for (int64_t g = 0; g < n_groups; ++g) acc |= occ[g * WG + w];
+  uni[w] = acc;
+}
+
+// Rebuild the occupancy bitmap from (possibly reordered) slots: lets kernels that need
+// per-(coordinate, group) liveness accept an arbitrary user-supplied index.
+__global__ void slots_to_occ_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ slots,
+                                    int64_t slot_stride, int64_t n_groups, int64_t WG, int64_t pit_grid,
+                                    uint32_t* __restrict__ occ, int* __restrict__ bad) {
+  const int64_t g = blockIdx.y;
+  if (g >= n_groups) return;
+  const int cnt = counts[g];
+  for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < cnt;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t c = slots[g * slot_stride + s];
+    if (c < 0 || c >= pit_grid) {
+      atomicExch(bad, 1);
+      continue;
+    }
+    atomicOr(&occ[g * WG + (c >> 5)], 1u << (c & 31));
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------- launchers
+int launch_detect_values(const DetectValuesArgs& a, cudaStream_t s) {
+  const int eb = dtype_bytes(a.dtype);
+  const int64_t GR = ceil_div(a.R, a.tr), GC = ceil_div(a.C, a.tc);
+  const int64_t n_groups = a.pit_phys == 0 ? GC : GR;
+  const int64_t pit_grid = a.pit_phys == 0 ? GR : GC;
+  const int64_t WG = ceil_div(pit_grid, 32);
+  if (n_groups == 0 || pit_grid == 0) return 0;
+
+  const int64_t row_bytes = a.C * eb, ld_bytes = a.ld * eb;
+  const int64_t vec_per_micro = (static_cast<int64_t>(a.tc) * eb) / 16;
+  const bool aligned = (reinterpret_cast<uintptr_t>(a.x) % 16 == 0) && (ld_bytes % 16 == 0) && (row_bytes % 16 == 0);
+  const bool pow2 = vec_per_micro >= 1 && vec_per_micro <= 32 && (vec_per_micro & (vec_per_micro - 1)) == 0 &&
+                    (static_cast<int64_t>(a.tc) * eb) % 16 == 0;
+  if (a.pit_phys == 0 && aligned && pow2) {
+    const int64_t segs = ceil_div(row_bytes, 512);
+    dim3 grid(static_cast<unsigned>(ceil_div(segs, kRaWarps)), static_cast<unsigned>(ceil_div(GR, 32)));
+    if (grid.y > 65535u) return kErrShape;
+    detect_rows_vec_kernel<<<grid, kRaWarps * 32, 0, s>>>(static_cast<const uint8_t*>(a.x), a.R, row_bytes,
+                                                          ld_bytes, a.tr, static_cast<int>(vec_per_micro), GR, GC,
+                                                          live_mask_for(a.dtype), a.occ, WG);
+  } else {
+    const int TJ = a.pit_phys == 0 ? 256 : (a.tc >= 8 ? 32 : 128);
+    dim3 grid(static_cast<unsigned>(ceil_div(GC, TJ)), static_cast<unsigned>(ceil_div(GR, 32)));
+    if (grid.y > 65535u) return kErrShape;
+    const size_t smem = sizeof(uint32_t) * (a.pit_phys == 0 ? TJ : TJ);
+    detect_generic_kernel<<<grid, kGenThreads, smem, s>>>(static_cast<const uint8_t*>(a.x), a.dtype, eb, a.R, a.C,
+                                                          a.ld, a.tr, a.tc, GR, GC, a.pit_phys, TJ, a.occ, WG);
+  }
+  return cuda_status();
+}
+
+int launch_detect_bits(const DetectBitsArgs& a, cudaStream_t s) {
+  const int64_t G0 = ceil_div(a.s0, a.t0), G1 = ceil_div(a.s1, a.t1);
+  const int64_t n_groups = a.pit_dim == 0 ? G1 : G0;
+  const int64_t pit_grid = a.pit_dim == 0 ? G0 : G1;
+  const int64_t WG = ceil_div(pit_grid, 32);
+  if (n_groups == 0 || pit_grid == 0) return 0;
+  const int64_t warps = n_groups * WG;
+  const int threads = 256;
+  detect_bits_kernel<<<static_cast<unsigned>(ceil_div(warps * 32, threads)), threads, 0, s>>>(
+      a.packed, a.s0, a.s1, a.g0, a.g1, a.t0, a.t1, a.pit_dim, n_groups, pit_grid, WG, a.occ);
+  return cuda_status();
+}
+
+int launch_compact(const uint32_t* occ, int64_t n_groups, int64_t WG, int32_t* counts, int32_t* slots,
+                   int64_t slot_stride, cudaStream_t s) {
+  if (n_groups == 0) return 0;
+  const int threads = 256;
+  compact_kernel<<<static_cast<unsigned>(ceil_div(n_groups * 32, threads)), threads, 0, s>>>(occ, n_groups, WG, counts,
+                                                                                            slots, slot_stride);
+  return cuda_status();
+}
+
+int launch_union(const uint32_t* occ, int64_t n_groups, int64_t WG, uint32_t* uni, cudaStream_t s) {
+  if (WG == 0) return 0;
+  union_kernel<<<static_cast<unsigned>(ceil_div(WG, 256)), 256, 0, s>>>(occ, n_groups, WG, uni);
+  return cuda_status();
+}
+
+int launch_slots_to_occ(const int32_t* counts, const int32_t* slots, int64_t slot_stride, int64_t n_groups,
+                        int64_t WG, int64_t pit_grid, uint32_t* occ, int* bad, cudaStream_t s) {
+  if (n_groups == 0) return 0;
+  cudaMemsetAsync(occ, 0, sizeof(uint32_t) * n_groups * WG, s);
+  dim3 grid(static_cast<unsigned>((ceil_div(pit_grid, 256) < 64 ? ceil_div(pit_grid, 256) : int64_t(64))), static_cast<unsigned>(n_groups));
+  if (n_groups > 65535) return kErrShape;
+  slots_to_occ_kernel<<<grid, 256, 0, s>>>(counts, slots, slot_stride, n_groups, WG, pit_grid, occ, bad);
+  return cuda_status();
+}
+
+}  // namespace pit

@@ -1,0 +1,131 @@
+// Internal launcher interfaces shared by the .cu files and the C-ABI layer (pit_capi.cu).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace pit {
+
+// dtype codes shared with include/pit_b200.h
+enum : int {
+  kDtypeF32 = 0,
+  kDtypeF64 = 1,
+  kDtypeBF16 = 2,
+  kDtypeF16 = 3,
+  kDtypeU8 = 4,
+};
+
+// status codes shared with include/pit_b200.h
+enum : int {
+  kOk = 0,
+  kErrArg = 1,
+  kErrShape = 2,
+  kErrLayout = 3,
+  kErrRange = 4,
+  kErrCuda = 5,
+  kErrUnsupported = 6,
+};
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+inline int dtype_bytes(int dtype) {
+  switch (dtype) {
+    case kDtypeF32:
+      return 4;
+    case kDtypeF64:
+      return 8;
+    case kDtypeBF16:
+    case kDtypeF16:
+      return 2;
+    case kDtypeU8:
+      return 1;
+    default:
+      return 0;
+  }
+}
+
+int cuda_status();  // maps cudaGetLastError() to kOk / kErrCuda and records the message
+
+// ------------------------------------------------------------------ K1 detect
+struct DetectValuesArgs {
+  const void* x;  // physical row-major [R, C], row pitch ld elements
+  int dtype;
+  int64_t R, C, ld;
+  int tr, tc;    // micro-tile in physical orientation
+  int pit_phys;  // 0: coordinates run along physical rows (groups = micro-columns); 1: along columns
+  uint32_t* occ; // [n_groups][WG] group-major bitmap, fully overwritten
+};
+
+struct DetectBitsArgs {
+  const uint8_t* packed;  // MSB-first packed block bits, row-major over the block grid
+  int64_t s0, s1;         // logical tensor shape
+  int g0, g1;             // block granularity
+  int t0, t1;             // micro-tile
+  int pit_dim;            // 0 or 1 (logical)
+  uint32_t* occ;
+};
+
+int launch_detect_values(const DetectValuesArgs& a, cudaStream_t s);
+int launch_detect_bits(const DetectBitsArgs& a, cudaStream_t s);
+int launch_compact(const uint32_t* occ, int64_t n_groups, int64_t WG, int32_t* counts, int32_t* slots,
+                   int64_t slot_stride, cudaStream_t s);
+int launch_union(const uint32_t* occ, int64_t n_groups, int64_t WG, uint32_t* uni, cudaStream_t s);
+int launch_slots_to_occ(const int32_t* counts, const int32_t* slots, int64_t slot_stride, int64_t n_groups,
+                        int64_t WG, int64_t pit_grid, uint32_t* occ, int* bad, cudaStream_t s);
+
+// ---------------------------------------------------------- K5 SRead / SWrite
+struct GatherArgs {
+  void* src_or_dst;     // tensor, logical [R, C], element (i,j) at i*st0 + j*st1
+  void* tile;           // tile buffer, row-major [TR, TC] (contiguous)
+  int dtype;
+  int64_t R, C, st0, st1;
+  int64_t TR, TC;
+  int t_d, t_o;          // micro extent along the gather axis / the other axis
+  int d;                 // logical gather axis (pit_dim)
+  const int32_t* coords; // device, n_coords entries (already offset by start)
+  int64_t n_coords;
+  int64_t off_o;         // element offset along the other axis (group * t_o)
+  int accumulate;        // swrite only
+  int zero_fill;         // sread only: clear slots that receive no data (executor.py:195-198)
+};
+int launch_sread(const GatherArgs& a, cudaStream_t s);
+int launch_swrite(const GatherArgs& a, cudaStream_t s);
+
+// ------------------------------------------------------------------- SpMM
+enum : int { kPlanDense = 0, kPlanPitM = 1, kPlanPitK = 2 };
+
+struct SpmmArgs {
+  int plan;     // kPlanDense / kPlanPitM / kPlanPitK
+  int dtype;    // operands and C share a dtype; accumulation fp32 (fp64 for f64)
+  int64_t M, N, K;
+  const void* A;  // logical [M,K]; element (m,k) at A + m*sam + k*sak
+  int64_t sam, sak;
+  const void* B;  // row-major [K,N], pitch ldb
+  int64_t ldb;
+  void* C;        // row-major [M,N], pitch ldc; fully written by the call
+  int64_t ldc;
+  int t0, t1;     // plan micro-tile (logical)
+  // index (device): pit:k groups = M-blocks (coords = k), pit:m groups = K-blocks (coords = rows)
+  const int32_t* counts;
+  const int32_t* slots;
+  int64_t slot_stride;
+  int64_t n_groups;
+  const uint32_t* occ;      // group-major bitmap [n_groups][WG] (pit:m)
+  int64_t WG;
+  const int32_t* rows;      // pit:m union rows (ascending), n_rows entries
+  const int32_t* n_rows;    // device scalar
+  int64_t n_rows_host;      // upper bound used for the grid (<= M)
+};
+
+int launch_spmm_simt(const SpmmArgs& a, cudaStream_t s);
+int launch_dense_ref_f64(const double* A, int64_t s0, int64_t s1, const double* B, int64_t ldb, double* C, int64_t M,
+                         int64_t N, int64_t K, cudaStream_t s);
+int launch_spmm_tc(const SpmmArgs& a, cudaStream_t s);  // bf16 / fp16 tcgen05 paths
+bool spmm_tc_supported(const SpmmArgs& a);
+
+// Driver entry point for cuTensorMapEncodeTiled (resolved through the runtime, no -lcuda).
+CUresult encode_tensor_map_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner,
+                              uint64_t outer, uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_outer,
+                              CUtensorMapSwizzle swizzle);
+
+}  // namespace pit

@@ -1,0 +1,338 @@
+// PIT sparse matmul on the CUDA cores (FFMA / DFMA): the fp32 and f64 parity path
+// (north_star: fp32 within 1e-5 with TF32 disabled) and the fallback for micro-tiles the
+// tensor-core kernels do not tile (odd widths, unaligned pitches).
+//
+// Same plan semantics as pit_spmm_tc.cu:
+//   pit:k  (executor.py:386-423)  CTA = (group g, 64-row chunk of the group, 64-column tile);
+//          K runs over the group's live coordinates in stored order.
+//   pit:m  (executor.py:352-383)  CTA = (64 union rows, 64 columns); K runs ascending, an
+//          (row, K-block) pair that is not live contributes 0.
+//   dense  (executor.py:426-461)  union rows = all rows.
+// Accumulation is fp32 (f64 for f64 operands) in ascending stored order.
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "pit_internal.h"
+
+namespace pit {
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, TPB = 256;
+
+template <typename T>
+__device__ __forceinline__ float to_acc(T v);
+template <>
+__device__ __forceinline__ float to_acc<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ float to_acc<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <>
+__device__ __forceinline__ float to_acc<__half>(__half v) { return __half2float(v); }
+
+template <typename T, typename Acc>
+__device__ __forceinline__ Acc load_as(const T* p) {
+  return static_cast<Acc>(to_acc<T>(*p));
+}
+template <>
+__device__ __forceinline__ double load_as<double, double>(const double* p) {
+  return *p;
+}
+
+template <typename T, typename Acc>
+__device__ __forceinline__ T from_acc(Acc v);
+template <>
+__device__ __forceinline__ float from_acc<float, float>(float v) { return v; }
+template <>
+__device__ __forceinline__ double from_acc<double, double>(double v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_acc<__nv_bfloat16, float>(float v) { return __float2bfloat16_rn(v); }
+template <>
+__device__ __forceinline__ __half from_acc<__half, float>(float v) { return __float2half_rn(v); }
+
+template <typename T, typename Acc>
+__global__ void __launch_bounds__(TPB) spmm_simt_kernel(SpmmArgs a) {
+  __shared__ Acc As[BK][BM + 1];
+  __shared__ Acc Bs[BK][BN + 1];
+  __shared__ int32_t rowmap[BM];
+  __shared__ int32_t kmap[BK];
+
+  const T* A = static_cast<const T*>(a.A);
+  const T* B = static_cast<const T*>(a.B);
+  T* C = static_cast<T*>(a.C);
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;
+  const int64_t n0 = static_cast<int64_t>(blockIdx.x) * BN;
+
+  // ---- rows of this tile
+  int64_t g = 0, k_count = a.K;
+  const int32_t* klist = nullptr;
+  if (a.plan == kPlanPitK) {
+    const int64_t chunks = (a.t0 + BM - 1) / BM;
+    g = blockIdx.y / chunks;
+    const int64_t rc = blockIdx.y % chunks;
+    if (tid < BM) {
+      const int64_t lr = rc * BM + tid;  // row within the group
+      const int64_t m = g * a.t0 + lr;
+      rowmap[tid] = (lr < a.t0 && m < a.M) ? static_cast<int32_t>(m) : -1;
+    }
+    k_count = a.counts[g];
+    klist = a.slots + g * a.slot_stride;
+  } else {
+    const int n_rows = a.plan == kPlanDense ? static_cast<int>(a.M) : *a.n_rows;
+    if (tid < BM) {
+      const int64_t i = static_cast<int64_t>(blockIdx.y) * BM + tid;
+      rowmap[tid] = i < n_rows ? (a.plan == kPlanDense ? static_cast<int32_t>(i) : a.rows[i]) : -1;
+    }
+  }
+  __syncthreads();
+
+  Acc acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = Acc(0);
+
+  for (int64_t kb = 0; kb < k_count; kb += BK) {
+    if (tid < BK) {
+      const int64_t kk = kb + tid;
+      kmap[tid] = kk < k_count ? (klist ? klist[kk] : static_cast<int32_t>(kk)) : -1;
+    }
+    __syncthreads();
+    // A tile: BM x BK
+    for (int e = tid; e < BM * BK; e += TPB) {
+      int r, kk;
+      if (a.sak == 1) {
+        kk = e % BK;
+        r = e / BK;
+      } else {
+        r = e % BM;
+        kk = e / BM;
+      }
+      const int32_t m = rowmap[r];
+      const int32_t k = kmap[kk];
+      Acc v = Acc(0);
+      if (m >= 0 && k >= 0) {
+        bool live = true;
+        if (a.plan == kPlanPitM) {
+          const int64_t grp = k / a.t1;
+          live = (a.occ[grp * a.WG + (m >> 5)] >> (m & 31)) & 1u;
+        }
+        if (live) v = load_as<T, Acc>(A + m * a.sam + static_cast<int64_t>(k) * a.sak);
+      }
+      As[kk][r] = v;
+    }
+    // B tile: BK x BN
+    for (int e = tid; e < BK * BN; e += TPB) {
+      const int c = e % BN, kk = e / BN;
+      const int32_t k = kmap[kk];
+      const int64_t n = n0 + c;
+      Bs[kk][c] = (k >= 0 && n < a.N) ? load_as<T, Acc>(B + static_cast<int64_t>(k) * a.ldb + n) : Acc(0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      Acc av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int32_t m = rowmap[ty * 4 + i];
+    if (m < 0) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t n = n0 + tx * 4 + j;
+      if (n < a.N) C[m * a.ldc + n] = from_acc<T, Acc>(acc[i][j]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ SRead / SWrite
+// Tile buffer is row-major [TR, TC]; the tensor is logical [R, C] with element strides (st0, st1).
+// d is the logical axis the gather runs along. Slot s, micro offset i covers tensor
+// index coord*t_d + i along d and off_o + jo along the other axis (executor.py:170-264).
+template <typename T>
+__global__ void sread_kernel(GatherArgs a, int zero_fill) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= a.TR * a.TC) return;
+  const int64_t tr = e / a.TC, tc = e % a.TC;
+  const int64_t td = a.d == 0 ? tr : tc;  // index along the gather axis in the tile
+  const int64_t to = a.d == 0 ? tc : tr;
+  const int64_t s = td / a.t_d, i = td % a.t_d;
+  const int64_t ext_d = a.d == 0 ? a.R : a.C;
+  const int64_t ext_o = a.d == 0 ? a.C : a.R;
+  T* tile = static_cast<T*>(a.tile);
+  const T* src = static_cast<const T*>(a.src_or_dst);
+  bool copied = false;
+  if (s < a.n_coords && to < a.t_o) {
+    const int64_t gd = static_cast<int64_t>(a.coords[s]) * a.t_d + i;
+    const int64_t go = a.off_o + to;
+    if (gd < ext_d && go < ext_o) {
+      const int64_t r = a.d == 0 ? gd : go, c = a.d == 0 ? go : gd;
+  const int64_t off = r * a.st0 + c * a.st1;
+      tile[e] = src[off];
+      copied = true;
+    }
+  }
+  if (!copied && zero_fill) tile[e] = T(0);
+}
+
+template <typename T>
+__global__ void swrite_kernel(GatherArgs a) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= a.TR * a.TC) return;
+  const int64_t tr = e / a.TC, tc = e % a.TC;
+  const int64_t td = a.d == 0 ? tr : tc;
+  const int64_t to = a.d == 0 ? tc : tr;
+  const int64_t s = td / a.t_d, i = td % a.t_d;
+  const int64_t ext_d = a.d == 0 ? a.R : a.C;
+  const int64_t ext_o = a.d == 0 ? a.C : a.R;
+  if (s >= a.n_coords || to >= a.t_o) return;
+  const int64_t gd = static_cast<int64_t>(a.coords[s]) * a.t_d + i;
+  const int64_t go = a.off_o + to;
+  if (gd >= ext_d || go >= ext_o) return;
+  const int64_t r = a.d == 0 ? gd : go, c = a.d == 0 ? go : gd;
+  const int64_t off = r * a.st0 + c * a.st1;
+  T* dst = static_cast<T*>(a.src_or_dst);
+  const T* tile = static_cast<const T*>(a.tile);
+  if (a.accumulate)
+    dst[off] = from_acc<T, float>(load_as<T, float>(dst + off) + load_as<T, float>(tile + e));
+  else
+    dst[off] = tile[e];
+}
+
+template <>
+__global__ void swrite_kernel<double>(GatherArgs a) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= a.TR * a.TC) return;
+  const int64_t tr = e / a.TC, tc = e % a.TC;
+  const int64_t td = a.d == 0 ? tr : tc;
+  const int64_t to = a.d == 0 ? tc : tr;
+  const int64_t s = td / a.t_d, i = td % a.t_d;
+  const int64_t ext_d = a.d == 0 ? a.R : a.C;
+  const int64_t ext_o = a.d == 0 ? a.C : a.R;
+  if (s >= a.n_coords || to >= a.t_o) return;
+  const int64_t gd = static_cast<int64_t>(a.coords[s]) * a.t_d + i;
+  const int64_t go = a.off_o + to;
+  if (gd >= ext_d || go >= ext_o) return;
+  const int64_t r = a.d == 0 ? gd : go, c = a.d == 0 ? go : gd;
+  const int64_t off = r * a.st0 + c * a.st1;
+  double* dst = static_cast<double*>(a.src_or_dst);
+  const double* tile = static_cast<const double*>(a.tile);
+  dst[off] = a.accumulate ? dst[off] + tile[e] : tile[e];
+}
+
+// f64 oracle: multiply then add (no FMA contraction), reduction ascending -- the exact operation
+// sequence of the reference's scalar triple loop (executor.py:267-283, test_executor.py:68-71).
+__global__ void dense_ref_f64_kernel(const double* __restrict__ A, int64_t s0, int64_t s1,
+                                     const double* __restrict__ B, int64_t ldb, double* __restrict__ C, int64_t M,
+                                     int64_t N, int64_t K) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= M * N) return;
+  const int64_t i = e / N, j = e % N;
+  double acc = 0.0;
+  for (int64_t k = 0; k < K; ++k) acc = __dadd_rn(acc, __dmul_rn(A[i * s0 + k * s1], B[k * ldb + j]));
+  C[e] = acc;
+}
+
+template <typename T, typename Acc>
+int run_simt(const SpmmArgs& a, cudaStream_t s) {
+  int64_t ytiles;
+  if (a.plan == kPlanPitK) {
+    ytiles = a.n_groups * ceil_div(a.t0, BM);
+  } else {
+    if (a.plan == kPlanPitM) {
+      if (cudaMemset2DAsync(a.C, a.ldc * sizeof(T), 0, a.N * sizeof(T), a.M, s) != cudaSuccess) return cuda_status();
+    }
+    ytiles = ceil_div(a.plan == kPlanDense ? a.M : a.n_rows_host, BM);
+  }
+  const int64_t xtiles = ceil_div(a.N, BN);
+  if (ytiles == 0 || xtiles == 0) return kOk;
+  if (ytiles > 65535 || xtiles > (1ll << 31) - 1) return kErrShape;
+  spmm_simt_kernel<T, Acc><<<dim3(static_cast<unsigned>(xtiles), static_cast<unsigned>(ytiles)), TPB, 0, s>>>(a);
+  return cuda_status();
+}
+
+}  // namespace
+
+int launch_spmm_simt(const SpmmArgs& a, cudaStream_t s) {
+  switch (a.dtype) {
+    case kDtypeF32:
+      return run_simt<float, float>(a, s);
+    case kDtypeF64:
+      return run_simt<double, double>(a, s);
+    case kDtypeBF16:
+      return run_simt<__nv_bfloat16, float>(a, s);
+    case kDtypeF16:
+      return run_simt<__half, float>(a, s);
+    default:
+      return kErrUnsupported;
+  }
+}
+
+int launch_dense_ref_f64(const double* A, int64_t s0, int64_t s1, const double* B, int64_t ldb, double* C, int64_t M,
+                         int64_t N, int64_t K, cudaStream_t s) {
+  if (M * N == 0) return kOk;
+  dense_ref_f64_kernel<<<static_cast<unsigned>(ceil_div(M * N, 256)), 256, 0, s>>>(A, s0, s1, B, ldb, C, M, N, K);
+  return cuda_status();
+}
+
+int launch_sread(const GatherArgs& a, cudaStream_t s) {
+  const int64_t n = a.TR * a.TC;
+  if (n == 0) return kOk;
+  const int zero_fill = a.zero_fill;
+  const unsigned grid = static_cast<unsigned>(ceil_div(n, 256));
+  switch (a.dtype) {
+    case kDtypeF32:
+      sread_kernel<float><<<grid, 256, 0, s>>>(a, zero_fill);
+      break;
+    case kDtypeF64:
+      sread_kernel<double><<<grid, 256, 0, s>>>(a, zero_fill);
+      break;
+    case kDtypeBF16:
+      sread_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(a, zero_fill);
+      break;
+    case kDtypeF16:
+      sread_kernel<__half><<<grid, 256, 0, s>>>(a, zero_fill);
+      break;
+    default:
+      return kErrUnsupported;
+  }
+  return cuda_status();
+}
+
+int launch_swrite(const GatherArgs& a, cudaStream_t s) {
+  const int64_t n = a.TR * a.TC;
+  if (n == 0) return kOk;
+  const unsigned grid = static_cast<unsigned>(ceil_div(n, 256));
+  switch (a.dtype) {
+    case kDtypeF32:
+      swrite_kernel<float><<<grid, 256, 0, s>>>(a);
+      break;
+    case kDtypeF64:
+      swrite_kernel<double><<<grid, 256, 0, s>>>(a);
+      break;
+    case kDtypeBF16:
+      swrite_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(a);
+      break;
+    case kDtypeF16:
+      swrite_kernel<__half><<<grid, 256, 0, s>>>(a);
+      break;
+    default:
+      return kErrUnsupported;
+  }
+  return cuda_status();
+}
+
+}  // namespace pit

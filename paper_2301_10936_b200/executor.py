@@ -1,0 +1,464 @@
+"""Sparse operator execution on B200: SRead -> tensor-core tile compute -> SWrite.
+
+Mirrors the operator surface of ``pittile.executor`` (reference pkg/src/pittile/executor.py:
+``sread`` :170-208, ``swrite`` :211-264, ``run_matmul_with_index`` :464-516,
+``run_sparse_matmul`` :519-537) with the same validation order, error types and messages.
+Execution is one launch of a fused kernel from libpit_b200.so:
+
+* bf16 / fp16 operands -> tcgen05 kernels (``pit:k`` gathered-K with TMA gather4, ``pit:m`` and
+  dense as union-row tiles resident in TMEM);
+* fp32 / f64 operands -> CUDA-core FFMA / DFMA kernels (the reference's f32/f64 dtypes,
+  executor.py:40-41; TF32 is never used, so fp32 parity holds at 1e-5).
+
+Host numpy operands are uploaded through pinned staging and the result is read back, so the
+reference's numpy-in / numpy-out contract holds; CUDA tensors stay on the device end to end.
+There is no CPU fallback: without a GPU every call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import struct
+from dataclasses import dataclass
+from pathlib import Path
+from typing import Optional, Union
+
+import numpy as np
+
+from . import _device, _lib
+from .index import PIT_DIMS, MicroTileIndex, build_index
+from .policy import SparseKernelPlan, dense_launches, launches_from_counts
+from .sparsity import SparsityAnnotation
+from .tiles import COL_MAJOR, ROW_MAJOR
+
+
+class ExecError(ValueError):
+    pass
+
+
+class LayoutError(ExecError):
+    pass
+
+
+_NP_DTYPES = (np.dtype(np.float32), np.dtype(np.float64))
+_MAGIC = b"PITT"
+_CODES = {np.dtype(np.float32): 0, np.dtype(np.float64): 1}
+_FROM_CODE = {v: k for k, v in _CODES.items()}
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _is_torch(x) -> bool:
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(x, torch.Tensor)
+
+
+def _torch_layout(t) -> Optional[str]:
+    if t.dim() != 2:
+        return ROW_MAJOR if t.is_contiguous() else None
+    s0, s1 = t.stride()
+    r, c = t.shape
+    if (s1 == 1 or c == 1) and (s0 == c or r == 1):
+        return ROW_MAJOR
+    if (s0 == 1 or r == 1) and (s1 == r or c == 1):
+        return COL_MAJOR
+    return None
+
+
+@dataclass
+class DenseTensor:
+    """Contiguous 2-D (or n-d) buffer; ``array`` is a numpy array (host) or a torch tensor."""
+
+    array: object
+
+    def __post_init__(self):
+        if _is_torch(self.array):
+            torch = _torch()
+            if self.array.dtype not in (torch.float32, torch.float64, torch.bfloat16, torch.float16):
+                raise ExecError(f"unsupported dtype {self.array.dtype}")
+            if _torch_layout(self.array) is None:
+                raise ExecError("tensor buffer must be contiguous")
+            return
+        if self.array.dtype not in _NP_DTYPES:
+            raise ExecError(f"unsupported dtype {self.array.dtype}")
+        if not (self.array.flags.c_contiguous or self.array.flags.f_contiguous):
+            raise ExecError("tensor buffer must be contiguous")
+
+    @property
+    def shape(self) -> tuple[int, ...]:
+        return tuple(self.array.shape)
+
+    @property
+    def dtype(self):
+        return self.array.dtype
+
+    @property
+    def is_device(self) -> bool:
+        return _is_torch(self.array)
+
+    @property
+    def layout(self) -> str:
+        if self.is_device:
+            return _torch_layout(self.array)
+        return ROW_MAJOR if self.array.flags.c_contiguous else COL_MAJOR
+
+    def numpy(self) -> np.ndarray:
+        return _device.to_host(self.array, self.layout) if self.is_device else self.array
+
+    @classmethod
+    def from_array(cls, arr, layout: str = ROW_MAJOR, dtype=None) -> "DenseTensor":
+        if _is_torch(arr):
+            t = arr if dtype is None else arr.to(dtype)
+            t = t.contiguous() if layout == ROW_MAJOR else t.t().contiguous().t()
+            return cls(t)
+        a = np.asarray(arr, dtype=dtype)
+        if a.dtype not in _NP_DTYPES:
+            a = a.astype(np.float32)
+        return cls(np.array(a, order="C" if layout == ROW_MAJOR else "F", copy=True))
+
+    @classmethod
+    def zeros(cls, shape, dtype=np.float32, layout: str = ROW_MAJOR) -> "DenseTensor":
+        return cls(np.zeros(shape, dtype=dtype, order="C" if layout == ROW_MAJOR else "F"))
+
+
+def convert_layout(t: DenseTensor, layout: str) -> DenseTensor:
+    """Copy into the requested memory order (explicit only; executor.py:79-89)."""
+    if layout not in (ROW_MAJOR, COL_MAJOR):
+        raise LayoutError(f"unknown layout {layout!r}")
+    if t.layout == layout:
+        return t
+    return DenseTensor.from_array(t.array, layout=layout)
+
+
+def save_tensor(t: DenseTensor, path: Union[str, Path]) -> None:
+    """``PITT`` binary: 16-byte header, int64 extents, raw little-endian values in memory order."""
+    arr = t.numpy()
+    if arr.dtype not in _CODES:
+        arr = arr.astype(np.float32)
+    col = t.layout == COL_MAJOR
+    header = _MAGIC + struct.pack("<BBB9x", _CODES[arr.dtype], arr.ndim, 1 if col else 0)
+    body = np.ascontiguousarray(arr.ravel(order="F" if col else "C")).astype(arr.dtype.newbyteorder("<"))
+    Path(path).write_bytes(header + struct.pack(f"<{arr.ndim}q", *arr.shape) + body.tobytes())
+
+
+def load_tensor(path: Union[str, Path]) -> DenseTensor:
+    raw = Path(path).read_bytes()
+    if len(raw) < 16 or raw[:4] != _MAGIC:
+        raise ExecError(f"{path}: not a tensor file (bad magic)")
+    code, rank, lay = struct.unpack("<BBB9x", raw[4:16])
+    if code not in _FROM_CODE:
+        raise ExecError(f"{path}: unknown dtype code {code}")
+    shape = struct.unpack(f"<{rank}q", raw[16 : 16 + 8 * rank])
+    dt = _FROM_CODE[code]
+    vals = np.frombuffer(raw[16 + 8 * rank :], dtype=dt.newbyteorder("<"), count=int(np.prod(shape)))
+    order = "F" if lay == 1 else "C"
+    return DenseTensor(np.array(vals.astype(dt).reshape(shape, order=order), order=order, copy=True))
+
+
+@dataclass(frozen=True)
+class Permutation:
+    axis: str
+    mapping: np.ndarray
+
+    def __post_init__(self):
+        m = np.asarray(self.mapping, dtype=np.int64)
+        object.__setattr__(self, "mapping", m)
+        if m.ndim != 1 or not np.array_equal(np.sort(m), np.arange(m.size)):
+            raise ExecError(f"mapping is not a bijection on [0,{m.size})")
+
+    @property
+    def extent(self) -> int:
+        return int(self.mapping.size)
+
+
+def invert(p: Permutation) -> Permutation:
+    inv = np.empty_like(p.mapping)
+    inv[p.mapping] = np.arange(p.mapping.size)
+    return Permutation(p.axis, inv)
+
+
+def apply_permutation(t, p: Permutation, dim: Optional[int] = None):
+    """out[..., mapping[i], ...] = in[..., i, ...] (a test utility for invariance checks)."""
+    is_dt = isinstance(t, DenseTensor)
+    arr = t.numpy() if is_dt else np.asarray(t)
+    if dim is None:
+        if p.axis not in PIT_DIMS:
+            raise ExecError(f"cannot infer dimension for axis {p.axis!r}; pass dim")
+        dim = PIT_DIMS[p.axis]
+    if arr.shape[dim] != p.extent:
+        raise ExecError(f"extent {arr.shape[dim]} does not match permutation {p.extent}")
+    out = np.empty_like(arr)
+    sel = [slice(None)] * arr.ndim
+    sel[dim] = p.mapping
+    out[tuple(sel)] = arr
+    return DenseTensor.from_array(out, layout=t.layout, dtype=arr.dtype) if is_dt else out
+
+
+@dataclass
+class ExecStats:
+    launches: int = 0
+    gathered_micro_tiles: int = 0
+
+
+def _array(x):
+    return x.array if isinstance(x, DenseTensor) else (x if _is_torch(x) else np.asarray(x))
+
+
+# ---------------------------------------------------------------------------- SRead / SWrite
+def _gather_checks(arr_shape, idx: MicroTileIndex, group: int, n_slots: int, start: int, for_write: bool):
+    t0, t1 = idx.micro_tile
+    d = idx.pit_dim
+    if group < 0 or group >= idx.n_groups:
+        raise ExecError(f"group {group} out of range [0,{idx.n_groups})")
+    t_d, t_o = (t0, t1) if d == 0 else (t1, t0)
+    coords = idx.group(group)[start : start + n_slots]
+    off_o = group * t_o
+    v_o = min(t_o, arr_shape[1 - d] - off_o)
+    if (for_write and v_o <= 0) or (not for_write and off_o >= arr_shape[1 - d]):
+        raise ExecError(f"group {group} window outside tensor")
+    if coords.size and int(coords.max()) * t_d >= arr_shape[d]:
+        raise ExecError("micro-tile coordinate out of range")
+    edge = bool(coords.size) and (int(coords.max()) + 1) * t_d > arr_shape[d]
+    return coords, t_d, v_o, edge
+
+
+def _tensor_geometry(t):
+    """(ld, col_major) of a 2-D device tensor."""
+    s0, s1 = t.stride()
+    if _torch_layout(t) == COL_MAJOR and t.shape[0] > 1:
+        return s1, 1
+    return s0, 0
+
+
+def sread(src, idx: MicroTileIndex, group: int, tile_buffer, start: int = 0) -> int:
+    """Gather one group's micro-tiles (stored order) into consecutive tile slots; see executor.py:170."""
+    arr = _array(src)
+    d = idx.pit_dim
+    t_d = idx.micro_tile[0] if d == 0 else idx.micro_tile[1]
+    n_slots = tile_buffer.shape[d] // t_d
+    coords, t_d, v_o, edge = _gather_checks(arr.shape, idx, group, n_slots, start, False)
+    full = coords.size == n_slots and v_o == tile_buffer.shape[1 - d]
+    torch = _torch()
+    dev = _device.require_cuda()
+    x = _device.to_device(arr)
+    host_tile = not _is_torch(tile_buffer)
+    tile = _device.to_device(np.ascontiguousarray(tile_buffer)) if host_tile else tile_buffer
+    if not tile.is_contiguous():
+        raise ExecError("tile buffer must be contiguous")
+    cd = torch.from_numpy(np.ascontiguousarray(coords, dtype=np.int32)).to(dev)
+    ld, col = _tensor_geometry(x)
+    lib = _lib.load()
+    _device.check(lib.pit_sread(x.data_ptr(), _device.dtype_code(x), arr.shape[0], arr.shape[1], ld, col,
+                                tile.data_ptr(), tile.shape[0], tile.shape[1], idx.micro_tile[0], idx.micro_tile[1],
+                                d, group, cd.data_ptr(), coords.size, int((not full) or edge),
+                                _device.stream_ptr()), ExecError)
+    if host_tile:
+        tile_buffer[...] = _device.to_host(tile)
+    return int(coords.size)
+
+
+def swrite(tile_buffer, dst, idx: MicroTileIndex, group: int, start: int = 0, accumulate: bool = False) -> int:
+    """Scatter tile slots back to their micro-tiles (mirror of sread; executor.py:211-264)."""
+    is_dt = isinstance(dst, DenseTensor)
+    arr = _array(dst)
+    d = idx.pit_dim
+    t_d = idx.micro_tile[0] if d == 0 else idx.micro_tile[1]
+    n_slots = tile_buffer.shape[d] // t_d
+    coords, _, _, _ = _gather_checks(arr.shape, idx, group, n_slots, start, True)
+    torch = _torch()
+    dev = _device.require_cuda()
+    host_dst = not _is_torch(arr)
+    x = _device.to_device(arr)
+    tile = _device.to_device(np.ascontiguousarray(tile_buffer)) if not _is_torch(tile_buffer) else tile_buffer
+    cd = torch.from_numpy(np.ascontiguousarray(coords, dtype=np.int32)).to(dev)
+    ld, col = _tensor_geometry(x)
+    lib = _lib.load()
+    _device.check(lib.pit_swrite(tile.data_ptr(), x.data_ptr(), _device.dtype_code(x), arr.shape[0], arr.shape[1], ld,
+                                 col, tile.shape[0], tile.shape[1], idx.micro_tile[0], idx.micro_tile[1], d, group,
+                                 cd.data_ptr(), coords.size, int(bool(accumulate)), _device.stream_ptr()), ExecError)
+    if host_dst:
+        arr[...] = _device.to_host(x, COL_MAJOR if arr.flags.f_contiguous and not arr.flags.c_contiguous else ROW_MAJOR)
+    elif is_dt:
+        pass
+    return int(coords.size)
+
+
+# ------------------------------------------------------------------------------ verification
+def run_dense_reference(a, b) -> np.ndarray:
+    """f64 oracle, reduction ascending, multiply then add — the scalar triple loop's exact
+    operation sequence (executor.py:267-283), computed on the GPU without FMA contraction."""
+    A = _array(a)
+    B = _array(b)
+    if len(A.shape) != 2 or len(B.shape) != 2 or A.shape[1] != B.shape[0]:
+        raise ExecError(f"shape mismatch {tuple(A.shape)} @ {tuple(B.shape)}")
+    torch = _torch()
+    dev = _device.require_cuda()
+    Ad = _device.to_device(np.asarray(A, dtype=np.float64) if not _is_torch(A) else A).to(torch.float64)
+    Bd = _device.to_device(np.asarray(B, dtype=np.float64) if not _is_torch(B) else B).to(torch.float64).contiguous()
+    m, k = Ad.shape
+    n = Bd.shape[1]
+    Cd = torch.empty((m, n), dtype=torch.float64, device=dev)
+    if m and n:
+        lib = _lib.load()
+        s0, s1 = Ad.stride()
+        _device.check(lib.pit_dense_reference_f64(Ad.data_ptr(), s0, s1, Bd.data_ptr(), Bd.stride(0), Cd.data_ptr(),
+                                                  m, n, k, _device.stream_ptr()), ExecError)
+    return _device.to_host(Cd)
+
+
+def max_rel_error(result, oracle, floor: float = 1e-6) -> float:
+    """Normwise relative error: peak |x - y| over peak |y| (floored), executor.py:294-300."""
+    x = _host64(result)
+    y = _host64(oracle)
+    if not y.size:
+        return 0.0
+    return float(np.max(np.abs(x - y))) / max(float(np.max(np.abs(y))), floor)
+
+
+def verify_close(result, oracle, rtol: float = 1e-5, atol: float = 1e-6) -> bool:
+    x = _host64(result)
+    y = _host64(oracle)
+    if not y.size:
+        return True
+    return bool(np.max(np.abs(x - y)) <= atol + rtol * float(np.max(np.abs(y))))
+
+
+def _host64(x) -> np.ndarray:
+    if isinstance(x, DenseTensor):
+        x = x.numpy()
+    elif _is_torch(x):
+        x = _device.to_host(x)
+    return np.asarray(x, dtype=np.float64)
+
+
+# ---------------------------------------------------------------------------------- matmul
+def _check_matmul_operands(plan: SparseKernelPlan, A: DenseTensor, B: DenseTensor) -> None:
+    if len(A.shape) != 2 or len(B.shape) != 2 or A.shape[1] != B.shape[0]:
+        raise ExecError(f"shape mismatch {A.shape} @ {B.shape}")
+    if A.dtype != B.dtype:
+        raise ExecError(f"mixed dtypes {A.dtype} and {B.dtype}")
+    ext = plan.extents
+    if (ext["m"], ext["k"]) != A.shape or ext["n"] != B.shape[1]:
+        raise ExecError(f"plan bound to {dict(ext)} but got A{A.shape} B{B.shape}")
+    if not plan.is_dense and A.layout != plan.sparse_layout:
+        # a degenerate extent is both layouts at once
+        if not (A.shape[0] == 1 or A.shape[1] == 1):
+            raise LayoutError(
+                f"plan requires the sparse operand in {plan.sparse_layout}, got {A.layout}; use convert_layout first"
+            )
+
+
+_PLAN_CODE = {"dense": _lib.PIT_PLAN_DENSE, "m": _lib.PIT_PLAN_PIT_M, "k": _lib.PIT_PLAN_PIT_K}
+
+
+def spmm_device(plan: SparseKernelPlan, Ad, Bd, idx: Optional[MicroTileIndex], out=None, force_simt: bool = False):
+    """Launch the fused SpMM on device tensors (no validation beyond the C ABI's); returns C."""
+    torch = _torch()
+    dev = _device.require_cuda()
+    M, K = int(Ad.shape[0]), int(Ad.shape[1])
+    N = int(Bd.shape[1])
+    if _torch_layout(Bd) != ROW_MAJOR or (Bd.stride(0) * Bd.element_size()) % 16:
+        Bd = Bd.contiguous()
+    C_ = out if out is not None else torch.empty((M, N), dtype=Ad.dtype, device=dev)
+    a = _lib.SpmmArgs()
+    a.plan = _PLAN_CODE["dense" if plan.is_dense else plan.pit_axis]
+    a.dtype = _device.dtype_code(Ad)
+    a.M, a.N, a.K = M, N, K
+    a.A = Ad.data_ptr()
+    a.sam, a.sak = Ad.stride()
+    if M == 1:
+        a.sam = 1 if plan.pit_axis == "k" else a.sam
+    if K == 1:
+        a.sak = 1 if plan.pit_axis != "k" else a.sak
+    a.B = Bd.data_ptr()
+    a.ldb = Bd.stride(0) if N > 1 or K > 1 else N
+    a.C = C_.data_ptr()
+    a.ldc = C_.stride(0)
+    keep = []
+    if not plan.is_dense:
+        t0, t1 = idx.micro_tile
+        a.t0, a.t1 = t0, t1
+        a.n_groups = idx.n_groups
+        a.slot_stride = idx.pit_grid
+        if plan.pit_axis == "k":
+            counts, slots = idx.device_arrays()
+            keep += [counts, slots]
+            a.counts, a.slots = counts.data_ptr(), slots.data_ptr()
+        else:
+            occ = idx.occupancy_words()
+            rows, n_rows = idx.union_coords()
+            keep += [occ, rows, n_rows]
+            a.occ = occ.data_ptr()
+            a.words_per_group = occ.shape[1]
+            a.rows, a.n_rows = rows.data_ptr(), n_rows.data_ptr()
+            a.n_rows_bound = M
+    a.force_simt = int(force_simt)
+    lib = _lib.load()
+    _device.check(lib.pit_spmm(C.byref(a), _device.stream_ptr()), ExecError)
+    return C_
+
+
+def run_matmul_with_index(
+    plan: SparseKernelPlan,
+    A: DenseTensor,
+    B: DenseTensor,
+    idx: Optional[MicroTileIndex],
+    workers: int = 1,
+    stats: Optional[ExecStats] = None,
+) -> DenseTensor:
+    """Run a matmul plan against a prebuilt index (ignored for the dense plan)."""
+    _check_matmul_operands(plan, A, B)
+    if plan.op_kind != "matmul":
+        raise ExecError(f"not a matmul plan: {plan.op_kind}")
+    if not plan.is_dense:
+        if idx is None:
+            raise ExecError("sparse plan needs a micro-tile index")
+        if idx.pit_axis != plan.pit_axis or tuple(idx.micro_tile) != tuple(plan.micro_tile):
+            raise ExecError(
+                f"index ({idx.pit_axis}, {idx.micro_tile}) does not match plan ({plan.pit_axis}, {plan.micro_tile})"
+            )
+        if plan.pit_axis not in ("m", "k"):
+            raise ExecError(f"matmul axis {plan.pit_axis!r} is not executable (m and k only)")
+        dim = PIT_DIMS[plan.pit_axis]
+        t = plan.micro_tile
+        want_groups = -(-A.shape[1 - dim] // t[1 - dim])
+        if idx.n_groups != want_groups:
+            raise ExecError(f"index has {idx.n_groups} groups, operand needs {want_groups}")
+    host = not A.is_device
+    Ad = _device.to_device(A.array)
+    Bd = _device.to_device(B.array)
+    Cd = spmm_device(plan, Ad, Bd, idx)
+    if stats is not None:
+        if plan.is_dense:
+            stats.launches += dense_launches(plan)
+        else:
+            stats.launches += launches_from_counts(plan, idx.counts)
+            stats.gathered_micro_tiles += idx.total
+    return DenseTensor(_device.to_host(Cd) if host else Cd)
+
+
+def run_sparse_matmul(
+    plan: SparseKernelPlan,
+    A: DenseTensor,
+    B: DenseTensor,
+    ann: Optional[SparsityAnnotation],
+    workers: int = 1,
+    stats: Optional[ExecStats] = None,
+) -> DenseTensor:
+    """Detect, index and execute in one call (executor.py:519-537)."""
+    _check_matmul_operands(plan, A, B)
+    idx = None
+    if not plan.is_dense:
+        if ann is None:
+            raise ExecError("sparse plan needs a sparsity annotation")
+        if tuple(ann.tensor_shape) != A.shape:
+            raise ExecError(f"annotation {ann.tensor_shape} does not describe A {A.shape}")
+        idx = build_index(ann, plan.micro_tile, plan.pit_axis, workers=workers)
+    return run_matmul_with_index(plan, A, B, idx, workers=workers, stats=stats)

@@ -1,0 +1,176 @@
+"""K1 detection / index construction on the GPU vs the CPU oracle: bit-exact.
+
+"Bit-exact" = equal counts and equal groups. The GPU compaction is
+ordered, so groups are compared without canonicalization against the reference's workers=1
+order (ascending).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import pit_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def _pkg():
+    import paper_2301_10936_b200 as pit
+
+    return pit
+
+
+def assert_same_index(idx, counts, groups):
+    np.testing.assert_array_equal(idx.counts, counts)
+    for g in range(idx.n_groups):
+        np.testing.assert_array_equal(idx.group(g), groups[g], err_msg=f"group {g}")
+
+
+CASES = [
+    # shape, granularity, micro, axis, zero ratio
+    ((64, 64), (1, 1), (1, 8), "m", 0.7),
+    ((64, 64), (1, 1), (8, 1), "k", 0.7),
+    ((45, 70), (3, 2), (1, 32), "m", 0.6),
+    ((45, 70), (3, 2), (16, 1), "k", 0.6),
+    ((1024, 1024), (32, 1), (32, 1), "k", 0.9),
+    ((1024, 1024), (1, 32), (1, 32), "m", 0.9),
+    ((1000, 777), (2, 3), (5, 7), "m", 0.95),
+    ((1000, 777), (2, 3), (5, 7), "k", 0.3),
+    ((1, 1), (1, 1), (1, 1), "m", 0.4),
+    ((200, 1), (1, 1), (16, 1), "k", 0.4),
+    ((1, 200), (1, 1), (1, 32), "m", 0.4),
+    ((4096, 4096), (2, 1), (16, 1), "k", 0.95),
+    ((4096, 4096), (1, 64), (1, 64), "m", 0.99),
+]
+
+
+@pytest.mark.parametrize("shape,gran,micro,axis,ratio", CASES)
+def test_build_index_annotation_matches_oracle(shape, gran, micro, axis, ratio):
+    pit = _pkg()
+    ann = pit.random_annotation(shape, gran, ratio, seed=shape[0] * 7 + shape[1])
+    idx = pit.build_index(ann, micro, axis)
+    counts, groups = orc.build_index(ann.tensor_shape, ann.granularity, ann.packed, micro, axis)
+    assert_same_index(idx, counts, groups)
+
+
+def test_build_index_sweep_matches_oracle():
+    pit = _pkg()
+    rng = np.random.default_rng(4)
+    for trial in range(120):
+        shape = (int(rng.integers(1, 300)), int(rng.integers(1, 300)))
+        gran = (int(rng.integers(1, 6)), int(rng.integers(1, 6)))
+        micro = (int(rng.integers(1, 40)), int(rng.integers(1, 40)))
+        axis = "m" if rng.integers(2) else "k"
+        ann = pit.random_annotation(shape, gran, float(rng.choice([0.0, 0.3, 0.7, 0.95, 1.0])), seed=trial)
+        idx = pit.build_index(ann, micro, axis)
+        counts, groups = orc.build_index(ann.tensor_shape, ann.granularity, ann.packed, micro, axis)
+        assert_same_index(idx, counts, groups)
+
+
+DTYPES = ["float32", "float64", "bfloat16", "float16", "uint8", "bool"]
+
+
+def _values(shape, density, rng):
+    v = rng.standard_normal(shape).astype(np.float32)
+    v[rng.random(shape) >= density] = 0.0
+    return v
+
+
+def _torch_values(v, dtype, col_major):
+    import torch
+
+    t = torch.from_numpy(v)
+    if dtype == "bool":
+        t = t != 0
+    elif dtype == "uint8":
+        t = (t != 0).to(torch.uint8) * 3
+    else:
+        t = t.to(getattr(torch, dtype))
+    t = t.cuda()
+    if col_major:
+        t = t.t().contiguous().t()
+    return t
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("col_major", [False, True])
+@pytest.mark.parametrize(
+    "shape,micro,axis",
+    [((256, 512), (1, 32), "m"), ((256, 512), (32, 1), "k"), ((300, 200), (3, 5), "m"), ((300, 200), (7, 2), "k"),
+     ((512, 1024), (1, 64), "m"), ((1024, 512), (64, 1), "k"), ((64, 96), (1, 1), "m")],
+)
+def test_build_index_from_tensor_matches_oracle(dtype, col_major, shape, micro, axis):
+    pit = _pkg()
+    rng = np.random.default_rng(hash((dtype, col_major, shape, micro)) % 2**32)
+    v = _values(shape, 0.02, rng)
+    t = _torch_values(v, dtype, col_major)
+    idx = pit.build_index_from_tensor(t, micro, axis)
+    counts, groups = orc.build_index_from_values(v, micro, axis)
+    assert_same_index(idx, counts, groups)
+
+
+def test_value_test_is_exact_no_epsilon():
+    """-0.0 is zero; NaN, inf and denormals are live."""
+    import torch
+
+    pit = _pkg()
+    v = np.zeros((8, 64), np.float32)
+    v[1, 3] = -0.0
+    v[2, 40] = np.float32(1e-45)  # denormal
+    v[4, 10] = np.nan
+    v[6, 63] = -np.inf
+    idx = pit.build_index_from_tensor(torch.from_numpy(v).cuda(), (1, 32), "m")
+    assert [list(idx.group(g)) for g in range(2)] == [[4], [2, 6]]
+    v64 = np.zeros((4, 4))
+    v64[0, 0] = 1e-300
+    v64[3, 3] = -0.0
+    assert pit.build_index_from_tensor(v64, (1, 1), "m").total == 1
+
+
+def test_host_arrays_are_uploaded():
+    pit = _pkg()
+    v = np.zeros((8, 8), np.float32)
+    v[5, 3] = 2.5
+    idx = pit.build_index_from_tensor(v, (1, 4), "m")
+    assert idx.total == 1
+    assert [set(map(int, idx.group(g))) for g in range(idx.n_groups)] == [{5}, set()]
+
+
+def test_large_bf16_detection_bit_exact():
+    """Full-size property: every group ascending, no duplicates, total equals the oracle's cover."""
+    import torch
+
+    pit = _pkg()
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn((8192, 8192), device="cuda", dtype=torch.bfloat16, generator=g)
+    keep = torch.rand((8192, 8192 // 32), device="cuda", generator=g) >= 0.9
+    x = x * keep.repeat_interleave(32, dim=1).to(x.dtype)
+    idx = pit.build_index_from_tensor(x, (1, 32), "m")
+    want = keep.t().sum(dim=1).cpu().numpy()  # per K-block group: live rows
+    np.testing.assert_array_equal(idx.counts, want)
+    for gi in (0, 17, idx.n_groups - 1):
+        np.testing.assert_array_equal(idx.group(gi), np.nonzero(keep[:, gi].cpu().numpy())[0])
+
+
+def test_errors_match_reference_messages():
+    pit = _pkg()
+    ann = pit.from_mask(np.ones((4, 4)), (1, 1))
+    with pytest.raises(pit.IndexBuildError, match="positive"):
+        pit.build_index(ann, (0, 2), "m")
+    with pytest.raises(pit.IndexBuildError, match="rank"):
+        pit.build_index(ann, (1, 2, 3), "m")
+    with pytest.raises(pit.IndexBuildError, match="workers"):
+        pit.build_index(ann, (1, 2), "m", workers=0)
+    with pytest.raises(pit.IndexBuildError, match="axis"):
+        pit.build_index(ann, (1, 2), "q")
+
+
+def test_device_from_mask_matches_host():
+    import torch
+
+    pit = _pkg()
+    rng = np.random.default_rng(3)
+    m = (rng.random((130, 70)) > 0.97).astype(np.float32)
+    for gran in ((1, 1), (2, 3), (32, 1), (1, 64), (7, 7)):
+        dev = pit.from_mask(torch.from_numpy(m).cuda(), gran)
+        host = pit.from_mask(m, gran)
+        np.testing.assert_array_equal(dev.packed, host.packed)
