@@ -1,0 +1,430 @@
+#!/usr/bin/env python
+"""PIT hot-path benchmark on B200 (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload NAME]
+
+A step is one pass of the PIT hot path over one synthetic batch: online detection of the
+sparse operand's live micro-tiles from its values (K1, ``build_index_from_tensor``) followed by
+the PIT sparse matmul against that index (``run_matmul_with_index``). The headline workload is
+BASELINE config C1's distribution — random 32x1 micro-tiles, 90% zero, PIT axis k — at the
+roofline scale SURVEY.md section 8(d) names (8192^3, bf16; C1's 1024^3 fp32 is the parity and
+CPU-comparison size and is covered by the tests).
+
+metric  = effective TFLOP/s: 2 * N * (A elements inside live micro-tiles) per step / step time
+value   = device-resident inputs, CUDA events on the launching stream, L2 flushed between steps
+e2e     = same metric through the public API with host (pinned) buffers, H2D + D2H inside the timing
+roofline= the dominant kernel (spmm_gk) vs the measured bf16 peak (MEASURED_PEAKS.json)
+--impl reference = the reference algorithm's CPU restatement (oracle/, the reference itself is
+          pure Python and cannot travel) on the host cores, bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import os
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")  # the reference is fastest single-threaded
+
+import argparse
+import json
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    # name: geometry of the sparse matmul C[M,N] = A[M,K] @ B[K,N]
+    "pitk_c1_8192": dict(M=8192, K=8192, N=8192, micro=(32, 1), axis="k", zero=0.90, tile=(32, 64, 32),
+                         desc="pit:k SpMM, C1 distribution (random 32x1 micro-tiles, 90% zero) at 8192^3 bf16; "
+                              "online detection from values + SpMM"),
+    "pitk_128_8192": dict(M=8192, K=8192, N=8192, micro=(128, 1), axis="k", zero=0.90, tile=(128, 64, 256),
+                          desc="pit:k SpMM, B200-native 128x1 micro-tiles, 90% zero, 8192^3 bf16"),
+    "pitm_32_8192": dict(M=8192, K=8192, N=8192, micro=(1, 32), axis="m", zero=0.90, tile=(16, 32, 128),
+                         desc="pit:m SpMM, random 1x32 micro-tiles, 90% zero, 8192^3 bf16"),
+    "bert_ffn1": dict(M=4096, K=768, N=3072, micro=(1, 768), axis="m", zero=None, tile=(128, 768, 256),
+                      desc="BERT-base FFN1 varlen (batch 32 x 128, lengths U[16,128]), padding removed via pit:m"),
+}
+DEFAULT_WORKLOAD = "pitk_c1_8192"
+FLUSH_BYTES = 256 << 20
+
+
+# ----------------------------------------------------------------------------------- helpers
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return dict(hbm=float(d["hbm_gbs"]), bf16=float(d["bf16_tflops"]),
+                    bf16_sustained=float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), source="measured")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sustained=1400.0, source="fallback")
+
+
+def load_traffic():
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except ValueError:
+            return {}
+    return {}
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons through NVML while the timed region runs."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover - NVML missing
+            self._nv = None
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM))
+                mask = self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._nv is not None:
+            self._t.join(timeout=1)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ------------------------------------------------------------------------- synthetic inputs
+def make_operands(w: dict, seed: int, device):
+    """Synthetic A (sparse, masked at micro-tile granularity), B dense; bf16 on `device`."""
+    import torch
+
+    g = torch.Generator(device=device).manual_seed(seed)
+    M, K, N = w["M"], w["K"], w["N"]
+    t0, t1 = w["micro"]
+    if w["name"].startswith("bert"):
+        rng = np.random.default_rng(seed)
+        lengths = rng.integers(16, 129, size=M // 128)
+        rows = torch.from_numpy(np.concatenate([np.arange(128) < L for L in lengths])).to(device)
+        A = torch.randn((M, K), device=device, dtype=torch.bfloat16, generator=g) * rows[:, None].to(torch.bfloat16)
+        live_elems = int(rows.sum().item()) * K
+    elif w["axis"] == "k":
+        # A column-major: build A^T [K, M] row-major; micro-tile (t0, 1) = t0 consecutive m of one k
+        keep = torch.rand((K, -(-M // t0)), device=device, generator=g) >= w["zero"]
+        At = torch.randn((K, M), device=device, dtype=torch.bfloat16, generator=g)
+        At.mul_(keep.repeat_interleave(t0, dim=1)[:, :M].to(torch.bfloat16))
+        A = At.t()
+        live_elems = int(keep.sum().item()) * t0
+    else:
+        keep = torch.rand((M, -(-K // t1)), device=device, generator=g) >= w["zero"]
+        A = torch.randn((M, K), device=device, dtype=torch.bfloat16, generator=g)
+        A.mul_(keep.repeat_interleave(t1, dim=1)[:, :K].to(torch.bfloat16))
+        live_elems = int(keep.sum().item()) * t1
+    B = torch.randn((K, N), device=device, dtype=torch.bfloat16, generator=g)
+    return A, B, live_elems
+
+
+def make_plan(w: dict):
+    import paper_2301_10936_b200 as pit
+
+    reg = pit.register_builtin_kernels()
+    if reg.get("matmul", w["tile"]) is None:
+        reg.register(pit.TileKernelDescriptor("matmul", tuple(w["tile"]), "bench"))
+    expr = pit.bind_extents(pit.parse_expr("C[m,n] += A[m,k] * B[k,n]"), dict(m=w["M"], k=w["K"], n=w["N"]))
+    plan = pit.forced_plan(expr, w["axis"], reg, tile_shape=w["tile"])
+    assert tuple(plan.micro_tile) == tuple(w["micro"]), (plan.micro_tile, w["micro"])
+    return plan
+
+
+# --------------------------------------------------------------------------- our arm (GPU)
+def run_ours(args, w):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2301_10936_b200 as pit
+    from paper_2301_10936_b200 import _lib
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    _lib.load()
+
+    A, B, live = make_operands(w, seed=1234 + rank, device=dev)
+    eff_flops = 2.0 * w["N"] * live
+    plan = make_plan(w)
+    micro, axis = w["micro"], w["axis"]
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        idx = pit.build_index_from_tensor(A, micro, axis)
+        mark = torch.cuda.Event(enable_timing=True)
+        mark.record(stream)
+        C = pit.run_matmul_with_index(plan, pit.DenseTensor(A), pit.DenseTensor(B), idx)
+        return C, idx, mark
+
+    # correctness spot check of the benchmarked configuration (cheap, outside timing)
+    C0, idx0, _ = step()
+    assert idx0.total * micro[0] * micro[1] >= live or w["name"].startswith("bert")
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    launches0 = _lib.kernel_launches()
+    step_ms, spmm_ms, det_ms = [], [], []
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e2 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            _, _, e1 = step()
+            e2.record(stream)
+            step_ms.append((e0, e1, e2))
+        torch.cuda.synchronize()
+    launches = _lib.kernel_launches() - launches0
+    for e0, e1, e2 in step_ms:
+        det_ms.append(e0.elapsed_time(e1))
+        spmm_ms.append(e1.elapsed_time(e2))
+    total_ms = sum(d + s for d, s in zip(det_ms, spmm_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    ms_per_step = total_ms / args.steps
+    value = world * eff_flops * args.steps / (total_ms * 1e-3) / 1e12
+
+    peaks = load_peaks()
+    spmm_avg = statistics.mean(spmm_ms)
+    det_avg = statistics.mean(det_ms)
+    achieved = eff_flops / (spmm_avg * 1e-3) / 1e12
+    scanned = A.numel() * A.element_size()
+    traffic = load_traffic().get(w["name"], {}).get("spmm_dram_bytes")
+    roofline = {
+        "bound": "tensor", "kernel": "spmm_gk" if axis == "k" else "spmm_gm",
+        "achieved": round(achieved, 2), "peak": peaks["bf16"], "unit": "TFLOP/s",
+        "frac": round(achieved / peaks["bf16"], 4), "peak_source": peaks["source"] + " burst bf16",
+        "traffic": traffic, "algorithmic_flops": eff_flops,
+        "kernel_ms": round(spmm_avg, 4),
+    }
+    detection = {
+        "kernel": "detect+compact", "ms": round(det_avg, 4), "bytes_scanned": scanned,
+        "achieved_GBps": round(scanned / (det_avg * 1e-3) / 1e9, 1), "peak_GBps": peaks["hbm"],
+        "frac": round(scanned / (det_avg * 1e-3) / 1e9 / peaks["hbm"], 4),
+    }
+
+    result = {
+        "metric": "PIT sparse matmul effective TFLOP/s (online detection + SpMM)",
+        "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": w["desc"], "name": w["name"], "M": w["M"], "K": w["K"], "N": w["N"],
+                   "micro_tile": list(micro), "pit_axis": axis, "zero_ratio": w["zero"],
+                   "plan_tile": list(w["tile"]), "parallelism": f"replica x{world} (per-GPU work fixed)",
+                   "l2": "flushed (256 MiB write) before every step; inputs also exceed L2"},
+        "roofline": roofline, "detection": detection,
+        "clocks": clocks.summary(), "gpu_launches": int(launches),
+    }
+
+    # ---- end to end through the public API with host buffers
+    if rank == 0 and not args.no_e2e:
+        result["e2e"] = e2e_ours(args, w, A, B, plan, eff_flops)
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        result["cpu_baseline"] = cpu_reference(w, target_s=args.cpu_seconds, procs=1)
+    if world > 1:
+        dist.destroy_process_group()
+    return result if rank == 0 else None
+
+
+def e2e_ours(args, w, A, B, plan, eff_flops):
+    """Host pinned A, B -> H2D -> detection -> SpMM -> D2H of C, all inside the timed region."""
+    import torch
+
+    import paper_2301_10936_b200 as pit
+
+    Ah = torch.empty(A.t().shape, dtype=A.dtype, pin_memory=True) if w["axis"] == "k" else \
+        torch.empty(A.shape, dtype=A.dtype, pin_memory=True)
+    Ah.copy_(A.t() if w["axis"] == "k" else A)
+    Bh = torch.empty(B.shape, dtype=B.dtype, pin_memory=True)
+    Bh.copy_(B)
+    Ch = torch.empty((w["M"], w["N"]), dtype=A.dtype, pin_memory=True)
+    stream = torch.cuda.current_stream()
+
+    def once():
+        Ad = Ah.to("cuda", non_blocking=True)
+        Ad = Ad.t() if w["axis"] == "k" else Ad
+        Bd = Bh.to("cuda", non_blocking=True)
+        idx = pit.build_index_from_tensor(Ad, w["micro"], w["axis"])
+        C = pit.run_matmul_with_index(plan, pit.DenseTensor(Ad), pit.DenseTensor(Bd), idx)
+        Ch.copy_(C.array, non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        once()
+    torch.cuda.synchronize()
+    n = max(3, min(args.steps, 10))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(n):
+        once()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / n
+    return {"value": round(eff_flops / (ms * 1e-3) / 1e12, 3), "unit": "TFLOP/s", "ms_per_step": round(ms, 3),
+            "h2d_bytes_per_step": Ah.numel() * 2 + Bh.numel() * 2, "d2h_bytes_per_step": Ch.numel() * 2,
+            "api": "build_index_from_tensor + run_matmul_with_index on pinned host buffers"}
+
+
+# ------------------------------------------------------------------ reference CPU restatement
+_CPU = {}
+
+
+def _cpu_worker(groups):
+    from oracle import pit_oracle as orc
+
+    w = _CPU["w"]
+    t0 = w["micro"][0]
+    flops = 0.0
+    for g in groups:
+        A = _CPU["A"][g]                     # [t0, K] rows of one M-block (fp32)
+        ann = _CPU["ann"][g]                 # annotation restricted to the group's rows
+        counts, groups_k = orc.build_index(*ann, w["micro"], w["axis"])
+        orc.matmul_pit_k(A, _CPU["B"], groups_k, w["micro"], w["tile"])
+        flops += 2.0 * w["N"] * t0 * int(counts.sum())
+    return flops
+
+
+def _cpu_setup(w, n_groups, seed=7):
+    """Host operands for a bounded sample of M-block groups of the same workload (fp32: the
+    reference has no bf16, executor.py:40-41)."""
+    from oracle import pit_oracle as orc
+
+    rng = np.random.default_rng(seed)
+    t0 = w["micro"][0]
+    K, N = w["K"], w["N"]
+    _CPU["w"] = w
+    _CPU["B"] = rng.standard_normal((K, N), dtype=np.float32)
+    _CPU["A"], _CPU["ann"] = [], []
+    for g in range(n_groups):
+        ann = orc.random_ann((t0, K), w["micro"], w["zero"], seed=seed + g)
+        _CPU["A"].append(rng.standard_normal((t0, K), dtype=np.float32) * orc.materialize(*ann))
+        _CPU["ann"].append(ann)
+
+
+def cpu_reference(w, target_s=8.0, procs=None):
+    """Time the reference algorithm (oracle port: detection + gather/tile-dot/scatter) on a bounded
+    sample of the workload; returns the cpu_baseline object."""
+    if w["axis"] != "k":
+        return {"value": None, "unit": "TFLOP/s", "note": "CPU sampler implemented for pit:k workloads"}
+    import multiprocessing as mp
+
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    procs = cores if procs is None else procs
+    _cpu_setup(w, 1)
+    t = time.perf_counter()
+    _cpu_worker([0])
+    per_group = time.perf_counter() - t
+    n = int(max(procs, min(4096, target_s * procs / max(per_group, 1e-3))))
+    n = min(n, w["M"] // w["micro"][0])
+    _cpu_setup(w, n)
+    chunks = [list(range(i, n, procs)) for i in range(procs)]
+    t = time.perf_counter()
+    if procs == 1:
+        flops = _cpu_worker(chunks[0])
+    else:
+        with mp.get_context("fork").Pool(procs) as pool:
+            t = time.perf_counter()
+            flops = sum(pool.map(_cpu_worker, chunks))
+    secs = time.perf_counter() - t
+    return {"value": round(flops / secs / 1e12, 6), "unit": "TFLOP/s", "cores": procs, "kind": "port",
+            "seconds": round(secs, 2),
+            "sample": f"{n} of {w['M'] // w['micro'][0]} M-block groups (all K, all N) of {w['name']}, fp32, "
+                      f"detection + tile loop (oracle/pit_oracle.py), OPENBLAS_NUM_THREADS=1"}
+
+
+def run_reference(args, w):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return None
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    vals = []
+    base = None
+    for i in range(args.warmup + args.steps):
+        r = cpu_reference(w, target_s=args.ref_seconds, procs=cores)
+        if i >= args.warmup:
+            vals.append(r["value"])
+            base = r
+    value = statistics.mean(vals)
+    return {
+        "impl": "reference", "metric": "PIT sparse matmul effective TFLOP/s (online detection + SpMM)",
+        "value": round(value, 6), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": w["desc"], "name": w["name"]},
+        "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": base["cores"], "kind": "port",
+                         "sample": base["sample"]},
+        "e2e": {"value": round(value, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default=DEFAULT_WORKLOAD)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--ref-seconds", type=float, default=4.0)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3  # timing rule: at least 3 warm-up steps
+    w = dict(WORKLOADS[args.workload], name=args.workload)
+    res = run_reference(args, w) if args.impl == "reference" else run_ours(args, w)
+    if res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

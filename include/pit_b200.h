@@ -50,6 +50,9 @@ PIT_API const char* pit_last_error(void);
 /* ABI version (major*100 + minor). */
 PIT_API int pit_abi_version(void);
 
+/* Number of kernels this library has launched in the process (monotonic; for launch accounting). */
+PIT_API long long pit_kernel_launches(void);
+
 /* Micro-grid geometry of a (s0 x s1) operand under micro-tile (t0,t1) and PIT dim. */
 PIT_API int pit_index_geometry(int64_t s0, int64_t s1, int t0, int t1, int pit_dim, int64_t* n_groups, int64_t* pit_grid,
                        int64_t* words_per_group);

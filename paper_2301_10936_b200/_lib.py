@@ -32,6 +32,7 @@ PIT_PLAN_DENSE, PIT_PLAN_PIT_M, PIT_PLAN_PIT_K = 0, 1, 2
 EXPORTS = (
     "pit_last_error",
     "pit_abi_version",
+    "pit_kernel_launches",
     "pit_index_geometry",
     "pit_build_index_from_tensor",
     "pit_build_index",
@@ -81,6 +82,8 @@ def _declare(lib) -> None:
     lib.pit_last_error.restype = C.c_char_p
     lib.pit_last_error.argtypes = []
     lib.pit_abi_version.restype = i32
+    lib.pit_kernel_launches.restype = C.c_longlong
+    lib.pit_kernel_launches.argtypes = []
     lib.pit_index_geometry.argtypes = [i64, i64, i32, i32, i32, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]
     lib.pit_build_index_from_tensor.argtypes = [vp, i32, i64, i64, i64, i64, i32, i32, i32, vp, vp, vp, vp]
     lib.pit_build_index.argtypes = [vp, i64, i64, i32, i32, i32, i32, i32, vp, vp, vp, vp]
@@ -92,7 +95,7 @@ def _declare(lib) -> None:
     lib.pit_spmm_uses_tensor_cores.argtypes = [C.POINTER(SpmmArgs)]
     lib.pit_dense_reference_f64.argtypes = [vp, i64, i64, vp, i64, vp, i64, i64, i64, vp]
     for name in EXPORTS:
-        if name not in ("pit_last_error", "pit_abi_version"):
+        if name not in ("pit_last_error", "pit_abi_version", "pit_kernel_launches"):
             getattr(lib, name).restype = i32
 
 
@@ -125,3 +128,8 @@ def load(build_if_missing: bool = True):
 
 def last_error() -> str:
     return load().pit_last_error().decode(errors="replace")
+
+
+def kernel_launches() -> int:
+    """Kernels launched by libpit_b200.so in this process so far."""
+    return int(load().pit_kernel_launches())

@@ -2,6 +2,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 
@@ -35,6 +36,10 @@ std::once_flag g_encode_once;
 
 bool dtype_ok(int dt) { return dt >= kDtypeF32 && dt <= kDtypeU8; }
 }  // namespace
+
+std::atomic<long long> g_launches{0};
+
+void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 int cuda_status() {
   const cudaError_t e = cudaGetLastError();
@@ -95,6 +100,8 @@ extern "C" {
 const char* pit_last_error(void) { return g_err.c_str(); }
 
 int pit_abi_version(void) { return 100; }
+
+long long pit_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int pit_index_geometry(int64_t s0, int64_t s1, int t0, int t1, int pit_dim, int64_t* n_groups, int64_t* pit_grid,
                        int64_t* words_per_group) {

@@ -300,6 +300,7 @@ int launch_detect_values(const DetectValuesArgs& a, cudaStream_t s) {
     detect_rows_vec_kernel<<<grid, kRaWarps * 32, 0, s>>>(static_cast<const uint8_t*>(a.x), a.R, row_bytes,
                                                           ld_bytes, a.tr, static_cast<int>(vec_per_micro), GR, GC,
                                                           live_mask_for(a.dtype), a.occ, WG);
+    note_launch();
   } else {
     const int TJ = a.pit_phys == 0 ? 256 : (a.tc >= 8 ? 32 : 128);
     dim3 grid(static_cast<unsigned>(ceil_div(GC, TJ)), static_cast<unsigned>(ceil_div(GR, 32)));
@@ -307,6 +308,7 @@ int launch_detect_values(const DetectValuesArgs& a, cudaStream_t s) {
     const size_t smem = sizeof(uint32_t) * (a.pit_phys == 0 ? TJ : TJ);
     detect_generic_kernel<<<grid, kGenThreads, smem, s>>>(static_cast<const uint8_t*>(a.x), a.dtype, eb, a.R, a.C,
                                                           a.ld, a.tr, a.tc, GR, GC, a.pit_phys, TJ, a.occ, WG);
+    note_launch();
   }
   return cuda_status();
 }
@@ -321,6 +323,7 @@ int launch_detect_bits(const DetectBitsArgs& a, cudaStream_t s) {
   const int threads = 256;
   detect_bits_kernel<<<static_cast<unsigned>(ceil_div(warps * 32, threads)), threads, 0, s>>>(
       a.packed, a.s0, a.s1, a.g0, a.g1, a.t0, a.t1, a.pit_dim, n_groups, pit_grid, WG, a.occ);
+  note_launch();
   return cuda_status();
 }
 
@@ -330,12 +333,14 @@ int launch_compact(const uint32_t* occ, int64_t n_groups, int64_t WG, int32_t* c
   const int threads = 256;
   compact_kernel<<<static_cast<unsigned>(ceil_div(n_groups * 32, threads)), threads, 0, s>>>(occ, n_groups, WG, counts,
                                                                                             slots, slot_stride);
+  note_launch();
   return cuda_status();
 }
 
 int launch_union(const uint32_t* occ, int64_t n_groups, int64_t WG, uint32_t* uni, cudaStream_t s) {
   if (WG == 0) return 0;
   union_kernel<<<static_cast<unsigned>(ceil_div(WG, 256)), 256, 0, s>>>(occ, n_groups, WG, uni);
+  note_launch();
   return cuda_status();
 }
 
@@ -346,6 +351,7 @@ int launch_slots_to_occ(const int32_t* counts, const int32_t* slots, int64_t slo
   dim3 grid(static_cast<unsigned>((ceil_div(pit_grid, 256) < 64 ? ceil_div(pit_grid, 256) : int64_t(64))), static_cast<unsigned>(n_groups));
   if (n_groups > 65535) return kErrShape;
   slots_to_occ_kernel<<<grid, 256, 0, s>>>(counts, slots, slot_stride, n_groups, WG, pit_grid, occ, bad);
+  note_launch();
   return cuda_status();
 }
 

@@ -45,6 +45,7 @@ inline int dtype_bytes(int dtype) {
 }
 
 int cuda_status();  // maps cudaGetLastError() to kOk / kErrCuda and records the message
+void note_launch(int n = 1);  // process-wide count of kernels this library launched
 
 // ------------------------------------------------------------------ K1 detect
 struct DetectValuesArgs {

@@ -261,6 +261,7 @@ int run_simt(const SpmmArgs& a, cudaStream_t s) {
   if (ytiles == 0 || xtiles == 0) return kOk;
   if (ytiles > 65535 || xtiles > (1ll << 31) - 1) return kErrShape;
   spmm_simt_kernel<T, Acc><<<dim3(static_cast<unsigned>(xtiles), static_cast<unsigned>(ytiles)), TPB, 0, s>>>(a);
+  note_launch();
   return cuda_status();
 }
 
@@ -285,6 +286,7 @@ int launch_dense_ref_f64(const double* A, int64_t s0, int64_t s1, const double* 
                          int64_t N, int64_t K, cudaStream_t s) {
   if (M * N == 0) return kOk;
   dense_ref_f64_kernel<<<static_cast<unsigned>(ceil_div(M * N, 256)), 256, 0, s>>>(A, s0, s1, B, ldb, C, M, N, K);
+  note_launch();
   return cuda_status();
 }
 
@@ -296,15 +298,19 @@ int launch_sread(const GatherArgs& a, cudaStream_t s) {
   switch (a.dtype) {
     case kDtypeF32:
       sread_kernel<float><<<grid, 256, 0, s>>>(a, zero_fill);
+      note_launch();
       break;
     case kDtypeF64:
       sread_kernel<double><<<grid, 256, 0, s>>>(a, zero_fill);
+      note_launch();
       break;
     case kDtypeBF16:
       sread_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(a, zero_fill);
+      note_launch();
       break;
     case kDtypeF16:
       sread_kernel<__half><<<grid, 256, 0, s>>>(a, zero_fill);
+      note_launch();
       break;
     default:
       return kErrUnsupported;
@@ -319,15 +325,19 @@ int launch_swrite(const GatherArgs& a, cudaStream_t s) {
   switch (a.dtype) {
     case kDtypeF32:
       swrite_kernel<float><<<grid, 256, 0, s>>>(a);
+      note_launch();
       break;
     case kDtypeF64:
       swrite_kernel<double><<<grid, 256, 0, s>>>(a);
+      note_launch();
       break;
     case kDtypeBF16:
       swrite_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(a);
+      note_launch();
       break;
     case kDtypeF16:
       swrite_kernel<__half><<<grid, 256, 0, s>>>(a);
+      note_launch();
       break;
     default:
       return kErrUnsupported;

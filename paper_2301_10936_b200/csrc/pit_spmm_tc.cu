@@ -33,8 +33,14 @@ namespace pit {
 
 namespace {
 
-constexpr int kThreads = 256;  // 8 warps
-constexpr int kEpiWarp0 = 4;
+// Warp roles: 0..3 TMA producers (gather issue is instruction-bound from a single thread, so four
+// warps split each stage's gathers), 4 MMA issuer, 5 TMEM allocator, 8..11 epilogue (one per TMEM
+// lane quarter).
+constexpr int kProdWarps = 4;
+constexpr int kMmaWarp = 4;
+constexpr int kAllocWarp = 5;
+constexpr int kEpiWarp0 = 8;
+constexpr int kThreads = 384;
 
 template <bool kBF16>
 struct OutT;
@@ -65,28 +71,43 @@ __host__ __device__ constexpr uint32_t tmem_cols_pow2() {
 
 // =============================================================================================
 // spmm_gk: PIT axis k.
+//
+// Orientation T (GW < 128, and GW == 256): D[n, m] += B^T[n, k] * A^T[k, m] — M_mma = 128 output
+//   columns per accumulator, N_mma = GW group rows; the n tile holds N_TILE/128 accumulators.
+// Orientation N (GW == 128): D[m, n] += A[m, k] * B[k, n] — M_mma = the group's 128 rows,
+//   N_mma = 256 output columns; one MMA per k16 (less shared-memory operand traffic per FLOP) and a
+//   row-contiguous epilogue.
+// Both operands are MN-major 128B-swizzled gathers of k rows; only descriptors and the epilogue
+// differ between orientations.
 // =============================================================================================
-template <int GW, int NACC>
+template <int GW, bool kOrientN>
 struct GkCfg {
-  static constexpr int KS = 64;                                   // gathered k per stage
-  static constexpr int A_ROW_BYTES = GW * 2 < 128 ? GW * 2 : 128; // bytes per smem row of A^T strip
+  static constexpr int KS = 64;  // gathered k per stage
+  static constexpr int N_TILE = (kOrientN || GW < 256) ? 256 : 128;
+  static constexpr int B_ATOMS = N_TILE / 64;
+  static constexpr int A_ROW_BYTES = GW * 2 < 128 ? GW * 2 : 128;  // bytes per smem row of the A^T strip
   static constexpr int A_ATOMS = GW * 2 <= 128 ? 1 : GW * 2 / 128;
-  static constexpr int B_BYTES = NACC * 2 * KS * 128;             // NACC halves x 2 atoms x KS rows
+  static constexpr int B_BYTES = B_ATOMS * KS * 128;
   static constexpr int A_BYTES = A_ATOMS * KS * A_ROW_BYTES;
   static constexpr int STAGE_BYTES = ((B_BYTES + A_BYTES + 1023) / 1024) * 1024;
-  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
-  static constexpr int TMEM_COLS = tmem_cols_pow2<2 * NACC * GW>();
-  static constexpr int N_TILE = 128 * NACC;
+  static constexpr int STAGES = (216 * 1024) / STAGE_BYTES > 8 ? 8 : (216 * 1024) / STAGE_BYTES;
+  static constexpr int ACC_COLS = kOrientN ? N_TILE : (N_TILE / 128) * GW;  // TMEM columns per buffer
+  static constexpr int TMEM_COLS = tmem_cols_pow2<2 * ACC_COLS>();
   static constexpr size_t SMEM = static_cast<size_t>(STAGES) * STAGE_BYTES + 1024 + 256;
   static constexpr uint32_t A_SW = sw_layout_for_row(A_ROW_BYTES);
+  static constexpr uint32_t A_MASK = A_ROW_BYTES == 128 ? 7 : A_ROW_BYTES == 64 ? 3 : A_ROW_BYTES == 32 ? 1 : 0;
+  static constexpr int B_CPR = N_TILE / 8;       // 16-byte chunks per gathered B row
+  static constexpr int A_CPR = GW * 2 / 16;      // 16-byte chunks per gathered A^T row
+  static constexpr int A_CPA = A_ROW_BYTES / 16; // chunks per atom row
+  static constexpr int A_RPW = 32 / A_CPR;       // A rows covered by one warp instruction
 };
 
-template <int GW, int NACC, bool kBF16>
+template <int GW, bool kOrientN, bool kBF16>
 __global__ void __launch_bounds__(kThreads, 1)
-    spmm_gk_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmAt,
+    spmm_gk_kernel(const void* __restrict__ Bv, int64_t ldb, const void* __restrict__ Atv, int64_t lda,
                    const int32_t* __restrict__ counts, const int32_t* __restrict__ slots, int64_t slot_stride,
                    int n_groups, int n_tiles, int M, int N, int K, void* __restrict__ Cv, int64_t ldc) {
-  using Cfg = GkCfg<GW, NACC>;
+  using Cfg = GkCfg<GW, kOrientN>;
   using OT = OutT<kBF16>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -101,7 +122,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < Cfg::STAGES; ++i) {
-      mbar_init(&full_bar[i], 1);
+      mbar_init(&full_bar[i], kProdWarps * 32);
       mbar_init(&empty_bar[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -109,89 +130,154 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tempty_bar[i], 128);
     }
     fence_mbar_init();
-    tma_prefetch_desc(&tmB);
-    tma_prefetch_desc(&tmAt);
   }
-  if (warp == 2) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  if (warp == kAllocWarp) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  // Units are (n tile, group) pairs, n-tile major: the CTAs running concurrently share one
+  // [K, N_TILE] slab of B, which stays L2-resident while every group gathers from it.
   const int units = n_groups * n_tiles;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+  if (warp < kProdWarps) {
+    // ------------------------------------------------------------ cp.async producers
+    // Stage = KS gathered k rows. The 128 producer threads copy 16-byte chunks: a warp instruction
+    // moves one 512-byte B row segment (coalesced), the A^T strip rows are split across lanes.
+    // Shared-memory addresses are swizzled in software to the UMMA SWIZZLE_{32,64,128}B layouts.
+    // Rows past the live count are zero-filled (src size 0). Slot indices for the next stage are
+    // loaded while the current stage is issued.
+    const int tp = threadIdx.x;  // 0..127
     int stage = 0;
     uint32_t phase = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int g = u / n_tiles;
-      const int n0 = (u % n_tiles) * Cfg::N_TILE;
+    int u = blockIdx.x;
+    int cnt = u < units ? __ldg(counts + u % n_groups) : 0;
+    while (u < units && cnt == 0) {
+      u += gridDim.x;
+      cnt = u < units ? __ldg(counts + u % n_groups) : 0;
+    }
+    int kb = 0;
+    int c0 = 0, c1 = 0;
+    if (u < units) {
+      const int32_t* gs = slots + static_cast<int64_t>(u % n_groups) * slot_stride;
+      c0 = lane < cnt ? __ldg(gs + lane) : 0;
+      c1 = 32 + lane < cnt ? __ldg(gs + 32 + lane) : 0;
+    }
+    using T = typename OT::T;
+    const T* Bp = static_cast<const T*>(Bv);
+    const T* Ap = static_cast<const T*>(Atv);
+    const uint32_t ldb32 = static_cast<uint32_t>(ldb);  // host guarantees K * pitch < 2^32 elements
+    const uint32_t lda32 = static_cast<uint32_t>(lda);
+    while (u < units) {
+      int nu = u, nkb = kb + Cfg::KS, ncnt = cnt;
+      if (nkb >= cnt) {
+        nkb = 0;
+        do {
+          nu += gridDim.x;
+          ncnt = nu < units ? __ldg(counts + nu % n_groups) : 0;
+        } while (nu < units && ncnt == 0);
+      }
+      int d0 = 0, d1 = 0;
+      if (nu < units) {
+        const int32_t* ns = slots + static_cast<int64_t>(nu % n_groups) * slot_stride + nkb;
+        d0 = nkb + lane < ncnt ? __ldg(ns + lane) : 0;
+        d1 = nkb + 32 + lane < ncnt ? __ldg(ns + 32 + lane) : 0;
+      }
+      const int g = u % n_groups;
+      const int n0 = (u / n_groups) * Cfg::N_TILE;
       const int m0 = g * GW;
-      const int cnt = counts[g];
-      const int32_t* gs = slots + static_cast<int64_t>(g) * slot_stride;
-      for (int kb = 0; kb < cnt; kb += Cfg::KS) {
-        const int kvalid = min(Cfg::KS, cnt - kb);
-        const int kpad = (kvalid + 15) & ~15;
-        // lane l holds coordinates kb+l and kb+32+l (K => out of range => zero-filled rows)
-        const int c0 = (lane < kvalid) ? gs[kb + lane] : K;
-        const int c1 = (32 + lane < kvalid) ? gs[kb + 32 + lane] : K;
-        mbar_wait(&empty_bar[stage], phase ^ 1);
-        uint8_t* sB = smem + stage * Cfg::STAGE_BYTES;
-        uint8_t* sA = sB + Cfg::B_BYTES;
-        if (lane == 0) mbar_expect_tx(&full_bar[stage], kpad * (NACC * 256 + GW * 2));
-        for (int q = 0; q < kpad / 4; ++q) {
-          const int src = (4 * q) & 31;
-          const bool hi = 4 * q >= 32;
-          const int r0 = __shfl_sync(0xffffffffu, hi ? c1 : c0, src + 0);
-          const int r1 = __shfl_sync(0xffffffffu, hi ? c1 : c0, src + 1);
-          const int r2 = __shfl_sync(0xffffffffu, hi ? c1 : c0, src + 2);
-          const int r3 = __shfl_sync(0xffffffffu, hi ? c1 : c0, src + 3);
-          if (lane == 0) {
+      const int kvalid = min(Cfg::KS, cnt - kb);
+      const int kpad = (kvalid + 15) & ~15;
+      mbar_wait(&empty_bar[stage], phase ^ 1);
+      const uint32_t sB = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+      const uint32_t sA = sB + Cfg::B_BYTES;
+      // ---- B rows: row = warp + 4i (warp-uniform), lane = 16-byte chunk of the n tile. Invalid
+      // rows carry k = 0 and copy 0 bytes (zero fill), so addressing is branch-free; (row & 7) only
+      // takes the values warp and warp+4, so the two swizzled offsets are hoisted.
+      {
+        const int niter = kpad >> 4;  // 1..4 groups of four rows per warp
 #pragma unroll
-            for (int a = 0; a < 2 * NACC; ++a)
-              tma_gather4(sB + a * Cfg::KS * 128 + q * 512, &tmB, &full_bar[stage], n0 + a * 64, r0, r1, r2, r3);
+        for (int cb = 0; cb < Cfg::B_CPR; cb += 32) {
+          const int ch = cb + lane;
+          const int n = n0 + ch * 8;
+          const uint32_t nbytes = n < N ? static_cast<uint32_t>(min(16, (N - n) * 2)) : 0u;
+          const T* bcol = Bp + (nbytes ? n : 0);
+          const uint32_t base = sB + (ch >> 3) * (Cfg::KS * 128) + warp * 128;
+          const uint32_t off0 = static_cast<uint32_t>(((ch & 7) ^ (warp & 7)) << 4);
+          const uint32_t off1 = static_cast<uint32_t>(((ch & 7) ^ ((warp + 4) & 7)) << 4);
+          for (int i4 = 0; i4 < niter; ++i4) {
+            const int src = i4 < 2 ? c0 : c1;
 #pragma unroll
-            for (int a = 0; a < Cfg::A_ATOMS; ++a)
-              tma_gather4(sA + a * Cfg::KS * Cfg::A_ROW_BYTES + q * 4 * Cfg::A_ROW_BYTES, &tmAt, &full_bar[stage],
-                          m0 + a * 64, r0, r1, r2, r3);
+            for (int j = 0; j < 4; ++j) {
+              const int row = warp + 16 * i4 + 4 * j;
+              const int k = __shfl_sync(0xffffffffu, src, row & 31);
+              if (Cfg::B_CPR >= 32 || ch < Cfg::B_CPR)
+                cp_async_16(base + (4 * i4 + j) * (kProdWarps * 128) + ((j & 1) ? off1 : off0),
+                            bcol + static_cast<uint32_t>(k) * ldb32, row < kvalid ? nbytes : 0u);
+            }
           }
         }
-        __syncwarp();
-        if (++stage == Cfg::STAGES) {
-          stage = 0;
-          phase ^= 1;
+      }
+      // ---- A^T rows: A_CPR lanes per row, A_RPW rows per warp instruction
+      {
+        const int ch = lane % Cfg::A_CPR;
+        const int m = m0 + ch * 8;
+        const uint32_t mbytes = m < M ? static_cast<uint32_t>(min(16, (M - m) * 2)) : 0u;
+        const T* acol = Ap + (mbytes ? m : 0);
+        const uint32_t abase = sA + (ch / Cfg::A_CPA) * (Cfg::KS * Cfg::A_ROW_BYTES);
+        for (int rb = warp * Cfg::A_RPW; rb < kpad; rb += kProdWarps * Cfg::A_RPW) {
+          const int row = rb + lane / Cfg::A_CPR;
+          const int k = __shfl_sync(0xffffffffu, row < 32 ? c0 : c1, row & 31);
+          const uint32_t o = static_cast<uint32_t>(row * Cfg::A_ROW_BYTES + (ch % Cfg::A_CPA) * 16);
+          cp_async_16(abase + swz<Cfg::A_MASK>(o), acol + static_cast<uint32_t>(k) * lda32,
+                      row < kvalid ? mbytes : 0u);
         }
       }
+      cp_async_arrive_noinc(&full_bar[stage]);
+      if (++stage == Cfg::STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+      u = nu;
+      kb = nkb;
+      cnt = ncnt;
+      c0 = d0;
+      c1 = d1;
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = idesc_f16(128, GW, kBF16, true, true);
+    constexpr uint32_t idesc = kOrientN ? idesc_f16(128, Cfg::N_TILE, kBF16, true, true)
+                                        : idesc_f16(128, GW, kBF16, true, true);
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int g = u / n_tiles;
-      const int cnt = counts[g];
+      const int cnt = __ldg(counts + u % n_groups);
       mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc_fence_after();
       for (int kb = 0; kb < cnt; kb += Cfg::KS) {
-        const int kvalid = min(Cfg::KS, cnt - kb);
-        const int ksteps = (kvalid + 15) >> 4;
+        const int ksteps = (min(Cfg::KS, cnt - kb) + 15) >> 4;
         mbar_wait(&full_bar[stage], phase);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t sB = smem_u32(smem + stage * Cfg::STAGE_BYTES);
           const uint32_t sA = sB + Cfg::B_BYTES;
+          const uint32_t dbase = tmem_base + static_cast<uint32_t>(acc * Cfg::ACC_COLS);
           for (int ks = 0; ks < ksteps; ++ks) {
-            const uint64_t bdesc = smem_desc(sA + ks * 16 * Cfg::A_ROW_BYTES, Cfg::KS * Cfg::A_ROW_BYTES,
-                                             8 * Cfg::A_ROW_BYTES, Cfg::A_SW);
+            const uint32_t acc_flag = (kb > 0 || ks > 0) ? 1u : 0u;
+            const uint64_t a_strip = smem_desc(sA + ks * 16 * Cfg::A_ROW_BYTES, Cfg::KS * Cfg::A_ROW_BYTES,
+                                               8 * Cfg::A_ROW_BYTES, Cfg::A_SW);
+            if constexpr (kOrientN) {
+              const uint64_t b_strip = smem_desc(sB + ks * 2048, Cfg::KS * 128, 1024, kSw128);
+              umma_f16(dbase, a_strip, b_strip, idesc, acc_flag);
+            } else {
 #pragma unroll
-            for (int a = 0; a < NACC; ++a) {
-              const uint64_t adesc = smem_desc(sB + a * 2 * Cfg::KS * 128 + ks * 2048, Cfg::KS * 128, 1024, kSw128);
-              const uint32_t d = tmem_base + static_cast<uint32_t>((acc * NACC + a) * GW);
-              umma_f16(d, adesc, bdesc, idesc, (kb > 0 || ks > 0) ? 1u : 0u);
+              for (int a = 0; a < Cfg::N_TILE / 128; ++a) {
+                const uint64_t b_half = smem_desc(sB + a * 2 * Cfg::KS * 128 + ks * 2048, Cfg::KS * 128, 1024, kSw128);
+                umma_f16(dbase + static_cast<uint32_t>(a * GW), b_half, a_strip, idesc, acc_flag);
+              }
             }
           }
           umma_commit(&empty_bar[stage]);
@@ -215,32 +301,70 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int g = u / n_tiles;
-      const int n0 = (u % n_tiles) * Cfg::N_TILE;
+      const int g = u % n_groups;
+      const int n0 = (u / n_groups) * Cfg::N_TILE;
       const int m0 = g * GW;
-      const int cnt = counts[g];
+      const int cnt = __ldg(counts + g);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
-#pragma unroll
-      for (int a = 0; a < NACC; ++a) {
-        const int n = n0 + a * 128 + q * 32 + lane;
-#pragma unroll
-        for (int c = 0; c < GW; c += 16) {
-          uint32_t v[16];
+      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * Cfg::ACC_COLS);
+      if constexpr (kOrientN) {
+        // lane = group row, columns = n: 32 consecutive outputs per tcgen05.ld
+        const int m = m0 + q * 32 + lane;
+        const bool row_ok = m < M;
+        uint8_t* crow = reinterpret_cast<uint8_t*>(C + static_cast<int64_t>(row_ok ? m : 0) * ldc);
+        const bool vec_ok = (ldc % 8) == 0 && (reinterpret_cast<uintptr_t>(Cv) & 15) == 0;
+#pragma unroll 1
+        for (int c = 0; c < Cfg::N_TILE; c += 32) {
+          uint32_t v[32];
           if (cnt > 0) {
-            tmem_ld16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
-                          static_cast<uint32_t>((acc * NACC + a) * GW + c),
-                      v);
+            tmem_ld32(tbase + static_cast<uint32_t>(c), v);
             tmem_wait_ld();
           } else {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = 0u;
+            for (int i = 0; i < 32; ++i) v[i] = 0u;
           }
-          if (n < N) {
+          const int nb = n0 + c;
+          if (row_ok && nb < N) {
+            if (vec_ok && nb + 32 <= N) {
+              uint4* dst = reinterpret_cast<uint4*>(crow + static_cast<int64_t>(nb) * 2);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int m = m0 + c + i;
-              if (m < M) C[static_cast<int64_t>(m) * ldc + n] = OT::cvt(__uint_as_float(v[i]));
+              for (int j = 0; j < 4; ++j) {
+                uint4 w;
+                w.x = pack2(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]), kBF16);
+                w.y = pack2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]), kBF16);
+                w.z = pack2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]), kBF16);
+                w.w = pack2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]), kBF16);
+                dst[j] = w;
+              }
+            } else {
+              T* dst = reinterpret_cast<T*>(crow);
+              for (int j = 0; j < 32; ++j)
+                if (nb + j < N) dst[nb + j] = OT::cvt(__uint_as_float(v[j]));
+            }
+          }
+        }
+      } else {
+        // lane = output column n, columns = group rows
+#pragma unroll
+        for (int a = 0; a < Cfg::N_TILE / 128; ++a) {
+          const int n = n0 + a * 128 + q * 32 + lane;
+#pragma unroll
+          for (int c = 0; c < GW; c += 16) {
+            uint32_t v[16];
+            if (cnt > 0) {
+              tmem_ld16(tbase + static_cast<uint32_t>(a * GW + c), v);
+              tmem_wait_ld();
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v[i] = 0u;
+            }
+            if (n < N) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const int m = m0 + c + i;
+                if (m < M) C[static_cast<int64_t>(m) * ldc + n] = OT::cvt(__uint_as_float(v[i]));
+              }
             }
           }
         }
@@ -254,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == kAllocWarp) {
     tc_fence_after();
     tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
   }
@@ -279,7 +403,7 @@ struct GmCfg {
 
 template <int KS, bool kBF16>
 __global__ void __launch_bounds__(kThreads, 1)
-    spmm_gm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+    spmm_gm_kernel(const void* __restrict__ Av, int64_t lda, const __grid_constant__ CUtensorMap tmB,
                    const int32_t* __restrict__ rows, const int32_t* __restrict__ n_rows_dev, int dense,
                    const uint32_t* __restrict__ occ, int64_t WG, int t1, int row_tiles, int n_tiles, int M, int N,
                    int K, void* __restrict__ Cv, int64_t ldc) {
@@ -299,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < Cfg::STAGES; ++i) {
-      mbar_init(&full_bar[i], 1);
+      mbar_init(&full_bar[i], kProdWarps * 32 + 1);
       mbar_init(&empty_bar[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -307,10 +431,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tempty_bar[i], 128);
     }
     fence_mbar_init();
-    tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
   }
-  if (warp == 2) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  if (warp == kAllocWarp) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -320,58 +443,76 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int units = min(row_tiles, live_tiles) * n_tiles;
   const int kblocks = (K + KS - 1) / KS;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+  if (warp < kProdWarps) {
+    // ------------------------------------------------------------ producers
+    // A rows: cp.async 16-byte chunks by the 128 producer threads into the K-major swizzled layout;
+    // a row that is not live in this K-block is zero-filled (src size 0). B: plain 2-D TMA tiles.
+    // A K-block in which no row of the tile is live is skipped by every role (stage_live = 0).
+    constexpr int CPR = KS * 2 / 16;          // chunks per A row
+    constexpr uint32_t MASK = KS * 2 == 128 ? 7 : KS * 2 == 64 ? 3 : 1;
+    const int tp = threadIdx.x;               // 0..127
+    const int ch = tp % CPR;
+    using T = typename OutT<kBF16>::T;
+    const T* Ap = static_cast<const T*>(Av);
     int stage = 0;
     uint32_t phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int rt = u / n_tiles;
       const int n0 = (u % n_tiles) * Cfg::BN;
-      // lane l owns tile rows 4l..4l+3
-      int rid[4];
+      int rid[CPR];  // this thread's rows: tp / CPR + j * (128 / CPR)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int i = rt * Cfg::BM + 4 * lane + j;
-        rid[j] = (i < n_rows) ? (dense ? i : rows[i]) : -1;
+      for (int j = 0; j < CPR; ++j) {
+        const int i = rt * Cfg::BM + tp / CPR + j * (128 / CPR);
+        rid[j] = (i < n_rows) ? (dense ? i : __ldg(rows + i)) : -1;
       }
       for (int kb = 0; kb < kblocks; ++kb) {
         const int k0 = kb * KS;
         const int grp = dense ? 0 : k0 / t1;
-        int r[4];
+        bool live[CPR];
         bool any = false;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          bool live = rid[j] >= 0;
-          if (live && !dense) live = (occ[static_cast<int64_t>(grp) * WG + (rid[j] >> 5)] >> (rid[j] & 31)) & 1u;
-          r[j] = live ? rid[j] : M;  // M => out of range => zero row
-          any |= live;
+        for (int j = 0; j < CPR; ++j) {
+          live[j] = rid[j] >= 0;
+          if (live[j] && !dense)
+            live[j] = (__ldg(occ + static_cast<int64_t>(grp) * WG + (rid[j] >> 5)) >> (rid[j] & 31)) & 1u;
+          any |= live[j];
         }
-        const bool stage_any = __any_sync(0xffffffffu, any);
+        const bool stage_any = bar_or(1, kProdWarps * 32, any);
         mbar_wait(&empty_bar[stage], phase ^ 1);
-        uint8_t* sA = smem + stage * Cfg::STAGE_BYTES;
-        uint8_t* sB = sA + Cfg::A_BYTES;
-        if (lane == 0) stage_live[stage] = stage_any ? 1 : 0;
-        if (stage_any) {
-          if (lane == 0) {
-            mbar_expect_tx(&full_bar[stage], Cfg::A_BYTES + Cfg::B_BYTES);
+        uint8_t* sAp = smem + stage * Cfg::STAGE_BYTES;
+        const uint32_t sA = smem_u32(sAp);
+        uint8_t* sB = sAp + Cfg::A_BYTES;
+        if (tp == 0) {
+          stage_live[stage] = stage_any ? 1 : 0;
+          if (stage_any) {
+            mbar_expect_tx_only(&full_bar[stage], Cfg::B_BYTES);
 #pragma unroll
             for (int a = 0; a < Cfg::BN / 64; ++a)
               tma_load_2d(sB + a * KS * 128, &tmB, &full_bar[stage], n0 + a * 64, k0);
           }
-          __syncwarp();
-          // every lane issues the gather for its own four rows
-          tma_gather4(sA + lane * 4 * Cfg::A_ROW_BYTES, &tmA, &full_bar[stage], k0, r[0], r[1], r[2], r[3]);
-        } else if (lane == 0) {
+          mbar_arrive(&full_bar[stage]);  // publishes stage_live
+        }
+        if (stage_any) {
+          const int kc = k0 + ch * 8;
+          const uint32_t kbytes = kc < K ? static_cast<uint32_t>(min(16, (K - kc) * 2)) : 0u;
+#pragma unroll
+          for (int j = 0; j < CPR; ++j) {
+            const int row = tp / CPR + j * (128 / CPR);
+            const uint32_t bytes = live[j] ? kbytes : 0u;
+            const T* src = bytes ? Ap + static_cast<int64_t>(rid[j]) * lda + kc : Ap;
+            cp_async_16(sA + swz<MASK>(static_cast<uint32_t>(row * Cfg::A_ROW_BYTES + ch * 16)), src, bytes);
+          }
+          cp_async_arrive_noinc(&full_bar[stage]);
+        } else {
           mbar_arrive(&full_bar[stage]);
         }
-        __syncwarp();
         if (++stage == Cfg::STAGES) {
           stage = 0;
           phase ^= 1;
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idesc = idesc_f16(Cfg::BM, Cfg::BN, kBF16, false, true);
     int stage = 0;
@@ -460,7 +601,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == kAllocWarp) {
     tc_fence_after();
     tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
   }
@@ -485,27 +626,21 @@ CUtensorMapSwizzle swizzle_enum(int row_bytes) {
                            : CU_TENSOR_MAP_SWIZZLE_NONE;
 }
 
-template <int GW, int NACC, bool kBF16>
+template <int GW, bool kOrientN, bool kBF16>
 int run_gk(const SpmmArgs& a, cudaStream_t s) {
-  using Cfg = GkCfg<GW, NACC>;
-  const CUtensorMapDataType dt = kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-  CUtensorMap tmB, tmAt;
-  // B: row-major [K, N]
-  if (encode_tensor_map_2d(&tmB, dt, a.B, a.N, a.K, a.ldb * 2, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B) != CUDA_SUCCESS)
-    return kErrCuda;
-  // A^T: row-major [K, M] (A column-major, pitch sak)
-  const int box = GW < 64 ? GW : 64;
-  if (encode_tensor_map_2d(&tmAt, dt, a.A, a.M, a.K, a.sak * 2, box, 1, swizzle_enum(box * 2)) != CUDA_SUCCESS)
-    return kErrCuda;
+  using Cfg = GkCfg<GW, kOrientN>;
   const int n_tiles = static_cast<int>(ceil_div(a.N, Cfg::N_TILE));
   const int64_t units = a.n_groups * n_tiles;
   if (units == 0) return kOk;
-  auto kern = spmm_gk_kernel<GW, NACC, kBF16>;
+  if (units >= (1ll << 31)) return kErrShape;
+  auto kern = spmm_gk_kernel<GW, kOrientN, kBF16>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::SMEM));
   const int grid = static_cast<int>(units < num_sms() ? units : num_sms());
-  kern<<<grid, kThreads, Cfg::SMEM, s>>>(tmB, tmAt, a.counts, a.slots, a.slot_stride, static_cast<int>(a.n_groups),
-                                         n_tiles, static_cast<int>(a.M), static_cast<int>(a.N),
-                                         static_cast<int>(a.K), a.C, a.ldc);
+  // A column-major: A^T is row-major [K, M] with pitch sak
+  kern<<<grid, kThreads, Cfg::SMEM, s>>>(a.B, a.ldb, a.A, a.sak, a.counts, a.slots, a.slot_stride,
+                                         static_cast<int>(a.n_groups), n_tiles, static_cast<int>(a.M),
+                                         static_cast<int>(a.N), static_cast<int>(a.K), a.C, a.ldc);
+  note_launch();
   return cuda_status();
 }
 
@@ -513,10 +648,7 @@ template <int KS, bool kBF16>
 int run_gm(const SpmmArgs& a, cudaStream_t s) {
   using Cfg = GmCfg<KS>;
   const CUtensorMapDataType dt = kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-  CUtensorMap tmA, tmB;
-  // A: row-major [M, K], gather rows, box KS columns
-  if (encode_tensor_map_2d(&tmA, dt, a.A, a.K, a.M, a.sam * 2, KS, 1, swizzle_enum(KS * 2)) != CUDA_SUCCESS)
-    return kErrCuda;
+  CUtensorMap tmB;
   // B: row-major [K, N], tile box {64 n, KS k}
   if (encode_tensor_map_2d(&tmB, dt, a.B, a.N, a.K, a.ldb * 2, 64, KS, CU_TENSOR_MAP_SWIZZLE_128B) != CUDA_SUCCESS)
     return kErrCuda;
@@ -533,9 +665,10 @@ int run_gm(const SpmmArgs& a, cudaStream_t s) {
   auto kern = spmm_gm_kernel<KS, kBF16>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::SMEM));
   const int grid = static_cast<int>(units < num_sms() ? units : num_sms());
-  kern<<<grid, kThreads, Cfg::SMEM, s>>>(tmA, tmB, a.rows, a.n_rows, dense, a.occ, a.WG, a.t1, row_tiles, n_tiles,
+  kern<<<grid, kThreads, Cfg::SMEM, s>>>(a.A, a.sam, tmB, a.rows, a.n_rows, dense, a.occ, a.WG, a.t1, row_tiles, n_tiles,
                                          static_cast<int>(a.M), static_cast<int>(a.N), static_cast<int>(a.K), a.C,
                                          a.ldc);
+  note_launch();
   return cuda_status();
 }
 
@@ -544,15 +677,15 @@ int dispatch_tc(const SpmmArgs& a, cudaStream_t s) {
   if (a.plan == kPlanPitK) {
     switch (a.t0) {
       case 16:
-        return run_gk<16, 2, kBF16>(a, s);
+        return run_gk<16, false, kBF16>(a, s);
       case 32:
-        return run_gk<32, 2, kBF16>(a, s);
+        return run_gk<32, false, kBF16>(a, s);
       case 64:
-        return run_gk<64, 2, kBF16>(a, s);
+        return run_gk<64, false, kBF16>(a, s);
       case 128:
-        return run_gk<128, 2, kBF16>(a, s);
+        return run_gk<128, true, kBF16>(a, s);
       case 256:
-        return run_gk<256, 1, kBF16>(a, s);
+        return run_gk<256, false, kBF16>(a, s);
       default:
         return kErrUnsupported;
     }
@@ -574,6 +707,7 @@ bool spmm_tc_supported(const SpmmArgs& a) {
   if ((a.ldb * 2) % 16) return false;
   if (a.plan == kPlanPitK) {
     if (a.sam != 1 || (a.sak * 2) % 16) return false;  // A column-major
+    if (a.K * a.ldb >= (1ll << 32) || a.K * a.sak >= (1ll << 32)) return false;  // 32-bit element offsets
     return a.t0 == 16 || a.t0 == 32 || a.t0 == 64 || a.t0 == 128 || a.t0 == 256;
   }
   if (a.sak != 1 || (a.sam * 2) % 16) return false;  // A row-major

@@ -101,16 +101,16 @@ class DenseTensor:
 
     @property
     def is_device(self) -> bool:
-        return _is_torch(self.array)
+        return _is_torch(self.array) and self.array.is_cuda
 
     @property
     def layout(self) -> str:
-        if self.is_device:
+        if _is_torch(self.array):
             return _torch_layout(self.array)
         return ROW_MAJOR if self.array.flags.c_contiguous else COL_MAJOR
 
     def numpy(self) -> np.ndarray:
-        return _device.to_host(self.array, self.layout) if self.is_device else self.array
+        return _device.to_host(self.array, self.layout) if _is_torch(self.array) else self.array
 
     @classmethod
     def from_array(cls, arr, layout: str = ROW_MAJOR, dtype=None) -> "DenseTensor":

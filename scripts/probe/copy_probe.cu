@@ -1,0 +1,138 @@
+// Micro-probe: global->shared gather throughput on B200 for the three copy engines the PIT
+// mainloops can use. One CTA per SM, a ring of STAGES x 32 KiB stages, no consumer: a stage is
+// re-filled as soon as its previous fill has landed. Rows are random 128-byte windows of a
+// 8192 x 8192 bf16 matrix (the B-gather pattern of spmm_gk).
+//   mode 0: TMA tile::gather4 (4 rows x 128 B per instruction), issued by `warps` warps (lane 0)
+//   mode 1: cp.async 16 B per thread, `warps` warps
+//   mode 2: TMA 2-D tile (64 rows x 128 B per instruction, contiguous rows), `warps` warps
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../../paper_2301_10936_b200/csrc copy_probe.cu -o copy_probe
+#include <cstdio>
+#include <cstdlib>
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <vector>
+
+#include "pit_ptx.cuh"
+
+using namespace pit;
+
+constexpr int STAGES = 6;
+constexpr int STAGE_BYTES = 32768;
+constexpr int ROWS_PER_STAGE = STAGE_BYTES / 128;  // 256
+
+__global__ void __launch_bounds__(512, 1) probe(const __grid_constant__ CUtensorMap tm, const __nv_bfloat16* B,
+                                                  const int* rows, int nrows_total, int mode, int warps, int iters) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], mode == 1 ? warps * 32 : warps);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp >= warps) return;
+  uint32_t phase = 0;
+  int stage = 0;
+  int rbase = (blockIdx.x * 977) % nrows_total;
+  for (int it = 0; it < iters; ++it) {
+    if (it >= STAGES) mbar_wait(&full[stage], phase ^ 1);
+    uint8_t* dst = smem + stage * STAGE_BYTES;
+    if (mode == 0) {
+      const int quads = ROWS_PER_STAGE / 4;
+      const int myq = (quads - warp + warps - 1) / warps;
+      if (lane == 0) mbar_expect_tx(&full[stage], myq * 512);
+      for (int q = warp; q < quads; q += warps) {
+        const unsigned r = rbase + q * 4;
+        const int r0 = ((r + 0) * 2654435761u) >> 19, r1 = ((r + 1) * 2654435761u) >> 19;
+        const int r2 = ((r + 2) * 2654435761u) >> 19, r3 = ((r + 3) * 2654435761u) >> 19;
+        if (lane == 0) tma_gather4(dst + q * 512, &tm, &full[stage], (blockIdx.x % 128) * 64, r0, r1, r2, r3);
+      }
+    } else if (mode == 1) {
+      const uint32_t s = smem_u32(dst);
+      for (int row = warp * 4 + (lane >> 3); row < ROWS_PER_STAGE; row += warps * 4) {
+        const int k = ((unsigned)(rbase + row) * 2654435761u) >> 19;
+        const int ch = lane & 7;
+        cp_async_16(s + swz<7>(row * 128 + ch * 16), B + (int64_t)k * 8192 + (blockIdx.x % 128) * 64 + ch * 8, 16);
+      }
+      cp_async_arrive_noinc(&full[stage]);
+    } else {
+      const int tiles = ROWS_PER_STAGE / 64;
+      const int myt = (tiles - warp + warps - 1) / warps;
+      if (lane == 0) {
+        mbar_expect_tx(&full[stage], myt * 8192);
+        for (int t = warp; t < tiles; t += warps)
+          tma_load_2d(dst + t * 8192, &tm, &full[stage], (blockIdx.x % 128) * 64, (rbase + t * 64) % 8000);
+      }
+    }
+    rbase = (rbase + ROWS_PER_STAGE) % nrows_total;
+    if (++stage == STAGES) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+  // drain
+  for (int i = 0; i < STAGES; ++i) {
+    mbar_wait(&full[stage], phase ^ 1);
+    if (++stage == STAGES) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                             const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int main() {
+  const int R = 8192, C = 8192;
+  __nv_bfloat16* B;
+  cudaMalloc(&B, (size_t)R * C * 2);
+  cudaMemset(B, 0, (size_t)R * C * 2);
+  std::vector<int> h(1 << 20);
+  srand(1);
+  for (auto& x : h) x = rand() % R;
+  int* rows;
+  cudaMalloc(&rows, h.size() * 4);
+  cudaMemcpy(rows, h.data(), h.size() * 4, cudaMemcpyHostToDevice);
+  void* fn;
+  cudaDriverEntryPointQueryResult q;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  EncodeFn enc = (EncodeFn)fn;
+  CUtensorMap tm_g, tm_t;
+  cuuint64_t dims[2] = {(cuuint64_t)C, (cuuint64_t)R}, str[1] = {(cuuint64_t)C * 2};
+  cuuint32_t box_g[2] = {64, 1}, box_t[2] = {64, 64}, es[2] = {1, 1};
+  enc(&tm_g, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, dims, str, box_g, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  enc(&tm_t, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, dims, str, box_t, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  int smem = STAGES * STAGE_BYTES + 2048;
+  cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int clk;
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  const char* names[3] = {"tma_gather4", "cp.async16", "tma_tile2d"};
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 400;
+  for (int mode = 0; mode < 3; ++mode) {
+    for (int warps : {1, 2, 4, 8, 16}) {
+      const CUtensorMap& tm = mode == 2 ? tm_t : tm_g;
+      probe<<<sms, 512, smem>>>(tm, B, rows, (int)h.size(), mode, warps, 20);
+      cudaEventRecord(e0);
+      probe<<<sms, 512, smem>>>(tm, B, rows, (int)h.size(), mode, warps, iters);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      double bytes = (double)sms * iters * STAGE_BYTES;
+      double gbs = bytes / (ms * 1e-3) / 1e9;
+      printf("%-12s warps=%2d  %8.1f GB/s  %6.2f B/cycle/SM (at %d MHz)  err=%s\n", names[mode], warps, gbs,
+             gbs * 1e9 / sms / (clk * 1e3), clk / 1000, cudaGetErrorString(cudaGetLastError()));
+    }
+  }
+  return 0;
+}
