@@ -146,44 +146,49 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Stage = KS gathered k rows. The 128 producer threads copy 16-byte chunks: a warp instruction
     // moves one 512-byte B row segment (coalesced), the A^T strip rows are split across lanes.
     // Shared-memory addresses are swizzled in software to the UMMA SWIZZLE_{32,64,128}B layouts.
-    // Rows past the live count are zero-filled (src size 0). Slot indices for the next stage are
-    // loaded while the current stage is issued.
-    const int tp = threadIdx.x;  // 0..127
+    // Rows past the live count are zero-filled (src size 0).
     int stage = 0;
     uint32_t phase = 0;
-    int u = blockIdx.x;
-    int cnt = u < units ? __ldg(counts + u % n_groups) : 0;
-    while (u < units && cnt == 0) {
-      u += gridDim.x;
-      cnt = u < units ? __ldg(counts + u % n_groups) : 0;
-    }
-    int kb = 0;
-    int c0 = 0, c1 = 0;
-    if (u < units) {
-      const int32_t* gs = slots + static_cast<int64_t>(u % n_groups) * slot_stride;
-      c0 = lane < cnt ? __ldg(gs + lane) : 0;
-      c1 = 32 + lane < cnt ? __ldg(gs + 32 + lane) : 0;
-    }
+    // Stage positions (unit, chunk start, unit count) in this CTA's order; indices are loaded two
+    // stages ahead of their use so the L2 latency of the slot loads never stalls issue.
+    struct Pos {
+      int u, kb, cnt;
+    };
+    auto advance = [&](Pos p) {
+      Pos q{p.u, p.kb + Cfg::KS, p.cnt};
+      if (q.kb >= p.cnt) {
+        q.kb = 0;
+        do {
+          q.u += gridDim.x;
+          q.cnt = q.u < units ? __ldg(counts + q.u % n_groups) : 0;
+        } while (q.u < units && q.cnt == 0);
+      }
+      return q;
+    };
+    auto load_idx = [&](const Pos& p, int& x0, int& x1) {
+      x0 = x1 = 0;
+      if (p.u < units) {
+        const int32_t* ps = slots + static_cast<int64_t>(p.u % n_groups) * slot_stride + p.kb;
+        if (p.kb + lane < p.cnt) x0 = __ldg(ps + lane);
+        if (p.kb + 32 + lane < p.cnt) x1 = __ldg(ps + 32 + lane);
+      }
+    };
+    Pos cur{static_cast<int>(blockIdx.x) - static_cast<int>(gridDim.x), 0, 0};
+    cur = advance(cur);
+    Pos nxt = advance(cur);
+    int c0, c1, d0, d1;
+    load_idx(cur, c0, c1);
+    load_idx(nxt, d0, d1);
     using T = typename OT::T;
     const T* Bp = static_cast<const T*>(Bv);
     const T* Ap = static_cast<const T*>(Atv);
     const uint32_t ldb32 = static_cast<uint32_t>(ldb);  // host guarantees K * pitch < 2^32 elements
     const uint32_t lda32 = static_cast<uint32_t>(lda);
-    while (u < units) {
-      int nu = u, nkb = kb + Cfg::KS, ncnt = cnt;
-      if (nkb >= cnt) {
-        nkb = 0;
-        do {
-          nu += gridDim.x;
-          ncnt = nu < units ? __ldg(counts + nu % n_groups) : 0;
-        } while (nu < units && ncnt == 0);
-      }
-      int d0 = 0, d1 = 0;
-      if (nu < units) {
-        const int32_t* ns = slots + static_cast<int64_t>(nu % n_groups) * slot_stride + nkb;
-        d0 = nkb + lane < ncnt ? __ldg(ns + lane) : 0;
-        d1 = nkb + 32 + lane < ncnt ? __ldg(ns + 32 + lane) : 0;
-      }
+    while (cur.u < units) {
+      const Pos nn = advance(nxt);
+      int e0, e1;
+      load_idx(nn, e0, e1);
+      const int u = cur.u, kb = cur.kb, cnt = cur.cnt;
       const int g = u % n_groups;
       const int n0 = (u / n_groups) * Cfg::N_TILE;
       const int m0 = g * GW;
@@ -239,11 +244,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         stage = 0;
         phase ^= 1;
       }
-      u = nu;
-      kb = nkb;
-      cnt = ncnt;
+      cur = nxt;
+      nxt = nn;
       c0 = d0;
       c1 = d1;
+      d0 = e0;
+      d1 = e1;
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
