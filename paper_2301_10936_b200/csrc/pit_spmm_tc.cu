@@ -33,14 +33,15 @@ namespace pit {
 
 namespace {
 
-// Warp roles: 0..3 TMA producers (gather issue is instruction-bound from a single thread, so four
-// warps split each stage's gathers), 4 MMA issuer, 5 TMEM allocator, 8..11 epilogue (one per TMEM
-// lane quarter).
-constexpr int kProdWarps = 4;
-constexpr int kMmaWarp = 4;
-constexpr int kAllocWarp = 5;
-constexpr int kEpiWarp0 = 8;
-constexpr int kThreads = 384;
+// Warp roles: 0..7 producers (gather issue is instruction- and latency-bound per warp, so eight warps
+// split each stage's copies), 8 MMA issuer, 9 TMEM allocator, 12..15 epilogue (one per TMEM lane
+// quarter).
+constexpr int kProdWarps = 8;
+constexpr int kProdThreads = kProdWarps * 32;
+constexpr int kMmaWarp = 8;
+constexpr int kAllocWarp = 9;
+constexpr int kEpiWarp0 = 12;
+constexpr int kThreads = 512;
 
 template <bool kBF16>
 struct OutT;
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < Cfg::STAGES; ++i) {
-      mbar_init(&full_bar[i], kProdWarps * 32);
+      mbar_init(&full_bar[i], kProdThreads);
       mbar_init(&empty_bar[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -201,25 +202,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       // rows carry k = 0 and copy 0 bytes (zero fill), so addressing is branch-free; (row & 7) only
       // takes the values warp and warp+4, so the two swizzled offsets are hoisted.
       {
-        const int niter = kpad >> 4;  // 1..4 groups of four rows per warp
+        static_assert(kProdWarps == 8, "row mapping assumes eight producer warps");
+        const int niter = kpad >> 4;  // kpad / 16: pairs of rows per warp (row = warp + 8 i)
 #pragma unroll
         for (int cb = 0; cb < Cfg::B_CPR; cb += 32) {
           const int ch = cb + lane;
           const int n = n0 + ch * 8;
           const uint32_t nbytes = n < N ? static_cast<uint32_t>(min(16, (N - n) * 2)) : 0u;
           const T* bcol = Bp + (nbytes ? n : 0);
-          const uint32_t base = sB + (ch >> 3) * (Cfg::KS * 128) + warp * 128;
-          const uint32_t off0 = static_cast<uint32_t>(((ch & 7) ^ (warp & 7)) << 4);
-          const uint32_t off1 = static_cast<uint32_t>(((ch & 7) ^ ((warp + 4) & 7)) << 4);
-          for (int i4 = 0; i4 < niter; ++i4) {
-            const int src = i4 < 2 ? c0 : c1;
+          // row & 7 == warp for every row this warp copies: one swizzled offset
+          const uint32_t base = sB + (ch >> 3) * (Cfg::KS * 128) + warp * 128 + (((ch & 7) ^ warp) << 4);
+          for (int i2 = 0; i2 < niter; ++i2) {
+            const int src = i2 < 2 ? c0 : c1;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int row = warp + 16 * i4 + 4 * j;
+            for (int j = 0; j < 2; ++j) {
+              const int row = warp + 16 * i2 + 8 * j;
               const int k = __shfl_sync(0xffffffffu, src, row & 31);
               if (Cfg::B_CPR >= 32 || ch < Cfg::B_CPR)
-                cp_async_16(base + (4 * i4 + j) * (kProdWarps * 128) + ((j & 1) ? off1 : off0),
-                            bcol + static_cast<uint32_t>(k) * ldb32, row < kvalid ? nbytes : 0u);
+                cp_async_16(base + (2 * i2 + j) * (kProdWarps * 128), bcol + static_cast<uint32_t>(k) * ldb32,
+                            row < kvalid ? nbytes : 0u);
             }
           }
         }
@@ -429,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < Cfg::STAGES; ++i) {
-      mbar_init(&full_bar[i], kProdWarps * 32 + 1);
+      mbar_init(&full_bar[i], kProdThreads + 1);
       mbar_init(&empty_bar[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -455,8 +456,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // a row that is not live in this K-block is zero-filled (src size 0). B: plain 2-D TMA tiles.
     // A K-block in which no row of the tile is live is skipped by every role (stage_live = 0).
     constexpr int CPR = KS * 2 / 16;          // chunks per A row
+    constexpr int RPT = 128 * CPR / kProdThreads;  // rows per producer thread
+    constexpr int RSTEP = kProdThreads / CPR;      // row stride between a thread's rows
     constexpr uint32_t MASK = KS * 2 == 128 ? 7 : KS * 2 == 64 ? 3 : 1;
-    const int tp = threadIdx.x;               // 0..127
+    const int tp = threadIdx.x;               // 0..kProdThreads-1
     const int ch = tp % CPR;
     using T = typename OutT<kBF16>::T;
     const T* Ap = static_cast<const T*>(Av);
@@ -465,25 +468,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int rt = u / n_tiles;
       const int n0 = (u % n_tiles) * Cfg::BN;
-      int rid[CPR];  // this thread's rows: tp / CPR + j * (128 / CPR)
+      int rid[RPT];  // this thread's rows: tp / CPR + j * RSTEP
 #pragma unroll
-      for (int j = 0; j < CPR; ++j) {
-        const int i = rt * Cfg::BM + tp / CPR + j * (128 / CPR);
+      for (int j = 0; j < RPT; ++j) {
+        const int i = rt * Cfg::BM + tp / CPR + j * RSTEP;
         rid[j] = (i < n_rows) ? (dense ? i : __ldg(rows + i)) : -1;
       }
       for (int kb = 0; kb < kblocks; ++kb) {
         const int k0 = kb * KS;
         const int grp = dense ? 0 : k0 / t1;
-        bool live[CPR];
+        bool live[RPT];
         bool any = false;
 #pragma unroll
-        for (int j = 0; j < CPR; ++j) {
+        for (int j = 0; j < RPT; ++j) {
           live[j] = rid[j] >= 0;
           if (live[j] && !dense)
             live[j] = (__ldg(occ + static_cast<int64_t>(grp) * WG + (rid[j] >> 5)) >> (rid[j] & 31)) & 1u;
           any |= live[j];
         }
-        const bool stage_any = bar_or(1, kProdWarps * 32, any);
+        const bool stage_any = bar_or(1, kProdThreads, any);
         mbar_wait(&empty_bar[stage], phase ^ 1);
         uint8_t* sAp = smem + stage * Cfg::STAGE_BYTES;
         const uint32_t sA = smem_u32(sAp);
@@ -502,8 +505,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int kc = k0 + ch * 8;
           const uint32_t kbytes = kc < K ? static_cast<uint32_t>(min(16, (K - kc) * 2)) : 0u;
 #pragma unroll
-          for (int j = 0; j < CPR; ++j) {
-            const int row = tp / CPR + j * (128 / CPR);
+          for (int j = 0; j < RPT; ++j) {
+            const int row = tp / CPR + j * RSTEP;
             const uint32_t bytes = live[j] ? kbytes : 0u;
             const T* src = bytes ? Ap + static_cast<int64_t>(rid[j]) * lda + kc : Ap;
             cp_async_16(sA + swz<MASK>(static_cast<uint32_t>(row * Cfg::A_ROW_BYTES + ch * 16)), src, bytes);
