@@ -51,6 +51,7 @@ WORKLOADS = {
 }
 DEFAULT_WORKLOAD = "pitk_c1_8192"
 FLUSH_BYTES = 256 << 20
+L2_GATHER_CEILING_GBPS = 9425.0  # measured L2->SM gather ceiling (cp.async, 148 SMs, 1965 MHz)
 
 
 # ----------------------------------------------------------------------------------- helpers
@@ -241,12 +242,23 @@ def run_ours(args, w):
     achieved = eff_flops / (spmm_avg * 1e-3) / 1e12
     scanned = A.numel() * A.element_size()
     traffic = load_traffic().get(w["name"], {}).get("spmm_dram_bytes")
+    operand_feed = None
+    if axis == "k":
+        # gathered operand bytes per launch: every live (group, k) pair brings one B row strip of
+        # the n tile and one A^T strip of the group, for every n tile (csrc/pit_spmm_tc.cu spmm_gk)
+        gw = micro[0]
+        n_tile = 256 if gw < 256 else 128
+        gathered = idx0.total * (-(-w["N"] // n_tile)) * (n_tile + gw) * 2
+        feed = gathered / (spmm_avg * 1e-3) / 1e9
+        operand_feed = {"bytes_per_launch": gathered, "achieved_GBps": round(feed, 1),
+                        "ceiling_GBps": L2_GATHER_CEILING_GBPS, "frac": round(feed / L2_GATHER_CEILING_GBPS, 4),
+                        "ceiling_source": "measured cp.async gather, scripts/probe/copy_probe.cu (profiles/r1/copy_probe.txt)"}
     roofline = {
         "bound": "tensor", "kernel": "spmm_gk" if axis == "k" else "spmm_gm",
         "achieved": round(achieved, 2), "peak": peaks["bf16"], "unit": "TFLOP/s",
         "frac": round(achieved / peaks["bf16"], 4), "peak_source": peaks["source"] + " burst bf16",
         "traffic": traffic, "algorithmic_flops": eff_flops,
-        "kernel_ms": round(spmm_avg, 4),
+        "kernel_ms": round(spmm_avg, 4), "operand_feed": operand_feed,
     }
     detection = {
         "kernel": "detect+compact", "ms": round(det_avg, 4), "bytes_scanned": scanned,
