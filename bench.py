@@ -279,6 +279,9 @@ def run_ours(args, w):
         "clocks": clocks.summary(), "gpu_launches": int(launches),
     }
 
+    if not args.no_index_bench:
+        result["index_build"] = index_build_bench(dev, peaks)
+
     # ---- end to end through the public API with host buffers
     if rank == 0 and not args.no_e2e:
         result["e2e"] = e2e_ours(args, w, A, B, plan, eff_flops)
@@ -287,6 +290,43 @@ def run_ours(args, w):
     if world > 1:
         dist.destroy_process_group()
     return result if rank == 0 else None
+
+
+def index_build_bench(dev, peaks, side=16384, reps=20):
+    """K1 alone at the north-star size: online detection over a 16384^2 bf16 tensor (512 MiB),
+    C1 distribution (32x1 micro-tiles, 90% zero, column-major like the pit:k operand), launches
+    back to back so host overhead hides behind GPU time. Algorithmic bytes = tensor bytes + index
+    bytes written."""
+    import torch
+
+    import paper_2301_10936_b200 as pit
+
+    g = torch.Generator(device=dev).manual_seed(99)
+    keep = torch.rand((side, side // 32), device=dev, generator=g) >= 0.9
+    At = torch.randn((side, side), device=dev, dtype=torch.bfloat16, generator=g)
+    At.mul_(keep.repeat_interleave(32, dim=1).to(torch.bfloat16))
+    A = At.t()
+    del keep
+    idx = pit.build_index_from_tensor(A, (32, 1), "k")
+    total = idx.total
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    times = []
+    for _ in range(reps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        pit.build_index_from_tensor(A, (32, 1), "k")
+        e1.record(stream)
+        times.append((e0, e1))
+    torch.cuda.synchronize()
+    ms = statistics.median(a.elapsed_time(b) for a, b in times)
+    nbytes = A.numel() * 2 + 4 * (idx.n_groups + total)
+    gbps = nbytes / (ms * 1e-3) / 1e9
+    del At, A
+    return {"workload": f"build_index_from_tensor, {side}x{side} bf16 column-major, micro (32,1), 90% zero",
+            "ms": round(ms, 4), "bytes": nbytes, "achieved_GBps": round(gbps, 1), "peak_GBps": peaks["hbm"],
+            "frac": round(gbps / peaks["hbm"], 4), "bound": "hbm", "l2": "flushed before each call"}
 
 
 def e2e_ours(args, w, A, B, plan, eff_flops):
@@ -427,6 +467,7 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default=DEFAULT_WORKLOAD)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-index-bench", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--ref-seconds", type=float, default=4.0)
     args = ap.parse_args()

@@ -127,6 +127,63 @@ PIT_API int pit_spmm(const pit_spmm_args* args, void* stream);
 /* 1 if the tcgen05 tensor-core path covers these arguments, else 0 (CUDA-core path). */
 PIT_API int pit_spmm_uses_tensor_cores(const pit_spmm_args* args);
 
+/*
+ * Grouped gathered-row GEMM (batched / per-expert PIT plans). G groups; group g has
+ * counts[g] rows, packed at offsets[g] (offsets[G+1]); tile_offsets[G+1] = prefix of ceil(counts/128).
+ * Row i of group g reads A row row_src[g*src_stride + i] (or offsets[g]+i when row_src is NULL) and
+ * writes C row row_dst[g*dst_stride + i] (or offsets[g]+i), against rows [g*K, (g+1)*K) of the stacked
+ * B [G*K, N]. Epilogue: act (0 none, 1 ReLU) then * row_scale[C row] (if non-NULL). bf16 / fp16 only.
+ */
+typedef struct {
+  int dtype;
+  const void* A;
+  int64_t lda, rows_a;
+  const void* B;
+  int64_t ldb;
+  void* C;
+  int64_t ldc;
+  int64_t N, K, G;
+  const int32_t* counts;
+  const int32_t* offsets;
+  const int32_t* tile_offsets;
+  const int32_t* row_src;
+  int64_t src_stride;
+  const int32_t* row_dst;
+  int64_t dst_stride;
+  const float* row_scale;
+  int act;
+  int64_t max_tiles; /* host upper bound on tile_offsets[G] (e.g. ceil(total_rows/128) + G) */
+} pit_grouped_gemm_args;
+
+PIT_API int pit_grouped_gemm(const pit_grouped_gemm_args* args, void* stream);
+
+/*
+ * MoE routing as a PIT index: top-1 argmax of logits [T, E] (ties -> lowest expert), softmax
+ * probability of the winner as gate[T], expert[T], and the expert -> token index of the one-hot
+ * routing mask (== build_index(from_mask(onehot,(1,1)),(1,1),"m")): counts[E], slots[E*T] ascending.
+ * occ: workspace of E*ceil(T/32) words.
+ */
+PIT_API int pit_moe_route(const void* logits, int dtype, int64_t T, int64_t E, int32_t* expert, float* gate,
+                          uint32_t* occ, int32_t* counts, int32_t* slots, void* stream);
+
+/* offsets[G+1], tile_offsets[G+1] from counts[G]; if perm != NULL also the flattened token order
+ * perm[offsets[g]+i] = slots[g*stride+i] (max_count = an upper bound on any counts[g]). */
+PIT_API int pit_moe_plan(const int32_t* counts, int64_t G, const int32_t* slots, int64_t stride, int32_t* offsets,
+                         int32_t* tile_offsets, int32_t* perm, int64_t max_count, void* stream);
+
+/* Expert-parallel receive plan: rc[W*El] = tokens received from rank r for local expert e (rank-major
+ * receive buffer). rows[e*stride + i] = receive-buffer row of the i-th token of local expert e; counts[El]. */
+PIT_API int pit_moe_recv_plan(const int32_t* rc, int64_t W, int64_t El, int32_t* rows, int64_t stride,
+                              int32_t* counts, void* stream);
+
+/* SRead of whole rows: dst row i = src row rows[i] (row_bytes each; pitches in bytes). */
+PIT_API int pit_gather_rows(const void* src, int64_t ld_src_bytes, const int32_t* rows, int64_t n, int64_t row_bytes,
+                            void* dst, int64_t ld_dst_bytes, void* stream);
+
+/* SWrite of whole rows with a per-destination-row scale (MoE combine): dst[rows[i]] = scale[rows[i]] * src[i]. */
+PIT_API int pit_scatter_rows_scaled(const void* src, int dtype, int64_t ld_src, const int32_t* rows, int64_t n,
+                                    int64_t width, const float* scale, void* dst, int64_t ld_dst, void* stream);
+
 /* f64 verification oracle: C = A @ B with multiply-then-add in ascending k (no FMA), bit-identical to
  * the reference's run_dense_reference (executor.py:267-283). A(i,k) at A + i*s0 + k*s1. */
 PIT_API int pit_dense_reference_f64(const double* A, int64_t s0, int64_t s1, const double* B, int64_t ldb, double* C,

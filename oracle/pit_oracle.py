@@ -271,3 +271,35 @@ def plan_launches(counts, pit_axis, tile_shape, n) -> int:
     M_t, K_t, N_t = tile_shape
     chunk = M_t if pit_axis == "m" else K_t
     return int(np.sum(-(-np.asarray(counts) // chunk))) * cdiv(n, N_t)
+
+
+# ------------------------------------------------------------------------------------- MoE
+def switch_route(logits):
+    """Top-1 routing: expert = argmax (first maximum, like np.argmax), gate = softmax prob of it.
+    The expert -> token index is build_index(from_mask(onehot, (1,1)), (1,1), "m") (index.py:102-173,
+    sparsity.py:95-106): groups = experts, coordinates = tokens ascending."""
+    lg = np.asarray(logits, np.float64)
+    expert = np.argmax(lg, axis=1)
+    mx = lg[np.arange(lg.shape[0]), expert]
+    gate = 1.0 / np.exp(lg - mx[:, None]).sum(axis=1)
+    onehot = np.zeros_like(lg, dtype=bool)
+    onehot[np.arange(lg.shape[0]), expert] = True
+    counts, groups = build_index(*mask_to_ann(onehot, (1, 1)), (1, 1), "m")
+    return expert, gate, counts, groups
+
+
+def switch_forward(x, logits, w1, w2, round_hidden=None):
+    """Switch FFN: out[t] = gate[t] * relu(x[t] @ W1[e]) @ W2[e] in f64, per expert over its token
+    group (SRead rows -> two dense products -> SWrite * gate). `round_hidden` optionally rounds the
+    hidden activations (e.g. to bf16) to mirror a low-precision intermediate."""
+    x = np.asarray(x, np.float64)
+    expert, gate, counts, groups = switch_route(logits)
+    out = np.zeros((x.shape[0], np.asarray(w2).shape[2]))
+    for e, toks in enumerate(groups):
+        if toks.size == 0:
+            continue
+        h = np.maximum(x[toks] @ np.asarray(w1[e], np.float64), 0.0)
+        if round_hidden is not None:
+            h = round_hidden(h)
+        out[toks] = gate[toks, None] * (h @ np.asarray(w2[e], np.float64))
+    return out

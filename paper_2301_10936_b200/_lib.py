@@ -43,6 +43,12 @@ EXPORTS = (
     "pit_spmm",
     "pit_spmm_uses_tensor_cores",
     "pit_dense_reference_f64",
+    "pit_grouped_gemm",
+    "pit_moe_route",
+    "pit_moe_plan",
+    "pit_moe_recv_plan",
+    "pit_gather_rows",
+    "pit_scatter_rows_scaled",
 )
 
 
@@ -77,6 +83,34 @@ class SpmmArgs(C.Structure):
     ]
 
 
+class GroupedGemmArgs(C.Structure):
+    """Mirror of ``pit_grouped_gemm_args``."""
+
+    _fields_ = [
+        ("dtype", C.c_int),
+        ("A", C.c_void_p),
+        ("lda", C.c_int64),
+        ("rows_a", C.c_int64),
+        ("B", C.c_void_p),
+        ("ldb", C.c_int64),
+        ("C", C.c_void_p),
+        ("ldc", C.c_int64),
+        ("N", C.c_int64),
+        ("K", C.c_int64),
+        ("G", C.c_int64),
+        ("counts", C.c_void_p),
+        ("offsets", C.c_void_p),
+        ("tile_offsets", C.c_void_p),
+        ("row_src", C.c_void_p),
+        ("src_stride", C.c_int64),
+        ("row_dst", C.c_void_p),
+        ("dst_stride", C.c_int64),
+        ("row_scale", C.c_void_p),
+        ("act", C.c_int),
+        ("max_tiles", C.c_int64),
+    ]
+
+
 def _declare(lib) -> None:
     i64, i32, vp = C.c_int64, C.c_int, C.c_void_p
     lib.pit_last_error.restype = C.c_char_p
@@ -94,6 +128,12 @@ def _declare(lib) -> None:
     lib.pit_spmm.argtypes = [C.POINTER(SpmmArgs), vp]
     lib.pit_spmm_uses_tensor_cores.argtypes = [C.POINTER(SpmmArgs)]
     lib.pit_dense_reference_f64.argtypes = [vp, i64, i64, vp, i64, vp, i64, i64, i64, vp]
+    lib.pit_grouped_gemm.argtypes = [C.POINTER(GroupedGemmArgs), vp]
+    lib.pit_moe_route.argtypes = [vp, i32, i64, i64, vp, vp, vp, vp, vp, vp]
+    lib.pit_moe_plan.argtypes = [vp, i64, vp, i64, vp, vp, vp, i64, vp]
+    lib.pit_moe_recv_plan.argtypes = [vp, i64, i64, vp, i64, vp, vp]
+    lib.pit_gather_rows.argtypes = [vp, i64, vp, i64, i64, vp, i64, vp]
+    lib.pit_scatter_rows_scaled.argtypes = [vp, i32, i64, vp, i64, i64, vp, vp, i64, vp]
     for name in EXPORTS:
         if name not in ("pit_last_error", "pit_abi_version", "pit_kernel_launches"):
             getattr(lib, name).restype = i32

@@ -75,6 +75,24 @@ CUresult encode_tensor_map_2d(CUtensorMap* map, CUtensorMapDataType dt, const vo
   return r;
 }
 
+CUresult encode_tensor_map_3d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t d0, uint64_t d1,
+                              uint64_t d2, uint64_t pitch1_bytes, uint64_t pitch2_bytes, uint32_t box0, uint32_t box1,
+                              CUtensorMapSwizzle swizzle) {
+  CUtensorMap dummy;
+  if (encode_tensor_map_2d(&dummy, dt, base, d0, d1 > 0 ? d1 : 1, pitch1_bytes, box0, 1, swizzle) != CUDA_SUCCESS)
+    return CUDA_ERROR_INVALID_VALUE;  // resolves the entry point and validates the 2-D part
+  const cuuint64_t dims[3] = {d0, d1, d2};
+  const cuuint64_t strides[2] = {pitch1_bytes, pitch2_bytes};
+  const cuuint32_t box[3] = {box0, box1, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = g_encode(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    fail(kErrCuda, "cuTensorMapEncodeTiled (3-D) failed (%d)", static_cast<int>(r));
+  return r;
+}
+
 }  // namespace pit
 
 using namespace pit;
@@ -289,6 +307,82 @@ int pit_spmm(const pit_spmm_args* p, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (!p->force_simt && spmm_tc_supported(a)) return launch_spmm_tc(a, s);
   return launch_spmm_simt(a, s);
+}
+
+int pit_grouped_gemm(const pit_grouped_gemm_args* a, void* stream) {
+  if (!a) return fail(kErrArg, "null args");
+  if (a->G < 0 || a->N < 0 || a->K <= 0) return fail(kErrShape, "shape mismatch: bad grouped GEMM extents");
+  if (a->G == 0 || a->N == 0 || a->max_tiles == 0) return kOk;
+  if (!a->A || !a->B || !a->C || !a->counts || !a->offsets || !a->tile_offsets)
+    return fail(kErrArg, "null device pointer");
+  GroupedGemmArgs g{};
+  g.dtype = a->dtype;
+  g.A = a->A;
+  g.lda = a->lda;
+  g.rows_a = a->rows_a;
+  g.B = a->B;
+  g.ldb = a->ldb;
+  g.C = a->C;
+  g.ldc = a->ldc;
+  g.N = a->N;
+  g.K = a->K;
+  g.G = a->G;
+  g.counts = a->counts;
+  g.offsets = a->offsets;
+  g.tile_offsets = a->tile_offsets;
+  g.row_src = a->row_src;
+  g.src_stride = a->src_stride;
+  g.row_dst = a->row_dst;
+  g.dst_stride = a->dst_stride;
+  g.row_scale = a->row_scale;
+  g.act = a->act;
+  g.max_tiles = a->max_tiles;
+  const int st = launch_rowgemm(g, static_cast<cudaStream_t>(stream));
+  if (st == kErrUnsupported) return fail(st, "grouped GEMM needs bf16/fp16 with 16-byte aligned rows");
+  return st;
+}
+
+int pit_moe_route(const void* logits, int dtype, int64_t T, int64_t E, int32_t* expert, float* gate, uint32_t* occ,
+                  int32_t* counts, int32_t* slots, void* stream) {
+  if (E <= 0 || T < 0) return fail(kErrShape, "bad routing shape (T=%lld, E=%lld)", (long long)T, (long long)E);
+  if (!logits || !expert || !gate || !occ || !counts || !slots) return fail(kErrArg, "null device pointer");
+  const int st = launch_moe_route(logits, dtype, T, static_cast<int>(E), expert, gate, occ, counts, slots,
+                                  static_cast<cudaStream_t>(stream));
+  if (st == kErrUnsupported) return fail(st, "router logits must be f32, bf16 or f16");
+  return st;
+}
+
+int pit_moe_plan(const int32_t* counts, int64_t G, const int32_t* slots, int64_t stride, int32_t* offsets,
+                 int32_t* tile_offsets, int32_t* perm, int64_t max_count, void* stream) {
+  if (G < 0) return fail(kErrShape, "negative group count");
+  if (!counts || !offsets || !tile_offsets) return fail(kErrArg, "null device pointer");
+  return launch_moe_plan(counts, static_cast<int>(G), slots, stride, offsets, tile_offsets, perm, max_count,
+                         static_cast<cudaStream_t>(stream));
+}
+
+int pit_moe_recv_plan(const int32_t* rc, int64_t W, int64_t El, int32_t* rows, int64_t stride, int32_t* counts,
+                      void* stream) {
+  if (W <= 0 || El <= 0) return fail(kErrShape, "bad expert-parallel geometry");
+  if (!rc || !rows || !counts) return fail(kErrArg, "null device pointer");
+  return launch_moe_recv_plan(rc, static_cast<int>(W), static_cast<int>(El), rows, stride, counts,
+                              static_cast<cudaStream_t>(stream));
+}
+
+int pit_gather_rows(const void* src, int64_t ld_src_bytes, const int32_t* rows, int64_t n, int64_t row_bytes, void* dst,
+                    int64_t ld_dst_bytes, void* stream) {
+  if (n < 0 || row_bytes < 0) return fail(kErrShape, "negative extent");
+  if (n && (!src || !rows || !dst)) return fail(kErrArg, "null device pointer");
+  return launch_gather_rows(src, ld_src_bytes, rows, n, row_bytes, dst, ld_dst_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int pit_scatter_rows_scaled(const void* src, int dtype, int64_t ld_src, const int32_t* rows, int64_t n, int64_t width,
+                            const float* scale, void* dst, int64_t ld_dst, void* stream) {
+  if (n < 0 || width < 0) return fail(kErrShape, "negative extent");
+  if (n && (!src || !rows || !dst)) return fail(kErrArg, "null device pointer");
+  const int st = launch_scatter_rows_scaled(src, dtype, ld_src, rows, n, width, scale, dst, ld_dst,
+                                            static_cast<cudaStream_t>(stream));
+  if (st == kErrUnsupported) return fail(st, "unsupported dtype code %d", dtype);
+  return st;
 }
 
 int pit_dense_reference_f64(const double* A, int64_t s0, int64_t s1, const double* B, int64_t ldb, double* C, int64_t M,

@@ -80,53 +80,57 @@ __global__ void __launch_bounds__(kRaWarps * 32) detect_rows_vec_kernel(const ui
                                                                           int64_t row_bytes, int64_t ld_bytes, int tr,
                                                                           int V, int64_t GR, int64_t GC,
                                                                           LiveMask mk, uint32_t* __restrict__ occ,
-                                                                          int64_t WG) {
+                                                                          int64_t WG, int64_t seg_groups,
+                                                                          int64_t tiles) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int64_t seg = static_cast<int64_t>(blockIdx.x) * kRaWarps + warp;  // 512-byte segment
-  const int64_t vec = seg * 32 + lane;                                     // 16-byte vector index in a row
-  const bool col_ok = vec * 16 < row_bytes;
-  const int64_t i0 = static_cast<int64_t>(blockIdx.y) * 32;  // first micro-row band of the block
-  const int64_t r0 = i0 * tr;
-  const int64_t r1 = min(R, (i0 + 32) * tr);
-  const uint8_t* base = x + vec * 16;
-
   const bool is_start = (lane % V) == 0;
   const uint32_t vmask = V >= 32 ? 0xffffffffu : ((1u << V) - 1u);
-  uint32_t bits = 0;
-  uint4 acc = make_uint4(0, 0, 0, 0);
-  int band_left = tr;
-  int band = 0;
-  for (int64_t r = r0; r < r1; r += 8) {
-    uint4 buf[8];
+  // persistent: tile = (row block of 32 micro-rows, group of kRaWarps 512-byte column segments)
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t rb = tile / seg_groups;
+    const int64_t seg = (tile % seg_groups) * kRaWarps + warp;
+    const int64_t vec = seg * 32 + lane;  // 16-byte vector index in a row
+    const bool col_ok = vec * 16 < row_bytes;
+    const int64_t i0 = rb * 32;  // first micro-row band of the tile
+    const int64_t r0 = i0 * tr;
+    const int64_t r1 = min(R, (i0 + 32) * tr);
+    const uint8_t* base = x + vec * 16;
+    uint32_t bits = 0;
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    int band_left = tr;
+    int band = 0;
+    for (int64_t r = r0; r < r1; r += 8) {
+      uint4 buf[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int64_t rr = r + u;
-      buf[u] = (rr < r1 && col_ok) ? ldg_stream(base + rr * ld_bytes) : make_uint4(0, 0, 0, 0);
-    }
+      for (int u = 0; u < 8; ++u) {
+        const int64_t rr = r + u;
+        buf[u] = (rr < r1 && col_ok) ? ldg_stream(base + rr * ld_bytes) : make_uint4(0, 0, 0, 0);
+      }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      if (r + u >= r1) break;  // warp-uniform
-      acc.x |= buf[u].x & mk.even;
-      acc.y |= buf[u].y & mk.odd;
-      acc.z |= buf[u].z & mk.even;
-      acc.w |= buf[u].w & mk.odd;
-      if (--band_left == 0 || r + u + 1 == r1) {
-        const bool live = (acc.x | acc.y | acc.z | acc.w) != 0;
-        const uint32_t b = __ballot_sync(0xffffffffu, live);
-        if (is_start) {
-          const uint32_t f = V >= 32 ? b : ((b >> lane) & vmask);
-          bits |= (f != 0 ? 1u : 0u) << band;
+      for (int u = 0; u < 8; ++u) {
+        if (r + u >= r1) break;  // warp-uniform
+        acc.x |= buf[u].x & mk.even;
+        acc.y |= buf[u].y & mk.odd;
+        acc.z |= buf[u].z & mk.even;
+        acc.w |= buf[u].w & mk.odd;
+        if (--band_left == 0 || r + u + 1 == r1) {
+          const bool live = (acc.x | acc.y | acc.z | acc.w) != 0;
+          const uint32_t b = __ballot_sync(0xffffffffu, live);
+          if (is_start) {
+            const uint32_t f = V >= 32 ? b : ((b >> lane) & vmask);
+            bits |= (f != 0 ? 1u : 0u) << band;
+          }
+          acc = make_uint4(0, 0, 0, 0);
+          band_left = tr;
+          ++band;
         }
-        acc = make_uint4(0, 0, 0, 0);
-        band_left = tr;
-        ++band;
       }
     }
-  }
-  if (is_start && col_ok) {
-    const int64_t j = vec / V;
-    if (j < GC) occ[j * WG + (i0 >> 5)] = bits;
+    if (is_start && col_ok) {
+      const int64_t j = vec / V;
+      if (j < GC) occ[j * WG + rb] = bits;
+    }
   }
 }
 
@@ -219,17 +223,22 @@ __global__ void detect_bits_kernel(const uint8_t* __restrict__ packed, int64_t s
 // ---------------------------------------------------------------------------
 // Pass 2: per-group ordered compaction. One warp per group.
 // ---------------------------------------------------------------------------
-__global__ void compact_kernel(const uint32_t* __restrict__ occ, int64_t n_groups, int64_t WG,
-                               int32_t* __restrict__ counts, int32_t* __restrict__ slots, int64_t slot_stride) {
-  const int64_t g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (g >= n_groups) return;
+constexpr int kCompactThreads = 256;
+
+// One block per group; thread t owns word t of each 256-word chunk (coordinates stay ascending
+// across threads); block-wide exclusive scan of per-word popcounts gives each thread its slot base.
+__global__ void __launch_bounds__(kCompactThreads) compact_kernel(const uint32_t* __restrict__ occ, int64_t n_groups,
+                                                                  int64_t WG, int32_t* __restrict__ counts,
+                                                                  int32_t* __restrict__ slots, int64_t slot_stride) {
+  __shared__ int warp_tot[kCompactThreads / 32];
+  const int64_t g = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t* row = occ + g * WG;
   int32_t* out = slots + g * slot_stride;
   int base = 0;
-  for (int64_t w0 = 0; w0 < WG; w0 += 32) {
-    const int64_t w = w0 + lane;
-    uint32_t word = w < WG ? row[w] : 0u;
+  for (int64_t w0 = 0; w0 < WG; w0 += kCompactThreads) {
+    const int64_t w = w0 + threadIdx.x;
+    uint32_t word = w < WG ? __ldg(row + w) : 0u;
     const int c = __popc(word);
     int incl = c;
 #pragma unroll
@@ -237,15 +246,25 @@ __global__ void compact_kernel(const uint32_t* __restrict__ occ, int64_t n_group
       const int t = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += t;
     }
-    int pos = base + incl - c;
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    int wbase = 0, total = 0;
+#pragma unroll
+    for (int i = 0; i < kCompactThreads / 32; ++i) {
+      const int v = warp_tot[i];
+      wbase += i < warp ? v : 0;
+      total += v;
+    }
+    int pos = base + wbase + incl - c;
     while (word) {
       const int b = __ffs(word) - 1;
       word &= word - 1;
       out[pos++] = static_cast<int32_t>(w * 32 + b);
     }
-    base += __shfl_sync(0xffffffffu, incl, 31);
+    base += total;
+    __syncthreads();
   }
-  if (lane == 0) counts[g] = base;
+  if (threadIdx.x == 0) counts[g] = base;
 }
 
 // OR of all group rows: the union of live coordinates (used by pit:m union-row tiles).
@@ -295,11 +314,15 @@ int launch_detect_values(const DetectValuesArgs& a, cudaStream_t s) {
                     (static_cast<int64_t>(a.tc) * eb) % 16 == 0;
   if (a.pit_phys == 0 && aligned && pow2) {
     const int64_t segs = ceil_div(row_bytes, 512);
-    dim3 grid(static_cast<unsigned>(ceil_div(segs, kRaWarps)), static_cast<unsigned>(ceil_div(GR, 32)));
-    if (grid.y > 65535u) return kErrShape;
-    detect_rows_vec_kernel<<<grid, kRaWarps * 32, 0, s>>>(static_cast<const uint8_t*>(a.x), a.R, row_bytes,
-                                                          ld_bytes, a.tr, static_cast<int>(vec_per_micro), GR, GC,
-                                                          live_mask_for(a.dtype), a.occ, WG);
+    const int64_t seg_groups = ceil_div(segs, kRaWarps);
+    const int64_t tiles = seg_groups * ceil_div(GR, 32);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t grid = tiles < 4ll * sms ? tiles : 4ll * sms;  // 4 resident CTAs per SM
+    detect_rows_vec_kernel<<<static_cast<unsigned>(grid), kRaWarps * 32, 0, s>>>(
+        static_cast<const uint8_t*>(a.x), a.R, row_bytes, ld_bytes, a.tr, static_cast<int>(vec_per_micro), GR, GC,
+        live_mask_for(a.dtype), a.occ, WG, seg_groups, tiles);
     note_launch();
   } else {
     const int TJ = a.pit_phys == 0 ? 256 : (a.tc >= 8 ? 32 : 128);
@@ -330,9 +353,9 @@ int launch_detect_bits(const DetectBitsArgs& a, cudaStream_t s) {
 int launch_compact(const uint32_t* occ, int64_t n_groups, int64_t WG, int32_t* counts, int32_t* slots,
                    int64_t slot_stride, cudaStream_t s) {
   if (n_groups == 0) return 0;
-  const int threads = 256;
-  compact_kernel<<<static_cast<unsigned>(ceil_div(n_groups * 32, threads)), threads, 0, s>>>(occ, n_groups, WG, counts,
-                                                                                            slots, slot_stride);
+  if (n_groups >= (1ll << 31)) return kErrShape;
+  compact_kernel<<<static_cast<unsigned>(n_groups), kCompactThreads, 0, s>>>(occ, n_groups, WG, counts, slots,
+                                                                            slot_stride);
   note_launch();
   return cuda_status();
 }

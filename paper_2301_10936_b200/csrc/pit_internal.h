@@ -124,9 +124,47 @@ int launch_dense_ref_f64(const double* A, int64_t s0, int64_t s1, const double* 
 int launch_spmm_tc(const SpmmArgs& a, cudaStream_t s);  // bf16 / fp16 tcgen05 paths
 bool spmm_tc_supported(const SpmmArgs& a);
 
+// Grouped gathered-row GEMM (MoE experts, batched per-slice plans): see rowgemm in pit_spmm_tc.cu.
+struct GroupedGemmArgs {
+  int dtype;
+  const void* A;  // row-major [rows_a, K], pitch lda
+  int64_t lda, rows_a;
+  const void* B;  // stacked row-major [G, K, N], pitch ldb
+  int64_t ldb;
+  void* C;        // row-major, pitch ldc
+  int64_t ldc;
+  int64_t N, K, G;
+  const int32_t* counts;        // [G]
+  const int32_t* offsets;       // [G+1]
+  const int32_t* tile_offsets;  // [G+1]
+  const int32_t* row_src;
+  int64_t src_stride;
+  const int32_t* row_dst;
+  int64_t dst_stride;
+  const float* row_scale;
+  int act;
+  int64_t max_tiles;
+};
+int launch_rowgemm(const GroupedGemmArgs& g, cudaStream_t s);
+
+// ------------------------------------------------------------------- MoE dispatch
+int launch_moe_route(const void* logits, int dtype, int64_t T, int E, int32_t* expert, float* gate, uint32_t* occ,
+                     int32_t* counts, int32_t* slots, cudaStream_t s);
+int launch_moe_plan(const int32_t* counts, int G, const int32_t* slots, int64_t stride, int32_t* offsets,
+                    int32_t* tile_offsets, int32_t* perm, int64_t max_count, cudaStream_t s);
+int launch_moe_recv_plan(const int32_t* rc, int W, int El, int32_t* rows, int64_t stride, int32_t* counts,
+                         cudaStream_t s);
+int launch_gather_rows(const void* src, int64_t ld_src_bytes, const int32_t* rows, int64_t n, int64_t row_bytes,
+                       void* dst, int64_t ld_dst_bytes, cudaStream_t s);
+int launch_scatter_rows_scaled(const void* src, int dtype, int64_t ld_src, const int32_t* rows, int64_t n,
+                               int64_t width, const float* scale, void* dst, int64_t ld_dst, cudaStream_t s);
+
 // Driver entry point for cuTensorMapEncodeTiled (resolved through the runtime, no -lcuda).
 CUresult encode_tensor_map_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner,
                               uint64_t outer, uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_outer,
+                              CUtensorMapSwizzle swizzle);
+CUresult encode_tensor_map_3d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t d0, uint64_t d1,
+                              uint64_t d2, uint64_t pitch1_bytes, uint64_t pitch2_bytes, uint32_t box0, uint32_t box1,
                               CUtensorMapSwizzle swizzle);
 
 }  // namespace pit

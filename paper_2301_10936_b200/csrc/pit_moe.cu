@@ -1,0 +1,309 @@
+// MoE dispatch built from the PIT primitives: the routing mask is a
+// [T, E] one-hot whose PIT index (groups = experts, coordinates = tokens, ascending) is exactly
+// build_index(from_mask(onehot, (1,1)), (1,1), "m") (index.py:102-173). It is produced directly
+// from the router logits (top-1 argmax + softmax gate) into the K1 occupancy bitmap, then compacted
+// by K1's ordered compaction. Pack (SRead of token rows), the expert GEMMs (grouped rowgemm) and the
+// gate-scaled combine (SWrite) consume that index.
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "pit_internal.h"
+
+namespace pit {
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ float as_float(T v);
+template <>
+__device__ __forceinline__ float as_float<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ float as_float<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <>
+__device__ __forceinline__ float as_float<__half>(__half v) { return __half2float(v); }
+
+// One warp per token: argmax over E logits (ties -> lowest expert, like np.argmax), softmax
+// probability of the winner as the gate, and the token's bit in the expert's occupancy row.
+template <typename T>
+__global__ void route_kernel(const T* __restrict__ logits, int64_t T_, int E, int32_t* __restrict__ expert,
+                             float* __restrict__ gate, uint32_t* __restrict__ occ, int64_t WG) {
+  const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= T_) return;
+  const T* row = logits + t * E;
+  float best = -INFINITY;
+  int arg = E;
+  for (int e = lane; e < E; e += 32) {
+    const float v = as_float<T>(row[e]);
+    if (v > best || (v == best && e < arg)) {
+      best = v;
+      arg = e;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+    if (ob > best || (ob == best && oa < arg)) {
+      best = ob;
+      arg = oa;
+    }
+  }
+  float sum = 0.f;
+  for (int e = lane; e < E; e += 32) sum += __expf(as_float<T>(row[e]) - best);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if (lane == 0) {
+    expert[t] = arg;
+    gate[t] = 1.0f / sum;
+    atomicOr(&occ[static_cast<int64_t>(arg) * WG + (t >> 5)], 1u << (t & 31));
+  }
+}
+
+// Single block: exclusive prefix of counts and of ceil(counts / 128) (row tiles of the grouped GEMM).
+__global__ void plan_kernel(const int32_t* __restrict__ counts, int G, int32_t* __restrict__ offsets,
+                            int32_t* __restrict__ tile_offsets) {
+  __shared__ int32_t s_off, s_tile;
+  if (threadIdx.x == 0) {
+    s_off = 0;
+    s_tile = 0;
+  }
+  __syncthreads();
+  for (int g0 = 0; g0 < G; g0 += blockDim.x) {
+    const int g = g0 + threadIdx.x;
+    const int c = g < G ? counts[g] : 0;
+    const int tl = (c + 127) / 128;
+    // block-wide inclusive scan of (c, tl)
+    __shared__ int32_t sc[1024], st[1024];
+    sc[threadIdx.x] = c;
+    st[threadIdx.x] = tl;
+    __syncthreads();
+    for (int o = 1; o < blockDim.x; o <<= 1) {
+      const int vc = threadIdx.x >= o ? sc[threadIdx.x - o] : 0;
+      const int vt = threadIdx.x >= o ? st[threadIdx.x - o] : 0;
+      __syncthreads();
+      sc[threadIdx.x] += vc;
+      st[threadIdx.x] += vt;
+      __syncthreads();
+    }
+    if (g < G) {
+      offsets[g] = s_off + sc[threadIdx.x] - c;
+      tile_offsets[g] = s_tile + st[threadIdx.x] - tl;
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) {
+      s_off += sc[threadIdx.x];
+      s_tile += st[threadIdx.x];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    offsets[G] = s_off;
+    tile_offsets[G] = s_tile;
+  }
+}
+
+// perm[offsets[g] + i] = slots[g * stride + i]: the expert-sorted token order, flattened.
+__global__ void flatten_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ offsets,
+                               const int32_t* __restrict__ slots, int64_t stride, int32_t* __restrict__ perm) {
+  const int g = blockIdx.y;
+  const int c = counts[g];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x)
+    perm[offsets[g] + i] = slots[static_cast<int64_t>(g) * stride + i];
+}
+
+// Receive-side plan for expert parallelism: tokens from source rank r for local expert e sit at
+// recv rows base_r + sum_{e' < e} rc[r][e'] + j. rows[e * stride + i] lists them in source-rank order.
+__global__ void recv_rows_kernel(const int32_t* __restrict__ rc, int W, int El, int32_t* __restrict__ rows,
+                                 int64_t stride) {
+  const int e = blockIdx.y;
+  // rank bases and the within-rank offset of expert e (W, El small: recomputed per block)
+  int out = 0;
+  int base = 0;
+  for (int r = 0; r < W; ++r) {
+    int before = 0, tot = 0;
+    for (int x = 0; x < El; ++x) {
+      const int v = rc[r * El + x];
+      before += x < e ? v : 0;
+      tot += v;
+    }
+    const int n = rc[r * El + e];
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+      rows[static_cast<int64_t>(e) * stride + out + j] = base + before + j;
+    out += n;
+    base += tot;
+  }
+}
+
+__global__ void recv_counts_kernel(const int32_t* __restrict__ rc, int W, int El, int32_t* __restrict__ counts) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= El) return;
+  int c = 0;
+  for (int r = 0; r < W; ++r) c += rc[r * El + e];
+  counts[e] = c;
+}
+
+// dst[i] = src[rows[i]] (SRead of whole rows): 16-byte vectors when aligned.
+__global__ void gather_rows_kernel(const uint8_t* __restrict__ src, int64_t ld_src, const int32_t* __restrict__ rows,
+                                   int64_t n, int64_t row_bytes, uint8_t* __restrict__ dst, int64_t ld_dst, int vec) {
+  const int64_t i = blockIdx.y * static_cast<int64_t>(gridDim.z) + blockIdx.z;
+  if (i >= n) return;
+  const uint8_t* s = src + static_cast<int64_t>(rows[i]) * ld_src;
+  uint8_t* d = dst + i * ld_dst;
+  if (vec) {
+    for (int64_t c = (blockIdx.x * blockDim.x + threadIdx.x) * 16; c < row_bytes; c += gridDim.x * blockDim.x * 16)
+      *reinterpret_cast<uint4*>(d + c) = __ldg(reinterpret_cast<const uint4*>(s + c));
+  } else {
+    for (int64_t c = blockIdx.x * blockDim.x + threadIdx.x; c < row_bytes; c += gridDim.x * blockDim.x) d[c] = s[c];
+  }
+}
+
+// dst[rows[i]] = scale[rows[i]] * src[i] (SWrite with the router gate), bf16/fp16/fp32 rows.
+template <typename T>
+__global__ void scatter_rows_scaled_kernel(const T* __restrict__ src, int64_t ld_src, const int32_t* __restrict__ rows,
+                                           int64_t n, int64_t width, const float* __restrict__ scale,
+                                           T* __restrict__ dst, int64_t ld_dst);
+
+template <>
+__global__ void scatter_rows_scaled_kernel<__nv_bfloat16>(const __nv_bfloat16* __restrict__ src, int64_t ld_src,
+                                                          const int32_t* __restrict__ rows, int64_t n, int64_t width,
+                                                          const float* __restrict__ scale,
+                                                          __nv_bfloat16* __restrict__ dst, int64_t ld_dst) {
+  const int64_t i = blockIdx.y * static_cast<int64_t>(gridDim.z) + blockIdx.z;
+  if (i >= n) return;
+  const int r = rows[i];
+  const float sc = scale ? scale[r] : 1.0f;
+  for (int64_t c = blockIdx.x * blockDim.x + threadIdx.x; c < width; c += gridDim.x * blockDim.x)
+    dst[static_cast<int64_t>(r) * ld_dst + c] = __float2bfloat16_rn(sc * __bfloat162float(src[i * ld_src + c]));
+}
+
+template <>
+__global__ void scatter_rows_scaled_kernel<__half>(const __half* __restrict__ src, int64_t ld_src,
+                                                   const int32_t* __restrict__ rows, int64_t n, int64_t width,
+                                                   const float* __restrict__ scale, __half* __restrict__ dst,
+                                                   int64_t ld_dst) {
+  const int64_t i = blockIdx.y * static_cast<int64_t>(gridDim.z) + blockIdx.z;
+  if (i >= n) return;
+  const int r = rows[i];
+  const float sc = scale ? scale[r] : 1.0f;
+  for (int64_t c = blockIdx.x * blockDim.x + threadIdx.x; c < width; c += gridDim.x * blockDim.x)
+    dst[static_cast<int64_t>(r) * ld_dst + c] = __float2half_rn(sc * __half2float(src[i * ld_src + c]));
+}
+
+template <>
+__global__ void scatter_rows_scaled_kernel<float>(const float* __restrict__ src, int64_t ld_src,
+                                                  const int32_t* __restrict__ rows, int64_t n, int64_t width,
+                                                  const float* __restrict__ scale, float* __restrict__ dst,
+                                                  int64_t ld_dst) {
+  const int64_t i = blockIdx.y * static_cast<int64_t>(gridDim.z) + blockIdx.z;
+  if (i >= n) return;
+  const int r = rows[i];
+  const float sc = scale ? scale[r] : 1.0f;
+  for (int64_t c = blockIdx.x * blockDim.x + threadIdx.x; c < width; c += gridDim.x * blockDim.x)
+    dst[static_cast<int64_t>(r) * ld_dst + c] = sc * src[i * ld_src + c];
+}
+
+dim3 row_grid(int64_t n, int64_t width_units, int threads) {
+  // y*z covers n rows (z <= 65535), x covers the row
+  const int64_t z = n < 65535 ? (n > 0 ? n : 1) : 65535;
+  const int64_t y = (n + z - 1) / z;
+  const int64_t x = (width_units + threads - 1) / threads;
+  return dim3(static_cast<unsigned>(x < 8 ? (x > 0 ? x : 1) : 8), static_cast<unsigned>(y > 0 ? y : 1),
+              static_cast<unsigned>(z));
+}
+
+}  // namespace
+
+int launch_moe_route(const void* logits, int dtype, int64_t T_, int E, int32_t* expert, float* gate, uint32_t* occ,
+                     int32_t* counts, int32_t* slots, cudaStream_t s) {
+  const int64_t WG = ceil_div(T_, 32);
+  if (cudaMemsetAsync(occ, 0, sizeof(uint32_t) * E * WG, s) != cudaSuccess) return cuda_status();
+  if (T_ > 0) {
+    const unsigned grid = static_cast<unsigned>(ceil_div(T_ * 32, 256));
+    switch (dtype) {
+      case kDtypeF32:
+        route_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(logits), T_, E, expert, gate, occ, WG);
+        break;
+      case kDtypeBF16:
+        route_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(logits), T_, E, expert,
+                                                         gate, occ, WG);
+        break;
+      case kDtypeF16:
+        route_kernel<__half><<<grid, 256, 0, s>>>(static_cast<const __half*>(logits), T_, E, expert, gate, occ, WG);
+        break;
+      default:
+        return kErrUnsupported;
+    }
+    note_launch();
+    if (int st = cuda_status()) return st;
+  }
+  return launch_compact(occ, E, WG, counts, slots, T_, s);
+}
+
+int launch_moe_plan(const int32_t* counts, int G, const int32_t* slots, int64_t stride, int32_t* offsets,
+                    int32_t* tile_offsets, int32_t* perm, int64_t max_count, cudaStream_t s) {
+  plan_kernel<<<1, 1024, 0, s>>>(counts, G, offsets, tile_offsets);
+  note_launch();
+  if (int st = cuda_status()) return st;
+  if (perm && slots && G > 0 && max_count > 0) {
+    dim3 grid(static_cast<unsigned>(ceil_div(max_count, 256) < 64 ? ceil_div(max_count, 256) : 64),
+              static_cast<unsigned>(G));
+    flatten_kernel<<<grid, 256, 0, s>>>(counts, offsets, slots, stride, perm);
+    note_launch();
+    return cuda_status();
+  }
+  return kOk;
+}
+
+int launch_moe_recv_plan(const int32_t* rc, int W, int El, int32_t* rows, int64_t stride, int32_t* counts,
+                         cudaStream_t s) {
+  recv_counts_kernel<<<static_cast<unsigned>(ceil_div(El, 128)), 128, 0, s>>>(rc, W, El, counts);
+  note_launch();
+  if (int st = cuda_status()) return st;
+  dim3 grid(static_cast<unsigned>(ceil_div(stride, 256) < 32 ? (ceil_div(stride, 256) > 0 ? ceil_div(stride, 256) : 1)
+                                                               : 32),
+            static_cast<unsigned>(El));
+  recv_rows_kernel<<<grid, 256, 0, s>>>(rc, W, El, rows, stride);
+  note_launch();
+  return cuda_status();
+}
+
+int launch_gather_rows(const void* src, int64_t ld_src_bytes, const int32_t* rows, int64_t n, int64_t row_bytes,
+                       void* dst, int64_t ld_dst_bytes, cudaStream_t s) {
+  if (n == 0 || row_bytes == 0) return kOk;
+  const int vec = (reinterpret_cast<uintptr_t>(src) % 16 == 0) && (reinterpret_cast<uintptr_t>(dst) % 16 == 0) &&
+                  ld_src_bytes % 16 == 0 && ld_dst_bytes % 16 == 0 && row_bytes % 16 == 0;
+  const dim3 grid = row_grid(n, vec ? row_bytes / 16 : row_bytes, 128);
+  gather_rows_kernel<<<grid, 128, 0, s>>>(static_cast<const uint8_t*>(src), ld_src_bytes, rows, n, row_bytes,
+                                          static_cast<uint8_t*>(dst), ld_dst_bytes, vec);
+  note_launch();
+  return cuda_status();
+}
+
+int launch_scatter_rows_scaled(const void* src, int dtype, int64_t ld_src, const int32_t* rows, int64_t n,
+                               int64_t width, const float* scale, void* dst, int64_t ld_dst, cudaStream_t s) {
+  if (n == 0 || width == 0) return kOk;
+  const dim3 grid = row_grid(n, width, 128);
+  switch (dtype) {
+    case kDtypeBF16:
+      scatter_rows_scaled_kernel<__nv_bfloat16><<<grid, 128, 0, s>>>(
+          static_cast<const __nv_bfloat16*>(src), ld_src, rows, n, width, scale, static_cast<__nv_bfloat16*>(dst), ld_dst);
+      break;
+    case kDtypeF16:
+      scatter_rows_scaled_kernel<__half><<<grid, 128, 0, s>>>(static_cast<const __half*>(src), ld_src, rows, n, width,
+                                                              scale, static_cast<__half*>(dst), ld_dst);
+      break;
+    case kDtypeF32:
+      scatter_rows_scaled_kernel<float><<<grid, 128, 0, s>>>(static_cast<const float*>(src), ld_src, rows, n, width,
+                                                             scale, static_cast<float*>(dst), ld_dst);
+      break;
+    default:
+      return kErrUnsupported;
+  }
+  note_launch();
+  return cuda_status();
+}
+
+}  // namespace pit

@@ -392,8 +392,40 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // =============================================================================================
-// spmm_gm: PIT axis m (union-row tiles) and the dense plan.
+// rowgemm ("gathered M"): PIT axis m, the dense plan, and grouped / MoE expert GEMMs.
+//
+// G groups; group g owns rows_g rows, tiled 128 at a time. Row i of group g reads A row
+//   src(g,i) = row_src ? row_src[g*src_stride + i] : off[g] + i
+// and writes C row
+//   dst(g,i) = row_dst ? row_dst[g*dst_stride + i] : off[g] + i,
+// against B_g = rows [g*K, (g+1)*K) of a stacked [G*K, N] matrix (3-D tensor map, so K tails stay
+// inside the group). Optional per-(row, K-block) liveness (pit:m occupancy bitmap, G == 1) zero-fills
+// dead rows and skips K-blocks with no live row. Epilogue: optional ReLU, optional per-C-row scale.
+// With G == 1 and off == nullptr the row count comes from *n_rows (pit:m union) or is M (dense).
 // =============================================================================================
+struct RowGemmParams {
+  const void* A;
+  int64_t lda;
+  void* C;
+  int64_t ldc;
+  int M, N, K;  // M: rows of A (bounds) ; N, K: GEMM extents per group
+  int G;
+  const int32_t* cnt;       // [G] rows per group (nullptr: single group, see n_rows)
+  const int32_t* off;       // [G+1] packed row offsets
+  const int32_t* tile_off;  // [G+1] prefix of ceil(cnt/128)
+  const int32_t* n_rows;    // single group: device row count (nullptr: dense, M rows)
+  const int32_t* row_src;
+  int64_t src_stride;
+  const int32_t* row_dst;
+  int64_t dst_stride;
+  const float* row_scale;   // indexed by C row
+  int act;                  // 0 none, 1 relu
+  const uint32_t* occ;      // liveness bitmap (G == 1) or nullptr
+  int64_t WG;
+  int t1;
+  int max_tiles;            // host bound on the total number of row tiles
+};
+
 template <int KS>
 struct GmCfg {
   static constexpr int BM = 128;
@@ -408,12 +440,41 @@ struct GmCfg {
   static constexpr uint32_t A_SW = sw_layout_for_row(A_ROW_BYTES);
 };
 
+struct RowTile {
+  int g, base, rows;  // group, packed offset of the tile's first row, rows in the tile (<= 128)
+};
+
+// Decode row tile t (global index) -> group and rows. Identical in every role.
+__device__ __forceinline__ RowTile decode_tile(const RowGemmParams& p, int t, int single_rows) {
+  if (p.cnt == nullptr) {
+    const int base = t * 128;
+    return {0, base, min(128, single_rows - base)};
+  }
+  int lo = 0, hi = p.G;  // last g with tile_off[g] <= t
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(p.tile_off + mid) <= t) lo = mid; else hi = mid;
+  }
+  const int rt = t - __ldg(p.tile_off + lo);
+  const int start = rt * 128;
+  return {lo, __ldg(p.off + lo) + start, min(128, __ldg(p.cnt + lo) - start)};
+}
+
+__device__ __forceinline__ int tile_src_row(const RowGemmParams& p, const RowTile& rt, int i) {
+  if (p.row_src == nullptr) return rt.base + i;
+  const int within = rt.base - (p.cnt ? __ldg(p.off + rt.g) : 0) + i;
+  return __ldg(p.row_src + static_cast<int64_t>(rt.g) * p.src_stride + within);
+}
+
+__device__ __forceinline__ int tile_dst_row(const RowGemmParams& p, const RowTile& rt, int i) {
+  if (p.row_dst == nullptr) return rt.base + i;
+  const int within = rt.base - (p.cnt ? __ldg(p.off + rt.g) : 0) + i;
+  return __ldg(p.row_dst + static_cast<int64_t>(rt.g) * p.dst_stride + within);
+}
+
 template <int KS, bool kBF16>
 __global__ void __launch_bounds__(kThreads, 1)
-    spmm_gm_kernel(const void* __restrict__ Av, int64_t lda, const __grid_constant__ CUtensorMap tmB,
-                   const int32_t* __restrict__ rows, const int32_t* __restrict__ n_rows_dev, int dense,
-                   const uint32_t* __restrict__ occ, int64_t WG, int t1, int row_tiles, int n_tiles, int M, int N,
-                   int K, void* __restrict__ Cv, int64_t ldc) {
+    rowgemm_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ RowGemmParams p, int n_tiles) {
   using Cfg = GmCfg<KS>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -426,7 +487,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int n_rows = dense ? M : *n_rows_dev;
+  const int single_rows = p.cnt ? 0 : (p.n_rows ? *p.n_rows : p.M);
+  const int total_tiles = p.cnt ? __ldg(p.tile_off + p.G) : (single_rows + 127) / 128;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < Cfg::STAGES; ++i) {
@@ -446,47 +508,45 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int live_tiles = (n_rows + Cfg::BM - 1) / Cfg::BM;
-  const int units = min(row_tiles, live_tiles) * n_tiles;
-  const int kblocks = (K + KS - 1) / KS;
+  const int units = min(p.max_tiles, total_tiles) * n_tiles;
+  const int kblocks = (p.K + KS - 1) / KS;
 
   if (warp < kProdWarps) {
     // ------------------------------------------------------------ producers
-    // A rows: cp.async 16-byte chunks by the 128 producer threads into the K-major swizzled layout;
-    // a row that is not live in this K-block is zero-filled (src size 0). B: plain 2-D TMA tiles.
+    // A rows: cp.async 16-byte chunks into the K-major swizzled layout; a row that is not live in
+    // this K-block is zero-filled (src size 0). B: 2-D boxes of the 3-D [G, K, N] tensor map.
     // A K-block in which no row of the tile is live is skipped by every role (stage_live = 0).
-    constexpr int CPR = KS * 2 / 16;          // chunks per A row
-    constexpr int RPT = 128 * CPR / kProdThreads;  // rows per producer thread
-    constexpr int RSTEP = kProdThreads / CPR;      // row stride between a thread's rows
+    constexpr int CPR = KS * 2 / 16;                // chunks per A row
+    constexpr int RPT = 128 * CPR / kProdThreads;   // rows per producer thread
+    constexpr int RSTEP = kProdThreads / CPR;       // row stride between a thread's rows
     constexpr uint32_t MASK = KS * 2 == 128 ? 7 : KS * 2 == 64 ? 3 : 1;
-    const int tp = threadIdx.x;               // 0..kProdThreads-1
+    const int tp = threadIdx.x;  // 0..kProdThreads-1
     const int ch = tp % CPR;
     using T = typename OutT<kBF16>::T;
-    const T* Ap = static_cast<const T*>(Av);
+    const T* Ap = static_cast<const T*>(p.A);
     int stage = 0;
     uint32_t phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int rt = u / n_tiles;
+      const RowTile rt = decode_tile(p, u / n_tiles, single_rows);
       const int n0 = (u % n_tiles) * Cfg::BN;
       int rid[RPT];  // this thread's rows: tp / CPR + j * RSTEP
 #pragma unroll
       for (int j = 0; j < RPT; ++j) {
-        const int i = rt * Cfg::BM + tp / CPR + j * RSTEP;
-        rid[j] = (i < n_rows) ? (dense ? i : __ldg(rows + i)) : -1;
+        const int i = tp / CPR + j * RSTEP;
+        rid[j] = i < rt.rows ? tile_src_row(p, rt, i) : -1;
       }
       for (int kb = 0; kb < kblocks; ++kb) {
         const int k0 = kb * KS;
-        const int grp = dense ? 0 : k0 / t1;
         bool live[RPT];
         bool any = false;
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
           live[j] = rid[j] >= 0;
-          if (live[j] && !dense)
-            live[j] = (__ldg(occ + static_cast<int64_t>(grp) * WG + (rid[j] >> 5)) >> (rid[j] & 31)) & 1u;
+          if (live[j] && p.occ)
+            live[j] = (__ldg(p.occ + static_cast<int64_t>(k0 / p.t1) * p.WG + (rid[j] >> 5)) >> (rid[j] & 31)) & 1u;
           any |= live[j];
         }
-        const bool stage_any = bar_or(1, kProdThreads, any);
+        const bool stage_any = p.occ ? bar_or(1, kProdThreads, any) : true;
         mbar_wait(&empty_bar[stage], phase ^ 1);
         uint8_t* sAp = smem + stage * Cfg::STAGE_BYTES;
         const uint32_t sA = smem_u32(sAp);
@@ -497,18 +557,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_expect_tx_only(&full_bar[stage], Cfg::B_BYTES);
 #pragma unroll
             for (int a = 0; a < Cfg::BN / 64; ++a)
-              tma_load_2d(sB + a * KS * 128, &tmB, &full_bar[stage], n0 + a * 64, k0);
+              tma_load_3d(sB + a * KS * 128, &tmB, &full_bar[stage], n0 + a * 64, k0, rt.g);
           }
           mbar_arrive(&full_bar[stage]);  // publishes stage_live
         }
         if (stage_any) {
           const int kc = k0 + ch * 8;
-          const uint32_t kbytes = kc < K ? static_cast<uint32_t>(min(16, (K - kc) * 2)) : 0u;
+          const uint32_t kbytes = kc < p.K ? static_cast<uint32_t>(min(16, (p.K - kc) * 2)) : 0u;
 #pragma unroll
           for (int j = 0; j < RPT; ++j) {
             const int row = tp / CPR + j * RSTEP;
             const uint32_t bytes = live[j] ? kbytes : 0u;
-            const T* src = bytes ? Ap + static_cast<int64_t>(rid[j]) * lda + kc : Ap;
+            const T* src = bytes ? Ap + static_cast<int64_t>(rid[j]) * p.lda + kc : Ap;
             cp_async_16(sA + swz<MASK>(static_cast<uint32_t>(row * Cfg::A_ROW_BYTES + ch * 16)), src, bytes);
           }
           cp_async_arrive_noinc(&full_bar[stage]);
@@ -563,41 +623,50 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (acc == 0) acc_phase ^= 1;
     }
   } else if (warp >= kEpiWarp0) {
-    // ------------------------------------------------------------ epilogue: row scatter
+    // ------------------------------------------------------------ epilogue: row scatter (SWrite)
     const int q = warp & 3;
+    const bool vec_ok = (p.ldc % 8) == 0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int rt = u / n_tiles;
+      const RowTile rt = decode_tile(p, u / n_tiles, single_rows);
       const int n0 = (u % n_tiles) * Cfg::BN;
-      const int i = rt * Cfg::BM + q * 32 + lane;
-      const int row = (i < n_rows) ? (dense ? i : rows[i]) : -1;
+      const int i = q * 32 + lane;
+      const int row = i < rt.rows ? tile_dst_row(p, rt, i) : -1;
+      const float scale = (row >= 0 && p.row_scale) ? __ldg(p.row_scale + row) : 1.0f;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
-      uint8_t* crow = row >= 0 ? static_cast<uint8_t*>(Cv) + (static_cast<int64_t>(row) * ldc) * 2 : nullptr;
+      uint8_t* crow = row >= 0 ? static_cast<uint8_t*>(p.C) + (static_cast<int64_t>(row) * p.ldc) * 2 : nullptr;
 #pragma unroll 1
       for (int c = 0; c < Cfg::BN; c += 32) {
         uint32_t v[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * Cfg::BN + c), v);
         tmem_wait_ld();
         if (row >= 0) {
+          float f[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float x = __uint_as_float(v[j]);
+            if (p.act == 1) x = fmaxf(x, 0.0f);
+            f[j] = x * scale;
+          }
           const int nb = n0 + c;
-          if (nb + 32 <= N && (ldc % 8) == 0) {
+          if (nb + 32 <= p.N && vec_ok) {
             uint4* dst = reinterpret_cast<uint4*>(crow + static_cast<int64_t>(nb) * 2);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               uint4 w;
-              w.x = pack2(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]), kBF16);
-              w.y = pack2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]), kBF16);
-              w.z = pack2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]), kBF16);
-              w.w = pack2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]), kBF16);
+              w.x = pack2(f[8 * j + 0], f[8 * j + 1], kBF16);
+              w.y = pack2(f[8 * j + 2], f[8 * j + 3], kBF16);
+              w.z = pack2(f[8 * j + 4], f[8 * j + 5], kBF16);
+              w.w = pack2(f[8 * j + 6], f[8 * j + 7], kBF16);
               dst[j] = w;
             }
           } else {
             using T = typename OutT<kBF16>::T;
             T* dst = reinterpret_cast<T*>(crow);
             for (int j = 0; j < 32; ++j)
-              if (nb + j < N) dst[nb + j] = OutT<kBF16>::cvt(__uint_as_float(v[j]));
+              if (nb + j < p.N) dst[nb + j] = OutT<kBF16>::cvt(f[j]);
           }
         }
       }
@@ -654,31 +723,58 @@ int run_gk(const SpmmArgs& a, cudaStream_t s) {
 }
 
 template <int KS, bool kBF16>
-int run_gm(const SpmmArgs& a, cudaStream_t s) {
+int run_rowgemm(const RowGemmParams& p, const void* B, int64_t ldb, cudaStream_t s) {
   using Cfg = GmCfg<KS>;
   const CUtensorMapDataType dt = kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tmB;
-  // B: row-major [K, N], tile box {64 n, KS k}
-  if (encode_tensor_map_2d(&tmB, dt, a.B, a.N, a.K, a.ldb * 2, 64, KS, CU_TENSOR_MAP_SWIZZLE_128B) != CUDA_SUCCESS)
+  // B: stacked [G, K, N] (row-major per group, pitch ldb), box {64 n, KS k, 1 group}
+  if (encode_tensor_map_3d(&tmB, dt, B, p.N, p.K, p.G, ldb * 2, static_cast<uint64_t>(ldb) * 2 * p.K, 64, KS,
+                           CU_TENSOR_MAP_SWIZZLE_128B) != CUDA_SUCCESS)
     return kErrCuda;
+  const int n_tiles = static_cast<int>(ceil_div(p.N, Cfg::BN));
+  const int64_t units = static_cast<int64_t>(p.max_tiles) * n_tiles;
+  if (units == 0) return kOk;
+  if (units >= (1ll << 31)) return kErrShape;
+  auto kern = rowgemm_kernel<KS, kBF16>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::SMEM));
+  const int grid = static_cast<int>(units < num_sms() ? units : num_sms());
+  kern<<<grid, kThreads, Cfg::SMEM, s>>>(tmB, p, n_tiles);
+  note_launch();
+  return cuda_status();
+}
+
+template <bool kBF16>
+int rowgemm_dispatch(const RowGemmParams& p, const void* B, int64_t ldb, int ks, cudaStream_t s) {
+  if (ks == 64) return run_rowgemm<64, kBF16>(p, B, ldb, s);
+  if (ks == 32) return run_rowgemm<32, kBF16>(p, B, ldb, s);
+  if (ks == 16) return run_rowgemm<16, kBF16>(p, B, ldb, s);
+  return kErrUnsupported;
+}
+
+template <bool kBF16>
+int run_gm(const SpmmArgs& a, int ks, cudaStream_t s) {
   const int dense = a.plan == kPlanDense ? 1 : 0;
   if (!dense) {
     // rows named by no group stay exactly zero
     if (cudaMemset2DAsync(a.C, a.ldc * 2, 0, a.N * 2, a.M, s) != cudaSuccess) return cuda_status();
   }
-  const int64_t rows_bound = dense ? a.M : a.n_rows_host;
-  const int row_tiles = static_cast<int>(ceil_div(rows_bound, Cfg::BM));
-  const int n_tiles = static_cast<int>(ceil_div(a.N, Cfg::BN));
-  const int64_t units = static_cast<int64_t>(row_tiles) * n_tiles;
-  if (units == 0) return kOk;
-  auto kern = spmm_gm_kernel<KS, kBF16>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::SMEM));
-  const int grid = static_cast<int>(units < num_sms() ? units : num_sms());
-  kern<<<grid, kThreads, Cfg::SMEM, s>>>(a.A, a.sam, tmB, a.rows, a.n_rows, dense, a.occ, a.WG, a.t1, row_tiles, n_tiles,
-                                         static_cast<int>(a.M), static_cast<int>(a.N), static_cast<int>(a.K), a.C,
-                                         a.ldc);
-  note_launch();
-  return cuda_status();
+  RowGemmParams p{};
+  p.A = a.A;
+  p.lda = a.sam;
+  p.C = a.C;
+  p.ldc = a.ldc;
+  p.M = static_cast<int>(a.M);
+  p.N = static_cast<int>(a.N);
+  p.K = static_cast<int>(a.K);
+  p.G = 1;
+  p.n_rows = dense ? nullptr : a.n_rows;
+  p.row_src = dense ? nullptr : a.rows;
+  p.row_dst = dense ? nullptr : a.rows;
+  p.occ = dense ? nullptr : a.occ;
+  p.WG = a.WG;
+  p.t1 = dense ? 1 : a.t1;
+  p.max_tiles = static_cast<int>(ceil_div(dense ? a.M : a.n_rows_host, 128));
+  return rowgemm_dispatch<kBF16>(p, a.B, a.ldb, ks, s);
 }
 
 template <bool kBF16>
@@ -700,9 +796,9 @@ int dispatch_tc(const SpmmArgs& a, cudaStream_t s) {
     }
   }
   const int t1 = a.plan == kPlanDense ? 64 : a.t1;
-  if (t1 % 64 == 0) return run_gm<64, kBF16>(a, s);
-  if (t1 == 32) return run_gm<32, kBF16>(a, s);
-  if (t1 == 16) return run_gm<16, kBF16>(a, s);
+  if (t1 % 64 == 0) return run_gm<kBF16>(a, 64, s);
+  if (t1 == 32) return run_gm<kBF16>(a, 32, s);
+  if (t1 == 16) return run_gm<kBF16>(a, 16, s);
   return kErrUnsupported;
 }
 
@@ -722,6 +818,34 @@ bool spmm_tc_supported(const SpmmArgs& a) {
   if (a.sak != 1 || (a.sam * 2) % 16) return false;  // A row-major
   if (a.plan == kPlanDense) return true;
   return a.t1 % 64 == 0 || a.t1 == 32 || a.t1 == 16;
+}
+
+int launch_rowgemm(const GroupedGemmArgs& g, cudaStream_t s) {
+  if (g.dtype != kDtypeBF16 && g.dtype != kDtypeF16) return kErrUnsupported;
+  if (reinterpret_cast<uintptr_t>(g.A) % 16 || reinterpret_cast<uintptr_t>(g.B) % 16) return kErrUnsupported;
+  if ((g.lda * 2) % 16 || (g.ldb * 2) % 16) return kErrUnsupported;
+  RowGemmParams p{};
+  p.A = g.A;
+  p.lda = g.lda;
+  p.C = g.C;
+  p.ldc = g.ldc;
+  p.M = static_cast<int>(g.rows_a);
+  p.N = static_cast<int>(g.N);
+  p.K = static_cast<int>(g.K);
+  p.G = static_cast<int>(g.G);
+  p.cnt = g.counts;
+  p.off = g.offsets;
+  p.tile_off = g.tile_offsets;
+  p.row_src = g.row_src;
+  p.src_stride = g.src_stride;
+  p.row_dst = g.row_dst;
+  p.dst_stride = g.dst_stride;
+  p.row_scale = g.row_scale;
+  p.act = g.act;
+  p.t1 = 1;
+  p.max_tiles = static_cast<int>(g.max_tiles);
+  const int ks = g.K % 64 == 0 || g.K > 64 ? 64 : g.K % 32 == 0 ? 32 : 16;
+  return g.dtype == kDtypeBF16 ? rowgemm_dispatch<true>(p, g.B, g.ldb, ks, s) : rowgemm_dispatch<false>(p, g.B, g.ldb, ks, s);
 }
 
 int launch_spmm_tc(const SpmmArgs& a, cudaStream_t s) {

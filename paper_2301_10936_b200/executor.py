@@ -388,9 +388,8 @@ def spmm_device(plan: SparseKernelPlan, Ad, Bd, idx: Optional[MicroTileIndex], o
         a.n_groups = idx.n_groups
         a.slot_stride = idx.pit_grid
         if plan.pit_axis == "k":
-            counts, slots = idx.device_arrays()
-            keep += [counts, slots]
-            a.counts, a.slots = counts.data_ptr(), slots.data_ptr()
+            a.counts, a.slots, alive = idx.device_ptrs()
+            keep += list(alive)
         else:
             occ = idx.occupancy_words()
             rows, n_rows = idx.union_coords()

@@ -58,21 +58,44 @@ def _geometry(shape, micro, dim) -> tuple[int, int, int]:
 class MicroTileIndex:
     """Per group (position along the non-PIT micro grid), the live PIT-axis micro coordinates."""
 
-    def __init__(self, micro_tile, pit_axis, pit_dim, pit_grid, n_groups, *, shape=None, counts_dev=None,
-                 slots_dev=None, occ_dev=None, counts=None, slots=None):
+    def __init__(self, micro_tile, pit_axis, pit_dim, pit_grid, n_groups, *, shape=None, buf=None, counts=None,
+                 slots=None):
         self.micro_tile = tuple(micro_tile)
         self.pit_axis = pit_axis
         self.pit_dim = pit_dim
         self.pit_grid = int(pit_grid)
         self._n_groups = int(n_groups)
         self.shape = shape  # operand shape the index was built for (None if unknown)
-        self._counts_dev = counts_dev
-        self._slots_dev = slots_dev
-        self._occ_dev = occ_dev
+        # device storage: one int32 buffer = counts [n_groups] | slots [n_groups*pit_grid] | occ [n_groups*WG]
+        self._buf = buf
+        self._occ_valid = buf is not None
         self._union = None
         self._counts = counts
         self._slots = slots
         self._host_authoritative = counts is not None
+
+    @property
+    def words_per_group(self) -> int:
+        return -(-self.pit_grid // 32)
+
+    def _ptrs(self):
+        base = self._buf.data_ptr()
+        ng, pg = self._n_groups, self.pit_grid
+        return base, base + 4 * ng, base + 4 * (ng + ng * pg)
+
+    @property
+    def _counts_dev(self):
+        return self._buf[: self._n_groups]
+
+    @property
+    def _slots_dev(self):
+        ng, pg = self._n_groups, self.pit_grid
+        return self._buf[ng : ng + ng * pg].view(ng, pg)
+
+    @property
+    def _occ_dev(self):
+        ng, pg = self._n_groups, self.pit_grid
+        return self._buf[ng + ng * pg :].view(ng, self.words_per_group)
 
     # ------------------------------------------------------------------ host view
     @property
@@ -118,11 +141,19 @@ class MicroTileIndex:
             return counts, slots
         return self._counts_dev, self._slots_dev
 
+    def device_ptrs(self):
+        """(counts, slots) device pointers plus the tensors keeping them alive."""
+        if self._host_authoritative:
+            c, sl = self.device_arrays()
+            return c.data_ptr(), sl.data_ptr(), (c, sl)
+        pc, ps, _ = self._ptrs()
+        return pc, ps, (self._buf,)
+
     def occupancy_words(self):
         """Group-major occupancy bitmap (int32 storage of uint32 words) on the device."""
         import torch
 
-        if self._occ_dev is not None and not self._host_authoritative:
+        if self._occ_valid and not self._host_authoritative:
             return self._occ_dev
         dev = _device.require_cuda()
         counts, slots = self.device_arrays()
@@ -136,8 +167,6 @@ class MicroTileIndex:
             from .executor import ExecError
 
             raise ExecError("micro-tile coordinate out of range")
-        if not self._host_authoritative:
-            self._occ_dev = occ
         return occ
 
     def union_coords(self):
@@ -170,11 +199,8 @@ def _empty_index(micro, axis, dim, shape):
 
     dev = _device.require_cuda()
     n_groups, pit_grid, wg = _geometry(shape, micro, dim)
-    counts = torch.empty(n_groups, dtype=torch.int32, device=dev)
-    slots = torch.empty((n_groups, pit_grid), dtype=torch.int32, device=dev)
-    occ = torch.empty((n_groups, wg), dtype=torch.int32, device=dev)
-    return MicroTileIndex(micro, axis, dim, pit_grid, n_groups, shape=tuple(shape), counts_dev=counts,
-                          slots_dev=slots, occ_dev=occ)
+    buf = torch.empty(n_groups * (1 + pit_grid + wg), dtype=torch.int32, device=dev)
+    return MicroTileIndex(micro, axis, dim, pit_grid, n_groups, shape=tuple(shape), buf=buf)
 
 
 def _axis_name(pit_axis, dim) -> str:
@@ -193,13 +219,13 @@ def build_index(ann: SparsityAnnotation, micro_tile, pit_axis: Union[str, int], 
         raise IndexBuildError("workers must be >= 1")
     dim = _pit_dim(pit_axis)
     idx = _empty_index(micro, _axis_name(pit_axis, dim), dim, ann.tensor_shape)
-    packed = torch.from_numpy(np.ascontiguousarray(ann.packed, dtype=np.uint8)).to(idx._counts_dev.device)
+    packed = torch.from_numpy(np.ascontiguousarray(ann.packed, dtype=np.uint8)).to(idx._buf.device)
     lib = _lib.load()
     s0, s1 = ann.tensor_shape
     g0, g1 = ann.granularity
-    _device.check(lib.pit_build_index(packed.data_ptr(), s0, s1, g0, g1, micro[0], micro[1], dim,
-                                      idx._occ_dev.data_ptr(), idx._counts_dev.data_ptr(),
-                                      idx._slots_dev.data_ptr(), _device.stream_ptr()), IndexBuildError)
+    pc, ps, po = idx._ptrs()
+    _device.check(lib.pit_build_index(packed.data_ptr(), s0, s1, g0, g1, micro[0], micro[1], dim, po, pc, ps,
+                                      _device.stream_ptr()), IndexBuildError)
     return idx
 
 
@@ -229,10 +255,9 @@ def build_index_from_tensor(values, micro_tile, pit_axis: Union[str, int], worke
         st0, st1 = x.stride()
     idx = _empty_index(micro, _axis_name(pit_axis, dim), dim, (s0, s1))
     lib = _lib.load()
+    pc, ps, po = idx._ptrs()
     _device.check(lib.pit_build_index_from_tensor(x.data_ptr(), _device.dtype_code(x), s0, s1, st0, st1, micro[0],
-                                                  micro[1], dim, idx._occ_dev.data_ptr(),
-                                                  idx._counts_dev.data_ptr(), idx._slots_dev.data_ptr(),
-                                                  _device.stream_ptr()), IndexBuildError)
+                                                  micro[1], dim, po, pc, ps, _device.stream_ptr()), IndexBuildError)
     return idx
 
 

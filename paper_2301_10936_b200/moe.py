@@ -1,0 +1,210 @@
+"""Switch-style MoE layer (top-1, dropless) on the PIT path, with expert parallelism.
+
+PIT's view of an MoE layer: the router produces a [T, E]
+one-hot mask whose PIT index (groups = experts, coordinates = tokens) is built online; the expert
+FFNs are per-expert gathered-row GEMMs (SRead of the token rows fused into the mainloop), and the
+combine is an SWrite scaled by the gate. No capacity padding: every token is computed once.
+
+Expert parallelism over W ranks (rank r owns experts [r*E/W, (r+1)*E/W)):
+  route -> plan -> pack (SRead by expert order) -> all_to_all(counts) -> all_to_all(tokens)
+  -> receive plan -> FFN1 (ReLU) -> FFN2 -> all_to_all(back) -> combine (SWrite * gate)
+The orchestration is written against a backend: `CudaBackend` (libpit_b200.so kernels) is the
+product; the exchange logic is backend-agnostic so it can be exercised over gloo in tests.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+from . import _device, _lib
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+class CudaBackend:
+    """Device kernels for the MoE path (all tensors on the current CUDA device)."""
+
+    def __init__(self):
+        self.lib = _lib.load()
+
+    def _stream(self):
+        return _device.stream_ptr()
+
+    def route(self, logits):
+        torch = _torch()
+        T, E = logits.shape
+        dev = logits.device
+        expert = torch.empty(T, dtype=torch.int32, device=dev)
+        gate = torch.empty(T, dtype=torch.float32, device=dev)
+        occ = torch.empty(E * max(1, -(-T // 32)), dtype=torch.int32, device=dev)
+        counts = torch.empty(E, dtype=torch.int32, device=dev)
+        slots = torch.empty((E, max(T, 1)), dtype=torch.int32, device=dev)
+        logits = logits.contiguous()
+        _device.check(self.lib.pit_moe_route(logits.data_ptr(), _device.dtype_code(logits), T, E, expert.data_ptr(),
+                                             gate.data_ptr(), occ.data_ptr(), counts.data_ptr(), slots.data_ptr(),
+                                             self._stream()))
+        return expert, gate, counts, slots
+
+    def plan(self, counts, slots=None, stride=0, total=0):
+        torch = _torch()
+        G = counts.numel()
+        dev = counts.device
+        offsets = torch.empty(G + 1, dtype=torch.int32, device=dev)
+        tiles = torch.empty(G + 1, dtype=torch.int32, device=dev)
+        perm = torch.empty(max(total, 1), dtype=torch.int32, device=dev) if slots is not None else None
+        _device.check(self.lib.pit_moe_plan(counts.data_ptr(), G, slots.data_ptr() if slots is not None else None,
+                                            stride, offsets.data_ptr(), tiles.data_ptr(),
+                                            perm.data_ptr() if perm is not None else None, max(total, 1),
+                                            self._stream()))
+        return offsets, tiles, perm
+
+    def recv_plan(self, rc, R):
+        torch = _torch()
+        W, El = rc.shape
+        rows = torch.empty((El, max(R, 1)), dtype=torch.int32, device=rc.device)
+        counts = torch.empty(El, dtype=torch.int32, device=rc.device)
+        rc = rc.to(torch.int32).contiguous()
+        _device.check(self.lib.pit_moe_recv_plan(rc.data_ptr(), W, El, rows.data_ptr(), max(R, 1), counts.data_ptr(),
+                                                 self._stream()))
+        return rows, counts
+
+    def gather_rows(self, src, rows, n):
+        torch = _torch()
+        out = torch.empty((n, src.shape[1]), dtype=src.dtype, device=src.device)
+        eb = src.element_size()
+        _device.check(self.lib.pit_gather_rows(src.data_ptr(), src.stride(0) * eb, rows.data_ptr(), n,
+                                               src.shape[1] * eb, out.data_ptr(), out.stride(0) * eb, self._stream()))
+        return out
+
+    def scatter_rows_scaled(self, src, rows, n, scale, out):
+        _device.check(self.lib.pit_scatter_rows_scaled(src.data_ptr(), _device.dtype_code(src), src.stride(0),
+                                                       rows.data_ptr(), n, src.shape[1],
+                                                       scale.data_ptr() if scale is not None else None,
+                                                       out.data_ptr(), out.stride(0), self._stream()))
+        return out
+
+    def grouped_gemm(self, A, W, counts, offsets, tiles, out, *, row_src=None, src_stride=0, row_dst=None,
+                     dst_stride=0, row_scale=None, act=0, max_tiles=None):
+        G, K, N = W.shape
+        a = _lib.GroupedGemmArgs()
+        a.dtype = _device.dtype_code(A)
+        a.A, a.lda, a.rows_a = A.data_ptr(), A.stride(0), A.shape[0]
+        a.B, a.ldb = W.data_ptr(), W.stride(1)
+        a.C, a.ldc = out.data_ptr(), out.stride(0)
+        a.N, a.K, a.G = N, K, G
+        a.counts, a.offsets, a.tile_offsets = counts.data_ptr(), offsets.data_ptr(), tiles.data_ptr()
+        a.row_src = row_src.data_ptr() if row_src is not None else None
+        a.src_stride = src_stride
+        a.row_dst = row_dst.data_ptr() if row_dst is not None else None
+        a.dst_stride = dst_stride
+        a.row_scale = row_scale.data_ptr() if row_scale is not None else None
+        a.act = act
+        a.max_tiles = max_tiles if max_tiles is not None else -(-A.shape[0] // 128) + G
+        _device.check(self.lib.pit_grouped_gemm(C.byref(a), self._stream()))
+        return out
+
+
+@dataclass
+class MoEStats:
+    tokens: int = 0
+    sent: int = 0
+    received: int = 0
+
+
+class SwitchMoE:
+    """Top-1 Switch FFN layer: out[t] = gate[t] * W2_e(relu(W1_e x[t])), e = argmax(logits[t]).
+
+    w1: [E_local, d_model, d_ff], w2: [E_local, d_ff, d_model] (bf16/fp16, the rank's experts).
+    With a process group of W ranks, E = W * E_local and tokens are exchanged with all-to-all.
+    """
+
+    def __init__(self, w1, w2, n_experts: int, group=None, backend=None):
+        torch = _torch()
+        self.w1 = w1.contiguous()
+        self.w2 = w2.contiguous()
+        self.E = int(n_experts)
+        self.El = int(w1.shape[0])
+        self.d_model = int(w1.shape[1])
+        self.d_ff = int(w1.shape[2])
+        self.group = group
+        if group is not None:
+            import torch.distributed as dist
+
+            self.world = dist.get_world_size(group)
+            self.rank = dist.get_rank(group)
+        else:
+            self.world, self.rank = 1, 0
+        if self.El * self.world != self.E:
+            raise ValueError(f"{self.E} experts do not split over {self.world} ranks of {self.El}")
+        if tuple(w2.shape) != (self.El, self.d_ff, self.d_model):
+            raise ValueError(f"w2 shape {tuple(w2.shape)} does not match w1 {tuple(w1.shape)}")
+        self.backend = backend if backend is not None else CudaBackend()
+        self.stats = MoEStats()
+        self._torch = torch
+
+    # --------------------------------------------------------------------------- forward
+    def forward(self, x, logits):
+        if self.world == 1:
+            return self._forward_local(x, logits)
+        return self._forward_ep(x, logits)
+
+    __call__ = forward
+
+    def _forward_local(self, x, logits):
+        torch = self._torch
+        be = self.backend
+        T = x.shape[0]
+        expert, gate, counts, slots = be.route(logits)
+        offsets, tiles, _ = be.plan(counts)
+        h = torch.empty((T, self.d_ff), dtype=x.dtype, device=x.device)
+        be.grouped_gemm(x, self.w1, counts, offsets, tiles, h, row_src=slots, src_stride=slots.shape[1], act=1)
+        out = torch.empty((T, self.d_model), dtype=x.dtype, device=x.device)
+        be.grouped_gemm(h, self.w2, counts, offsets, tiles, out, row_dst=slots, dst_stride=slots.shape[1],
+                        row_scale=gate)
+        self.stats = MoEStats(tokens=T, sent=0, received=T)
+        return out
+
+    def _forward_ep(self, x, logits):
+        import torch.distributed as dist
+
+        torch = self._torch
+        be = self.backend
+        W, El, E = self.world, self.El, self.E
+        T = x.shape[0]
+        expert, gate, counts, slots = be.route(logits)
+        offsets, _, perm = be.plan(counts, slots, slots.shape[1], T)
+        send = be.gather_rows(x, perm, T)  # SRead: tokens in expert (= destination rank) order
+        recv_counts = torch.empty(W * El, dtype=torch.int32, device=counts.device)
+        dist.all_to_all_single(recv_counts, counts, group=self.group)
+        # split sizes are host-side arguments of all-to-all-v: one small D2H for both directions
+        both = torch.cat([offsets[::El], recv_counts.view(W, El).sum(dim=1, dtype=torch.int32)]).cpu().tolist()
+        send_off = both[: W + 1]
+        send_splits = [send_off[r + 1] - send_off[r] for r in range(W)]
+        recv_splits = both[W + 1 :]
+        R = sum(recv_splits)
+        recv = torch.empty((R, self.d_model), dtype=x.dtype, device=x.device)
+        dist.all_to_all_single(recv, send, recv_splits, send_splits, group=self.group)
+        rows, lcounts = be.recv_plan(recv_counts.view(W, El), R)
+        loff, ltiles, _ = be.plan(lcounts)
+        h = torch.empty((R, self.d_ff), dtype=x.dtype, device=x.device)
+        y = torch.empty((R, self.d_model), dtype=x.dtype, device=x.device)
+        if R:
+            be.grouped_gemm(recv, self.w1, lcounts, loff, ltiles, h, row_src=rows, src_stride=rows.shape[1], act=1)
+            be.grouped_gemm(h, self.w2, lcounts, loff, ltiles, y, row_dst=rows, dst_stride=rows.shape[1])
+        back = torch.empty((T, self.d_model), dtype=x.dtype, device=x.device)
+        dist.all_to_all_single(back, y, send_splits, recv_splits, group=self.group)
+        out = torch.empty((T, self.d_model), dtype=x.dtype, device=x.device)
+        be.scatter_rows_scaled(back, perm, T, gate, out)  # SWrite * gate back to token order
+        self.stats = MoEStats(tokens=T, sent=T, received=R)
+        return out
+
+
+def switch_flops(tokens: int, d_model: int, d_ff: int) -> float:
+    """Expert FFN FLOPs of a top-1 layer: two GEMMs per token."""
+    return 4.0 * tokens * d_model * d_ff
