@@ -281,6 +281,11 @@ def run_ours(args, w):
 
     if not args.no_index_bench:
         result["index_build"] = index_build_bench(dev, peaks)
+    if not args.no_moe:
+        try:
+            result["moe"] = moe_bench(args, world, rank, dev, peaks)
+        except Exception as e:  # never lose the headline line to the secondary workload
+            result["moe"] = {"error": f"{type(e).__name__}: {e}"[:300]}
 
     # ---- end to end through the public API with host buffers
     if rank == 0 and not args.no_e2e:
@@ -290,6 +295,56 @@ def run_ours(args, w):
     if world > 1:
         dist.destroy_process_group()
     return result if rank == 0 else None
+
+
+def moe_bench(args, world, rank, dev, peaks, tokens_per_gpu=16384, n_experts=128, d_model=768, d_ff=3072):
+    """C5: Switch-base-128 MoE layer (top-1, dropless), tokens sharded per GPU (weak scaling), experts
+    sharded over ranks (expert parallelism, NCCL all-to-all) when world > 1. Synthetic activations,
+    Gaussian router logits (imbalanced top-1), random bf16 expert weights. Layer time = route + index +
+    pack + all-to-all + FFN1(ReLU) + FFN2 + all-to-all + combine (router GEMM excluded). Max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2301_10936_b200 import _lib
+    from paper_2301_10936_b200.moe import SwitchMoE, switch_flops
+
+    E, El = n_experts, n_experts // world
+    g = torch.Generator(device=dev).manual_seed(7 + rank)
+    x = torch.randn((tokens_per_gpu, d_model), device=dev, dtype=torch.bfloat16, generator=g)
+    logits = torch.randn((tokens_per_gpu, E), device=dev, dtype=torch.float32, generator=g)
+    w1 = (torch.randn((El, d_model, d_ff), device=dev, generator=g) / d_model ** 0.5).to(torch.bfloat16)
+    w2 = (torch.randn((El, d_ff, d_model), device=dev, generator=g) / d_ff ** 0.5).to(torch.bfloat16)
+    layer = SwitchMoE(w1, w2, E, group=dist.group.WORLD if world > 1 else None)
+    for _ in range(max(3, args.warmup)):
+        layer(x, logits)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    stream = torch.cuda.current_stream()
+    launches0 = _lib.kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(5, args.steps)
+    e0.record(stream)
+    for _ in range(steps):
+        layer(x, logits)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    received = layer.stats.received
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    toks = world * tokens_per_gpu / (ms * 1e-3)
+    flops = switch_flops(world * tokens_per_gpu, d_model, d_ff) / (ms * 1e-3) / 1e12
+    return {"metric": "MoE layer tokens/s", "value": round(toks, 1), "unit": "tokens/s", "n_gpus": world,
+            "ms_per_layer": round(ms, 4), "expert_tflops_per_gpu": round(flops / world, 2),
+            "frac_bf16_peak": round(flops / world / peaks["bf16"], 4),
+            "config": {"experts": E, "experts_per_gpu": El, "d_model": d_model, "d_ff": d_ff,
+                       "tokens_per_gpu": tokens_per_gpu, "routing": "top-1 argmax, Gaussian logits, dropless",
+                       "parallelism": f"ep{world}" if world > 1 else "single GPU", "received_rank0": int(received)},
+            "gpu_launches_per_layer": (_lib.kernel_launches() - launches0) // steps}
 
 
 def index_build_bench(dev, peaks, side=16384, reps=20):
@@ -468,6 +523,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-index-bench", action="store_true")
+    ap.add_argument("--no-moe", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--ref-seconds", type=float, default=4.0)
     args = ap.parse_args()
