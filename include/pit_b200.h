@@ -184,6 +184,11 @@ PIT_API int pit_gather_rows(const void* src, int64_t ld_src_bytes, const int32_t
 PIT_API int pit_scatter_rows_scaled(const void* src, int dtype, int64_t ld_src, const int32_t* rows, int64_t n,
                                     int64_t width, const float* scale, void* dst, int64_t ld_dst, void* stream);
 
+/* Pitched host<->device copy on the caller's stream (cudaMemcpy2DAsync, direction inferred): moves
+ * column slabs of row-major operands for the pipelined host-buffer path. */
+PIT_API int pit_copy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width_bytes,
+                             int64_t height, void* stream);
+
 /* f64 verification oracle: C = A @ B with multiply-then-add in ascending k (no FMA), bit-identical to
  * the reference's run_dense_reference (executor.py:267-283). A(i,k) at A + i*s0 + k*s1. */
 PIT_API int pit_dense_reference_f64(const double* A, int64_t s0, int64_t s1, const double* B, int64_t ldb, double* C,

@@ -49,6 +49,7 @@ EXPORTS = (
     "pit_moe_recv_plan",
     "pit_gather_rows",
     "pit_scatter_rows_scaled",
+    "pit_copy2d_async",
 )
 
 
@@ -134,6 +135,7 @@ def _declare(lib) -> None:
     lib.pit_moe_recv_plan.argtypes = [vp, i64, i64, vp, i64, vp, vp]
     lib.pit_gather_rows.argtypes = [vp, i64, vp, i64, i64, vp, i64, vp]
     lib.pit_scatter_rows_scaled.argtypes = [vp, i32, i64, vp, i64, i64, vp, vp, i64, vp]
+    lib.pit_copy2d_async.argtypes = [vp, i64, vp, i64, i64, i64, vp]
     for name in EXPORTS:
         if name not in ("pit_last_error", "pit_abi_version", "pit_kernel_launches"):
             getattr(lib, name).restype = i32

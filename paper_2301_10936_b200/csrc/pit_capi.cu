@@ -385,6 +385,16 @@ int pit_scatter_rows_scaled(const void* src, int dtype, int64_t ld_src, const in
   return st;
 }
 
+int pit_copy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width_bytes, int64_t height,
+                     void* stream) {
+  if (width_bytes < 0 || height < 0) return fail(kErrShape, "negative extent");
+  if (width_bytes == 0 || height == 0) return kOk;
+  if (cudaMemcpy2DAsync(dst, dpitch, src, spitch, width_bytes, height, cudaMemcpyDefault,
+                        static_cast<cudaStream_t>(stream)) != cudaSuccess)
+    return cuda_status();
+  return kOk;
+}
+
 int pit_dense_reference_f64(const double* A, int64_t s0, int64_t s1, const double* B, int64_t ldb, double* C, int64_t M,
                             int64_t N, int64_t K, void* stream) {
   if (M < 0 || N < 0 || K < 0) return fail(kErrShape, "shape mismatch: negative extent");

@@ -364,8 +364,8 @@ def spmm_device(plan: SparseKernelPlan, Ad, Bd, idx: Optional[MicroTileIndex], o
     dev = _device.require_cuda()
     M, K = int(Ad.shape[0]), int(Ad.shape[1])
     N = int(Bd.shape[1])
-    if _torch_layout(Bd) != ROW_MAJOR or (Bd.stride(0) * Bd.element_size()) % 16:
-        Bd = Bd.contiguous()
+    if (Bd.stride(1) != 1 and N > 1) or (Bd.stride(0) * Bd.element_size()) % 16:
+        Bd = Bd.contiguous()  # pitched row-major views (column slabs) are used as they are
     C_ = out if out is not None else torch.empty((M, N), dtype=Ad.dtype, device=dev)
     a = _lib.SpmmArgs()
     a.plan = _PLAN_CODE["dense" if plan.is_dense else plan.pit_axis]
@@ -430,17 +430,77 @@ def run_matmul_with_index(
         want_groups = -(-A.shape[1 - dim] // t[1 - dim])
         if idx.n_groups != want_groups:
             raise ExecError(f"index has {idx.n_groups} groups, operand needs {want_groups}")
-    host = not A.is_device
-    Ad = _device.to_device(A.array)
-    Bd = _device.to_device(B.array)
-    Cd = spmm_device(plan, Ad, Bd, idx)
+    host = not (A.is_device and B.is_device)
+    if host and _pipelined_ok(A, B):
+        Cres = _run_host_pipelined(plan, A, B, idx)
+    else:
+        Ad = _device.to_device(A.array)
+        Bd = _device.to_device(B.array)
+        Cd = spmm_device(plan, Ad, Bd, idx)
+        Cres = _device.to_host(Cd) if host else Cd
     if stats is not None:
         if plan.is_dense:
             stats.launches += dense_launches(plan)
         else:
             stats.launches += launches_from_counts(plan, idx.counts)
             stats.gathered_micro_tiles += idx.total
-    return DenseTensor(_device.to_host(Cd) if host else Cd)
+    return DenseTensor(Cres)
+
+
+# host-buffer path: B column slabs upload, per-slab SpMM and C slab download run on three streams
+_PIPE_MIN_BYTES = 32 << 20
+_pipe_streams = {}
+
+
+def _pipelined_ok(A: DenseTensor, B: DenseTensor) -> bool:
+    """Large host-resident B (pinned torch tensor): overlap PCIe with compute."""
+    b = B.array
+    return (_is_torch(b) and not b.is_cuda and b.is_pinned() and _torch_layout(b) == ROW_MAJOR
+            and b.numel() * b.element_size() >= _PIPE_MIN_BYTES and b.shape[1] >= 1024)
+
+
+def _run_host_pipelined(plan: SparseKernelPlan, A: DenseTensor, B: DenseTensor, idx):
+    torch = _torch()
+    dev = _device.require_cuda()
+    lib = _lib.load()
+    main = torch.cuda.current_stream()
+    if dev.index not in _pipe_streams:
+        _pipe_streams[dev.index] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+    s_up, s_down = _pipe_streams[dev.index]
+    Ad = _device.to_device(A.array)
+    Bh = B.array
+    K, N = Bh.shape
+    M = Ad.shape[0]
+    eb = Bh.element_size()
+    Bd = torch.empty((K, N), dtype=Bh.dtype, device=dev)
+    Cd = torch.empty((M, N), dtype=Bh.dtype, device=dev)
+    Ch = torch.empty((M, N), dtype=Bh.dtype, pin_memory=True)
+    slab = max(1024, -(-(-(-N // 8)) // 256) * 256)
+    up_done = []
+    s_up.wait_stream(main)
+    for j0 in range(0, N, slab):
+        w = min(slab, N - j0)
+        with torch.cuda.stream(s_up):
+            _device.check(lib.pit_copy2d_async(Bd.data_ptr() + j0 * eb, N * eb, Bh.data_ptr() + j0 * eb, N * eb,
+                                               w * eb, K, s_up.cuda_stream))
+            ev = torch.cuda.Event()
+            ev.record(s_up)
+        up_done.append((j0, w, ev))
+    for j0, w, ev in up_done:
+        main.wait_event(ev)
+        spmm_device(plan, Ad, Bd[:, j0 : j0 + w], idx, out=Cd[:, j0 : j0 + w])
+        ev_c = torch.cuda.Event()
+        ev_c.record(main)
+        s_down.wait_event(ev_c)
+        with torch.cuda.stream(s_down):
+            _device.check(lib.pit_copy2d_async(Ch.data_ptr() + j0 * eb, N * eb, Cd.data_ptr() + j0 * eb, N * eb,
+                                               w * eb, M, s_down.cuda_stream))
+    main.wait_stream(s_down)
+    for t in (Bd, Cd):
+        t.record_stream(s_up)
+        t.record_stream(s_down)
+    main.synchronize()
+    return Ch
 
 
 def run_sparse_matmul(
