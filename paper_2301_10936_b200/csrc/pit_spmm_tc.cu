@@ -22,6 +22,7 @@
 //    up front), which keeps the reference's exact-zero guarantee (executor.py:8-9).
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -81,9 +82,9 @@ __host__ __device__ constexpr uint32_t tmem_cols_pow2() {
 // Both operands are MN-major 128B-swizzled gathers of k rows; only descriptors and the epilogue
 // differ between orientations.
 // =============================================================================================
-template <int GW, bool kOrientN>
+template <int GW, bool kOrientN, int kKS = 64>
 struct GkCfg {
-  static constexpr int KS = 64;  // gathered k per stage
+  static constexpr int KS = kKS;  // gathered k per stage
   static constexpr int N_TILE = (kOrientN || GW < 256) ? 256 : 128;
   static constexpr int B_ATOMS = N_TILE / 64;
   static constexpr int A_ROW_BYTES = GW * 2 < 128 ? GW * 2 : 128;  // bytes per smem row of the A^T strip
@@ -91,7 +92,7 @@ struct GkCfg {
   static constexpr int B_BYTES = B_ATOMS * KS * 128;
   static constexpr int A_BYTES = A_ATOMS * KS * A_ROW_BYTES;
   static constexpr int STAGE_BYTES = ((B_BYTES + A_BYTES + 1023) / 1024) * 1024;
-  static constexpr int STAGES = (216 * 1024) / STAGE_BYTES > 8 ? 8 : (216 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES = (216 * 1024) / STAGE_BYTES > 16 ? 16 : (216 * 1024) / STAGE_BYTES;
   static constexpr int ACC_COLS = kOrientN ? N_TILE : (N_TILE / 128) * GW;  // TMEM columns per buffer
   static constexpr int TMEM_COLS = tmem_cols_pow2<2 * ACC_COLS>();
   static constexpr size_t SMEM = static_cast<size_t>(STAGES) * STAGE_BYTES + 1024 + 256;
@@ -103,12 +104,12 @@ struct GkCfg {
   static constexpr int A_RPW = 32 / A_CPR;       // A rows covered by one warp instruction
 };
 
-template <int GW, bool kOrientN, bool kBF16>
+template <int GW, bool kOrientN, bool kBF16, int kKS>
 __global__ void __launch_bounds__(kThreads, 1)
     spmm_gk_kernel(const void* __restrict__ Bv, int64_t ldb, const void* __restrict__ Atv, int64_t lda,
                    const int32_t* __restrict__ counts, const int32_t* __restrict__ slots, int64_t slot_stride,
                    int n_groups, int n_tiles, int M, int N, int K, void* __restrict__ Cv, int64_t ldc) {
-  using Cfg = GkCfg<GW, kOrientN>;
+  using Cfg = GkCfg<GW, kOrientN, kKS>;
   using OT = OutT<kBF16>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -153,33 +154,56 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Stage positions (unit, chunk start, unit count) in this CTA's order; indices are loaded two
     // stages ahead of their use so the L2 latency of the slot loads never stalls issue.
     struct Pos {
-      int u, kb, cnt;
+      int u, g, t, kb, cnt;  // unit, its group and n tile (tracked without division), chunk, count
+    };
+    const int step_t = static_cast<int>(gridDim.x) / n_groups;
+    const int step_g = static_cast<int>(gridDim.x) % n_groups;
+    auto next_unit = [&](Pos& q) {
+      q.u += gridDim.x;
+      q.g += step_g;
+      q.t += step_t;
+      if (q.g >= n_groups) {
+        q.g -= n_groups;
+        ++q.t;
+      }
     };
     auto advance = [&](Pos p) {
-      Pos q{p.u, p.kb + Cfg::KS, p.cnt};
+      Pos q = p;
+      q.kb = p.kb + Cfg::KS;
       if (q.kb >= p.cnt) {
         q.kb = 0;
         do {
-          q.u += gridDim.x;
-          q.cnt = q.u < units ? __ldg(counts + q.u % n_groups) : 0;
+          next_unit(q);
+          q.cnt = q.u < units ? __ldg(counts + q.g) : 0;
         } while (q.u < units && q.cnt == 0);
       }
       return q;
     };
-    auto load_idx = [&](const Pos& p, int& x0, int& x1) {
-      x0 = x1 = 0;
-      if (p.u < units) {
-        const int32_t* ps = slots + static_cast<int64_t>(p.u % n_groups) * slot_stride + p.kb;
-        if (p.kb + lane < p.cnt) x0 = __ldg(ps + lane);
-        if (p.kb + 32 + lane < p.cnt) x1 = __ldg(ps + 32 + lane);
-      }
+    constexpr int NI = Cfg::KS / 32;  // slot indices per lane per stage
+    struct Idx {
+      int v[NI];
     };
-    Pos cur{static_cast<int>(blockIdx.x) - static_cast<int>(gridDim.x), 0, 0};
-    cur = advance(cur);
+    auto load_idx = [&](const Pos& p) {
+      Idx x;
+#pragma unroll
+      for (int q = 0; q < NI; ++q) x.v[q] = 0;
+      if (p.u < units) {
+        const int32_t* ps = slots + static_cast<int64_t>(p.g) * slot_stride + p.kb;
+#pragma unroll
+        for (int q = 0; q < NI; ++q)
+          if (p.kb + 32 * q + lane < p.cnt) x.v[q] = __ldg(ps + 32 * q + lane);
+      }
+      return x;
+    };
+    Pos cur{static_cast<int>(blockIdx.x), static_cast<int>(blockIdx.x) % n_groups,
+            static_cast<int>(blockIdx.x) / n_groups, 0, 0};
+    cur.cnt = cur.u < units ? __ldg(counts + cur.g) : 0;
+    if (cur.u < units && cur.cnt == 0) {
+      cur.kb = Cfg::KS;  // force advance() past the empty unit
+      cur = advance(cur);
+    }
     Pos nxt = advance(cur);
-    int c0, c1, d0, d1;
-    load_idx(cur, c0, c1);
-    load_idx(nxt, d0, d1);
+    Idx ci = load_idx(cur), di = load_idx(nxt);
     using T = typename OT::T;
     const T* Bp = static_cast<const T*>(Bv);
     const T* Ap = static_cast<const T*>(Atv);
@@ -187,11 +211,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lda32 = static_cast<uint32_t>(lda);
     while (cur.u < units) {
       const Pos nn = advance(nxt);
-      int e0, e1;
-      load_idx(nn, e0, e1);
-      const int u = cur.u, kb = cur.kb, cnt = cur.cnt;
-      const int g = u % n_groups;
-      const int n0 = (u / n_groups) * Cfg::N_TILE;
+      const Idx ei = load_idx(nn);
+      const int kb = cur.kb, cnt = cur.cnt;
+      const int g = cur.g;
+      const int n0 = cur.t * Cfg::N_TILE;
       const int m0 = g * GW;
       const int kvalid = min(Cfg::KS, cnt - kb);
       const int kpad = (kvalid + 15) & ~15;
@@ -212,15 +235,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           const T* bcol = Bp + (nbytes ? n : 0);
           // row & 7 == warp for every row this warp copies: one swizzled offset
           const uint32_t base = sB + (ch >> 3) * (Cfg::KS * 128) + warp * 128 + (((ch & 7) ^ warp) << 4);
-          for (int i2 = 0; i2 < niter; ++i2) {
-            const int src = i2 < 2 ? c0 : c1;
+          // slot block q (32 rows) holds rows warp + 32q + {0, 8, 16, 24}: i2 = 2q + (0|1), j = 0|1
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              const int row = warp + 16 * i2 + 8 * j;
-              const int k = __shfl_sync(0xffffffffu, src, row & 31);
-              if (Cfg::B_CPR >= 32 || ch < Cfg::B_CPR)
-                cp_async_16(base + (2 * i2 + j) * (kProdWarps * 128), bcol + static_cast<uint32_t>(k) * ldb32,
-                            row < kvalid ? nbytes : 0u);
+          for (int q = 0; q < NI; ++q) {
+            const int src = ci.v[q];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int i2 = 2 * q + h;
+              if (i2 < niter) {
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                  const int row = warp + 16 * i2 + 8 * j;
+                  const int k = __shfl_sync(0xffffffffu, src, row & 31);
+                  if (Cfg::B_CPR >= 32 || ch < Cfg::B_CPR)
+                    cp_async_16(base + (2 * i2 + j) * (kProdWarps * 128), bcol + static_cast<uint32_t>(k) * ldb32,
+                                row < kvalid ? nbytes : 0u);
+                }
+              }
             }
           }
         }
@@ -234,7 +265,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t abase = sA + (ch / Cfg::A_CPA) * (Cfg::KS * Cfg::A_ROW_BYTES);
         for (int rb = warp * Cfg::A_RPW; rb < kpad; rb += kProdWarps * Cfg::A_RPW) {
           const int row = rb + lane / Cfg::A_CPR;
-          const int k = __shfl_sync(0xffffffffu, row < 32 ? c0 : c1, row & 31);
+          int k = 0;
+#pragma unroll
+          for (int q = 0; q < NI; ++q) {  // shuffle every slot block, keep the row's (no local memory)
+            const int kq = __shfl_sync(0xffffffffu, ci.v[q], row & 31);
+            k = (row >> 5) == q ? kq : k;
+          }
           const uint32_t o = static_cast<uint32_t>(row * Cfg::A_ROW_BYTES + (ch % Cfg::A_CPA) * 16);
           cp_async_16(abase + swz<Cfg::A_MASK>(o), acol + static_cast<uint32_t>(k) * lda32,
                       row < kvalid ? mbytes : 0u);
@@ -247,10 +283,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       cur = nxt;
       nxt = nn;
-      c0 = d0;
-      c1 = d1;
-      d0 = e0;
-      d1 = e1;
+      ci = di;
+      di = ei;
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
@@ -704,14 +738,14 @@ CUtensorMapSwizzle swizzle_enum(int row_bytes) {
                            : CU_TENSOR_MAP_SWIZZLE_NONE;
 }
 
-template <int GW, bool kOrientN, bool kBF16>
+template <int GW, bool kOrientN, bool kBF16, int kKS = 64>
 int run_gk(const SpmmArgs& a, cudaStream_t s) {
-  using Cfg = GkCfg<GW, kOrientN>;
+  using Cfg = GkCfg<GW, kOrientN, kKS>;
   const int n_tiles = static_cast<int>(ceil_div(a.N, Cfg::N_TILE));
   const int64_t units = a.n_groups * n_tiles;
   if (units == 0) return kOk;
   if (units >= (1ll << 31)) return kErrShape;
-  auto kern = spmm_gk_kernel<GW, kOrientN, kBF16>;
+  auto kern = spmm_gk_kernel<GW, kOrientN, kBF16, kKS>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::SMEM));
   const int grid = static_cast<int>(units < num_sms() ? units : num_sms());
   // A column-major: A^T is row-major [K, M] with pitch sak
@@ -777,20 +811,30 @@ int run_gm(const SpmmArgs& a, int ks, cudaStream_t s) {
   return rowgemm_dispatch<kBF16>(p, a.B, a.ldb, ks, s);
 }
 
+// Tuning knob: PIT_GK_KS=64|128 overrides the gathered-K stage depth (defaults: 128 for 16/32-row
+// groups up to 128 rows, 64 for 256-row groups — measured on B200).
+int gk_ks_override() {
+  static int v = [] {
+    const char* e = getenv("PIT_GK_KS");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 template <bool kBF16>
 int dispatch_tc(const SpmmArgs& a, cudaStream_t s) {
   if (a.plan == kPlanPitK) {
     switch (a.t0) {
       case 16:
-        return run_gk<16, false, kBF16>(a, s);
+        return gk_ks_override() == 64 ? run_gk<16, false, kBF16, 64>(a, s) : run_gk<16, false, kBF16, 128>(a, s);
       case 32:
-        return run_gk<32, false, kBF16>(a, s);
+        return gk_ks_override() == 64 ? run_gk<32, false, kBF16, 64>(a, s) : run_gk<32, false, kBF16, 128>(a, s);
       case 64:
-        return run_gk<64, false, kBF16>(a, s);
+        return gk_ks_override() == 64 ? run_gk<64, false, kBF16, 64>(a, s) : run_gk<64, false, kBF16, 128>(a, s);
       case 128:
-        return run_gk<128, true, kBF16>(a, s);
+        return gk_ks_override() == 64 ? run_gk<128, true, kBF16, 64>(a, s) : run_gk<128, true, kBF16, 128>(a, s);
       case 256:
-        return run_gk<256, false, kBF16>(a, s);
+        return run_gk<256, false, kBF16, 64>(a, s);
       default:
         return kErrUnsupported;
     }

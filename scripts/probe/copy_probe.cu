@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(512, 1) probe(const __grid_constant__ CUtensor
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], mode == 1 ? warps * 32 : warps);
+    for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], (mode == 1 || mode >= 3) ? warps * 32 : warps);
     fence_mbar_init();
   }
   __syncthreads();
@@ -48,6 +48,21 @@ __global__ void __launch_bounds__(512, 1) probe(const __grid_constant__ CUtensor
         const int r2 = ((r + 2) * 2654435761u) >> 19, r3 = ((r + 3) * 2654435761u) >> 19;
         if (lane == 0) tma_gather4(dst + q * 512, &tm, &full[stage], (blockIdx.x % 128) * 64, r0, r1, r2, r3);
       }
+    } else if (mode == 3 || mode == 4) {
+      // spmm_gk pattern: one 512-byte row per warp instruction (32 lanes x 16 B), zero-fill variant
+      const uint32_t s = smem_u32(dst);
+      const uint32_t nb = 16u - (lane == 99 ? 1u : 0u);  // opaque to the compiler: register src-size
+      for (int row = warp; row < ROWS_PER_STAGE / 4; row += warps) {
+        const int k = ((unsigned)(rbase + row) * 2654435761u) >> 19;
+        const int ch = lane;
+        const uint32_t o = (ch >> 3) * (64 * 128) + row * 128 + (((ch & 7) ^ (row & 7)) << 4);
+        if (mode == 3)
+          cp_async_16(s + o, B + (int64_t)k * 8192 + (blockIdx.x % 32) * 256 + ch * 8, nb);
+        else
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s + o),
+                       "l"(B + (int64_t)k * 8192 + (blockIdx.x % 32) * 256 + ch * 8) : "memory");
+      }
+      cp_async_arrive_noinc(&full[stage]);
     } else if (mode == 1) {
       const uint32_t s = smem_u32(dst);
       for (int row = warp * 4 + (lane >> 3); row < ROWS_PER_STAGE; row += warps * 4) {
@@ -113,13 +128,14 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   int clk;
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
-  const char* names[3] = {"tma_gather4", "cp.async16", "tma_tile2d"};
+  const char* names[5] = {"tma_gather4", "cp.async16", "tma_tile2d", "cp.async512z", "cp.async512"};
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   const int iters = 400;
-  for (int mode = 0; mode < 3; ++mode) {
+  for (int mode = 0; mode < 5; ++mode) {
     for (int warps : {1, 2, 4, 8, 16}) {
+      if (mode == 2 && warps > 1) continue;
       const CUtensorMap& tm = mode == 2 ? tm_t : tm_g;
       probe<<<sms, 512, smem>>>(tm, B, rows, (int)h.size(), mode, warps, 20);
       cudaEventRecord(e0);
