@@ -76,7 +76,7 @@ __device__ __forceinline__ bool elem_live(const uint8_t* p, int dtype) {
 // ---------------------------------------------------------------------------
 constexpr int kRaWarps = 8;
 
-__global__ void __launch_bounds__(kRaWarps * 32) detect_rows_vec_kernel(const uint8_t* __restrict__ x, int64_t R,
+__global__ void __launch_bounds__(kRaWarps * 32, 4) detect_rows_vec_kernel(const uint8_t* __restrict__ x, int64_t R,
                                                                           int64_t row_bytes, int64_t ld_bytes, int tr,
                                                                           int V, int64_t GR, int64_t GC,
                                                                           LiveMask mk, uint32_t* __restrict__ occ,
@@ -100,21 +100,25 @@ __global__ void __launch_bounds__(kRaWarps * 32) detect_rows_vec_kernel(const ui
     uint4 acc = make_uint4(0, 0, 0, 0);
     int band_left = tr;
     int band = 0;
-    for (int64_t r = r0; r < r1; r += 8) {
+    const uint8_t* rowp = base + r0 * ld_bytes;
+    const int nrows = static_cast<int>(r1 - r0);
+    for (int r = 0; r < nrows; r += 8) {
       uint4 buf[8];
+      const uint8_t* q = rowp;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int64_t rr = r + u;
-        buf[u] = (rr < r1 && col_ok) ? ldg_stream(base + rr * ld_bytes) : make_uint4(0, 0, 0, 0);
+        buf[u] = (r + u < nrows && col_ok) ? ldg_stream(q) : make_uint4(0, 0, 0, 0);
+        q += ld_bytes;
       }
+      rowp = q;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        if (r + u >= r1) break;  // warp-uniform
+        if (r + u >= nrows) break;  // warp-uniform
         acc.x |= buf[u].x & mk.even;
         acc.y |= buf[u].y & mk.odd;
         acc.z |= buf[u].z & mk.even;
         acc.w |= buf[u].w & mk.odd;
-        if (--band_left == 0 || r + u + 1 == r1) {
+        if (--band_left == 0 || r + u + 1 == nrows) {
           const bool live = (acc.x | acc.y | acc.z | acc.w) != 0;
           const uint32_t b = __ballot_sync(0xffffffffu, live);
           if (is_start) {
@@ -316,10 +320,13 @@ int launch_detect_values(const DetectValuesArgs& a, cudaStream_t s) {
     const int64_t segs = ceil_div(row_bytes, 512);
     const int64_t seg_groups = ceil_div(segs, kRaWarps);
     const int64_t tiles = seg_groups * ceil_div(GR, 32);
-    int dev = 0, sms = 148;
+    int dev = 0, sms = 148, per_sm = 4;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t grid = tiles < 4ll * sms ? tiles : 4ll * sms;  // 4 resident CTAs per SM
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, detect_rows_vec_kernel, kRaWarps * 32, 0);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t resident = static_cast<int64_t>(per_sm) * sms;  // one wave of persistent CTAs
+    const int64_t grid = tiles < resident ? tiles : resident;
     detect_rows_vec_kernel<<<static_cast<unsigned>(grid), kRaWarps * 32, 0, s>>>(
         static_cast<const uint8_t*>(a.x), a.R, row_bytes, ld_bytes, a.tr, static_cast<int>(vec_per_micro), GR, GC,
         live_mask_for(a.dtype), a.occ, WG, seg_groups, tiles);
