@@ -265,3 +265,26 @@ def test_dense_reference_f64_is_triple_loop():
     A = rng.standard_normal((8, 8))
     B = rng.standard_normal((8, 8))
     assert np.array_equal(pit.run_dense_reference(A, B), orc.dense_reference_f64(A, B))
+
+
+def test_captured_step_tracks_new_values():
+    """CUDA-graph replay re-runs detection + SpMM on the buffers' current contents."""
+    import torch
+
+    pit = _pkg()
+    from paper_2301_10936_b200.graph import CapturedSparseMatmul
+
+    m, k, n = 512, 1024, 512
+    reg = pit.register_builtin_kernels()
+    plan = pit.forced_plan(bound(m, k, n), "k", reg, tile_shape=(32, 64, 32))
+    A = torch.zeros((k, m), dtype=torch.bfloat16, device="cuda").t()  # column-major buffer
+    B = torch.randn((k, n), dtype=torch.bfloat16, device="cuda")
+    step = CapturedSparseMatmul(plan, A, B)
+    for seed in (1, 2):
+        ann = pit.random_annotation((m, k), (32, 1), 0.9, seed=seed)
+        Ah, _ = _operands(m, k, n, ann, seed=seed)
+        A.copy_(torch.from_numpy(Ah).to(torch.bfloat16).cuda())
+        C = step.replay().float().cpu().numpy()
+        ref = orc.dense_reference_f64(A.float().cpu().numpy(), B.float().cpu().numpy())
+        assert orc.max_rel_error(C, ref) <= BF16_TOL
+    assert step.kernels_per_replay == 3
