@@ -184,6 +184,14 @@ PIT_API int pit_gather_rows(const void* src, int64_t ld_src_bytes, const int32_t
 PIT_API int pit_scatter_rows_scaled(const void* src, int dtype, int64_t ld_src, const int32_t* rows, int64_t n,
                                     int64_t width, const float* scale, void* dst, int64_t ld_dst, void* stream);
 
+/*
+ * Sparse row reduction (run_sparse_reduce_sum, executor.py:540-613): out[r] = sum of A[r, l] (row-major,
+ * pitch lda) over live micro-tiles. mode 0 dense; mode 1 pit:l (occ groups = rows, micro (1,1));
+ * mode 2 pit:p (occ groups = l-blocks of block_l columns, coordinates = rows). Dead rows are exact 0.
+ */
+PIT_API int pit_reduce_rows(const void* A, int dtype, int64_t P, int64_t L, int64_t lda, const uint32_t* occ,
+                            int64_t words_per_group, int mode, int block_l, void* out, void* stream);
+
 /* Pitched host<->device copy on the caller's stream (cudaMemcpy2DAsync, direction inferred): moves
  * column slabs of row-major operands for the pipelined host-buffer path. */
 PIT_API int pit_copy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width_bytes,

@@ -303,3 +303,36 @@ def switch_forward(x, logits, w1, w2, round_hidden=None):
             h = round_hidden(h)
         out[toks] = gate[toks, None] * (h @ np.asarray(w2[e], np.float64))
     return out
+
+
+# ------------------------------------------------------------------------------ reduce_sum
+def reduce_sum(A, ann, pit_axis, tile_shape, dtype=np.float32):
+    """executor.py:540-613 (single worker): pit:l gathers each row's live elements (micro (1,1),
+    policy.py:95-97), pit:p gathers live rows per L-block (micro (1, L)); dense sums tiles.
+    Tile sums are accumulated into C in the reference's chunk order."""
+    P, L = tile_shape
+    A = np.asarray(A, dtype)
+    p, l = A.shape
+    C = np.zeros(p, dtype)
+    if pit_axis == "dense":
+        for p0 in range(0, p, P):
+            for l0 in range(0, l, L):
+                C[p0 : p0 + P] += A[p0 : p0 + P, l0 : l0 + L].sum(axis=1)
+        return C
+    if pit_axis == "p":
+        _, groups = build_index(*ann, (1, L), "p")
+        for g, rows in enumerate(groups):
+            for off in range(0, rows.size, P):
+                r = rows[off : off + P]
+                C[r] += A[r, g * L : (g + 1) * L].sum(axis=1)
+        return C
+    _, groups = build_index(*ann, (1, 1), "l")
+    for p0 in range(0, p, P):
+        rows = range(p0, min(p0 + P, p))
+        chunks = max((-(-groups[r].size // L) for r in rows), default=0)
+        for c in range(chunks):
+            for r in rows:
+                seg = groups[r][c * L : (c + 1) * L]
+                if seg.size:
+                    C[r] += A[r, seg].sum()
+    return C

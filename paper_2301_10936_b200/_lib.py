@@ -50,6 +50,7 @@ EXPORTS = (
     "pit_gather_rows",
     "pit_scatter_rows_scaled",
     "pit_copy2d_async",
+    "pit_reduce_rows",
 )
 
 
@@ -136,6 +137,7 @@ def _declare(lib) -> None:
     lib.pit_gather_rows.argtypes = [vp, i64, vp, i64, i64, vp, i64, vp]
     lib.pit_scatter_rows_scaled.argtypes = [vp, i32, i64, vp, i64, i64, vp, vp, i64, vp]
     lib.pit_copy2d_async.argtypes = [vp, i64, vp, i64, i64, i64, vp]
+    lib.pit_reduce_rows.argtypes = [vp, i32, i64, i64, i64, vp, i64, i32, i32, vp, vp]
     for name in EXPORTS:
         if name not in ("pit_last_error", "pit_abi_version", "pit_kernel_launches"):
             getattr(lib, name).restype = i32

@@ -385,6 +385,17 @@ int pit_scatter_rows_scaled(const void* src, int dtype, int64_t ld_src, const in
   return st;
 }
 
+int pit_reduce_rows(const void* A, int dtype, int64_t P, int64_t L, int64_t lda, const uint32_t* occ, int64_t WG,
+                    int mode, int block_l, void* out, void* stream) {
+  if (P < 0 || L < 0) return fail(kErrShape, "negative extent");
+  if (mode < 0 || mode > 2) return fail(kErrArg, "unknown reduce mode %d", mode);
+  if (mode && (!occ || block_l <= 0)) return fail(kErrArg, "sparse reduce needs an occupancy bitmap");
+  if (P && (!A || !out)) return fail(kErrArg, "null device pointer");
+  const int st = launch_reduce_rows(A, dtype, P, L, lda, occ, WG, mode, block_l, out, static_cast<cudaStream_t>(stream));
+  if (st == kErrUnsupported) return fail(st, "unsupported dtype code %d", dtype);
+  return st;
+}
+
 int pit_copy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width_bytes, int64_t height,
                      void* stream) {
   if (width_bytes < 0 || height < 0) return fail(kErrShape, "negative extent");

@@ -119,6 +119,8 @@ struct SpmmArgs {
 };
 
 int launch_spmm_simt(const SpmmArgs& a, cudaStream_t s);
+int launch_reduce_rows(const void* A, int dtype, int64_t P, int64_t L, int64_t lda, const uint32_t* occ, int64_t WG,
+                       int mode, int block_l, void* out, cudaStream_t s);
 int launch_dense_ref_f64(const double* A, int64_t s0, int64_t s1, const double* B, int64_t ldb, double* C, int64_t M,
                          int64_t N, int64_t K, cudaStream_t s);
 int launch_spmm_tc(const SpmmArgs& a, cudaStream_t s);  // bf16 / fp16 tcgen05 paths

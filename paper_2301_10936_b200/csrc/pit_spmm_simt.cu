@@ -246,6 +246,31 @@ __global__ void dense_ref_f64_kernel(const double* __restrict__ A, int64_t s0, i
   C[e] = acc;
 }
 
+// Row reduction over live micro-tiles (executor.py:540-613): one warp per row,
+// C[r] = sum of A[r, l] over l whose micro-tile is live; dead elements are selected out (never
+// multiplied), so NaN in a dead position cannot leak and rows with no survivor are exactly 0.
+//   mode 0: dense; mode 1 (pit:l): groups = rows, occ[r][l/32] bit l%32 (micro (1,1));
+//   mode 2 (pit:p): groups = l-blocks of block_l, occ[l/block_l][r/32] bit r%32.
+template <typename T, typename Acc>
+__global__ void reduce_rows_kernel(const T* __restrict__ A, int64_t P, int64_t L, int64_t lda,
+                                   const uint32_t* __restrict__ occ, int64_t WG, int mode, int block_l,
+                                   T* __restrict__ out) {
+  const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= P) return;
+  const T* row = A + r * lda;
+  Acc acc = Acc(0);
+  for (int64_t l = lane; l < L; l += 32) {
+    bool live = true;
+    if (mode == 1) live = (__ldg(occ + r * WG + (l >> 5)) >> (l & 31)) & 1u;
+    if (mode == 2) live = (__ldg(occ + (l / block_l) * WG + (r >> 5)) >> (r & 31)) & 1u;
+    if (live) acc += load_as<T, Acc>(row + l);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) out[r] = from_acc<T, Acc>(acc);
+}
+
 template <typename T, typename Acc>
 int run_simt(const SpmmArgs& a, cudaStream_t s) {
   int64_t ytiles;
@@ -280,6 +305,35 @@ int launch_spmm_simt(const SpmmArgs& a, cudaStream_t s) {
     default:
       return kErrUnsupported;
   }
+}
+
+int launch_reduce_rows(const void* A, int dtype, int64_t P, int64_t L, int64_t lda, const uint32_t* occ, int64_t WG,
+                       int mode, int block_l, void* out, cudaStream_t s) {
+  if (P == 0) return kOk;
+  const unsigned grid = static_cast<unsigned>(ceil_div(P * 32, 256));
+  switch (dtype) {
+    case kDtypeF32:
+      reduce_rows_kernel<float, float><<<grid, 256, 0, s>>>(static_cast<const float*>(A), P, L, lda, occ, WG, mode,
+                                                            block_l, static_cast<float*>(out));
+      break;
+    case kDtypeF64:
+      reduce_rows_kernel<double, double><<<grid, 256, 0, s>>>(static_cast<const double*>(A), P, L, lda, occ, WG, mode,
+                                                              block_l, static_cast<double*>(out));
+      break;
+    case kDtypeBF16:
+      reduce_rows_kernel<__nv_bfloat16, float><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(A), P, L, lda,
+                                                                    occ, WG, mode, block_l,
+                                                                    static_cast<__nv_bfloat16*>(out));
+      break;
+    case kDtypeF16:
+      reduce_rows_kernel<__half, float><<<grid, 256, 0, s>>>(static_cast<const __half*>(A), P, L, lda, occ, WG, mode,
+                                                             block_l, static_cast<__half*>(out));
+      break;
+    default:
+      return kErrUnsupported;
+  }
+  note_launch();
+  return cuda_status();
 }
 
 int launch_dense_ref_f64(const double* A, int64_t s0, int64_t s1, const double* B, int64_t ldb, double* C, int64_t M,

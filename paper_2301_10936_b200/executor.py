@@ -521,3 +521,71 @@ def run_sparse_matmul(
             raise ExecError(f"annotation {ann.tensor_shape} does not describe A {A.shape}")
         idx = build_index(ann, plan.micro_tile, plan.pit_axis, workers=workers)
     return run_matmul_with_index(plan, A, B, idx, workers=workers, stats=stats)
+
+
+# ------------------------------------------------------------------------------ reduce_sum
+def reduce_sum_reference(a) -> np.ndarray:
+    """f64 row sums (executor.py:286-291), computed on the GPU."""
+    A = _array(a)
+    if len(A.shape) != 2:
+        raise ExecError("reduce_sum oracle expects rank 2")
+    torch = _torch()
+    Ad = _device.to_device(np.asarray(A, dtype=np.float64) if not _is_torch(A) else A).to(torch.float64).contiguous()
+    out = torch.empty(Ad.shape[0], dtype=torch.float64, device=Ad.device)
+    lib = _lib.load()
+    _device.check(lib.pit_reduce_rows(Ad.data_ptr(), _lib.PIT_F64, Ad.shape[0], Ad.shape[1], Ad.stride(0), None, 0, 0,
+                                      1, out.data_ptr(), _device.stream_ptr()), ExecError)
+    return _device.to_host(out)
+
+
+def run_sparse_reduce_sum(
+    plan: SparseKernelPlan,
+    A: DenseTensor,
+    ann: Optional[SparsityAnnotation],
+    workers: int = 1,
+    stats: Optional[ExecStats] = None,
+) -> DenseTensor:
+    """Row reduction over live micro-tiles (executor.py:540-613): one GPU pass, a warp per row;
+    rows with no survivor stay exactly 0.0."""
+    if plan.op_kind != "reduce_sum":
+        raise ExecError(f"not a reduce_sum plan: {plan.op_kind}")
+    if len(A.shape) != 2:
+        raise ExecError("reduce_sum expects a rank-2 operand")
+    ext = plan.extents
+    if (ext["p"], ext["l"]) != A.shape:
+        raise ExecError(f"plan bound to {dict(ext)} but got A{A.shape}")
+    torch = _torch()
+    host = not A.is_device
+    Ad = _device.to_device(A.array)
+    if _torch_layout(Ad) != ROW_MAJOR:
+        Ad = Ad.contiguous()
+    p, l = A.shape
+    out = torch.empty(p, dtype=Ad.dtype, device=Ad.device)
+    lib = _lib.load()
+    idx = None
+    if plan.is_dense:
+        mode, occ, wg, block = 0, None, 0, 1
+    else:
+        if ann is None or tuple(ann.tensor_shape) != A.shape:
+            raise ExecError("per-row plan needs an annotation matching A")
+        idx = build_index(ann, plan.micro_tile, plan.pit_axis, workers=workers)
+        occ_t = idx.occupancy_words()
+        occ, wg = occ_t.data_ptr(), occ_t.shape[1]
+        mode = 1 if plan.pit_axis == "l" else 2
+        block = plan.micro_tile[1]
+    _device.check(lib.pit_reduce_rows(Ad.data_ptr(), _device.dtype_code(Ad), p, l, Ad.stride(0), occ, wg, mode, block,
+                                      out.data_ptr(), _device.stream_ptr()), ExecError)
+    if stats is not None:
+        if plan.is_dense:
+            stats.launches += dense_launches(plan)
+        elif plan.pit_axis == "l":
+            # executed tile launches: per block of P rows, the longest row's survivor chunks
+            # (executor.py:593-608; differs from the cost model's average, policy.py:181-184)
+            P, L = plan.tile.tile_shape
+            chunks = -(-idx.counts // L)
+            stats.launches += int(sum(chunks[i : i + P].max(initial=0) for i in range(0, p, P)))
+            stats.gathered_micro_tiles += idx.total
+        else:
+            stats.launches += launches_from_counts(plan, idx.counts)
+            stats.gathered_micro_tiles += idx.total
+    return DenseTensor(_device.to_host(out) if host else out)

@@ -188,7 +188,29 @@ def plan_cases():
     (OUT / "plan_cases.json").write_text(json.dumps(dict(micro=micro, cover_table=table, launches=launches)))
 
 
+def reduce_cases():
+    rng = np.random.default_rng(61)
+    reg = pt.register_builtin_kernels()
+    out, meta = {}, []
+    for i, (p_, l_, axis) in enumerate([(70, 200, "l"), (70, 200, "p"), (70, 200, "dense"), (8, 16, "l"),
+                                         (33, 129, "p"), (1, 300, "l")]):
+        expr = pt.bind_extents(pt.parse_expr("C[p] += A[p,l]"), dict(p=p_, l=l_))
+        lengths = [int(x) for x in rng.integers(0, l_ + 1, p_)]
+        ann = pt.from_ragged_lengths(lengths, [p_, l_])
+        A = rng.standard_normal((p_, l_)).astype(np.float32) * ann.materialize()
+        plan = pt.forced_plan(expr, axis, reg)
+        stats = pt.ExecStats()
+        C = pt.run_sparse_reduce_sum(plan, pt.DenseTensor.from_array(A), ann if axis != "dense" else None, stats=stats)
+        out[f"A{i}"] = A
+        out[f"C{i}"] = C.array
+        meta.append(dict(i=i, shape=[p_, l_], axis=axis, lengths=lengths, packed=ann.packed.tolist(),
+                         launches=stats.launches, gathered=stats.gathered_micro_tiles))
+    np.savez_compressed(OUT / "reduce_cases.npz", **out)
+    (OUT / "reduce_cases.json").write_text(json.dumps(meta))
+
+
 if __name__ == "__main__":
+    reduce_cases()
     index_cases()
     value_cases()
     gather_cases()

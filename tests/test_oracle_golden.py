@@ -119,3 +119,12 @@ def test_cover_table_matches_published_search_results():
         assert cov == row["cover"]
         grid = (4096 // mt[0]) * (4096 // mt[1])
         assert abs(100.0 * (1 - cov / grid) - pub) <= 1.0
+
+
+def test_oracle_reduce_sum_matches_reference():
+    data = np.load(GOLD / "reduce_cases.npz")
+    for c in _json("reduce_cases.json"):
+        i = c["i"]
+        ann = (tuple(c["shape"]), (1, 1), np.array(c["packed"], np.uint8))
+        got = orc.reduce_sum(data[f"A{i}"], ann, c["axis"], (16, 64))
+        assert orc.max_rel_error(got, data[f"C{i}"]) <= 1e-6, i
