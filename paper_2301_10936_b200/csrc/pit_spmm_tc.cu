@@ -108,7 +108,10 @@ template <int GW, bool kOrientN, bool kBF16, int kKS>
 __global__ void __launch_bounds__(kThreads, 1)
     spmm_gk_kernel(const void* __restrict__ Bv, int64_t ldb, const void* __restrict__ Atv, int64_t lda,
                    const int32_t* __restrict__ counts, const int32_t* __restrict__ slots, int64_t slot_stride,
-                   int n_groups, int n_tiles, int M, int N, int K, void* __restrict__ Cv, int64_t ldc) {
+                   int n_groups, int n_tiles, int M, int N, int K, void* __restrict__ Cv, int64_t ldc,
+                   int grp_rows) {
+  // grp_rows (<= GW, multiple of 8): rows per group. Micro-tiles narrower than the kernel's GW run
+  // in it with the A^T strip's extra columns zero-filled and never stored.
   using Cfg = GkCfg<GW, kOrientN, kKS>;
   using OT = OutT<kBF16>;
   extern __shared__ uint8_t smem_raw[];
@@ -215,7 +218,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int kb = cur.kb, cnt = cur.cnt;
       const int g = cur.g;
       const int n0 = cur.t * Cfg::N_TILE;
-      const int m0 = g * GW;
+      const int m0 = g * grp_rows;
+      const int m_end = min(M, m0 + grp_rows);
       const int kvalid = min(Cfg::KS, cnt - kb);
       const int kpad = (kvalid + 15) & ~15;
       mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -260,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       {
         const int ch = lane % Cfg::A_CPR;
         const int m = m0 + ch * 8;
-        const uint32_t mbytes = m < M ? static_cast<uint32_t>(min(16, (M - m) * 2)) : 0u;
+        const uint32_t mbytes = m < m_end ? static_cast<uint32_t>(min(16, (m_end - m) * 2)) : 0u;
         const T* acol = Ap + (mbytes ? m : 0);
         const uint32_t abase = sA + (ch / Cfg::A_CPA) * (Cfg::KS * Cfg::A_ROW_BYTES);
         for (int rb = warp * Cfg::A_RPW; rb < kpad; rb += kProdWarps * Cfg::A_RPW) {
@@ -344,7 +348,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int g = u % n_groups;
       const int n0 = (u / n_groups) * Cfg::N_TILE;
-      const int m0 = g * GW;
+      const int m0 = g * grp_rows;
+      const int m_end = min(M, m0 + grp_rows);
       const int cnt = __ldg(counts + g);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
@@ -352,7 +357,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (kOrientN) {
         // lane = group row, columns = n: 32 consecutive outputs per tcgen05.ld
         const int m = m0 + q * 32 + lane;
-        const bool row_ok = m < M;
+        const bool row_ok = m < m_end;
         uint8_t* crow = reinterpret_cast<uint8_t*>(C + static_cast<int64_t>(row_ok ? m : 0) * ldc);
         const bool vec_ok = (ldc % 8) == 0 && (reinterpret_cast<uintptr_t>(Cv) & 15) == 0;
 #pragma unroll 1
@@ -404,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
                 const int m = m0 + c + i;
-                if (m < M) C[static_cast<int64_t>(m) * ldc + n] = OT::cvt(__uint_as_float(v[i]));
+                if (m < m_end) C[static_cast<int64_t>(m) * ldc + n] = OT::cvt(__uint_as_float(v[i]));
               }
             }
           }
@@ -751,7 +756,8 @@ int run_gk(const SpmmArgs& a, cudaStream_t s) {
   // A column-major: A^T is row-major [K, M] with pitch sak
   kern<<<grid, kThreads, Cfg::SMEM, s>>>(a.B, a.ldb, a.A, a.sak, a.counts, a.slots, a.slot_stride,
                                          static_cast<int>(a.n_groups), n_tiles, static_cast<int>(a.M),
-                                         static_cast<int>(a.N), static_cast<int>(a.K), a.C, a.ldc);
+                                         static_cast<int>(a.N), static_cast<int>(a.K), a.C, a.ldc,
+                                         static_cast<int>(a.t0));
   note_launch();
   return cuda_status();
 }
@@ -824,7 +830,8 @@ int gk_ks_override() {
 template <bool kBF16>
 int dispatch_tc(const SpmmArgs& a, cudaStream_t s) {
   if (a.plan == kPlanPitK) {
-    switch (a.t0) {
+    const int gw = a.t0 <= 16 ? 16 : a.t0 <= 32 ? 32 : a.t0 <= 64 ? 64 : a.t0 <= 128 ? 128 : 256;
+    switch (gw) {
       case 16:
         return gk_ks_override() == 64 ? run_gk<16, false, kBF16, 64>(a, s) : run_gk<16, false, kBF16, 128>(a, s);
       case 32:
@@ -857,7 +864,7 @@ bool spmm_tc_supported(const SpmmArgs& a) {
   if (a.plan == kPlanPitK) {
     if (a.sam != 1 || (a.sak * 2) % 16) return false;  // A column-major
     if (a.K * a.ldb >= (1ll << 32) || a.K * a.sak >= (1ll << 32)) return false;  // 32-bit element offsets
-    return a.t0 == 16 || a.t0 == 32 || a.t0 == 64 || a.t0 == 128 || a.t0 == 256;
+    return a.t0 % 8 == 0 && a.t0 <= 256;  // narrower groups run in the next wider kernel
   }
   if (a.sak != 1 || (a.sam * 2) % 16) return false;  // A row-major
   if (a.plan == kPlanDense) return true;

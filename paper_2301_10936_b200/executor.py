@@ -589,3 +589,55 @@ def run_sparse_reduce_sum(
             stats.launches += launches_from_counts(plan, idx.counts)
             stats.gathered_micro_tiles += idx.total
     return DenseTensor(_device.to_host(out) if host else out)
+
+
+# ------------------------------------------------------------------------------ single tile
+def _scatter_whole(tile, dst, accumulate: bool) -> None:
+    """dst (rank 2, device) = / += tile through SWrite with one micro-tile covering all of dst."""
+    torch = _torch()
+    rows, cols = int(dst.shape[0]), int(dst.shape[1])
+    zero = torch.zeros(1, dtype=torch.int32, device=dst.device)
+    ld, col = _tensor_geometry(dst)
+    _device.check(_lib.load().pit_swrite(tile.contiguous().data_ptr(), dst.data_ptr(), _device.dtype_code(dst), rows,
+                                         cols, ld, col, rows, cols, rows, cols, 0, 0, zero.data_ptr(), 1,
+                                         int(accumulate), _device.stream_ptr()), ExecError)
+
+
+def run_tile(desc, inputs, out, scratch=None) -> None:
+    """Execute one dense tile (reference tiles.py:119-148) with the sm_100a kernels: matmul and
+    reduce_sum accumulate into ``out``, vec_add assigns. Buffers may be host arrays (``out`` is
+    updated in place) or CUDA tensors; ``scratch`` (M, N) is reused for the matmul product."""
+    from .tiles import TileError
+
+    in_shapes, out_shape = desc.buffer_shapes()
+    if len(inputs) != len(in_shapes):
+        raise TileError(f"{desc.op_kind} takes {len(in_shapes)} inputs, got {len(inputs)}")
+    for buf, want in zip(inputs, in_shapes):
+        if tuple(buf.shape) != want:
+            raise TileError(f"input shape {tuple(buf.shape)} does not match tile {want}")
+    if tuple(out.shape) != out_shape:
+        raise TileError(f"output shape {tuple(out.shape)} does not match tile {out_shape}")
+    torch = _torch()
+    host_out = not _is_torch(out)
+    ins = [_device.to_device(np.asarray(x) if not _is_torch(x) else x) for x in inputs]
+    o = _device.to_device(np.asarray(out)) if host_out else out
+    o2 = o.reshape(out_shape[0], -1) if desc.op_kind == "matmul" else o.reshape(-1, 1)
+    if desc.op_kind == "matmul":
+        a, b = ins
+        m, k, n = desc.tile_shape
+        plan = SparseKernelPlan("matmul", "dense", None, desc, 0.0, 0.0, ROW_MAJOR, dict(m=m, k=k, n=n))
+        prod = scratch if _is_torch(scratch) and scratch.is_cuda else torch.empty((m, n), dtype=a.dtype, device=a.device)
+        spmm_device(plan, a.contiguous(), b.contiguous(), None, out=prod)
+        _scatter_whole(prod, o2, True)
+    elif desc.op_kind == "reduce_sum":
+        a = ins[0].contiguous()
+        sums = torch.empty((a.shape[0], 1), dtype=a.dtype, device=a.device)
+        _device.check(_lib.load().pit_reduce_rows(a.data_ptr(), _device.dtype_code(a), a.shape[0], a.shape[1],
+                                                  a.stride(0), None, 0, 0, 1, sums.data_ptr(), _device.stream_ptr()),
+                      ExecError)
+        _scatter_whole(sums, o2, True)
+    else:
+        _scatter_whole(ins[0].reshape(-1, 1), o2, False)
+        _scatter_whole(ins[1].reshape(-1, 1), o2, True)
+    if host_out:
+        out[...] = _device.to_host(o).reshape(out_shape)

@@ -176,3 +176,86 @@ def format_plan(plan: SparseKernelPlan) -> str:
         f"plan op={plan.op_kind} pit_axis={plan.pit_axis} microtile={micro} "
         f"tile={'x'.join(map(str, plan.tile.tile_shape))} impl={plan.tile.impl_id} cost={plan.estimated_cost:.6e}"
     )
+
+
+# ------------------------------------------------------------------------- Alg. 1 selection
+@dataclass(frozen=True)
+class PlanCandidate:
+    plan: SparseKernelPlan
+    total_micro_tiles: int
+    total_launches: int
+    total_cost: float
+
+
+class _SampleCovers:
+    """Per-sample live micro-tile counts per group, memoised by (micro-tile, axis): tiles whose
+    projections coincide (e.g. every tile with M_t = 32 under pit:k) share one prefix-sum pass."""
+
+    def __init__(self, samples: Sequence[SparsityAnnotation]):
+        self.samples = list(samples)
+        self._memo: dict = {}
+
+    def counts(self, micro, dim: int) -> list:
+        key = (tuple(micro), dim)
+        if key not in self._memo:
+            self._memo[key] = [cover_group_counts(a, micro, dim) for a in self.samples]
+        return self._memo[key]
+
+
+def _preference(c: PlanCandidate):
+    # cheapest; on ties dense first, then the larger tile (fewer launches), then impl id
+    return (c.total_cost, not c.plan.is_dense, -c.plan.tile.flops, c.plan.tile.impl_id)
+
+
+def selection_candidates(expr: TensorExpr, samples, registry: KernelRegistry, profile, allow_dense: bool = True):
+    """All (tile, PIT axis) plans and the dense fallbacks, each costed as Σ_samples launches x the
+    profiled tile cost, sorted by preference (reference policy.py:201-276 contract, error messages
+    included). Dense costs `dense_launches` per sample (one sweep when there are no samples)."""
+    from dataclasses import replace
+
+    from .expr import pit_axes
+
+    op_kind = operator_kind(expr)
+    if op_kind not in ("matmul", "reduce_sum"):
+        raise PlanError(f"selection supports matmul and reduce_sum, got {op_kind}")
+    extents = {s: expr.extent(s) for s in expr.symbols()}
+    tiles = sorted(registry.by_op(op_kind), key=lambda d: d.impl_id)
+    if not tiles:
+        raise PlanError(f"registry has no {op_kind} tiles")
+    want = sparse_operand_shape(op_kind, extents)
+    bad = next((a for a in samples if tuple(a.tensor_shape) != want), None)
+    if bad is not None:
+        raise PlanError(f"sample shape {bad.tensor_shape} does not match operand {want}")
+    axes = [a for a in sparse_operand_axes(op_kind) if a in pit_axes(expr)]
+    if not axes and not allow_dense:
+        raise PlanError("no applicable permuted axis and dense fallback disabled")
+    covers = _SampleCovers(samples)
+    n_samples = len(samples)
+    out = []
+    for tile in tiles:
+        cost = profile.cost(tile)
+        for axis in axes if n_samples else ():
+            micro, layout = get_micro_tile(op_kind, tile.tile_shape, axis)
+            plan = SparseKernelPlan(op_kind, axis, micro, tile, cost, 0.0, layout, dict(extents))
+            per = covers.counts(micro, sparse_operand_axes(op_kind).index(axis))
+            launches = sum(launches_from_counts(plan, c) for c in per)
+            total = launches * cost
+            out.append(PlanCandidate(replace(plan, estimated_cost=total / n_samples),
+                                     int(sum(int(c.sum()) for c in per)), launches, total))
+        if allow_dense:
+            plan = SparseKernelPlan(op_kind, DENSE, None, tile, cost, 0.0, ROW_MAJOR, dict(extents))
+            sweeps = max(n_samples, 1)
+            launches = dense_launches(plan) * sweeps
+            total = launches * cost
+            out.append(PlanCandidate(replace(plan, estimated_cost=total / sweeps), launches, launches, total))
+    if not out:
+        raise PlanError("no viable plan candidates")
+    out.sort(key=_preference)
+    return out
+
+
+def kernel_selection(expr: TensorExpr, samples, registry: KernelRegistry, profile, allow_dense: bool = True):
+    """Alg. 1 (reference policy.py:279-292): the cheapest candidate. Scaling every profiled cost by a
+    positive constant cannot change the winner; all-dense samples fall to the dense tiling via the
+    tie-break."""
+    return selection_candidates(expr, samples, registry, profile, allow_dense)[0].plan

@@ -92,7 +92,7 @@ def _run_bf16(plan, A, B, ann, col_major):
     return C.array.float().cpu().numpy(), Ar, Br
 
 
-@pytest.mark.parametrize("t0", [16, 32, 64, 128, 256])
+@pytest.mark.parametrize("t0", [8, 16, 24, 32, 40, 64, 96, 128, 200, 256])
 @pytest.mark.parametrize("shape", [(1024, 1024, 1024), (512, 384, 520), (300, 200, 136)])
 def test_bf16_pit_k_tensor_cores(t0, shape):
     pit = _pkg()
