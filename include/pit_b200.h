@@ -75,6 +75,15 @@ PIT_API int pit_build_index_from_tensor(const void* values, int dtype, int64_t s
 PIT_API int pit_build_index(const uint8_t* packed, int64_t s0, int64_t s1, int g0, int g1, int t0, int t1, int pit_dim,
                     uint32_t* occ, int32_t* counts, int32_t* slots, void* stream);
 
+/* Plan-selection cover counts (policy.py:129-136 cover_group_counts, for every candidate of
+ * selection_candidates policy.py:241-276 at once): for candidate c = (t0, t1, pit_dim) given in the
+ * HOST array candidates[3c..3c+2], writes its n_groups live-micro-tile counts to the device array
+ * counts, candidates back to back in order. occ_ws is a device scratch of ws_words 32-bit words
+ * (at least max_c n_groups*words_per_group, see pit_index_geometry). */
+PIT_API int pit_cover_counts(const uint8_t* packed, int64_t s0, int64_t s1, int g0, int g1, int n_candidates,
+                             const int32_t* candidates, uint32_t* occ_ws, int64_t ws_words, int32_t* counts,
+                             void* stream);
+
 /* Occupancy bitmap from an arbitrary (e.g. reordered) index; *bad set to 1 on a coordinate out of
  * range (sread's "micro-tile coordinate out of range", executor.py:192-193). occ is overwritten. */
 PIT_API int pit_index_occupancy(const int32_t* counts, const int32_t* slots, int64_t n_groups, int64_t pit_grid,

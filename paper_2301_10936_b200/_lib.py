@@ -36,6 +36,7 @@ EXPORTS = (
     "pit_index_geometry",
     "pit_build_index_from_tensor",
     "pit_build_index",
+    "pit_cover_counts",
     "pit_index_occupancy",
     "pit_index_union",
     "pit_sread",
@@ -124,6 +125,7 @@ def _declare(lib) -> None:
     lib.pit_build_index_from_tensor.argtypes = [vp, i32, i64, i64, i64, i64, i32, i32, i32, vp, vp, vp, vp]
     lib.pit_build_index.argtypes = [vp, i64, i64, i32, i32, i32, i32, i32, vp, vp, vp, vp]
     lib.pit_index_occupancy.argtypes = [vp, vp, i64, i64, vp, vp, vp]
+    lib.pit_cover_counts.argtypes = [vp, i64, i64, i32, i32, i32, vp, vp, i64, vp, vp]
     lib.pit_index_union.argtypes = [vp, i64, i64, vp, vp, vp, vp]
     lib.pit_sread.argtypes = [vp, i32, i64, i64, i64, i32, vp, i64, i64, i32, i32, i32, i64, vp, i64, i32, vp]
     lib.pit_swrite.argtypes = [vp, vp, i32, i64, i64, i64, i32, i64, i64, i32, i32, i32, i64, vp, i64, i32, vp]

@@ -175,6 +175,32 @@ int pit_build_index(const uint8_t* packed, int64_t s0, int64_t s1, int g0, int g
   return launch_compact(occ, ng, wg, counts, slots, pg, s);
 }
 
+int pit_cover_counts(const uint8_t* packed, int64_t s0, int64_t s1, int g0, int g1, int n_candidates,
+                     const int32_t* candidates, uint32_t* occ_ws, int64_t ws_words, int32_t* counts, void* stream) {
+  if (g0 <= 0 || g1 <= 0) return fail(kErrArg, "granularity must be positive, got (%d,%d)", g0, g1);
+  if (n_candidates < 0 || (n_candidates > 0 && !candidates)) return fail(kErrArg, "bad candidate list");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int64_t off = 0;
+  for (int c = 0; c < n_candidates; ++c) {
+    const int t0 = candidates[3 * c], t1 = candidates[3 * c + 1], dim = candidates[3 * c + 2];
+    int64_t ng, pg, wg;
+    if (int st = geometry(s0, s1, t0, t1, dim, &ng, &pg, &wg)) return st;
+    if (ng == 0) continue;
+    if (pg == 0) {
+      cudaMemsetAsync(counts + off, 0, sizeof(int32_t) * ng, s);
+    } else {
+      if (ng * wg > ws_words) return fail(kErrArg, "cover-count workspace too small (%lld words, need %lld)",
+                                          static_cast<long long>(ws_words), static_cast<long long>(ng * wg));
+      if (!packed || !occ_ws || !counts) return fail(kErrArg, "null device pointer");
+      DetectBitsArgs a{packed, s0, s1, g0, g1, t0, t1, dim, occ_ws};
+      if (int st = launch_detect_bits(a, s)) return st;
+      if (int st = launch_occ_counts(occ_ws, ng, wg, counts + off, s)) return st;
+    }
+    off += ng;
+  }
+  return cuda_status();
+}
+
 int pit_index_occupancy(const int32_t* counts, const int32_t* slots, int64_t n_groups, int64_t pit_grid, uint32_t* occ,
                         int32_t* bad, void* stream) {
   if (n_groups < 0 || pit_grid < 0) return fail(kErrShape, "negative index geometry");

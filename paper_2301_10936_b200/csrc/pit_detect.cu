@@ -367,6 +367,28 @@ int launch_compact(const uint32_t* occ, int64_t n_groups, int64_t WG, int32_t* c
   return cuda_status();
 }
 
+// Live micro-tiles per group (popcount of the group's occupancy words): a warp per group. Used by
+// plan selection, which needs only counts for every candidate micro-tile.
+__global__ void occ_counts_kernel(const uint32_t* __restrict__ occ, int64_t n_groups, int64_t WG,
+                                  int32_t* __restrict__ counts) {
+  const int64_t g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (g >= n_groups) return;
+  const uint32_t* row = occ + g * WG;
+  int c = 0;
+  for (int64_t w = lane; w < WG; w += 32) c += __popc(__ldg(row + w));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) counts[g] = c;
+}
+
+int launch_occ_counts(const uint32_t* occ, int64_t n_groups, int64_t WG, int32_t* counts, cudaStream_t s) {
+  if (n_groups == 0) return 0;
+  occ_counts_kernel<<<static_cast<unsigned>(ceil_div(n_groups * 32, 256)), 256, 0, s>>>(occ, n_groups, WG, counts);
+  note_launch();
+  return cuda_status();
+}
+
 int launch_union(const uint32_t* occ, int64_t n_groups, int64_t WG, uint32_t* uni, cudaStream_t s) {
   if (WG == 0) return 0;
   union_kernel<<<static_cast<unsigned>(ceil_div(WG, 256)), 256, 0, s>>>(occ, n_groups, WG, uni);

@@ -71,6 +71,7 @@ int launch_detect_bits(const DetectBitsArgs& a, cudaStream_t s);
 int launch_compact(const uint32_t* occ, int64_t n_groups, int64_t WG, int32_t* counts, int32_t* slots,
                    int64_t slot_stride, cudaStream_t s);
 int launch_union(const uint32_t* occ, int64_t n_groups, int64_t WG, uint32_t* uni, cudaStream_t s);
+int launch_occ_counts(const uint32_t* occ, int64_t n_groups, int64_t WG, int32_t* counts, cudaStream_t s);
 int launch_slots_to_occ(const int32_t* counts, const int32_t* slots, int64_t slot_stride, int64_t n_groups,
                         int64_t WG, int64_t pit_grid, uint32_t* occ, int* bad, cudaStream_t s);
 

@@ -290,3 +290,31 @@ def dump_index(idx: MicroTileIndex) -> str:
         coords = " ".join(str(int(c)) for c in np.sort(idx.group(g)))
         out.append(f"group {g} {int(idx.counts[g])}:" + (f" {coords}" if coords else ""))
     return "\n".join(out) + "\n"
+
+
+def cover_counts_device(ann: SparsityAnnotation, candidates) -> list:
+    """Per-group live micro-tile counts for many (micro_tile, pit_dim) candidates in one device pass
+    over the annotation (pit_cover_counts): what plan selection needs from detection, without
+    building any index. Returns one int64 numpy array per candidate."""
+    import torch
+
+    dev = _device.require_cuda()
+    cands = [(_micro(m), int(d)) for m, d in candidates]
+    geo = [_geometry(ann.tensor_shape, m, d) for m, d in cands]
+    total = sum(ng for ng, _, _ in geo)
+    ws = max([ng * wg for ng, _, wg in geo] + [1])
+    packed = torch.from_numpy(np.ascontiguousarray(ann.packed, dtype=np.uint8)).to(dev)
+    occ = torch.empty(ws, dtype=torch.int32, device=dev)
+    out = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+    flat = np.array([[m[0], m[1], d] for m, d in cands], dtype=np.int32).reshape(-1)
+    s0, s1 = ann.tensor_shape
+    g0, g1 = ann.granularity
+    _device.check(_lib.load().pit_cover_counts(packed.data_ptr(), s0, s1, g0, g1, len(cands), flat.ctypes.data,
+                                               occ.data_ptr(), ws, out.data_ptr(), _device.stream_ptr()),
+                  IndexBuildError)
+    host = out.cpu().numpy().astype(np.int64)
+    res, off = [], 0
+    for ng, _, _ in geo:
+        res.append(host[off : off + ng])
+        off += ng
+    return res

@@ -189,17 +189,39 @@ class PlanCandidate:
 
 class _SampleCovers:
     """Per-sample live micro-tile counts per group, memoised by (micro-tile, axis): tiles whose
-    projections coincide (e.g. every tile with M_t = 32 under pit:k) share one prefix-sum pass."""
+    projections coincide (e.g. every tile with M_t = 32 under pit:k) share one count.
 
-    def __init__(self, samples: Sequence[SparsityAnnotation]):
+    With a GPU visible the counts for every candidate come from one ``pit_cover_counts`` call per
+    sample (the detection kernel's occupancy pass, counts only); otherwise from the host prefix-sum
+    restatement. Both are exact integer counts of the same rule."""
+
+    def __init__(self, samples: Sequence[SparsityAnnotation], keys=(), device: Optional[bool] = None):
         self.samples = list(samples)
         self._memo: dict = {}
+        if device is None:
+            device = _gpu_visible()
+        keys = list(dict.fromkeys(keys))
+        if device and keys and self.samples:
+            from .index import cover_counts_device
+
+            per_sample = [cover_counts_device(a, keys) for a in self.samples]
+            for i, key in enumerate(keys):
+                self._memo[key] = [counts[i] for counts in per_sample]
 
     def counts(self, micro, dim: int) -> list:
         key = (tuple(micro), dim)
         if key not in self._memo:
             self._memo[key] = [cover_group_counts(a, micro, dim) for a in self.samples]
         return self._memo[key]
+
+
+def _gpu_visible() -> bool:
+    try:
+        import torch
+
+        return torch.cuda.is_available()
+    except Exception:  # pragma: no cover
+        return False
 
 
 def _preference(c: PlanCandidate):
@@ -229,7 +251,9 @@ def selection_candidates(expr: TensorExpr, samples, registry: KernelRegistry, pr
     axes = [a for a in sparse_operand_axes(op_kind) if a in pit_axes(expr)]
     if not axes and not allow_dense:
         raise PlanError("no applicable permuted axis and dense fallback disabled")
-    covers = _SampleCovers(samples)
+    op_axes = sparse_operand_axes(op_kind)
+    keys = [(get_micro_tile(op_kind, t.tile_shape, a)[0], op_axes.index(a)) for t in tiles for a in axes]
+    covers = _SampleCovers(samples, keys)
     n_samples = len(samples)
     out = []
     for tile in tiles:
@@ -237,7 +261,7 @@ def selection_candidates(expr: TensorExpr, samples, registry: KernelRegistry, pr
         for axis in axes if n_samples else ():
             micro, layout = get_micro_tile(op_kind, tile.tile_shape, axis)
             plan = SparseKernelPlan(op_kind, axis, micro, tile, cost, 0.0, layout, dict(extents))
-            per = covers.counts(micro, sparse_operand_axes(op_kind).index(axis))
+            per = covers.counts(micro, op_axes.index(axis))
             launches = sum(launches_from_counts(plan, c) for c in per)
             total = launches * cost
             out.append(PlanCandidate(replace(plan, estimated_cost=total / n_samples),

@@ -69,3 +69,36 @@ def test_run_tile_device_buffers(registry):
     pit.run_tile(d, [a, b], out, scratch)
     ref = 1.0 + a.double() @ b.double()
     assert float((out.double() - ref).abs().max() / ref.abs().max()) <= 1e-5
+
+
+def test_device_cover_counts_match_reference_golden_and_host():
+    import json
+    from pathlib import Path
+
+    from paper_2301_10936_b200.index import cover_counts_device
+    from paper_2301_10936_b200.policy import cover_group_counts
+
+    cases = json.loads((Path(__file__).parent / "golden" / "index_cases.json").read_text())
+    for c in cases:
+        ann = pit.random_annotation(c["shape"], c["granularity"], c["zero_ratio"], seed=c["seed"])
+        dim = 0 if c["axis"] == "m" else 1
+        cands = [(tuple(c["micro"]), dim), ((1, 1), 0), ((3, 5), 1), (tuple(c["micro"]), 1 - dim)]
+        got = cover_counts_device(ann, cands)
+        assert got[0].tolist() == c["counts"]  # reference build_index counts
+        for (m, d), g in zip(cands, got):
+            assert g.tolist() == cover_group_counts(ann, m, d).tolist()
+
+
+def test_selection_device_and_host_candidates_identical(registry):
+    from paper_2301_10936_b200.policy import _SampleCovers
+
+    fp = pit.flop_proportional_profile(registry)
+    expr = pit.bind_extents(pit.parse_expr("C[m,n] += A[m,k] * B[k,n]"), dict(m=1024, k=768, n=512))
+    samples = [pit.random_annotation((1024, 768), (8, 1), 0.9, seed=s) for s in range(3)]
+    keys = [((8, 1), 1), ((1, 32), 0), ((128, 1), 1), ((1, 64), 0)]
+    dev = _SampleCovers(samples, keys, device=True)
+    host = _SampleCovers(samples, keys, device=False)
+    for m, d in keys:
+        assert [x.tolist() for x in dev.counts(m, d)] == [x.tolist() for x in host.counts(m, d)]
+    cands = pit.selection_candidates(expr, samples, registry, fp)
+    assert cands[0].plan == pit.kernel_selection(expr, samples, registry, fp)
