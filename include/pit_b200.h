@@ -48,7 +48,7 @@ typedef enum { PIT_PLAN_DENSE = 0, PIT_PLAN_PIT_M = 1, PIT_PLAN_PIT_K = 2 } pit_
 PIT_API const char* pit_last_error(void);
 
 /* ABI version (major*100 + minor). */
-PIT_API int pit_abi_version(void);
+PIT_API int pit_abi_version(void); /* 101: pit_spmm_args gained batch / b_batch_stride */
 
 /* Number of kernels this library has launched in the process (monotonic; for launch accounting). */
 PIT_API long long pit_kernel_launches(void);
@@ -129,6 +129,13 @@ typedef struct {
   const int32_t* n_rows; /* pit:m: device scalar */
   int64_t n_rows_bound;  /* pit:m: host upper bound on *n_rows (M is always safe) */
   int force_simt;        /* 1: CUDA-core path even for bf16/fp16 */
+  /* Batched product over a prevalent axis (heads / slices), pit:k and dense only.
+   * batch <= 1: a single product. batch > 1: M is the per-slice extent; A and C hold the slices
+   * stacked along M ([batch*M, K] col-major / [batch*M, N] row-major), slice b of B starts at
+   * B + b*b_batch_stride elements, and the pit:k index is the stacked one (n_groups = batch*M/t0,
+   * so M must be a multiple of t0) -- what one detection pass over the stacked A produces. */
+  int64_t batch;
+  int64_t b_batch_stride;
 } pit_spmm_args;
 
 PIT_API int pit_spmm(const pit_spmm_args* args, void* stream);

@@ -83,6 +83,8 @@ class SpmmArgs(C.Structure):
         ("n_rows", C.c_void_p),
         ("n_rows_bound", C.c_int64),
         ("force_simt", C.c_int),
+        ("batch", C.c_int64),
+        ("b_batch_stride", C.c_int64),
     ]
 
 

@@ -117,7 +117,7 @@ extern "C" {
 
 const char* pit_last_error(void) { return g_err.c_str(); }
 
-int pit_abi_version(void) { return 100; }
+int pit_abi_version(void) { return 101; }
 
 long long pit_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
@@ -296,6 +296,8 @@ static SpmmArgs to_internal(const pit_spmm_args* p) {
   a.rows = p->rows;
   a.n_rows = p->n_rows;
   a.n_rows_host = p->n_rows_bound;
+  a.batch = p->batch > 1 ? p->batch : 1;
+  a.b_batch_stride = p->b_batch_stride;
   return a;
 }
 
@@ -311,12 +313,15 @@ int pit_spmm(const pit_spmm_args* p, void* stream) {
   if (p->M < 0 || p->N < 0 || p->K < 0) return fail(kErrShape, "shape mismatch: negative extent");
   if (p->M == 0 || p->N == 0) return kOk;
   if (!p->A || !p->B || !p->C) return fail(kErrArg, "null operand pointer");
+  const int64_t batch = p->batch > 1 ? p->batch : 1;
+  if (batch > 1 && p->plan == kPlanPitM) return fail(kErrArg, "batched products support pit:k and dense plans");
   if (p->plan == kPlanPitK) {
-    if (p->sam != 1 && p->M > 1)
+    if (p->sam != 1 && p->M * batch > 1)
       return fail(kErrLayout, "plan requires the sparse operand in col_major; use convert_layout first");
     if (!p->counts || !p->slots) return fail(kErrArg, "sparse plan needs a micro-tile index");
     if (p->t1 != 1) return fail(kErrArg, "pit:k micro-tile must be (t0,1)");
-    if (p->n_groups != ceil_div(p->M, p->t0)) return fail(kErrShape, "index groups do not match M");
+    if (batch > 1 && p->M % p->t0) return fail(kErrShape, "batched pit:k needs M to be a multiple of t0");
+    if (p->n_groups != batch * ceil_div(p->M, p->t0)) return fail(kErrShape, "index groups do not match M");
   } else if (p->plan == kPlanPitM) {
     if (p->sak != 1 && p->K > 1)
       return fail(kErrLayout, "plan requires the sparse operand in row_major; use convert_layout first");
@@ -327,10 +332,34 @@ int pit_spmm(const pit_spmm_args* p, void* stream) {
   SpmmArgs a = to_internal(p);
   if (a.K == 0) {  // empty contraction: C = 0
     const int eb = dtype_bytes(a.dtype);
-    cudaMemset2DAsync(a.C, a.ldc * eb, 0, a.N * eb, a.M, static_cast<cudaStream_t>(stream));
+    cudaMemset2DAsync(a.C, a.ldc * eb, 0, a.N * eb, a.M * batch, static_cast<cudaStream_t>(stream));
     return cuda_status();
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (batch > 1) {
+    // pit:k on tensor cores: one launch over the stacked groups
+    SpmmArgs st = a;
+    st.M = a.M * batch;
+    if (a.plan == kPlanPitK && !p->force_simt && spmm_tc_supported(st)) return launch_spmm_tc(st, s);
+    // otherwise slice by slice
+    const int eb = dtype_bytes(a.dtype);
+    const int64_t gpb = a.plan == kPlanPitK ? a.n_groups / batch : 0;
+    for (int64_t b = 0; b < batch; ++b) {
+      SpmmArgs sl = a;
+      sl.batch = 1;
+      sl.A = static_cast<const uint8_t*>(a.A) + b * a.M * a.sam * eb;
+      sl.B = static_cast<const uint8_t*>(a.B) + b * a.b_batch_stride * eb;
+      sl.C = static_cast<uint8_t*>(a.C) + b * a.M * a.ldc * eb;
+      if (a.plan == kPlanPitK) {
+        sl.counts = a.counts + b * gpb;
+        sl.slots = a.slots + b * gpb * a.slot_stride;
+        sl.n_groups = gpb;
+      }
+      const int st2 = (!p->force_simt && spmm_tc_supported(sl)) ? launch_spmm_tc(sl, s) : launch_spmm_simt(sl, s);
+      if (st2) return st2;
+    }
+    return kOk;
+  }
   if (!p->force_simt && spmm_tc_supported(a)) return launch_spmm_tc(a, s);
   return launch_spmm_simt(a, s);
 }

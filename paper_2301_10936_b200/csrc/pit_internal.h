@@ -117,6 +117,8 @@ struct SpmmArgs {
   const int32_t* rows;      // pit:m union rows (ascending), n_rows entries
   const int32_t* n_rows;    // device scalar
   int64_t n_rows_host;      // upper bound used for the grid (<= M)
+  int64_t batch = 1;        // pit:k slices stacked along M (see pit_spmm_args)
+  int64_t b_batch_stride = 0;
 };
 
 int launch_spmm_simt(const SpmmArgs& a, cudaStream_t s);

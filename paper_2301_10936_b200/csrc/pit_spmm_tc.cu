@@ -82,10 +82,11 @@ __host__ __device__ constexpr uint32_t tmem_cols_pow2() {
 // Both operands are MN-major 128B-swizzled gathers of k rows; only descriptors and the epilogue
 // differ between orientations.
 // =============================================================================================
-template <int GW, bool kOrientN, int kKS = 64>
+template <int GW, bool kOrientN, int kKS = 64, int kNT = 0>
 struct GkCfg {
   static constexpr int KS = kKS;  // gathered k per stage
-  static constexpr int N_TILE = (kOrientN || GW < 256) ? 256 : 128;
+  // n columns per unit; kNT = 128 serves narrow N (e.g. attention P.V with head dim 64)
+  static constexpr int N_TILE = kNT ? kNT : (kOrientN || GW < 256) ? 256 : 128;
   static constexpr int B_ATOMS = N_TILE / 64;
   static constexpr int A_ROW_BYTES = GW * 2 < 128 ? GW * 2 : 128;  // bytes per smem row of the A^T strip
   static constexpr int A_ATOMS = GW * 2 <= 128 ? 1 : GW * 2 / 128;
@@ -104,15 +105,17 @@ struct GkCfg {
   static constexpr int A_RPW = 32 / A_CPR;       // A rows covered by one warp instruction
 };
 
-template <int GW, bool kOrientN, bool kBF16, int kKS>
+template <int GW, bool kOrientN, bool kBF16, int kKS, int kNT>
 __global__ void __launch_bounds__(kThreads, 1)
     spmm_gk_kernel(const void* __restrict__ Bv, int64_t ldb, const void* __restrict__ Atv, int64_t lda,
                    const int32_t* __restrict__ counts, const int32_t* __restrict__ slots, int64_t slot_stride,
                    int n_groups, int n_tiles, int M, int N, int K, void* __restrict__ Cv, int64_t ldc,
-                   int grp_rows) {
+                   int grp_rows, int gpb, int64_t b_batch_stride) {
   // grp_rows (<= GW, multiple of 8): rows per group. Micro-tiles narrower than the kernel's GW run
   // in it with the A^T strip's extra columns zero-filled and never stored.
-  using Cfg = GkCfg<GW, kOrientN, kKS>;
+  // Batched (prevalent axis, e.g. attention heads): slices are stacked along M in A and C (slice b
+  // owns groups [b*gpb, (b+1)*gpb)); only B differs per slice, at b * b_batch_stride elements.
+  using Cfg = GkCfg<GW, kOrientN, kKS, kNT>;
   using OT = OutT<kBF16>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -158,6 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // stages ahead of their use so the L2 latency of the slot loads never stalls issue.
     struct Pos {
       int u, g, t, kb, cnt;  // unit, its group and n tile (tracked without division), chunk, count
+      int b;                 // batch slice of the group (one division per unit, not per stage)
     };
     const int step_t = static_cast<int>(gridDim.x) / n_groups;
     const int step_g = static_cast<int>(gridDim.x) % n_groups;
@@ -179,6 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           next_unit(q);
           q.cnt = q.u < units ? __ldg(counts + q.g) : 0;
         } while (q.u < units && q.cnt == 0);
+        q.b = q.g / gpb;
       }
       return q;
     };
@@ -199,8 +204,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       return x;
     };
     Pos cur{static_cast<int>(blockIdx.x), static_cast<int>(blockIdx.x) % n_groups,
-            static_cast<int>(blockIdx.x) / n_groups, 0, 0};
+            static_cast<int>(blockIdx.x) / n_groups, 0, 0, 0};
     cur.cnt = cur.u < units ? __ldg(counts + cur.g) : 0;
+    cur.b = cur.g / gpb;
     if (cur.u < units && cur.cnt == 0) {
       cur.kb = Cfg::KS;  // force advance() past the empty unit
       cur = advance(cur);
@@ -236,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int ch = cb + lane;
           const int n = n0 + ch * 8;
           const uint32_t nbytes = n < N ? static_cast<uint32_t>(min(16, (N - n) * 2)) : 0u;
-          const T* bcol = Bp + (nbytes ? n : 0);
+          const T* bcol = Bp + cur.b * b_batch_stride + (nbytes ? n : 0);
           // row & 7 == warp for every row this warp copies: one swizzled offset
           const uint32_t base = sB + (ch >> 3) * (Cfg::KS * 128) + warp * 128 + (((ch & 7) ^ warp) << 4);
           // slot block q (32 rows) holds rows warp + 32q + {0, 8, 16, 24}: i2 = 2q + (0|1), j = 0|1
@@ -743,21 +749,23 @@ CUtensorMapSwizzle swizzle_enum(int row_bytes) {
                            : CU_TENSOR_MAP_SWIZZLE_NONE;
 }
 
-template <int GW, bool kOrientN, bool kBF16, int kKS = 64>
+template <int GW, bool kOrientN, bool kBF16, int kKS = 64, int kNT = 0>
 int run_gk(const SpmmArgs& a, cudaStream_t s) {
-  using Cfg = GkCfg<GW, kOrientN, kKS>;
+  using Cfg = GkCfg<GW, kOrientN, kKS, kNT>;
   const int n_tiles = static_cast<int>(ceil_div(a.N, Cfg::N_TILE));
   const int64_t units = a.n_groups * n_tiles;
   if (units == 0) return kOk;
   if (units >= (1ll << 31)) return kErrShape;
-  auto kern = spmm_gk_kernel<GW, kOrientN, kBF16, kKS>;
+  auto kern = spmm_gk_kernel<GW, kOrientN, kBF16, kKS, kNT>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::SMEM));
   const int grid = static_cast<int>(units < num_sms() ? units : num_sms());
   // A column-major: A^T is row-major [K, M] with pitch sak
   kern<<<grid, kThreads, Cfg::SMEM, s>>>(a.B, a.ldb, a.A, a.sak, a.counts, a.slots, a.slot_stride,
                                          static_cast<int>(a.n_groups), n_tiles, static_cast<int>(a.M),
                                          static_cast<int>(a.N), static_cast<int>(a.K), a.C, a.ldc,
-                                         static_cast<int>(a.t0));
+                                         static_cast<int>(a.t0),
+                                         static_cast<int>(a.batch > 1 ? a.n_groups / a.batch : a.n_groups),
+                                         a.batch > 1 ? a.b_batch_stride : 0);
   note_launch();
   return cuda_status();
 }
@@ -827,24 +835,31 @@ int gk_ks_override() {
   return v;
 }
 
+template <bool kBF16, int kNT>
+int dispatch_gk(const SpmmArgs& a, int gw, cudaStream_t s) {
+  const bool ks64 = gk_ks_override() == 64;
+  switch (gw) {
+    case 16:
+      return ks64 ? run_gk<16, false, kBF16, 64, kNT>(a, s) : run_gk<16, false, kBF16, 128, kNT>(a, s);
+    case 32:
+      return ks64 ? run_gk<32, false, kBF16, 64, kNT>(a, s) : run_gk<32, false, kBF16, 128, kNT>(a, s);
+    case 64:
+      return ks64 ? run_gk<64, false, kBF16, 64, kNT>(a, s) : run_gk<64, false, kBF16, 128, kNT>(a, s);
+    case 128:
+      return ks64 ? run_gk<128, true, kBF16, 64, kNT>(a, s) : run_gk<128, true, kBF16, 128, kNT>(a, s);
+    case 256:
+      return run_gk<256, false, kBF16, 64, 128>(a, s);
+    default:
+      return kErrUnsupported;
+  }
+}
+
 template <bool kBF16>
 int dispatch_tc(const SpmmArgs& a, cudaStream_t s) {
   if (a.plan == kPlanPitK) {
     const int gw = a.t0 <= 16 ? 16 : a.t0 <= 32 ? 32 : a.t0 <= 64 ? 64 : a.t0 <= 128 ? 128 : 256;
-    switch (gw) {
-      case 16:
-        return gk_ks_override() == 64 ? run_gk<16, false, kBF16, 64>(a, s) : run_gk<16, false, kBF16, 128>(a, s);
-      case 32:
-        return gk_ks_override() == 64 ? run_gk<32, false, kBF16, 64>(a, s) : run_gk<32, false, kBF16, 128>(a, s);
-      case 64:
-        return gk_ks_override() == 64 ? run_gk<64, false, kBF16, 64>(a, s) : run_gk<64, false, kBF16, 128>(a, s);
-      case 128:
-        return gk_ks_override() == 64 ? run_gk<128, true, kBF16, 64>(a, s) : run_gk<128, true, kBF16, 128>(a, s);
-      case 256:
-        return run_gk<256, false, kBF16, 64>(a, s);
-      default:
-        return kErrUnsupported;
-    }
+    // narrow products (N <= 128, e.g. attention P.V) use 128-column units: no zero-filled half tile
+    return a.N <= 128 ? dispatch_gk<kBF16, 128>(a, gw, s) : dispatch_gk<kBF16, 0>(a, gw, s);
   }
   const int t1 = a.plan == kPlanDense ? 64 : a.t1;
   if (t1 % 64 == 0) return run_gm<kBF16>(a, 64, s);

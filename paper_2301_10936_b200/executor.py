@@ -641,3 +641,127 @@ def run_tile(desc, inputs, out, scratch=None) -> None:
         _scatter_whole(ins[1].reshape(-1, 1), o2, True)
     if host_out:
         out[...] = _device.to_host(o).reshape(out_shape)
+
+
+# ------------------------------------------------------------------ batched (prevalent axis)
+def stack_slices(A3, plan: SparseKernelPlan):
+    """Explicit layout conversion for batched products (convert_layout's counterpart): returns the
+    [batch, M, K] operand as a device view over ONE buffer with the slices stacked along M, col-major
+    for pit:k ([K, batch*M] row-major underneath) and row-major for dense."""
+    torch = _torch()
+    x = _device.to_device(np.ascontiguousarray(A3) if not _is_torch(A3) else A3)
+    if x.dim() != 3:
+        raise ExecError(f"batched operand must have rank 3, got {x.dim()}")
+    b, m, k = x.shape
+    if plan.is_dense:
+        return x.contiguous()
+    flat = torch.empty((k, b * m), dtype=x.dtype, device=x.device)
+    flat.view(k, b, m).copy_(x.permute(2, 0, 1))
+    return flat.view(k, b, m).permute(1, 2, 0)
+
+
+def _stacked_2d(A3, plan: SparseKernelPlan):
+    """The [batch*M, K] 2-D view of a stacked batched operand; LayoutError if A3 is not stacked."""
+    b, m, k = (int(d) for d in A3.shape)
+    s0, s1, s2 = A3.stride()
+    if plan.is_dense:
+        ok = s2 == 1 and s1 == k and s0 == m * k
+        return A3.reshape(b * m, k) if ok or b * m * k == 0 else _layout_error(plan)
+    ok = s1 == 1 and s0 == m and s2 == b * m
+    if not (ok or b * m * k == 0 or (m == 1 and b == 1)):
+        _layout_error(plan)
+    return A3.permute(2, 0, 1).reshape(k, b * m).t()
+
+
+def _layout_error(plan):
+    raise LayoutError(f"batched plan requires slices stacked along M in {plan.sparse_layout}; use stack_slices first")
+
+
+def build_batched_index_from_tensor(A3, micro_tile, pit_axis="k") -> MicroTileIndex:
+    """One detection pass over a stacked [batch, M, K] operand (see stack_slices): the index of the
+    stacked [batch*M, K] view, i.e. the per-slice indices back to back (slice b owns groups
+    [b*M/t0, (b+1)*M/t0))."""
+    from .index import build_index_from_tensor
+
+    if int(A3.shape[1]) % int(micro_tile[0]):
+        raise ExecError("batched pit:k needs M to be a multiple of the micro-tile height")
+    dummy = SparseKernelPlan("matmul", "k", tuple(micro_tile), None, 0.0, 0.0, COL_MAJOR, {})
+    return build_index_from_tensor(_stacked_2d(A3, dummy), micro_tile, pit_axis)
+
+
+def build_batched_index(anns, micro_tile, pit_axis="k") -> MicroTileIndex:
+    """Stacked index from one annotation per slice (each slice's block grid must tile M exactly)."""
+    from .sparsity import from_bits
+
+    anns = list(anns)
+    if not anns:
+        raise ExecError("batched index needs at least one annotation")
+    shape, gran = tuple(anns[0].tensor_shape), tuple(anns[0].granularity)
+    if any(tuple(a.tensor_shape) != shape or tuple(a.granularity) != gran for a in anns):
+        raise ExecError("batched annotations must share shape and granularity")
+    if shape[0] % gran[0] or shape[0] % int(micro_tile[0]):
+        raise ExecError("batched pit:k needs M to be a multiple of the granularity and the micro-tile height")
+    stacked = from_bits(np.concatenate([a.bits() for a in anns], axis=0), (len(anns) * shape[0], shape[1]), gran)
+    return build_index(stacked, micro_tile, pit_axis)
+
+
+def run_batched_matmul_with_index(plan: SparseKernelPlan, A3, B3, idx: Optional[MicroTileIndex],
+                                  stats: Optional[ExecStats] = None):
+    """C[b] = A[b] @ B[b] for every slice in ONE launch (pit:k on tensor cores), with A stacked along
+    M (stack_slices) and idx the stacked index. Same per-slice semantics as run_matmul_with_index
+    (an independent index per slice of the prevalent axis). Returns a [batch, M, N]
+    tensor on the device (or numpy when B3 is a host array)."""
+    torch = _torch()
+    if plan.op_kind != "matmul" or plan.pit_axis == "m":
+        raise ExecError("batched products support pit:k and dense matmul plans")
+    host = not _is_torch(B3) or not B3.is_cuda
+    Ad = _stacked_2d(A3 if _is_torch(A3) and A3.is_cuda else stack_slices(A3, plan), plan)
+    Bd = _device.to_device(np.ascontiguousarray(B3) if not _is_torch(B3) else B3)
+    batch, M, K = (int(d) for d in A3.shape)
+    if Bd.dim() != 3 or int(Bd.shape[0]) != batch or int(Bd.shape[1]) != K:
+        raise ExecError(f"shape mismatch {tuple(A3.shape)} @ {tuple(Bd.shape)}")
+    N = int(Bd.shape[2])
+    if (plan.extents["m"], plan.extents["k"], plan.extents["n"]) != (M, K, N):
+        raise ExecError(f"plan bound to {dict(plan.extents)} but got slices {M}x{K}x{N}")
+    if Bd.stride(2) != 1 and N > 1:
+        Bd = Bd.contiguous()
+    if Ad.dtype != Bd.dtype:
+        raise ExecError(f"mixed dtypes {Ad.dtype} and {Bd.dtype}")
+    C3 = torch.empty((batch, M, N), dtype=Bd.dtype, device=Bd.device)
+    a = _lib.SpmmArgs()
+    a.plan = _PLAN_CODE["dense" if plan.is_dense else "k"]
+    a.dtype = _device.dtype_code(Bd)
+    a.M, a.N, a.K = M, N, K
+    a.A = Ad.data_ptr()
+    a.sam, a.sak = Ad.stride()
+    a.B = Bd.data_ptr()
+    a.ldb = Bd.stride(1)
+    a.C = C3.data_ptr()
+    a.ldc = N
+    a.batch = batch
+    a.b_batch_stride = Bd.stride(0)
+    keep = []
+    if not plan.is_dense:
+        if idx is None or idx.pit_axis != "k" or tuple(idx.micro_tile) != tuple(plan.micro_tile):
+            raise ExecError("batched pit:k plan needs the stacked index of its micro-tile")
+        if idx.n_groups != batch * -(-M // plan.micro_tile[0]):
+            raise ExecError(f"index has {idx.n_groups} groups, stacked operand needs {batch * -(-M // plan.micro_tile[0])}")
+        a.t0, a.t1 = plan.micro_tile
+        a.n_groups = idx.n_groups
+        a.slot_stride = idx.pit_grid
+        a.counts, a.slots, alive = idx.device_ptrs()
+        keep += list(alive)
+    _device.check(_lib.load().pit_spmm(C.byref(a), _device.stream_ptr()), ExecError)
+    if stats is not None:
+        if plan.is_dense:
+            stats.launches += batch * dense_launches(plan)
+        else:
+            stats.launches += launches_from_counts(plan, idx.counts)
+            stats.gathered_micro_tiles += idx.total
+    return _device.to_host(C3.reshape(batch * M, N)).reshape(batch, M, N) if host else C3
+
+
+def run_sparse_batched_matmul(plan: SparseKernelPlan, A3, B3, anns, stats: Optional[ExecStats] = None):
+    """Batched run_sparse_matmul: per-slice annotations -> stacked index -> one launch."""
+    idx = None if plan.is_dense else build_batched_index(anns, plan.micro_tile, plan.pit_axis)
+    return run_batched_matmul_with_index(plan, A3, B3, idx, stats=stats)

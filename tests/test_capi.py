@@ -65,7 +65,7 @@ def test_geometry_and_validation_without_gpu(lib):
     args.sam, args.sak = 64, 1
     assert lib.pit_spmm(C.byref(args), None) == _lib.PIT_ERR_LAYOUT
     assert "col_major" in _lib.last_error()
-    assert lib.pit_abi_version() == 100
+    assert lib.pit_abi_version() == 101
     assert lib.pit_kernel_launches() == 0
 
 
@@ -73,7 +73,10 @@ def test_spmm_args_struct_matches_header():
     """Field order of the ctypes mirror equals the C struct's."""
     from paper_2301_10936_b200 import _lib
 
+    import re
+
     body = HEADER.read_text().split("typedef struct {", 1)[1].split("} pit_spmm_args;", 1)[0]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
     names = []
     for line in body.splitlines():
         line = line.split("/*")[0].strip().rstrip(";")
