@@ -314,7 +314,6 @@ int pit_spmm(const pit_spmm_args* p, void* stream) {
   if (p->M == 0 || p->N == 0) return kOk;
   if (!p->A || !p->B || !p->C) return fail(kErrArg, "null operand pointer");
   const int64_t batch = p->batch > 1 ? p->batch : 1;
-  if (batch > 1 && p->plan == kPlanPitM) return fail(kErrArg, "batched products support pit:k and dense plans");
   if (p->plan == kPlanPitK) {
     if (p->sam != 1 && p->M * batch > 1)
       return fail(kErrLayout, "plan requires the sparse operand in col_major; use convert_layout first");
@@ -325,7 +324,7 @@ int pit_spmm(const pit_spmm_args* p, void* stream) {
   } else if (p->plan == kPlanPitM) {
     if (p->sak != 1 && p->K > 1)
       return fail(kErrLayout, "plan requires the sparse operand in row_major; use convert_layout first");
-    if (!p->occ || !p->rows || !p->n_rows) return fail(kErrArg, "sparse plan needs a micro-tile index");
+    if (!p->occ || (batch == 1 && (!p->rows || !p->n_rows))) return fail(kErrArg, "sparse plan needs a micro-tile index");
     if (p->t0 != 1) return fail(kErrArg, "pit:m micro-tile must be (1,t1)");
     if (p->n_groups != ceil_div(p->K, p->t1)) return fail(kErrShape, "index groups do not match K");
   }
@@ -339,8 +338,17 @@ int pit_spmm(const pit_spmm_args* p, void* stream) {
   if (batch > 1) {
     // pit:k on tensor cores: one launch over the stacked groups
     SpmmArgs st = a;
-    st.M = a.M * batch;
-    if (a.plan == kPlanPitK && !p->force_simt && spmm_tc_supported(st)) return launch_spmm_tc(st, s);
+    if (a.plan == kPlanPitK) {
+      st.M = a.M * batch;
+      if (!p->force_simt && spmm_tc_supported(st)) return launch_spmm_tc(st, s);
+    } else {
+      // pit:m / dense: one launch over uniform row groups, B slices through a 3-D tensor map
+      const bool tc = !p->force_simt && spmm_tc_supported(st) && (a.b_batch_stride * 2) % 16 == 0 &&
+                      a.M * batch < (1ll << 31);
+      if (tc) return launch_spmm_tc(st, s);
+      if (a.plan == kPlanPitM)
+        return fail(kErrUnsupported, "batched pit:m runs on the tensor-core path only (bf16/fp16, 16-byte aligned rows)");
+    }
     // otherwise slice by slice
     const int eb = dtype_bytes(a.dtype);
     const int64_t gpb = a.plan == kPlanPitK ? a.n_groups / batch : 0;

@@ -195,24 +195,40 @@ __global__ void __launch_bounds__(kGenThreads) detect_generic_kernel(const uint8
 // ---------------------------------------------------------------------------
 // Pass 1, annotation route: packed MSB-first block bits. One warp per (group, word).
 // ---------------------------------------------------------------------------
-__global__ void detect_bits_kernel(const uint8_t* __restrict__ packed, int64_t s0, int64_t s1, int g0, int g1,
-                                   int t0, int t1, int pit_dim, int64_t n_groups, int64_t pit_grid, int64_t WG,
-                                   uint32_t* __restrict__ occ) {
-  const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+// kPow2: micro-tile and granularity along the coordinate axis are powers of two (lct / lcg their
+// log2), so the coordinate's block range needs shifts, not divisions — the common PIT geometry.
+template <typename I, bool kPow2>
+__global__ void detect_bits_kernel(const uint8_t* __restrict__ packed, I s0, I s1, int g0, int g1, int t0, int t1,
+                                   int pit_dim, I n_groups, I pit_grid, I WG, uint32_t* __restrict__ occ,
+                                   int lct, int lcg) {
+  // I = int32_t whenever every index fits (the common case): 64-bit integer division costs ~5x more.
+  // Grid-stride over (group, word) warp items: one resident wave of blocks instead of short-lived ones.
   const int lane = threadIdx.x & 31;
-  if (gw >= n_groups * WG) return;
-  const int64_t g = gw / WG, w = gw % WG;
-  const int64_t coord = w * 32 + lane;
+  const I n_items = n_groups * WG;
+  const I step = static_cast<I>(gridDim.x) * (blockDim.x >> 5);
+  for (I gw = (static_cast<I>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; gw < n_items; gw += step) {
+  const I g = gw / WG, w = gw - g * WG;
+  const I coord = w * 32 + lane;
+  const I bg1 = (s1 + g1 - 1) / g1;
+  // block range of the group (warp-uniform) and of this lane's coordinate
+  const I gs = pit_dim == 0 ? s1 : s0, gt = pit_dim == 0 ? t1 : t0, gg = pit_dim == 0 ? g1 : g0;
+  const I glo = (g * gt) / gg, ghi = (min((g + 1) * gt, gs) + gg - 1) / gg;
   bool live = false;
   if (coord < pit_grid) {
-    const int64_t i = pit_dim == 0 ? coord : g;
-    const int64_t j = pit_dim == 0 ? g : coord;
-    const int64_t bg1 = (s1 + g1 - 1) / g1;
-    const int64_t b0 = (i * t0) / g0, b1 = (min((i + 1) * t0, s0) + g0 - 1) / g0;
-    const int64_t c0 = (j * t1) / g1, c1 = (min((j + 1) * t1, s1) + g1 - 1) / g1;
-    for (int64_t bi = b0; bi < b1 && !live; ++bi) {
-      for (int64_t bj = c0; bj < c1; ++bj) {
-        const int64_t f = bi * bg1 + bj;
+    const I cs = pit_dim == 0 ? s0 : s1, ct = pit_dim == 0 ? t0 : t1, cg = pit_dim == 0 ? g0 : g1;
+    I clo, chi;
+    if constexpr (kPow2) {
+      clo = (coord << lct) >> lcg;
+      chi = (min((coord + 1) << lct, cs) + cg - 1) >> lcg;
+    } else {
+      clo = (coord * ct) / cg;
+      chi = (min((coord + 1) * ct, cs) + cg - 1) / cg;
+    }
+    const I b0 = pit_dim == 0 ? clo : glo, b1 = pit_dim == 0 ? chi : ghi;
+    const I c0 = pit_dim == 0 ? glo : clo, c1 = pit_dim == 0 ? ghi : chi;
+    for (I bi = b0; bi < b1 && !live; ++bi) {
+      for (I bj = c0; bj < c1; ++bj) {
+        const I f = bi * bg1 + bj;
         if ((__ldg(packed + (f >> 3)) >> (7 - (f & 7))) & 1) {
           live = true;
           break;
@@ -221,28 +237,56 @@ __global__ void detect_bits_kernel(const uint8_t* __restrict__ packed, int64_t s
     }
   }
   const uint32_t word = __ballot_sync(0xffffffffu, live);
-  if (lane == 0) occ[g * WG + w] = word;
+  if (lane == 0) occ[static_cast<int64_t>(g) * WG + w] = word;
+  }
 }
 
 // ---------------------------------------------------------------------------
 // Pass 2: per-group ordered compaction. One warp per group.
 // ---------------------------------------------------------------------------
+int sm_count() {
+  static int sms = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+  }();
+  return sms;
+}
+
 constexpr int kCompactThreads = 256;
 
 // One block per group; thread t owns word t of each 256-word chunk (coordinates stay ascending
 // across threads); block-wide exclusive scan of per-word popcounts gives each thread its slot base.
+// Few long groups (e.g. pit:m over tall operands): blockIdx.y splits a group's words into ranges of
+// words_per_split; a split first counts the live coordinates before its range (re-reading those
+// words, cheap next to the scan) so every split writes its slots independently.
 __global__ void __launch_bounds__(kCompactThreads) compact_kernel(const uint32_t* __restrict__ occ, int64_t n_groups,
                                                                   int64_t WG, int32_t* __restrict__ counts,
-                                                                  int32_t* __restrict__ slots, int64_t slot_stride) {
+                                                                  int32_t* __restrict__ slots, int64_t slot_stride,
+                                                                  int64_t words_per_split) {
   __shared__ int warp_tot[kCompactThreads / 32];
   const int64_t g = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t* row = occ + g * WG;
   int32_t* out = slots + g * slot_stride;
+  const int64_t w_begin = static_cast<int64_t>(blockIdx.y) * words_per_split;
+  const int64_t w_end = w_begin + words_per_split < WG ? w_begin + words_per_split : WG;
   int base = 0;
-  for (int64_t w0 = 0; w0 < WG; w0 += kCompactThreads) {
+  if (w_begin > 0) {
+    int pre = 0;
+    for (int64_t w = threadIdx.x; w < w_begin; w += kCompactThreads) pre += __popc(__ldg(row + w));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+    if (lane == 0) warp_tot[warp] = pre;
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kCompactThreads / 32; ++i) base += warp_tot[i];
+    __syncthreads();
+  }
+  for (int64_t w0 = w_begin; w0 < w_end; w0 += kCompactThreads) {
     const int64_t w = w0 + threadIdx.x;
-    uint32_t word = w < WG ? __ldg(row + w) : 0u;
+    uint32_t word = w < w_end ? __ldg(row + w) : 0u;
     const int c = __popc(word);
     int incl = c;
 #pragma unroll
@@ -268,7 +312,7 @@ __global__ void __launch_bounds__(kCompactThreads) compact_kernel(const uint32_t
     base += total;
     __syncthreads();
   }
-  if (threadIdx.x == 0) counts[g] = base;
+  if (threadIdx.x == 0 && blockIdx.y == gridDim.y - 1) counts[g] = base;
 }
 
 // OR of all group rows: the union of live coordinates (used by pit:m union-row tiles).
@@ -351,8 +395,28 @@ int launch_detect_bits(const DetectBitsArgs& a, cudaStream_t s) {
   if (n_groups == 0 || pit_grid == 0) return 0;
   const int64_t warps = n_groups * WG;
   const int threads = 256;
-  detect_bits_kernel<<<static_cast<unsigned>(ceil_div(warps * 32, threads)), threads, 0, s>>>(
-      a.packed, a.s0, a.s1, a.g0, a.g1, a.t0, a.t1, a.pit_dim, n_groups, pit_grid, WG, a.occ);
+  const int64_t needed = ceil_div(warps * 32, threads);
+  const int64_t wave = static_cast<int64_t>(sm_count()) * 8;
+  const unsigned blocks = static_cast<unsigned>(needed < wave ? needed : wave);
+  // 32-bit indexing when the thread count, the block-grid size and every (i+1)*t product fit
+  const int64_t G0b = ceil_div(a.s0, a.g0), G1b = ceil_div(a.s1, a.g1);
+  const bool fits32 = warps * 32 < (1ll << 31) && G0b * G1b < (1ll << 31) &&
+                      (a.s0 + a.t0) * 2 < (1ll << 31) && (a.s1 + a.t1) * 2 < (1ll << 31);
+  const int ct = a.pit_dim == 0 ? a.t0 : a.t1, cg = a.pit_dim == 0 ? a.g0 : a.g1;
+  const bool pow2 = (ct & (ct - 1)) == 0 && (cg & (cg - 1)) == 0;
+  const int lct = pow2 ? __builtin_ctz(static_cast<unsigned>(ct)) : 0;
+  const int lcg = pow2 ? __builtin_ctz(static_cast<unsigned>(cg)) : 0;
+  if (fits32 && pow2)
+    detect_bits_kernel<int32_t, true><<<blocks, threads, 0, s>>>(
+        a.packed, static_cast<int32_t>(a.s0), static_cast<int32_t>(a.s1), a.g0, a.g1, a.t0, a.t1, a.pit_dim,
+        static_cast<int32_t>(n_groups), static_cast<int32_t>(pit_grid), static_cast<int32_t>(WG), a.occ, lct, lcg);
+  else if (fits32)
+    detect_bits_kernel<int32_t, false><<<blocks, threads, 0, s>>>(
+        a.packed, static_cast<int32_t>(a.s0), static_cast<int32_t>(a.s1), a.g0, a.g1, a.t0, a.t1, a.pit_dim,
+        static_cast<int32_t>(n_groups), static_cast<int32_t>(pit_grid), static_cast<int32_t>(WG), a.occ, 0, 0);
+  else
+    detect_bits_kernel<int64_t, false><<<blocks, threads, 0, s>>>(a.packed, a.s0, a.s1, a.g0, a.g1, a.t0, a.t1,
+                                                                  a.pit_dim, n_groups, pit_grid, WG, a.occ, 0, 0);
   note_launch();
   return cuda_status();
 }
@@ -361,8 +425,19 @@ int launch_compact(const uint32_t* occ, int64_t n_groups, int64_t WG, int32_t* c
                    int64_t slot_stride, cudaStream_t s) {
   if (n_groups == 0) return 0;
   if (n_groups >= (1ll << 31)) return kErrShape;
-  compact_kernel<<<static_cast<unsigned>(n_groups), kCompactThreads, 0, s>>>(occ, n_groups, WG, counts, slots,
-                                                                            slot_stride);
+  // split long groups when there are too few groups to fill the GPU
+  int64_t splits = 1, wps = WG;
+  const int64_t target = 2 * static_cast<int64_t>(sm_count());
+  if (n_groups < target && WG > 4 * kCompactThreads) {
+    splits = ceil_div(target, n_groups);
+    const int64_t max_splits = ceil_div(WG, kCompactThreads);
+    if (splits > max_splits) splits = max_splits;
+    if (splits > 65535) splits = 65535;
+    wps = ceil_div(ceil_div(WG, splits), kCompactThreads) * kCompactThreads;
+    splits = ceil_div(WG, wps);
+  }
+  dim3 grid(static_cast<unsigned>(n_groups), static_cast<unsigned>(splits));
+  compact_kernel<<<grid, kCompactThreads, 0, s>>>(occ, n_groups, WG, counts, slots, slot_stride, wps);
   note_launch();
   return cuda_status();
 }

@@ -115,6 +115,16 @@ __device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, uint32_t byte
 }
 
 // Named barrier over `count` threads returning the OR of `pred` across them.
+__device__ __forceinline__ void bar_sync_named(int id, int count) {
+  asm volatile("barrier.cta.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// bits [a, b) of a 32-bit word set, 0 <= a < b <= 32
+__device__ __forceinline__ uint32_t bit_range(int a, int b) {
+  const uint32_t hi = b >= 32 ? 0xffffffffu : ((1u << b) - 1u);
+  return hi & ~((1u << a) - 1u);
+}
+
 __device__ __forceinline__ bool bar_or(int id, int count, bool pred) {
   uint32_t r;
   asm volatile(

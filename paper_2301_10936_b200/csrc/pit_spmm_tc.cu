@@ -465,22 +465,27 @@ struct RowGemmParams {
   int64_t dst_stride;
   const float* row_scale;   // indexed by C row
   int act;                  // 0 none, 1 relu
-  const uint32_t* occ;      // liveness bitmap (G == 1) or nullptr
+  const uint32_t* occ;      // liveness bitmap [K/t1 groups][WG words over source rows] or nullptr
   int64_t WG;
   int t1;
   int max_tiles;            // host bound on the total number of row tiles
+  int uniform_rows;         // cnt == nullptr && G > 1: every group is this many consecutive rows
 };
 
-template <int KS>
+template <int KS, int kBN = 256>
 struct GmCfg {
   static constexpr int BM = 128;
-  static constexpr int BN = 256;
+  static constexpr int BN = kBN;  // 256, or 64 for narrow products (attention P.V)
   static constexpr int A_ROW_BYTES = KS * 2;  // K-major rows
   static constexpr int A_BYTES = BM * A_ROW_BYTES;
   static constexpr int B_BYTES = (BN / 64) * KS * 128;  // MN-major, 4 atoms of 64 n
   static constexpr int STAGE_BYTES = ((A_BYTES + B_BYTES + 1023) / 1024) * 1024;
   static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
-  static constexpr int TMEM_COLS = 512;  // 2 accumulators x 256 columns
+  static constexpr int TMEM_COLS = tmem_cols_pow2<2 * BN>();  // 2 accumulators
+  // occupancy words of the current row tile for every K-group (contiguous-row units): 5 words per
+  // group cover 128 rows at any 32-row alignment
+  static constexpr int OCC_MAX_GROUPS = 512;   // static shared: 5 words per K-group
+  static constexpr int KB_MAX = 1024;          // static shared: live-K-block bitmask
   static constexpr size_t SMEM = static_cast<size_t>(STAGES) * STAGE_BYTES + 1024 + 512;
   static constexpr uint32_t A_SW = sw_layout_for_row(A_ROW_BYTES);
 };
@@ -492,6 +497,11 @@ struct RowTile {
 // Decode row tile t (global index) -> group and rows. Identical in every role.
 __device__ __forceinline__ RowTile decode_tile(const RowGemmParams& p, int t, int single_rows) {
   if (p.cnt == nullptr) {
+    if (p.uniform_rows) {  // batched slices of equal height, stacked along M
+      const int tpg = (p.uniform_rows + 127) >> 7;
+      const int g = t / tpg, start = (t - g * tpg) * 128;
+      return {g, g * p.uniform_rows + start, min(128, p.uniform_rows - start)};
+    }
     const int base = t * 128;
     return {0, base, min(128, single_rows - base)};
   }
@@ -517,10 +527,10 @@ __device__ __forceinline__ int tile_dst_row(const RowGemmParams& p, const RowTil
   return __ldg(p.row_dst + static_cast<int64_t>(rt.g) * p.dst_stride + within);
 }
 
-template <int KS, bool kBF16>
+template <int KS, bool kBF16, int kBN>
 __global__ void __launch_bounds__(kThreads, 1)
     rowgemm_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ RowGemmParams p, int n_tiles) {
-  using Cfg = GmCfg<KS>;
+  using Cfg = GmCfg<KS, kBN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
@@ -528,12 +538,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull_bar = empty_bar + Cfg::STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  int32_t* acc_live = reinterpret_cast<int32_t*>(tmem_slot + 2);    // per accumulator: 0 = no MMA (all zero)
   int32_t* stage_live = reinterpret_cast<int32_t*>(tmem_slot + 4);  // per stage: 1 = MMA, 0 = skipped
+  __shared__ uint32_t tile_occ[Cfg::OCC_MAX_GROUPS * 5];  // the row tile's occupancy words per K-group
+  __shared__ uint32_t kb_live[Cfg::KB_MAX / 32];            // bit kb: some row of the tile is live
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int single_rows = p.cnt ? 0 : (p.n_rows ? *p.n_rows : p.M);
-  const int total_tiles = p.cnt ? __ldg(p.tile_off + p.G) : (single_rows + 127) / 128;
+  const int total_tiles = p.cnt ? __ldg(p.tile_off + p.G)
+                         : p.uniform_rows ? p.G * ((p.uniform_rows + 127) / 128) : (single_rows + 127) / 128;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < Cfg::STAGES; ++i) {
@@ -541,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&empty_bar[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&tfull_bar[i], 1);
+      mbar_init(&tfull_bar[i], 2);  // MMA commit + the issuer's release of acc_live
       mbar_init(&tempty_bar[i], 128);
     }
     fence_mbar_init();
@@ -571,6 +585,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     const T* Ap = static_cast<const T*>(p.A);
     int stage = 0;
     uint32_t phase = 0;
+    // Contiguous row tiles (dense, batched slices): the tile's occupancy words for every K-group are
+    // staged in shared memory once per unit, so a K-block's liveness costs no L2 round trip and no
+    // barrier (every producer derives the same stage verdict). Union-row tiles look bits up per row.
+    const int nkg = p.occ ? (p.K + p.t1 - 1) / p.t1 : 0;
+    const bool staged = p.occ != nullptr && p.row_src == nullptr && nkg <= Cfg::OCC_MAX_GROUPS &&
+                        kblocks <= Cfg::KB_MAX;
+    // next live K-block after kb (staged units): dead K-blocks cost no producer work at all
+    auto next_kb = [&](int kb) {
+      int start = kb + 1;
+      int w = start >> 5;
+      if (w * 32 >= kblocks) return kblocks;
+      uint32_t bits = kb_live[w] & (0xffffffffu << (start & 31));
+      while (!bits) {
+        if (++w * 32 >= kblocks) return kblocks;
+        bits = kb_live[w];
+      }
+      return min(w * 32 + __ffs(bits) - 1, kblocks);
+    };
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const RowTile rt = decode_tile(p, u / n_tiles, single_rows);
       const int n0 = (u % n_tiles) * Cfg::BN;
@@ -580,33 +612,70 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int i = tp / CPR + j * RSTEP;
         rid[j] = i < rt.rows ? tile_src_row(p, rt, i) : -1;
       }
-      for (int kb = 0; kb < kblocks; ++kb) {
+      const int w0 = rt.base >> 5, sh = rt.base & 31;
+      if (staged) {
+        bar_sync_named(2, kProdThreads);  // every producer is done with the previous unit's words
+        for (int e = tp; e < nkg * 5; e += kProdThreads) {
+          const int kg = e / 5;
+          const int64_t word = static_cast<int64_t>(w0) + (e - kg * 5);
+          tile_occ[e] = word < p.WG ? __ldg(p.occ + static_cast<int64_t>(kg) * p.WG + word) : 0u;
+        }
+        bar_sync_named(2, kProdThreads);
+        // one bit per K-block: does any row of this tile hold a live micro-tile there
+        for (int kb0 = (tp & ~31); kb0 < kblocks; kb0 += kProdThreads) {
+          const int kb = kb0 + (tp & 31);
+          uint32_t anyw = 0;
+          if (kb < kblocks) {
+            const uint32_t* wv = tile_occ + (kb * KS / p.t1) * 5;
+#pragma unroll
+            for (int w = 0; w < 5; ++w) {
+              const int a = max(sh - 32 * w, 0), b = min(sh + rt.rows - 32 * w, 32);
+              if (b > a) anyw |= wv[w] & bit_range(a, b);
+            }
+          }
+          const uint32_t word = __ballot_sync(0xffffffffu, anyw != 0);
+          if ((tp & 31) == 0) kb_live[kb0 >> 5] = word;
+        }
+        bar_sync_named(2, kProdThreads);
+      }
+      for (int kb = staged ? next_kb(-1) : 0; kb < kblocks; kb = staged ? next_kb(kb) : kb + 1) {
         const int k0 = kb * KS;
         bool live[RPT];
-        bool any = false;
+        bool stage_any = true;
+        if (staged) {
+          const uint32_t* wv = tile_occ + (k0 / p.t1) * 5;
 #pragma unroll
-        for (int j = 0; j < RPT; ++j) {
-          live[j] = rid[j] >= 0;
-          if (live[j] && p.occ)
-            live[j] = (__ldg(p.occ + static_cast<int64_t>(k0 / p.t1) * p.WG + (rid[j] >> 5)) >> (rid[j] & 31)) & 1u;
-          any |= live[j];
+          for (int j = 0; j < RPT; ++j) {
+            const int r = rid[j] - (w0 << 5);
+            live[j] = rid[j] >= 0 && ((wv[r >> 5] >> (r & 31)) & 1u);
+          }
+        } else {
+          bool any = false;
+#pragma unroll
+          for (int j = 0; j < RPT; ++j) {
+            live[j] = rid[j] >= 0;
+            if (live[j] && p.occ)
+              live[j] = (__ldg(p.occ + static_cast<int64_t>(k0 / p.t1) * p.WG + (rid[j] >> 5)) >> (rid[j] & 31)) & 1u;
+            any |= live[j];
+          }
+          stage_any = p.occ ? bar_or(1, kProdThreads, any) : true;
         }
-        const bool stage_any = p.occ ? bar_or(1, kProdThreads, any) : true;
+        // dead K-blocks take no ring slot: the ring holds only stages with data, so the copies in
+        // flight are all useful (a unit ends with an END marker stage when liveness is tracked)
+        if (!stage_any) continue;
         mbar_wait(&empty_bar[stage], phase ^ 1);
         uint8_t* sAp = smem + stage * Cfg::STAGE_BYTES;
         const uint32_t sA = smem_u32(sAp);
         uint8_t* sB = sAp + Cfg::A_BYTES;
         if (tp == 0) {
-          stage_live[stage] = stage_any ? 1 : 0;
-          if (stage_any) {
-            mbar_expect_tx_only(&full_bar[stage], Cfg::B_BYTES);
+          stage_live[stage] = 1;
+          mbar_expect_tx_only(&full_bar[stage], Cfg::B_BYTES);
 #pragma unroll
-            for (int a = 0; a < Cfg::BN / 64; ++a)
-              tma_load_3d(sB + a * KS * 128, &tmB, &full_bar[stage], n0 + a * 64, k0, rt.g);
-          }
+          for (int a = 0; a < Cfg::BN / 64; ++a)
+            tma_load_3d(sB + a * KS * 128, &tmB, &full_bar[stage], n0 + a * 64, k0, rt.g);
           mbar_arrive(&full_bar[stage]);  // publishes stage_live
         }
-        if (stage_any) {
+        {
           const int kc = k0 + ch * 8;
           const uint32_t kbytes = kc < p.K ? static_cast<uint32_t>(min(16, (p.K - kc) * 2)) : 0u;
 #pragma unroll
@@ -617,9 +686,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             cp_async_16(sA + swz<MASK>(static_cast<uint32_t>(row * Cfg::A_ROW_BYTES + ch * 16)), src, bytes);
           }
           cp_async_arrive_noinc(&full_bar[stage]);
-        } else {
+        }
+        if (++stage == Cfg::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (p.occ) {  // END marker: closes the unit for the MMA issuer
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        if (tp == 0) {
+          stage_live[stage] = 2;
           mbar_arrive(&full_bar[stage]);
         }
+        mbar_arrive(&full_bar[stage]);
         if (++stage == Cfg::STAGES) {
           stage = 0;
           phase ^= 1;
@@ -637,10 +716,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc_fence_after();
       bool first = true;
-      for (int kb = 0; kb < kblocks; ++kb) {
+      // dense: exactly kblocks data stages; tracked liveness: data stages until the END marker
+      for (int kb = 0; p.occ != nullptr || kb < kblocks; ++kb) {
         mbar_wait(&full_bar[stage], phase);
         tc_fence_after();
-        const bool live = stage_live[stage] != 0;
+        const int meta = stage_live[stage];
+        const bool live = meta == 1;
         if (lane == 0) {
           if (live) {
             const uint32_t sA = smem_u32(smem + stage * Cfg::STAGE_BYTES);
@@ -661,8 +742,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           stage = 0;
           phase ^= 1;
         }
+        if (meta == 2) break;
       }
-      if (lane == 0) umma_commit(&tfull_bar[acc]);
+      if (lane == 0) {
+        // a unit whose every K-block was skipped never wrote its accumulator: the epilogue stores
+        // zeros for it (rows named by no live micro-tile are exact zeros)
+        acc_live[acc] = first ? 0 : 1;
+        umma_commit(&tfull_bar[acc]);
+        mbar_arrive(&tfull_bar[acc]);
+      }
       __syncwarp();
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
@@ -681,12 +769,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float scale = (row >= 0 && p.row_scale) ? __ldg(p.row_scale + row) : 1.0f;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
+      const bool have = acc_live[acc] != 0;
       uint8_t* crow = row >= 0 ? static_cast<uint8_t*>(p.C) + (static_cast<int64_t>(row) * p.ldc) * 2 : nullptr;
 #pragma unroll 1
       for (int c = 0; c < Cfg::BN; c += 32) {
         uint32_t v[32];
-        tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * Cfg::BN + c), v);
-        tmem_wait_ld();
+        if (have) {
+          tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * Cfg::BN + c), v);
+          tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0u;
+        }
         if (row >= 0) {
           float f[32];
 #pragma unroll
@@ -770,20 +864,21 @@ int run_gk(const SpmmArgs& a, cudaStream_t s) {
   return cuda_status();
 }
 
-template <int KS, bool kBF16>
-int run_rowgemm(const RowGemmParams& p, const void* B, int64_t ldb, cudaStream_t s) {
-  using Cfg = GmCfg<KS>;
+template <int KS, bool kBF16, int kBN>
+int run_rowgemm(const RowGemmParams& p, const void* B, int64_t ldb, int64_t group_stride, cudaStream_t s) {
+  using Cfg = GmCfg<KS, kBN>;
   const CUtensorMapDataType dt = kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tmB;
   // B: stacked [G, K, N] (row-major per group, pitch ldb), box {64 n, KS k, 1 group}
-  if (encode_tensor_map_3d(&tmB, dt, B, p.N, p.K, p.G, ldb * 2, static_cast<uint64_t>(ldb) * 2 * p.K, 64, KS,
+  const uint64_t gstride = static_cast<uint64_t>(group_stride > 0 ? group_stride : ldb * p.K) * 2;
+  if (encode_tensor_map_3d(&tmB, dt, B, p.N, p.K, p.G, ldb * 2, gstride, 64, KS,
                            CU_TENSOR_MAP_SWIZZLE_128B) != CUDA_SUCCESS)
     return kErrCuda;
   const int n_tiles = static_cast<int>(ceil_div(p.N, Cfg::BN));
   const int64_t units = static_cast<int64_t>(p.max_tiles) * n_tiles;
   if (units == 0) return kOk;
   if (units >= (1ll << 31)) return kErrShape;
-  auto kern = rowgemm_kernel<KS, kBF16>;
+  auto kern = rowgemm_kernel<KS, kBF16, kBN>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::SMEM));
   const int grid = static_cast<int>(units < num_sms() ? units : num_sms());
   kern<<<grid, kThreads, Cfg::SMEM, s>>>(tmB, p, n_tiles);
@@ -792,10 +887,17 @@ int run_rowgemm(const RowGemmParams& p, const void* B, int64_t ldb, cudaStream_t
 }
 
 template <bool kBF16>
-int rowgemm_dispatch(const RowGemmParams& p, const void* B, int64_t ldb, int ks, cudaStream_t s) {
-  if (ks == 64) return run_rowgemm<64, kBF16>(p, B, ldb, s);
-  if (ks == 32) return run_rowgemm<32, kBF16>(p, B, ldb, s);
-  if (ks == 16) return run_rowgemm<16, kBF16>(p, B, ldb, s);
+int rowgemm_dispatch(const RowGemmParams& p, const void* B, int64_t ldb, int ks, cudaStream_t s,
+                     int64_t group_stride = 0) {
+  if (p.N <= 64) {  // narrow products: 64-column units, no zero-filled B atoms or idle MMA columns
+    if (ks == 64) return run_rowgemm<64, kBF16, 64>(p, B, ldb, group_stride, s);
+    if (ks == 32) return run_rowgemm<32, kBF16, 64>(p, B, ldb, group_stride, s);
+    if (ks == 16) return run_rowgemm<16, kBF16, 64>(p, B, ldb, group_stride, s);
+    return kErrUnsupported;
+  }
+  if (ks == 64) return run_rowgemm<64, kBF16, 256>(p, B, ldb, group_stride, s);
+  if (ks == 32) return run_rowgemm<32, kBF16, 256>(p, B, ldb, group_stride, s);
+  if (ks == 16) return run_rowgemm<16, kBF16, 256>(p, B, ldb, group_stride, s);
   return kErrUnsupported;
 }
 
@@ -823,6 +925,29 @@ int run_gm(const SpmmArgs& a, int ks, cudaStream_t s) {
   p.t1 = dense ? 1 : a.t1;
   p.max_tiles = static_cast<int>(ceil_div(dense ? a.M : a.n_rows_host, 128));
   return rowgemm_dispatch<kBF16>(p, a.B, a.ldb, ks, s);
+}
+
+// Batched pit:m / dense (slices stacked along M, SpmmArgs::batch): every row of every slice is a
+// unit row (no union list); the occupancy bitmap of the stacked index skips dead K-blocks per row
+// tile, and tiles with no live block store zeros. B slice g at B + g * b_batch_stride.
+template <bool kBF16>
+int run_gm_batched(const SpmmArgs& a, int ks, cudaStream_t s) {
+  const int dense = a.plan == kPlanDense ? 1 : 0;
+  RowGemmParams p{};
+  p.A = a.A;
+  p.lda = a.sam;
+  p.C = a.C;
+  p.ldc = a.ldc;
+  p.M = static_cast<int>(a.M * a.batch);
+  p.N = static_cast<int>(a.N);
+  p.K = static_cast<int>(a.K);
+  p.G = static_cast<int>(a.batch);
+  p.uniform_rows = static_cast<int>(a.M);
+  p.occ = dense ? nullptr : a.occ;
+  p.WG = a.WG;
+  p.t1 = dense ? 1 : a.t1;
+  p.max_tiles = static_cast<int>(a.batch * ceil_div(a.M, 128));
+  return rowgemm_dispatch<kBF16>(p, a.B, a.ldb, ks, s, a.b_batch_stride);
 }
 
 // Tuning knob: PIT_GK_KS=64|128 overrides the gathered-K stage depth (defaults: 128 for 16/32-row
@@ -862,6 +987,10 @@ int dispatch_tc(const SpmmArgs& a, cudaStream_t s) {
     return a.N <= 128 ? dispatch_gk<kBF16, 128>(a, gw, s) : dispatch_gk<kBF16, 0>(a, gw, s);
   }
   const int t1 = a.plan == kPlanDense ? 64 : a.t1;
+  if (a.batch > 1) {
+    const int ks = t1 % 64 == 0 ? 64 : t1 == 32 ? 32 : t1 == 16 ? 16 : 0;
+    return ks ? run_gm_batched<kBF16>(a, ks, s) : kErrUnsupported;
+  }
   if (t1 % 64 == 0) return run_gm<kBF16>(a, 64, s);
   if (t1 == 32) return run_gm<kBF16>(a, 32, s);
   if (t1 == 16) return run_gm<kBF16>(a, 16, s);

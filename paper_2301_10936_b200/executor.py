@@ -653,7 +653,7 @@ def stack_slices(A3, plan: SparseKernelPlan):
     if x.dim() != 3:
         raise ExecError(f"batched operand must have rank 3, got {x.dim()}")
     b, m, k = x.shape
-    if plan.is_dense:
+    if plan.is_dense or plan.pit_axis == "m":
         return x.contiguous()
     flat = torch.empty((k, b * m), dtype=x.dtype, device=x.device)
     flat.view(k, b, m).copy_(x.permute(2, 0, 1))
@@ -664,7 +664,7 @@ def _stacked_2d(A3, plan: SparseKernelPlan):
     """The [batch*M, K] 2-D view of a stacked batched operand; LayoutError if A3 is not stacked."""
     b, m, k = (int(d) for d in A3.shape)
     s0, s1, s2 = A3.stride()
-    if plan.is_dense:
+    if plan.is_dense or plan.pit_axis == "m":
         ok = s2 == 1 and s1 == k and s0 == m * k
         return A3.reshape(b * m, k) if ok or b * m * k == 0 else _layout_error(plan)
     ok = s1 == 1 and s0 == m and s2 == b * m
@@ -684,8 +684,10 @@ def build_batched_index_from_tensor(A3, micro_tile, pit_axis="k") -> MicroTileIn
     from .index import build_index_from_tensor
 
     if int(A3.shape[1]) % int(micro_tile[0]):
-        raise ExecError("batched pit:k needs M to be a multiple of the micro-tile height")
-    dummy = SparseKernelPlan("matmul", "k", tuple(micro_tile), None, 0.0, 0.0, COL_MAJOR, {})
+        raise ExecError("batched plans need M to be a multiple of the micro-tile height")
+    axis = pit_axis if isinstance(pit_axis, str) else ("m" if pit_axis == 0 else "k")
+    dummy = SparseKernelPlan("matmul", axis, tuple(micro_tile), None, 0.0, 0.0,
+                             COL_MAJOR if axis == "k" else ROW_MAJOR, {})
     return build_index_from_tensor(_stacked_2d(A3, dummy), micro_tile, pit_axis)
 
 
@@ -700,20 +702,21 @@ def build_batched_index(anns, micro_tile, pit_axis="k") -> MicroTileIndex:
     if any(tuple(a.tensor_shape) != shape or tuple(a.granularity) != gran for a in anns):
         raise ExecError("batched annotations must share shape and granularity")
     if shape[0] % gran[0] or shape[0] % int(micro_tile[0]):
-        raise ExecError("batched pit:k needs M to be a multiple of the granularity and the micro-tile height")
+        raise ExecError("batched plans need M to be a multiple of the granularity and the micro-tile height")
     stacked = from_bits(np.concatenate([a.bits() for a in anns], axis=0), (len(anns) * shape[0], shape[1]), gran)
     return build_index(stacked, micro_tile, pit_axis)
 
 
 def run_batched_matmul_with_index(plan: SparseKernelPlan, A3, B3, idx: Optional[MicroTileIndex],
                                   stats: Optional[ExecStats] = None):
-    """C[b] = A[b] @ B[b] for every slice in ONE launch (pit:k on tensor cores), with A stacked along
-    M (stack_slices) and idx the stacked index. Same per-slice semantics as run_matmul_with_index
-    (an independent index per slice of the prevalent axis). Returns a [batch, M, N]
-    tensor on the device (or numpy when B3 is a host array)."""
+    """C[b] = A[b] @ B[b] for every slice in ONE launch, with A stacked along M (stack_slices) and
+    idx the stacked index. Same per-slice semantics as run_matmul_with_index (an
+    independent index per slice of the prevalent axis). pit:k gathers k per query/row group; pit:m
+    runs every row tile over its slice's B and skips K-blocks in which no row of the tile is live
+    (bf16/fp16). Returns a [batch, M, N] tensor on the device (or numpy when B3 is a host array)."""
     torch = _torch()
-    if plan.op_kind != "matmul" or plan.pit_axis == "m":
-        raise ExecError("batched products support pit:k and dense matmul plans")
+    if plan.op_kind != "matmul":
+        raise ExecError(f"not a matmul plan: {plan.op_kind}")
     host = not _is_torch(B3) or not B3.is_cuda
     Ad = _stacked_2d(A3 if _is_torch(A3) and A3.is_cuda else stack_slices(A3, plan), plan)
     Bd = _device.to_device(np.ascontiguousarray(B3) if not _is_torch(B3) else B3)
@@ -729,7 +732,7 @@ def run_batched_matmul_with_index(plan: SparseKernelPlan, A3, B3, idx: Optional[
         raise ExecError(f"mixed dtypes {Ad.dtype} and {Bd.dtype}")
     C3 = torch.empty((batch, M, N), dtype=Bd.dtype, device=Bd.device)
     a = _lib.SpmmArgs()
-    a.plan = _PLAN_CODE["dense" if plan.is_dense else "k"]
+    a.plan = _PLAN_CODE["dense" if plan.is_dense else plan.pit_axis]
     a.dtype = _device.dtype_code(Bd)
     a.M, a.N, a.K = M, N, K
     a.A = Ad.data_ptr()
@@ -742,26 +745,57 @@ def run_batched_matmul_with_index(plan: SparseKernelPlan, A3, B3, idx: Optional[
     a.b_batch_stride = Bd.stride(0)
     keep = []
     if not plan.is_dense:
-        if idx is None or idx.pit_axis != "k" or tuple(idx.micro_tile) != tuple(plan.micro_tile):
-            raise ExecError("batched pit:k plan needs the stacked index of its micro-tile")
-        if idx.n_groups != batch * -(-M // plan.micro_tile[0]):
-            raise ExecError(f"index has {idx.n_groups} groups, stacked operand needs {batch * -(-M // plan.micro_tile[0])}")
+        if idx is None or idx.pit_axis != plan.pit_axis or tuple(idx.micro_tile) != tuple(plan.micro_tile):
+            raise ExecError(f"batched {plan.pit_axis} plan needs the stacked index of its micro-tile")
+        want = batch * -(-M // plan.micro_tile[0]) if plan.pit_axis == "k" else -(-K // plan.micro_tile[1])
+        if idx.n_groups != want or (plan.pit_axis == "m" and idx.pit_grid != batch * M):
+            raise ExecError(f"index has {idx.n_groups} groups, stacked operand needs {want}")
         a.t0, a.t1 = plan.micro_tile
         a.n_groups = idx.n_groups
         a.slot_stride = idx.pit_grid
-        a.counts, a.slots, alive = idx.device_ptrs()
-        keep += list(alive)
+        if plan.pit_axis == "k":
+            a.counts, a.slots, alive = idx.device_ptrs()
+            keep += list(alive)
+        else:
+            occ = idx.occupancy_words()
+            keep.append(occ)
+            a.occ = occ.data_ptr()
+            a.words_per_group = occ.shape[1]
     _device.check(_lib.load().pit_spmm(C.byref(a), _device.stream_ptr()), ExecError)
     if stats is not None:
         if plan.is_dense:
             stats.launches += batch * dense_launches(plan)
-        else:
+        elif plan.pit_axis == "k":
             stats.launches += launches_from_counts(plan, idx.counts)
+            stats.gathered_micro_tiles += idx.total
+        else:  # per slice: its rows' share of every K-block group
+            occ = idx.occupancy_words().cpu().numpy().view(np.uint32)
+            bits = np.unpackbits(occ.view(np.uint8), bitorder="little").reshape(idx.n_groups, -1)[:, : batch * M]
+            per_slice = bits.reshape(idx.n_groups, batch, M).sum(axis=2)
+            stats.launches += sum(launches_from_counts(plan, per_slice[:, b]) for b in range(batch))
             stats.gathered_micro_tiles += idx.total
     return _device.to_host(C3.reshape(batch * M, N)).reshape(batch, M, N) if host else C3
 
 
 def run_sparse_batched_matmul(plan: SparseKernelPlan, A3, B3, anns, stats: Optional[ExecStats] = None):
-    """Batched run_sparse_matmul: per-slice annotations -> stacked index -> one launch."""
+    """Batched run_sparse_matmul: per-slice annotations -> stacked index -> one launch. pit:m slices
+    the tensor-core path cannot take in one launch (fp32, or B rows not 16-byte aligned) run slice
+    by slice through run_matmul_with_index, each with its own index."""
+    if plan.pit_axis == "m" and not _batched_pit_m_ok(B3):
+        torch = _torch()
+        outs = []
+        for b, ann in enumerate(anns):
+            Ab = A3[b] if _is_torch(A3) else np.ascontiguousarray(A3[b])
+            outs.append(run_sparse_matmul(plan, DenseTensor(Ab), DenseTensor(B3[b]), ann, stats=stats).array)
+        return torch.stack(outs) if _is_torch(outs[0]) else np.stack(outs)
     idx = None if plan.is_dense else build_batched_index(anns, plan.micro_tile, plan.pit_axis)
     return run_batched_matmul_with_index(plan, A3, B3, idx, stats=stats)
+
+
+def _batched_pit_m_ok(B3) -> bool:
+    if not _is_torch(B3):
+        return False
+    torch = _torch()
+    es = B3.element_size()
+    return B3.dtype in (torch.bfloat16, torch.float16) and (B3.shape[2] * es) % 16 == 0 and \
+        (B3.stride(0) * es) % 16 == 0

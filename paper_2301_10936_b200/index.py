@@ -219,7 +219,12 @@ def build_index(ann: SparsityAnnotation, micro_tile, pit_axis: Union[str, int], 
         raise IndexBuildError("workers must be >= 1")
     dim = _pit_dim(pit_axis)
     idx = _empty_index(micro, _axis_name(pit_axis, dim), dim, ann.tensor_shape)
-    packed = torch.from_numpy(np.ascontiguousarray(ann.packed, dtype=np.uint8)).to(idx._buf.device)
+    if isinstance(ann.packed, torch.Tensor):  # SparsityAnnotation.on_device(): no copy, capturable
+        packed = ann.packed
+        if packed.dtype != torch.uint8 or not packed.is_cuda:
+            raise IndexBuildError("device annotation bits must be a CUDA uint8 tensor")
+    else:
+        packed = torch.from_numpy(np.ascontiguousarray(ann.packed, dtype=np.uint8)).to(idx._buf.device)
     lib = _lib.load()
     s0, s1 = ann.tensor_shape
     g0, g1 = ann.granularity

@@ -114,3 +114,61 @@ def test_narrow_n_units(t0, n):
     ref = orc.run_sparse_matmul(At.float().cpu().numpy(), Bt.float().cpu().numpy(),
                                 (ann.tensor_shape, ann.granularity, ann.packed), "k", plan.tile.tile_shape, np.float64)
     assert orc.max_rel_error(C, ref) <= BF16_TOL
+
+
+@pytest.mark.parametrize("t1", [16, 32, 64])
+@pytest.mark.parametrize("n", [40, 64, 300])
+def test_batched_pit_m_bf16_matches_per_slice_oracle(t1, n):
+    """Batched pit:m (rows x t1 micro-tiles, e.g. row-major attention P with 64-key blocks): one
+    launch over uniform row groups; slice 1 is all-zero so its rows must come out exactly 0."""
+    import torch
+
+    pit = _pit()
+    batch, m, k = 3, 320, 256
+    reg = pit.register_builtin_kernels()
+    tile = (16, t1, 128)
+    if reg.get("matmul", tile) is None:
+        reg.register(pit.TileKernelDescriptor("matmul", tile, f"m{t1}"))
+    plan = pit.forced_plan(_bound(m, k, n), "m", reg, tile_shape=tile)
+    assert plan.micro_tile == (1, t1)
+    ratios = [0.8, 1.0, 0.95]
+    anns = [pit.random_annotation((m, k), (32, t1), r, seed=7 * t1 + b) for b, r in enumerate(ratios)]
+    rng = np.random.default_rng(t1 * n)
+    A = np.stack([rng.standard_normal((m, k)).astype(np.float32) * a.materialize() for a in anns])
+    B = rng.standard_normal((batch, k, n)).astype(np.float32)
+    A3 = pit.stack_slices(torch.from_numpy(A).to(torch.bfloat16).cuda(), plan)
+    B3 = torch.from_numpy(B).to(torch.bfloat16).cuda()
+    stats = pit.ExecStats()
+    C3 = pit.run_sparse_batched_matmul(plan, A3, B3, anns, stats=stats)
+    Ar, Br, Cr = A3.float().cpu().numpy(), B3.float().cpu().numpy(), C3.float().cpu().numpy()
+    launches = 0
+    for b in range(batch):
+        ann = anns[b]
+        ref = orc.run_sparse_matmul(Ar[b], Br[b], (ann.tensor_shape, ann.granularity, ann.packed), "m",
+                                    tile, np.float64)
+        if not np.any(ref):
+            assert not np.any(Cr[b]), b
+        else:
+            assert orc.max_rel_error(Cr[b], ref) <= BF16_TOL, b
+        launches += pit.plan_launches(plan, ann)
+    assert stats.launches == launches
+    assert not np.any(Cr[1]) and np.all(np.signbit(Cr[1]) == False)  # noqa: E712  exact +0.0
+
+
+def test_pit_m_narrow_n_two_d():
+    import torch
+
+    pit = _pit()
+    m, k, n = 1000, 512, 48
+    reg = pit.register_builtin_kernels()
+    plan = pit.forced_plan(_bound(m, k, n), "m", reg, tile_shape=(16, 32, 128))
+    ann = pit.random_annotation((m, k), (1, 32), 0.9, seed=2)
+    rng = np.random.default_rng(2)
+    A = rng.standard_normal((m, k)).astype(np.float32) * ann.materialize()
+    B = rng.standard_normal((k, n)).astype(np.float32)
+    At = torch.from_numpy(A).to(torch.bfloat16).cuda()
+    Bt = torch.from_numpy(B).to(torch.bfloat16).cuda()
+    C = pit.run_sparse_matmul(plan, pit.DenseTensor(At), pit.DenseTensor(Bt), ann).array.float().cpu().numpy()
+    ref = orc.run_sparse_matmul(At.float().cpu().numpy(), Bt.float().cpu().numpy(),
+                                (ann.tensor_shape, ann.granularity, ann.packed), "m", (16, 32, 128), np.float64)
+    assert orc.max_rel_error(C, ref) <= BF16_TOL
