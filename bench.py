@@ -312,6 +312,11 @@ def run_ours(args, w):
             result["attention"] = attention_bench(args, dev, peaks)
         except Exception as e:
             result["attention"] = {"error": f"{type(e).__name__}: {e}"[:300]}
+    if not args.no_opt:
+        try:
+            result["opt_ffn2"] = opt_bench(args, dev, peaks)
+        except Exception as e:
+            result["opt_ffn2"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     if not args.no_moe:
         try:
             result["moe"] = moe_bench(args, world, rank, dev, peaks)
@@ -519,6 +524,94 @@ def attention_bench(args, dev, peaks, heads=12, seq=4096, hd=64):
     return out
 
 
+def opt_bench(args, dev, peaks, tokens=4096, d_model=2048, d_ff=8192, zeros=(0.9, 0.99)):
+    """C4: OPT-1.3B FFN2 under dynamic activation sparsity, one training step's two sparse products
+    (1x32 micro-tiles on the ReLU activations H [tokens, d_ff], bf16):
+      forward   Y  = H . W2        pit:m, micro (1,32) (live token rows per 32-neuron K-block)
+      backward  dW2 = H^T . dY     pit:k, micro (32,1) on H^T — H^T column-major IS H row-major, and
+                                   its index is the forward index transposed (one detection)
+    Step = detection from H's values + both products (CUDA graph). Effective FLOPs = 2 * 2048 *
+    live(H) per product."""
+    import torch
+
+    import paper_2301_10936_b200 as pit
+
+    reg = pit.register_builtin_kernels()
+    fwd_e = pit.bind_extents(pit.parse_expr("C[m,n] += A[m,k] * B[k,n]"), dict(m=tokens, k=d_ff, n=d_model))
+    bwd_e = pit.bind_extents(pit.parse_expr("C[m,n] += A[m,k] * B[k,n]"), dict(m=d_ff, k=tokens, n=d_model))
+    plan_f = pit.forced_plan(fwd_e, "m", reg, tile_shape=(16, 32, 128))
+    plan_b = pit.forced_plan(bwd_e, "k", reg, tile_shape=(32, 64, 32))
+    g = torch.Generator(device=dev).manual_seed(11)
+    W2 = torch.randn((d_ff, d_model), device=dev, dtype=torch.bfloat16, generator=g) * 0.02
+    dY = torch.randn((tokens, d_model), device=dev, dtype=torch.bfloat16, generator=g)
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    out = {"workload": f"OPT-1.3B FFN2, {tokens} tokens (8x512), d_ff {d_ff} -> d_model {d_model}, ReLU activations "
+                       "with random 1x32 micro-tile sparsity; fwd pit:m + weight-grad pit:k from one detection",
+           "unit": "TFLOP/s (effective)", "by_zero_ratio": {}}
+    for zr in zeros:
+        keep = torch.rand((tokens, d_ff // 32), device=dev, generator=g) >= zr
+        H = torch.relu(torch.randn((tokens, d_ff), device=dev, dtype=torch.bfloat16, generator=g))
+        H.mul_(keep.repeat_interleave(32, dim=1).to(torch.bfloat16))
+        live = int(keep.sum().item()) * 32
+        eff = 2 * 2.0 * d_model * live
+
+        def step():
+            idx = pit.build_index_from_tensor(H, (1, 32), "m")
+            Y = pit.run_matmul_with_index(plan_f, pit.DenseTensor(H), pit.DenseTensor(W2), idx)
+            dW2 = pit.run_matmul_with_index(plan_b, pit.DenseTensor(H.t()), pit.DenseTensor(dY), idx.transposed())
+            return Y.array, dW2.array
+
+        Y, dW2 = step()
+        ry = H.double() @ W2.double()
+        rw = H.t().double() @ dY.double()
+        err = max(float((Y.double() - ry).abs().max() / ry.abs().max()), float((dW2.double() - rw).abs().max() /
+                                                                                 rw.abs().max()))
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                step()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        for _ in range(args.warmup):
+            graph.replay()
+        ev = []
+        for _ in range(max(args.steps, 5)):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            graph.replay()
+            e1.record(stream)
+            ev.append((e0, e1))
+        torch.cuda.synchronize()
+        ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+        # per-product split (eager, events around each call)
+        idx = pit.build_index_from_tensor(H, (1, 32), "m")
+        split = []
+        for plan, A, B, ix in ((plan_f, H, W2, idx), (plan_b, H.t(), dY, idx.transposed())):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            pit.run_matmul_with_index(plan, pit.DenseTensor(A), pit.DenseTensor(B), ix)
+            e0.record(stream)
+            pit.run_matmul_with_index(plan, pit.DenseTensor(A), pit.DenseTensor(B), ix)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            split.append(e0.elapsed_time(e1))
+        out["by_zero_ratio"][str(zr)] = {
+            "value": round(eff / (ms * 1e-3) / 1e12, 2), "ms_per_step": round(ms, 4), "live_fraction": round(
+                live / (tokens * d_ff), 4),
+            "fwd_pit_m_TFLOPs": round(eff / 2 / (split[0] * 1e-3) / 1e12, 1),
+            "bwd_pit_k_TFLOPs": round(eff / 2 / (split[1] * 1e-3) / 1e12, 1),
+            "max_rel_err_vs_f64": err}
+        del H, keep
+    first = out["by_zero_ratio"][str(zeros[0])]
+    out["value"], out["ms_per_step"] = first["value"], first["ms_per_step"]
+    return out
+
+
 def e2e_ours(args, w, A, B, plan, eff_flops):
     """Host pinned A, B -> H2D -> detection -> SpMM -> D2H of C, all inside the timed region."""
     import torch
@@ -660,6 +753,7 @@ def main():
     ap.add_argument("--no-index-bench", action="store_true")
     ap.add_argument("--no-moe", action="store_true")
     ap.add_argument("--no-attn", action="store_true", help="skip the C3 block-sparse attention section")
+    ap.add_argument("--no-opt", action="store_true", help="skip the C4 OPT FFN2 section")
     ap.add_argument("--no-graph", action="store_true", help="time eager API calls instead of the captured step")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--ref-seconds", type=float, default=4.0)

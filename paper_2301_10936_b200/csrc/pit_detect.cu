@@ -195,6 +195,45 @@ __global__ void __launch_bounds__(kGenThreads) detect_generic_kernel(const uint8
 // ---------------------------------------------------------------------------
 // Pass 1, annotation route: packed MSB-first block bits. One warp per (group, word).
 // ---------------------------------------------------------------------------
+// Power-of-two geometry (the common PIT case: micro-tiles and block granularities like 1, 32, 64):
+// one THREAD per occupancy word, all index math in shifts, the word's 32 coordinates tested in a
+// register loop against L1-resident annotation bytes.
+template <typename I>
+__global__ void detect_bits_pow2_kernel(const uint8_t* __restrict__ packed, I s0, I s1, int lg0, int lg1, int lt0,
+                                        int lt1, int pit_dim, I n_groups, I pit_grid, I WG,
+                                        uint32_t* __restrict__ occ) {
+  const I bg1 = (s1 + (I(1) << lg1) - 1) >> lg1;
+  // group axis (warp-uniform-ish) and coordinate axis parameters
+  const I gs = pit_dim == 0 ? s1 : s0, cs = pit_dim == 0 ? s0 : s1;
+  const int lgt = pit_dim == 0 ? lt1 : lt0, lgg = pit_dim == 0 ? lg1 : lg0;
+  const int lct = pit_dim == 0 ? lt0 : lt1, lcg = pit_dim == 0 ? lg0 : lg1;
+  const I n_items = n_groups * WG;
+  for (I item = static_cast<I>(blockIdx.x) * blockDim.x + threadIdx.x; item < n_items;
+       item += static_cast<I>(gridDim.x) * blockDim.x) {
+    const I g = item / WG, w = item - g * WG;
+    const I glo = (g << lgt) >> lgg;
+    const I ghi = (min((g + 1) << lgt, gs) + (I(1) << lgg) - 1) >> lgg;
+    uint32_t word = 0;
+    const I c_end = min(w * 32 + 32, pit_grid);
+    for (I c = w * 32; c < c_end; ++c) {
+      const I clo = (c << lct) >> lcg;
+      const I chi = (min((c + 1) << lct, cs) + (I(1) << lcg) - 1) >> lcg;
+      bool live = false;
+      for (I gb = glo; gb < ghi && !live; ++gb) {
+        for (I cb = clo; cb < chi; ++cb) {
+          const I f = pit_dim == 0 ? cb * bg1 + gb : gb * bg1 + cb;
+          if ((__ldg(packed + (f >> 3)) >> (7 - (f & 7))) & 1) {
+            live = true;
+            break;
+          }
+        }
+      }
+      word |= static_cast<uint32_t>(live) << (c - w * 32);
+    }
+    occ[static_cast<int64_t>(g) * WG + w] = word;
+  }
+}
+
 // kPow2: micro-tile and granularity along the coordinate axis are powers of two (lct / lcg their
 // log2), so the coordinate's block range needs shifts, not divisions — the common PIT geometry.
 template <typename I, bool kPow2>
@@ -406,7 +445,18 @@ int launch_detect_bits(const DetectBitsArgs& a, cudaStream_t s) {
   const bool pow2 = (ct & (ct - 1)) == 0 && (cg & (cg - 1)) == 0;
   const int lct = pow2 ? __builtin_ctz(static_cast<unsigned>(ct)) : 0;
   const int lcg = pow2 ? __builtin_ctz(static_cast<unsigned>(cg)) : 0;
-  if (fits32 && pow2)
+  const bool all_pow2 = pow2 && (a.t0 & (a.t0 - 1)) == 0 && (a.t1 & (a.t1 - 1)) == 0 && (a.g0 & (a.g0 - 1)) == 0 &&
+                        (a.g1 & (a.g1 - 1)) == 0;
+  if (fits32 && all_pow2) {
+    const int64_t items = n_groups * WG;
+    const int64_t need = ceil_div(items, threads);
+    const unsigned b2 = static_cast<unsigned>(need < wave ? need : wave);
+    detect_bits_pow2_kernel<int32_t><<<b2, threads, 0, s>>>(
+        a.packed, static_cast<int32_t>(a.s0), static_cast<int32_t>(a.s1), __builtin_ctz(static_cast<unsigned>(a.g0)),
+        __builtin_ctz(static_cast<unsigned>(a.g1)), __builtin_ctz(static_cast<unsigned>(a.t0)),
+        __builtin_ctz(static_cast<unsigned>(a.t1)), a.pit_dim, static_cast<int32_t>(n_groups),
+        static_cast<int32_t>(pit_grid), static_cast<int32_t>(WG), a.occ);
+  } else if (fits32 && pow2)
     detect_bits_kernel<int32_t, true><<<blocks, threads, 0, s>>>(
         a.packed, static_cast<int32_t>(a.s0), static_cast<int32_t>(a.s1), a.g0, a.g1, a.t0, a.t1, a.pit_dim,
         static_cast<int32_t>(n_groups), static_cast<int32_t>(pit_grid), static_cast<int32_t>(WG), a.occ, lct, lcg);

@@ -95,8 +95,11 @@ struct GkCfg {
   static constexpr int STAGE_BYTES = ((B_BYTES + A_BYTES + 1023) / 1024) * 1024;
   static constexpr int STAGES = (216 * 1024) / STAGE_BYTES > 16 ? 16 : (216 * 1024) / STAGE_BYTES;
   static constexpr int ACC_COLS = kOrientN ? N_TILE : (N_TILE / 128) * GW;  // TMEM columns per buffer
-  static constexpr int TMEM_COLS = tmem_cols_pow2<2 * ACC_COLS>();
-  static constexpr size_t SMEM = static_cast<size_t>(STAGES) * STAGE_BYTES + 1024 + 256;
+  // accumulator ring: as many units in flight as TMEM holds (<= 8), so short units (few live k per
+  // group) overlap their load, MMA and epilogue across units instead of serialising on 2 buffers
+  static constexpr int NBUF = (512 / ACC_COLS) > 8 ? 8 : (512 / ACC_COLS);
+  static constexpr int TMEM_COLS = tmem_cols_pow2<NBUF * ACC_COLS>();
+  static constexpr size_t SMEM = static_cast<size_t>(STAGES) * STAGE_BYTES + 1024 + 512;
   static constexpr uint32_t A_SW = sw_layout_for_row(A_ROW_BYTES);
   static constexpr uint32_t A_MASK = A_ROW_BYTES == 128 ? 7 : A_ROW_BYTES == 64 ? 3 : A_ROW_BYTES == 32 ? 1 : 0;
   static constexpr int B_CPR = N_TILE / 8;       // 16-byte chunks per gathered B row
@@ -122,8 +125,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
   uint64_t* empty_bar = full_bar + Cfg::STAGES;
   uint64_t* tfull_bar = empty_bar + Cfg::STAGES;
-  uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* tempty_bar = tfull_bar + Cfg::NBUF;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + Cfg::NBUF);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -133,7 +136,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&full_bar[i], kProdThreads);
       mbar_init(&empty_bar[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < Cfg::NBUF; ++i) {
       mbar_init(&tfull_bar[i], 1);
       mbar_init(&tempty_bar[i], 128);
     }
@@ -162,6 +165,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     struct Pos {
       int u, g, t, kb, cnt;  // unit, its group and n tile (tracked without division), chunk, count
       int b;                 // batch slice of the group (one division per unit, not per stage)
+      int ncnt;              // count of the CTA's next unit, loaded one unit ahead of its use
     };
     const int step_t = static_cast<int>(gridDim.x) / n_groups;
     const int step_g = static_cast<int>(gridDim.x) % n_groups;
@@ -174,15 +178,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++q.t;
       }
     };
+    auto prefetch_next = [&](Pos& q) {
+      int gn = q.g + step_g;
+      if (gn >= n_groups) gn -= n_groups;
+      q.ncnt = q.u + static_cast<int>(gridDim.x) < units ? __ldg(counts + gn) : 0;
+    };
     auto advance = [&](Pos p) {
       Pos q = p;
       q.kb = p.kb + Cfg::KS;
       if (q.kb >= p.cnt) {
         q.kb = 0;
-        do {
+        next_unit(q);
+        q.cnt = q.u < units ? p.ncnt : 0;  // prefetched: short units do not stall on the count
+        while (q.u < units && q.cnt == 0) {
           next_unit(q);
           q.cnt = q.u < units ? __ldg(counts + q.g) : 0;
-        } while (q.u < units && q.cnt == 0);
+        }
+        prefetch_next(q);
         q.b = q.g / gpb;
       }
       return q;
@@ -204,9 +216,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       return x;
     };
     Pos cur{static_cast<int>(blockIdx.x), static_cast<int>(blockIdx.x) % n_groups,
-            static_cast<int>(blockIdx.x) / n_groups, 0, 0, 0};
+            static_cast<int>(blockIdx.x) / n_groups, 0, 0, 0, 0};
     cur.cnt = cur.u < units ? __ldg(counts + cur.g) : 0;
     cur.b = cur.g / gpb;
+    prefetch_next(cur);
     if (cur.u < units && cur.cnt == 0) {
       cur.kb = Cfg::KS;  // force advance() past the empty unit
       cur = advance(cur);
@@ -341,8 +354,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (lane == 0) umma_commit(&tfull_bar[acc]);
       __syncwarp();
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
+      if (++acc == Cfg::NBUF) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
     }
   } else if (warp >= kEpiWarp0) {
     // ------------------------------------------------------------ epilogue
@@ -423,8 +438,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&tempty_bar[acc]);
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
+      if (++acc == Cfg::NBUF) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
     }
   }
 

@@ -189,6 +189,19 @@ class MicroTileIndex:
             self._union = res
         return res
 
+    def transposed(self) -> "MicroTileIndex":
+        """The same index for the transposed operand: micro-tile (t0,t1) -> (t1,t0), pit axis m <-> k,
+        identical groups and coordinates (no copy, shares the device buffer). E.g. the (1,32) pit:m
+        index of activations H is the (32,1) pit:k index of H^T used by the weight-gradient
+        product H^T.dY — one detection serves forward and backward."""
+        axis = {"m": "k", "k": "m", "p": "l", "l": "p"}.get(self.pit_axis, self.pit_axis)
+        shape = None if self.shape is None else (self.shape[1], self.shape[0])
+        t = MicroTileIndex((self.micro_tile[1], self.micro_tile[0]), axis, 1 - self.pit_dim, self.pit_grid,
+                           self._n_groups, shape=shape, buf=self._buf, counts=self._counts, slots=self._slots)
+        t._occ_valid = self._occ_valid
+        t._host_authoritative = self._host_authoritative
+        return t
+
     def __repr__(self) -> str:
         return (f"MicroTileIndex(micro_tile={self.micro_tile}, pit_axis={self.pit_axis!r}, "
                 f"n_groups={self._n_groups}, pit_grid={self.pit_grid})")
