@@ -1001,7 +1001,12 @@ int dispatch_tc(const SpmmArgs& a, cudaStream_t s) {
   if (a.plan == kPlanPitK) {
     const int gw = a.t0 <= 16 ? 16 : a.t0 <= 32 ? 32 : a.t0 <= 64 ? 64 : a.t0 <= 128 ? 128 : 256;
     // narrow products (N <= 128, e.g. attention P.V) use 128-column units: no zero-filled half tile
-    return a.N <= 128 ? dispatch_gk<kBF16, 128>(a, gw, s) : dispatch_gk<kBF16, 0>(a, gw, s);
+    // (PIT_GK_NT=128 forces them for every N: a tuning knob)
+    static const int nt_override = [] {
+      const char* e = getenv("PIT_GK_NT");
+      return e ? atoi(e) : 0;
+    }();
+    return (a.N <= 128 || nt_override == 128) ? dispatch_gk<kBF16, 128>(a, gw, s) : dispatch_gk<kBF16, 0>(a, gw, s);
   }
   const int t1 = a.plan == kPlanDense ? 64 : a.t1;
   if (a.batch > 1) {

@@ -27,10 +27,11 @@ __global__ void __launch_bounds__(512, 1) probe(const __grid_constant__ CUtensor
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], (mode == 1 || mode >= 3) ? warps * 32 : warps);
+    for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], mode == 20 ? 2 : (mode == 1 || mode >= 3) ? warps * 32 : warps);
     fence_mbar_init();
   }
   __syncthreads();
+  if (mode == 20 && warp >= 2) return;
   if (warp >= warps) return;
   uint32_t phase = 0;
   int stage = 0;
@@ -72,6 +73,34 @@ __global__ void __launch_bounds__(512, 1) probe(const __grid_constant__ CUtensor
         const int k = ((unsigned)(rbase + row) * 2654435761u) >> rshift;
         const uint32_t o = (ch >> 3) * (64 * 128) + row * 128 + (((ch & 7) ^ (row & 7)) << 4);
         cp_async_16(s + o, B + (int64_t)k * 8192 + (blockIdx.x % nwin) * 256 + ch * 8, 16u - (lane == 99 ? 1u : 0u));
+      }
+      cp_async_arrive_noinc(&full[stage]);
+    } else if (mode == 20) {
+      // TMA gather4 issued by EVERY lane: lane l of warp w fetches quad q = w*32 + l (4 rows x 128 B)
+      const int quads = ROWS_PER_STAGE / 4;  // 64
+      const int q = warp * 32 + lane;
+      const bool act = q < quads;
+      const uint32_t mine = __ballot_sync(0xffffffffu, act);
+      if (lane == 0) mbar_expect_tx(&full[stage], __popc(mine) * 512);
+      __syncwarp();
+      if (act) {
+        const unsigned r = rbase + q * 4;
+        const int r0 = ((r + 0) * 2654435761u) >> rshift, r1 = ((r + 1) * 2654435761u) >> rshift;
+        const int r2 = ((r + 2) * 2654435761u) >> rshift, r3 = ((r + 3) * 2654435761u) >> rshift;
+        tma_gather4(dst + q * 512, &tm, &full[stage], (blockIdx.x % (nwin * 4)) * 64, r0, r1, r2, r3);
+      }
+    } else if (mode == 8 || mode == 9) {
+      // spmm_gk row pattern (one 512 B row per warp instruction) but the row's four 128 B chunks at
+      // byte offsets {0, 256, 1024, 1280} (mode 8) or {0, 128, 256, 384} contiguous (mode 9, = mode 3)
+      const uint32_t s = smem_u32(dst);
+      const int j = lane >> 3;
+      const int off_el = mode == 8 ? ((j & 1) * 128 + (j >> 1) * 512) : j * 64;  // elements
+      for (int row = warp; row < ROWS_PER_STAGE / 4; row += warps) {
+        const int k = ((unsigned)(rbase + row) * 2654435761u) >> rshift;
+        const int ch = lane;
+        const uint32_t o = (ch >> 3) * (64 * 128) + row * 128 + (((ch & 7) ^ (row & 7)) << 4);
+        cp_async_16(s + o, B + (int64_t)k * 8192 + (blockIdx.x % nwin) * 1024 + off_el + (lane & 7) * 8,
+                    16u - (lane == 99 ? 1u : 0u));
       }
       cp_async_arrive_noinc(&full[stage]);
     } else if (mode == 6 || mode == 7) {
@@ -174,7 +203,7 @@ int main(int argc, char** argv) {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   const int iters = 400;
-  for (int mode : {1, 3, 6, 7}) {
+  for (int mode : {0, 1, 9, 20}) {
     for (int warps : {4, 8, 16}) {
       if (mode == 2 && warps > 1) continue;
       const CUtensorMap& tm = mode == 2 ? tm_t : tm_g;
@@ -187,7 +216,7 @@ int main(int argc, char** argv) {
       cudaEventElapsedTime(&ms, e0, e1);
       double bytes = (double)sms * iters * STAGE_BYTES;
       double gbs = bytes / (ms * 1e-3) / 1e9;
-      printf("mode %2d %-12s warps=%2d  %8.1f GB/s  %6.2f B/cycle/SM (at %d MHz)  err=%s\n", mode, mode < 6 ? names[mode] : "4x128", warps, gbs,
+      printf("mode %2d %-12s warps=%2d  %8.1f GB/s  %6.2f B/cycle/SM (at %d MHz)  err=%s\n", mode, mode < 6 ? names[mode] : (mode == 8 ? "512B-spread" : mode == 20 ? "gather4x32" : "512B-contig"), warps, gbs,
              gbs * 1e9 / sms / (clk * 1e3), clk / 1000, cudaGetErrorString(cudaGetLastError()));
     }
   }
