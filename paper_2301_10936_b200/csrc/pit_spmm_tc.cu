@@ -97,7 +97,10 @@ struct GkCfg {
   static constexpr int ACC_COLS = kOrientN ? N_TILE : (N_TILE / 128) * GW;  // TMEM columns per buffer
   // accumulator ring: as many units in flight as TMEM holds (<= 8), so short units (few live k per
   // group) overlap their load, MMA and epilogue across units instead of serialising on 2 buffers
-  static constexpr int NBUF = (512 / ACC_COLS) > 8 ? 8 : (512 / ACC_COLS);
+#ifndef PIT_GK_NBUF_MAX
+#define PIT_GK_NBUF_MAX 8
+#endif
+  static constexpr int NBUF = (512 / ACC_COLS) > PIT_GK_NBUF_MAX ? PIT_GK_NBUF_MAX : (512 / ACC_COLS);
   static constexpr int TMEM_COLS = tmem_cols_pow2<NBUF * ACC_COLS>();
   static constexpr size_t SMEM = static_cast<size_t>(STAGES) * STAGE_BYTES + 1024 + 512;
   static constexpr uint32_t A_SW = sw_layout_for_row(A_ROW_BYTES);
