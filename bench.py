@@ -44,6 +44,8 @@ WORKLOADS = {
                               "online detection from values + SpMM"),
     "pitk_128_8192": dict(M=8192, K=8192, N=8192, micro=(128, 1), axis="k", zero=0.90, tile=(128, 64, 256),
                           desc="pit:k SpMM, B200-native 128x1 micro-tiles, 90% zero, 8192^3 bf16"),
+    "pitk_256_8192": dict(M=8192, K=8192, N=8192, micro=(256, 1), axis="k", zero=0.90, tile=(256, 64, 256),
+                          desc="pit:k SpMM, B200-native 256x1 micro-tiles on CTA pairs, 90% zero, 8192^3 bf16"),
     "pitm_32_8192": dict(M=8192, K=8192, N=8192, micro=(1, 32), axis="m", zero=0.90, tile=(16, 32, 128),
                          desc="pit:m SpMM, random 1x32 micro-tiles, 90% zero, 8192^3 bf16"),
     "bert_ffn1": dict(M=4096, K=768, N=3072, micro=(1, 768), axis="m", zero=None, tile=(128, 768, 256),
@@ -271,14 +273,15 @@ def run_ours(args, w):
         # gathered operand bytes per launch: every live (group, k) pair brings one B row strip of
         # the n tile and one A^T strip of the group, for every n tile (csrc/pit_spmm_tc.cu spmm_gk)
         gw = micro[0]
-        n_tile = 256 if gw < 256 else 128
+        pair = gw > 128 and w["N"] > 128 and os.environ.get("PIT_GK2", "1") != "0"  # spmm_gk2 (CTA pairs)
+        n_tile = 256 if (gw < 256 or pair) else 128
         gathered = idx0.total * (-(-w["N"] // n_tile)) * (n_tile + gw) * 2
         feed = gathered / (spmm_avg * 1e-3) / 1e9
         operand_feed = {"bytes_per_launch": gathered, "achieved_GBps": round(feed, 1),
                         "ceiling_GBps": L2_GATHER_CEILING_GBPS, "frac": round(feed / L2_GATHER_CEILING_GBPS, 4),
                         "ceiling_source": "measured cp.async gather, scripts/probe/copy_probe.cu (profiles/r1/copy_probe.txt)"}
     roofline = {
-        "bound": "tensor", "kernel": "spmm_gk" if axis == "k" else "spmm_gm",
+        "bound": "tensor", "kernel": ("spmm_gk2" if axis == "k" and micro[0] > 128 and w["N"] > 128 and os.environ.get("PIT_GK2", "1") != "0" else "spmm_gk") if axis == "k" else "spmm_gm",
         "achieved": round(achieved, 2), "peak": peaks["bf16"], "unit": "TFLOP/s",
         "frac": round(achieved / peaks["bf16"], 4), "peak_source": peaks["source"] + " burst bf16",
         "traffic": traffic, "algorithmic_flops": eff_flops,

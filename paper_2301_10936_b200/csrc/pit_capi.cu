@@ -119,6 +119,9 @@ const char* pit_last_error(void) { return g_err.c_str(); }
 
 int pit_abi_version(void) { return 101; }
 
+// Diagnostic (not part of include/pit_b200.h): the CTA-pair gathered-K kernel's stage timeline.
+PIT_API int pit_debug_gk2_trace(unsigned long long* host_out_1024) { return pit::gk2_trace_read(host_out_1024); }
+
 long long pit_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int pit_index_geometry(int64_t s0, int64_t s1, int t0, int t1, int pit_dim, int64_t* n_groups, int64_t* pit_grid,

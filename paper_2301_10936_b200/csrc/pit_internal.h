@@ -128,6 +128,7 @@ int launch_dense_ref_f64(const double* A, int64_t s0, int64_t s1, const double* 
                          int64_t N, int64_t K, cudaStream_t s);
 int launch_spmm_tc(const SpmmArgs& a, cudaStream_t s);  // bf16 / fp16 tcgen05 paths
 bool spmm_tc_supported(const SpmmArgs& a);
+int gk2_trace_read(unsigned long long* host);  // diagnostic timeline (PIT_GK2_DIAG bit 4)
 
 // Grouped gathered-row GEMM (MoE experts, batched per-slice plans): see rowgemm in pit_spmm_tc.cu.
 struct GroupedGemmArgs {

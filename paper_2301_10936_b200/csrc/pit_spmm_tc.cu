@@ -23,6 +23,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -327,6 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kb = 0; kb < cnt; kb += Cfg::KS) {
         const int ksteps = (min(Cfg::KS, cnt - kb) + 15) >> 4;
         mbar_wait(&full_bar[stage], phase);
+        fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05.mma reads
         tc_fence_after();
         if (lane == 0) {
           const uint32_t sB = smem_u32(smem + stage * Cfg::STAGE_BYTES);
@@ -453,6 +455,406 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kAllocWarp) {
     tc_fence_after();
     tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+  }
+}
+
+// =============================================================================================
+// spmm_gk2: PIT axis k with 256-row groups on a CTA pair (tcgen05 cta_group::2).
+//
+// The pair computes one (group, 256-column n tile) unit as D[256 m, 256 n] += A[m, k] * B[k, n]
+// over the group's live k: CTA r gathers, per live k, the 128 A^T values of its m half and the 128
+// B values of its n half (one 512-byte warp instruction per k row: lanes 0-15 A, 16-31 B). Every
+// gathered B byte then serves 256 output rows, 128 FLOP per gathered byte against 85 for a
+// single-CTA 128-row group — the L2->SM gather feed, not the tensor pipe, is what bounds PIT's
+// gathered-K product (K2).
+// Pipeline: producers arrive on a local full barrier (cp.async.mbarrier.arrive.noinc); a relay
+// thread per CTA waits on it, fences the generic->async proxy and arrives on the even CTA's pair
+// barrier; the even CTA's MMA thread issues the pair MMA and multicasts its commits to both CTAs'
+// empty / TMEM-full barriers; each CTA drains its own 128 TMEM lanes and arrives remotely on the
+// even CTA's TMEM-empty barrier.
+// =============================================================================================
+template <int kKS>
+struct Gk2Cfg {
+  static constexpr int KS = kKS;
+  static constexpr int N_TILE = 256;
+  static constexpr int OP_BYTES = KS * 256;  // one operand half: 2 swizzle atoms x KS rows x 128 B
+  static constexpr int STAGE_BYTES = 2 * OP_BYTES;
+  static constexpr int STAGES = (208 * 1024) / STAGE_BYTES > 12 ? 12 : (208 * 1024) / STAGE_BYTES;
+  static constexpr int NBUF = 2;
+  static constexpr int ACC_COLS = 256;
+  static constexpr int TMEM_COLS = 512;
+  // epilogue staging for TMA stores: per epilogue warp two 32-row x 64-column bf16 boxes (4 KB each)
+  static constexpr int STG_BYTES = 4 * 2 * 4096;
+  static constexpr size_t SMEM = static_cast<size_t>(STAGES) * STAGE_BYTES + STG_BYTES + 1024 + 1024;
+};
+constexpr int kRelayWarp = 10;
+// Diagnostic timeline (PIT_GK2_DIAG bit 4): globaltimer stamps of pair 0's first 128 stages.
+__device__ unsigned long long g_gk2_trace[8 * 128];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <bool kBF16, int kKS>
+__global__ void __launch_bounds__(kThreads, 1)
+    spmm_gk2_kernel(const __grid_constant__ CUtensorMap tmC, int use_tma_store, const void* __restrict__ Bv, int64_t ldb, const void* __restrict__ Atv, int64_t lda,
+                    const int32_t* __restrict__ counts, const int32_t* __restrict__ slots, int64_t slot_stride,
+                    int n_groups, int n_tiles, int M, int N, void* __restrict__ Cv, int64_t ldc, int grp_rows,
+                    int gpb, int64_t b_batch_stride, int diag) {
+  using Cfg = Gk2Cfg<kKS>;
+  using OT = OutT<kBF16>;
+  using T = typename OT::T;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stg = smem + Cfg::STAGES * Cfg::STAGE_BYTES;  // epilogue staging (1024-aligned boxes)
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(stg + Cfg::STG_BYTES);
+  uint64_t* pair_full = full_bar + Cfg::STAGES;  // even CTA: both halves of a stage landed
+  uint64_t* empty_bar = pair_full + Cfg::STAGES;
+  uint64_t* tfull_bar = empty_bar + Cfg::STAGES;
+  uint64_t* tempty_bar = tfull_bar + Cfg::NBUF;  // even CTA: both CTAs drained the accumulator
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + Cfg::NBUF);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = static_cast<int>(blockIdx.x >> 1);
+  const int npairs = static_cast<int>(gridDim.x >> 1);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < Cfg::STAGES; ++i) {
+      mbar_init(&full_bar[i], kProdThreads);
+      mbar_init(&pair_full[i], 2);
+      mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < Cfg::NBUF; ++i) {
+      mbar_init(&tfull_bar[i], 1);
+      mbar_init(&tempty_bar[i], 8);  // 4 epilogue warps x 2 CTAs
+    }
+    fence_mbar_init();
+  }
+  if (warp == kAllocWarp) tmem_alloc2<Cfg::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int units = n_groups * n_tiles;
+
+  if (warp < kProdWarps) {
+    // ------------------------------------------------------------ cp.async producers
+    int stage = 0;
+    uint32_t phase = 0;
+    struct Pos {
+      int u, g, t, kb, cnt, b, ncnt;
+    };
+    const int step_t = npairs / n_groups;
+    const int step_g = npairs % n_groups;
+    auto next_unit = [&](Pos& q) {
+      q.u += npairs;
+      q.g += step_g;
+      q.t += step_t;
+      if (q.g >= n_groups) {
+        q.g -= n_groups;
+        ++q.t;
+      }
+    };
+    auto prefetch_next = [&](Pos& q) {
+      int gn = q.g + step_g;
+      if (gn >= n_groups) gn -= n_groups;
+      q.ncnt = q.u + npairs < units ? __ldg(counts + gn) : 0;
+    };
+    auto advance = [&](Pos p) {
+      Pos q = p;
+      q.kb = p.kb + Cfg::KS;
+      if (q.kb >= p.cnt) {
+        q.kb = 0;
+        next_unit(q);
+        q.cnt = q.u < units ? p.ncnt : 0;
+        while (q.u < units && q.cnt == 0) {
+          next_unit(q);
+          q.cnt = q.u < units ? __ldg(counts + q.g) : 0;
+        }
+        prefetch_next(q);
+        q.b = q.g / gpb;
+      }
+      return q;
+    };
+    // warp w copies the stage's rows [RW w, RW (w + 1)): the row's k is warp-uniform, so each warp
+    // loads its RW slot indices with uniform (broadcast) vector loads one stage ahead — no shuffles
+    // on the issue path, and every cp.async depends only on a register loaded long before.
+    constexpr int RW = Cfg::KS / kProdWarps;
+    static_assert(RW % 8 == 0, "rows per warp must cover whole swizzle phases");
+    struct Idx {
+      int v[RW];
+    };
+    const bool vec_idx = (slot_stride & 3) == 0 && (reinterpret_cast<uintptr_t>(slots) & 15) == 0;
+    auto load_idx = [&](const Pos& p) {
+      Idx x;
+#pragma unroll
+      for (int q = 0; q < RW; ++q) x.v[q] = 0;
+      if (p.u < units) {
+        const int r0 = p.kb + RW * warp;
+        const int32_t* ps = slots + static_cast<int64_t>(p.g) * slot_stride + r0;
+        if (vec_idx && r0 + RW <= p.cnt) {
+#pragma unroll
+          for (int q = 0; q < RW / 4; ++q) {
+            const int4 t = __ldg(reinterpret_cast<const int4*>(ps) + q);
+            x.v[4 * q + 0] = t.x;
+            x.v[4 * q + 1] = t.y;
+            x.v[4 * q + 2] = t.z;
+            x.v[4 * q + 3] = t.w;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < RW; ++q)
+            if (r0 + q < p.cnt) x.v[q] = __ldg(ps + q);
+        }
+      }
+      return x;
+    };
+    Pos cur{pair, pair % n_groups, pair / n_groups, 0, 0, 0, 0};
+    cur.cnt = cur.u < units ? __ldg(counts + cur.g) : 0;
+    cur.b = cur.g / gpb;
+    prefetch_next(cur);
+    if (cur.u < units && cur.cnt == 0) {
+      cur.kb = Cfg::KS;
+      cur = advance(cur);
+    }
+    // lane roles: lanes 0-15 copy the A^T half (m), lanes 16-31 the B half (n); chunk c = 8 elements
+    const bool is_a = lane < 16;
+    const int c = lane & 15;
+    const uint32_t pitch = static_cast<uint32_t>(is_a ? lda : ldb);  // host: K * pitch < 2^32
+    const uint32_t lane_off = (is_a ? 0u : static_cast<uint32_t>(Cfg::OP_BYTES)) +
+                              static_cast<uint32_t>((c >> 3) * (Cfg::KS * 128) + warp * RW * 128);
+    const uint32_t cc = static_cast<uint32_t>(c & 7);
+    int trace_j = 0;
+    auto issue = [&](const Pos& p, const Idx& x) {
+      const int kvalid = min(Cfg::KS, p.cnt - p.kb);
+      const int kpad = (kvalid + 15) & ~15;
+      const int m0 = p.g * grp_rows;
+      const int m_end = min(M, m0 + grp_rows);
+      const T* src;
+      uint32_t nbytes;
+      if (is_a) {
+        const int m = m0 + 128 * static_cast<int>(rank) + 8 * c;
+        nbytes = m < m_end ? static_cast<uint32_t>(min(16, (m_end - m) * 2)) : 0u;
+        src = static_cast<const T*>(Atv) + (nbytes ? m : 0);
+      } else {
+        const int n = p.t * Cfg::N_TILE + 128 * static_cast<int>(rank) + 8 * c;
+        nbytes = n < N ? static_cast<uint32_t>(min(16, (N - n) * 2)) : 0u;
+        src = static_cast<const T*>(Bv) + p.b * b_batch_stride + (nbytes ? n : 0);
+      }
+      mbar_wait(&empty_bar[stage], phase ^ 1);
+      if ((diag & 16) && pair == 0 && threadIdx.x == 0 && trace_j < 128) g_gk2_trace[rank * 128 + trace_j] = gtimer();
+      ++trace_j;
+      // rows [kvalid, kpad) are zero-filled; a warp's RW rows are all below kpad or all above it
+      const int r0 = RW * warp;
+      if (r0 < kpad && !(diag & 2)) {
+        const uint32_t dst = smem_u32(smem + stage * Cfg::STAGE_BYTES) + lane_off;
+#pragma unroll
+        for (int i = 0; i < RW; ++i) {
+          const bool ok = r0 + i < kvalid;
+          const uint32_t k = ok ? static_cast<uint32_t>(x.v[i]) : 0u;
+          cp_async_16(dst + i * 128 + ((cc ^ static_cast<uint32_t>(i & 7)) << 4), src + k * pitch, ok ? nbytes : 0u);
+        }
+      }
+      cp_async_arrive_noinc(&full_bar[stage]);
+      if (++stage == Cfg::STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+    };
+    // Three stages in flight with fixed register roles (no loop-carried copies: a register move of
+    // an index whose load is still pending would stall the warp on it, defeating the prefetch).
+    Pos P0 = cur, P1 = advance(P0), P2;
+    Idx X0 = load_idx(P0), X1 = load_idx(P1), X2;
+    while (true) {
+      if (P0.u >= units) break;
+      P2 = advance(P1);
+      X2 = load_idx(P2);
+      issue(P0, X0);
+      if (P1.u >= units) break;
+      P0 = advance(P2);
+      X0 = load_idx(P0);
+      issue(P1, X1);
+      if (P2.u >= units) break;
+      P1 = advance(P0);
+      X1 = load_idx(P1);
+      issue(P2, X2);
+    }
+  } else if (warp == kRelayWarp) {
+    // ------------------------------------------------------------ relay: local full -> pair full
+    if (lane == 0) {
+      const uint32_t leader_pf = mapa_shared(smem_u32(pair_full), 0);
+      int tj = 0;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = pair; u < units; u += npairs) {
+        const int cnt = __ldg(counts + u % n_groups);
+        for (int kb = 0; kb < cnt; kb += Cfg::KS) {
+          mbar_wait(&full_bar[stage], phase);
+          if ((diag & 16) && pair == 0 && tj < 128) g_gk2_trace[(2 + rank) * 128 + tj] = gtimer();
+          ++tj;
+          fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05.mma reads
+          mbar_arrive_cluster(leader_pf + stage * 8);
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ------------------------------------------------------------ MMA issuer (even CTA)
+    if (rank == 0) {
+      constexpr uint32_t idesc = idesc_f16(256, Cfg::N_TILE, kBF16, true, true);
+      int tj = 0;
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = pair; u < units; u += npairs) {
+        const int cnt = __ldg(counts + u % n_groups);
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < cnt; kb += Cfg::KS) {
+          const int ksteps = (min(Cfg::KS, cnt - kb) + 15) >> 4;
+          mbar_wait(&pair_full[stage], phase);
+          tc_fence_after();
+          if ((diag & 16) && pair == 0 && lane == 0 && tj < 128) g_gk2_trace[4 * 128 + tj] = gtimer();
+          if (lane == 0) {
+            const uint32_t sA = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+            const uint32_t sB = sA + Cfg::OP_BYTES;
+            const uint32_t d = tmem_base + static_cast<uint32_t>(acc * Cfg::ACC_COLS);
+            for (int ks = 0; ks < ((diag & 1) ? 0 : ksteps); ++ks) {
+              const uint64_t adesc = smem_desc(sA + ks * 2048, Cfg::KS * 128, 1024, kSw128);
+              const uint64_t bdesc = smem_desc(sB + ks * 2048, Cfg::KS * 128, 1024, kSw128);
+              umma2_f16(d, adesc, bdesc, idesc, (kb > 0 || ks > 0) ? 1u : 0u);
+            }
+            umma2_commit_mc(&empty_bar[stage], 3);
+            if ((diag & 16) && pair == 0 && tj < 128) g_gk2_trace[5 * 128 + tj] = gtimer();
+          }
+          ++tj;
+          __syncwarp();
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (lane == 0) umma2_commit_mc(&tfull_bar[acc], 3);
+        __syncwarp();
+        if (++acc == Cfg::NBUF) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= kEpiWarp0) {
+    // ------------------------------------------------------------ epilogue (each CTA: its 128 rows)
+    // TMEM -> registers -> bf16 -> swizzled shared staging -> TMA tile store (whole 128-byte lines,
+    // asynchronous). Per-thread row stores (16 bytes at a 2*ldc stride per lane) clogged the LSU the
+    // producers' gathers share and stretched the copies in flight at every unit boundary.
+    T* C = static_cast<T*>(Cv);
+    const int q = warp & 3;
+    const uint32_t leader_te = mapa_shared(smem_u32(tempty_bar), 0);
+    const bool vec_ok = (ldc % 8) == 0 && (reinterpret_cast<uintptr_t>(Cv) & 15) == 0;
+    const uint32_t stg_w = smem_u32(stg) + static_cast<uint32_t>(q * 2 * 4096);
+    int sbuf = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = pair; u < units; u += npairs) {
+      const int g = u % n_groups;
+      const int n0 = (u / n_groups) * Cfg::N_TILE;
+      const int m0 = g * grp_rows;
+      const int m_end = min(M, m0 + grp_rows);
+      const int cnt = __ldg(counts + g);
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * Cfg::ACC_COLS);
+      const int wrow0 = m0 + 128 * static_cast<int>(rank) + q * 32;  // the warp's first output row
+      const int m = wrow0 + lane;
+      const bool row_ok = m < m_end;
+      if (use_tma_store) {
+        // grp_rows % 32 == 0 (host): a warp's 32 rows are all inside the group or all outside it
+        const bool warp_rows = wrow0 < m_end;
+#pragma unroll 1
+        for (int bx = 0; bx < Cfg::N_TILE / 64; ++bx) {
+          uint32_t v[64];
+          if (cnt > 0) {
+            tmem_ld32(tbase + static_cast<uint32_t>(bx * 64), *reinterpret_cast<uint32_t(*)[32]>(v));
+            tmem_ld32(tbase + static_cast<uint32_t>(bx * 64 + 32), *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+            tmem_wait_ld();
+          } else {
+#pragma unroll
+            for (int i = 0; i < 64; ++i) v[i] = 0u;
+          }
+          const uint32_t buf = stg_w + static_cast<uint32_t>(sbuf * 4096);
+          if (lane == 0) bulk_wait_read<1>();  // the store issued from this buffer two boxes ago read it
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            st_shared_v4(buf + lane * 128 + ((static_cast<uint32_t>(j) ^ static_cast<uint32_t>(lane & 7)) << 4),
+                         pack2(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]), kBF16),
+                         pack2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]), kBF16),
+                         pack2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]), kBF16),
+                         pack2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]), kBF16));
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0 && warp_rows && n0 + bx * 64 < N) {
+            tma_store_2d(&tmC, buf, n0 + bx * 64, wrow0);
+            bulk_commit();
+          }
+          sbuf ^= 1;
+        }
+      } else {
+        uint8_t* crow = reinterpret_cast<uint8_t*>(C + static_cast<int64_t>(row_ok ? m : 0) * ldc);
+#pragma unroll 1
+        for (int cc = 0; cc < Cfg::N_TILE; cc += 32) {
+          uint32_t v[32];
+          if (cnt > 0) {
+            tmem_ld32(tbase + static_cast<uint32_t>(cc), v);
+            tmem_wait_ld();
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0u;
+          }
+          const int nb = n0 + cc;
+          if (row_ok && nb < N && !(diag & 4)) {
+            if (vec_ok && nb + 32 <= N) {
+              uint4* dstp = reinterpret_cast<uint4*>(crow + static_cast<int64_t>(nb) * 2);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                uint4 w;
+                w.x = pack2(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]), kBF16);
+                w.y = pack2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]), kBF16);
+                w.z = pack2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]), kBF16);
+                w.w = pack2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]), kBF16);
+                dstp[j] = w;
+              }
+            } else {
+              T* dstp = reinterpret_cast<T*>(crow);
+              for (int j = 0; j < 32; ++j)
+                if (nb + j < N) dstp[nb + j] = OT::cvt(__uint_as_float(v[j]));
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_te + acc * 8);
+      if (++acc == Cfg::NBUF) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+    if (lane == 0) bulk_wait<0>();  // staging must outlive every store that reads it
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == kAllocWarp) {
+    tc_fence_after();
+    tmem_dealloc2<Cfg::TMEM_COLS>(tmem_base);
   }
 }
 
@@ -739,6 +1141,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // dense: exactly kblocks data stages; tracked liveness: data stages until the END marker
       for (int kb = 0; p.occ != nullptr || kb < kblocks; ++kb) {
         mbar_wait(&full_bar[stage], phase);
+        fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05.mma reads
         tc_fence_after();
         const int meta = stage_live[stage];
         const bool live = meta == 1;
@@ -884,6 +1287,75 @@ int run_gk(const SpmmArgs& a, cudaStream_t s) {
   return cuda_status();
 }
 
+// Diagnostic knob (PIT_GK2_DIAG): bit 0 skips the MMAs, bit 1 the operand copies — isolates the
+// gather pipeline from the tensor pipe when profiling. Results are wrong with either bit set.
+int gk2_diag() {
+  static int v = [] {
+    const char* e = getenv("PIT_GK2_DIAG");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+int tma_store_enabled() {  // PIT_TMA_STORE=0: per-thread row stores (A/B knob)
+  static int v = [] {
+    const char* e = getenv("PIT_TMA_STORE");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
+// CTA-pair gathered-K launch: one pair per co-resident cluster slot (persistent).
+template <bool kBF16, int kKS>
+int run_gk2(const SpmmArgs& a, cudaStream_t s) {
+  using Cfg = Gk2Cfg<kKS>;
+  const int n_tiles = static_cast<int>(ceil_div(a.N, Cfg::N_TILE));
+  const int64_t units = a.n_groups * n_tiles;
+  if (units == 0) return kOk;
+  if (units >= (1ll << 31)) return kErrShape;
+  auto kern = spmm_gk2_kernel<kBF16, kKS>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::SMEM));
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  static int max_pairs = 0;  // co-resident clusters of 2 at this shared-memory footprint
+  if (max_pairs == 0) {
+    cfg.gridDim = dim3(static_cast<unsigned>(num_sms() & ~1));
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) != cudaSuccess || nc <= 0) {
+      cudaGetLastError();
+      nc = num_sms() / 2;
+    }
+    max_pairs = nc;
+  }
+  const int pairs = static_cast<int>(units < max_pairs ? units : max_pairs);
+  cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
+  const int gpb = static_cast<int>(a.batch > 1 ? a.n_groups / a.batch : a.n_groups);
+  // TMA-store epilogue: whole-warp row blocks must not straddle a group (t0 % 32 == 0) and C must be
+  // a 16-byte aligned bf16/fp16 tensor with a 16-byte multiple pitch
+  CUtensorMap tmC;
+  int use_tma = a.t0 % 32 == 0 && (reinterpret_cast<uintptr_t>(a.C) & 15) == 0 && (a.ldc * 2) % 16 == 0 && tma_store_enabled();
+  if (use_tma &&
+      encode_tensor_map_2d(&tmC, kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.C,
+                           static_cast<uint64_t>(a.N), static_cast<uint64_t>(a.M), static_cast<uint64_t>(a.ldc) * 2, 64,
+                           32, CU_TENSOR_MAP_SWIZZLE_128B) != CUDA_SUCCESS)
+    return kErrCuda;
+  if (!use_tma) memset(&tmC, 0, sizeof(tmC));
+  cudaLaunchKernelEx(&cfg, kern, tmC, use_tma, a.B, a.ldb, a.A, a.sak, a.counts, a.slots, a.slot_stride,
+                     static_cast<int>(a.n_groups), n_tiles, static_cast<int>(a.M), static_cast<int>(a.N), a.C, a.ldc,
+                     static_cast<int>(a.t0), gpb, a.batch > 1 ? a.b_batch_stride : int64_t{0}, gk2_diag());
+  note_launch();
+  return cuda_status();
+}
+
 template <int KS, bool kBF16, int kBN>
 int run_rowgemm(const RowGemmParams& p, const void* B, int64_t ldb, int64_t group_stride, cudaStream_t s) {
   using Cfg = GmCfg<KS, kBN>;
@@ -980,6 +1452,14 @@ int gk_ks_override() {
   return v;
 }
 
+int gk2_enabled() {
+  static int v = [] {
+    const char* e = getenv("PIT_GK2");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 template <bool kBF16, int kNT>
 int dispatch_gk(const SpmmArgs& a, int gw, cudaStream_t s) {
   const bool ks64 = gk_ks_override() == 64;
@@ -993,6 +1473,8 @@ int dispatch_gk(const SpmmArgs& a, int gw, cudaStream_t s) {
     case 128:
       return ks64 ? run_gk<128, true, kBF16, 64, kNT>(a, s) : run_gk<128, true, kBF16, 128, kNT>(a, s);
     case 256:
+      // N tiles of 256 columns: the CTA-pair kernel (PIT_GK2=0 selects the single-CTA one)
+      if (kNT == 0 && gk2_enabled()) return gk_ks_override() == 128 ? run_gk2<kBF16, 128>(a, s) : run_gk2<kBF16, 64>(a, s);
       return run_gk<256, false, kBF16, 64, 128>(a, s);
     default:
       return kErrUnsupported;
@@ -1023,6 +1505,10 @@ int dispatch_tc(const SpmmArgs& a, cudaStream_t s) {
 }
 
 }  // namespace
+
+int gk2_trace_read(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, g_gk2_trace, sizeof(g_gk2_trace)) == cudaSuccess ? kOk : kErrCuda;
+}
 
 bool spmm_tc_supported(const SpmmArgs& a) {
   if (a.dtype != kDtypeBF16 && a.dtype != kDtypeF16) return false;
