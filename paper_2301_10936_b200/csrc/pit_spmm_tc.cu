@@ -158,14 +158,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp < kProdWarps) {
     // ------------------------------------------------------------ cp.async producers
-    // Stage = KS gathered k rows. The 128 producer threads copy 16-byte chunks: a warp instruction
-    // moves one 512-byte B row segment (coalesced), the A^T strip rows are split across lanes.
-    // Shared-memory addresses are swizzled in software to the UMMA SWIZZLE_{32,64,128}B layouts.
-    // Rows past the live count are zero-filled (src size 0).
+    // Stage = KS gathered k rows; warp w copies rows [RW w, RW (w + 1)). A row's k is warp-uniform:
+    // each warp loads its RW slot indices with uniform (broadcast) vector loads two stages ahead into
+    // fixed registers (three-way rotation: a register move of an index whose load is still pending
+    // would stall the warp on it). B rows: 16-byte chunks across lanes (one 512-byte row per warp
+    // instruction at N_TILE 256). A^T rows (GW * 2 bytes): A_RPW rows per instruction, the lane's k
+    // picked from the uniform values by a compile-time select chain (no shuffles on the issue path).
+    // Shared-memory addresses are swizzled in software to the UMMA SWIZZLE_{32,64,128}B layouts;
+    // rows in [kvalid, kpad) are zero-filled (src size 0).
     int stage = 0;
     uint32_t phase = 0;
-    // Stage positions (unit, chunk start, unit count) in this CTA's order; indices are loaded two
-    // stages ahead of their use so the L2 latency of the slot loads never stalls issue.
     struct Pos {
       int u, g, t, kb, cnt;  // unit, its group and n tile (tracked without division), chunk, count
       int b;                 // batch slice of the group (one division per unit, not per stage)
@@ -203,19 +205,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       return q;
     };
-    constexpr int NI = Cfg::KS / 32;  // slot indices per lane per stage
+    constexpr int RW = Cfg::KS / kProdWarps;  // rows per warp per stage
+    static_assert(RW % 8 == 0, "a warp's rows must cover whole swizzle phases");
     struct Idx {
-      int v[NI];
+      int v[RW];
     };
+    const bool vec_idx = (slot_stride & 3) == 0 && (reinterpret_cast<uintptr_t>(slots) & 15) == 0;
     auto load_idx = [&](const Pos& p) {
       Idx x;
 #pragma unroll
-      for (int q = 0; q < NI; ++q) x.v[q] = 0;
+      for (int q = 0; q < RW; ++q) x.v[q] = 0;
       if (p.u < units) {
-        const int32_t* ps = slots + static_cast<int64_t>(p.g) * slot_stride + p.kb;
+        const int r0 = p.kb + RW * warp;
+        const int32_t* ps = slots + static_cast<int64_t>(p.g) * slot_stride + r0;
+        if (vec_idx && r0 + RW <= p.cnt) {
 #pragma unroll
-        for (int q = 0; q < NI; ++q)
-          if (p.kb + 32 * q + lane < p.cnt) x.v[q] = __ldg(ps + 32 * q + lane);
+          for (int q = 0; q < RW / 4; ++q) {
+            const int4 t = __ldg(reinterpret_cast<const int4*>(ps) + q);
+            x.v[4 * q + 0] = t.x;
+            x.v[4 * q + 1] = t.y;
+            x.v[4 * q + 2] = t.z;
+            x.v[4 * q + 3] = t.w;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < RW; ++q)
+            if (r0 + q < p.cnt) x.v[q] = __ldg(ps + q);
+        }
       }
       return x;
     };
@@ -228,79 +244,68 @@ __global__ void __launch_bounds__(kThreads, 1)
       cur.kb = Cfg::KS;  // force advance() past the empty unit
       cur = advance(cur);
     }
-    Pos nxt = advance(cur);
-    Idx ci = load_idx(cur), di = load_idx(nxt);
     using T = typename OT::T;
     const T* Bp = static_cast<const T*>(Bv);
     const T* Ap = static_cast<const T*>(Atv);
     const uint32_t ldb32 = static_cast<uint32_t>(ldb);  // host guarantees K * pitch < 2^32 elements
     const uint32_t lda32 = static_cast<uint32_t>(lda);
-    while (cur.u < units) {
-      const Pos nn = advance(nxt);
-      const Idx ei = load_idx(nn);
-      const int kb = cur.kb, cnt = cur.cnt;
-      const int g = cur.g;
-      const int n0 = cur.t * Cfg::N_TILE;
-      const int m0 = g * grp_rows;
-      const int m_end = min(M, m0 + grp_rows);
-      const int kvalid = min(Cfg::KS, cnt - kb);
+    // B: B_RPI rows per warp instruction (1 at N_TILE 256, 2 at 128), lane -> (row sub, chunk)
+    constexpr int B_RPI = Cfg::B_CPR >= 32 ? 1 : 32 / Cfg::B_CPR;
+    constexpr int B_IPR = Cfg::B_CPR >= 32 ? Cfg::B_CPR / 32 : 1;  // instructions per row
+    const int b_sub = B_RPI > 1 ? lane / Cfg::B_CPR : 0;
+    // A^T: A_RPW rows per warp instruction, lane -> (row sub, chunk)
+    const int a_sub = lane / Cfg::A_CPR;
+    const int a_ch = lane % Cfg::A_CPR;
+    const uint32_t a_base = static_cast<uint32_t>((a_ch / Cfg::A_CPA) * (Cfg::KS * Cfg::A_ROW_BYTES));
+    auto issue = [&](const Pos& p, const Idx& x) {
+      const int kvalid = min(Cfg::KS, p.cnt - p.kb);
       const int kpad = (kvalid + 15) & ~15;
+      const int n0 = p.t * Cfg::N_TILE;
+      const int m0 = p.g * grp_rows;
+      const int m_end = min(M, m0 + grp_rows);
       mbar_wait(&empty_bar[stage], phase ^ 1);
-      const uint32_t sB = smem_u32(smem + stage * Cfg::STAGE_BYTES);
-      const uint32_t sA = sB + Cfg::B_BYTES;
-      // ---- B rows: row = warp + 4i (warp-uniform), lane = 16-byte chunk of the n tile. Invalid
-      // rows carry k = 0 and copy 0 bytes (zero fill), so addressing is branch-free; (row & 7) only
-      // takes the values warp and warp+4, so the two swizzled offsets are hoisted.
-      {
-        static_assert(kProdWarps == 8, "row mapping assumes eight producer warps");
-        const int niter = kpad >> 4;  // kpad / 16: pairs of rows per warp (row = warp + 8 i)
+      const int r0 = RW * warp;
+      if (r0 < kpad) {  // a warp's RW rows are all below kpad or all above it
+        const uint32_t sB = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+        const uint32_t sA = sB + Cfg::B_BYTES;
+        // ---- B rows
 #pragma unroll
-        for (int cb = 0; cb < Cfg::B_CPR; cb += 32) {
-          const int ch = cb + lane;
+        for (int cb = 0; cb < B_IPR; ++cb) {
+          const int ch = cb * 32 + (B_RPI > 1 ? lane % Cfg::B_CPR : lane);
           const int n = n0 + ch * 8;
           const uint32_t nbytes = n < N ? static_cast<uint32_t>(min(16, (N - n) * 2)) : 0u;
-          const T* bcol = Bp + cur.b * b_batch_stride + (nbytes ? n : 0);
-          // row & 7 == warp for every row this warp copies: one swizzled offset
-          const uint32_t base = sB + (ch >> 3) * (Cfg::KS * 128) + warp * 128 + (((ch & 7) ^ warp) << 4);
-          // slot block q (32 rows) holds rows warp + 32q + {0, 8, 16, 24}: i2 = 2q + (0|1), j = 0|1
+          const T* bcol = Bp + p.b * b_batch_stride + (nbytes ? n : 0);
+          const uint32_t cbase = sB + (ch >> 3) * (Cfg::KS * 128) + r0 * 128;
 #pragma unroll
-          for (int q = 0; q < NI; ++q) {
-            const int src = ci.v[q];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int i2 = 2 * q + h;
-              if (i2 < niter) {
-#pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                  const int row = warp + 16 * i2 + 8 * j;
-                  const int k = __shfl_sync(0xffffffffu, src, row & 31);
-                  if (Cfg::B_CPR >= 32 || ch < Cfg::B_CPR)
-                    cp_async_16(base + (2 * i2 + j) * (kProdWarps * 128), bcol + static_cast<uint32_t>(k) * ldb32,
-                                row < kvalid ? nbytes : 0u);
-                }
-              }
-            }
+          for (int i = 0; i < RW; i += B_RPI) {
+            int kk = x.v[i];
+            if constexpr (B_RPI == 2) kk = b_sub ? x.v[i + 1] : kk;
+            const int row = i + b_sub;  // within the warp's rows; (r0 + row) & 7 == row & 7
+            const bool ok = r0 + row < kvalid;
+            const uint32_t k = ok ? static_cast<uint32_t>(kk) : 0u;
+            cp_async_16(cbase + row * 128 + ((static_cast<uint32_t>(ch & 7) ^ static_cast<uint32_t>(row & 7)) << 4),
+                        bcol + k * ldb32, ok ? nbytes : 0u);
           }
         }
-      }
-      // ---- A^T rows: A_CPR lanes per row, A_RPW rows per warp instruction
-      {
-        const int ch = lane % Cfg::A_CPR;
-        const int m = m0 + ch * 8;
-        const uint32_t mbytes = m < m_end ? static_cast<uint32_t>(min(16, (m_end - m) * 2)) : 0u;
-        const T* acol = Ap + (mbytes ? m : 0);
-        const uint32_t abase = sA + (ch / Cfg::A_CPA) * (Cfg::KS * Cfg::A_ROW_BYTES);
-        for (int rb = warp * Cfg::A_RPW; rb < kpad; rb += kProdWarps * Cfg::A_RPW) {
-          const int row = rb + lane / Cfg::A_CPR;
-          int k = 0;
+        // ---- A^T rows
+        {
+          const int m = m0 + a_ch * 8;
+          const uint32_t mbytes = m < m_end ? static_cast<uint32_t>(min(16, (m_end - m) * 2)) : 0u;
+          const T* acol = Ap + (mbytes ? m : 0);
 #pragma unroll
-          for (int q = 0; q < NI; ++q) {  // shuffle every slot block, keep the row's (no local memory)
-            const int kq = __shfl_sync(0xffffffffu, ci.v[q], row & 31);
-            k = (row >> 5) == q ? kq : k;
+          for (int j = 0; j < RW; j += Cfg::A_RPW) {
+            int kk = x.v[j];
+#pragma unroll
+            for (int r = 1; r < Cfg::A_RPW; ++r)
+              if (j + r < RW) kk = a_sub == r ? x.v[j + r] : kk;
+            // A_RPW > RW (16-row groups at KS 64): lanes past the warp's rows idle
+            if (Cfg::A_RPW > RW && a_sub >= RW) continue;
+            const int row = r0 + j + a_sub;
+            const bool ok = row < kvalid;
+            const uint32_t k = ok ? static_cast<uint32_t>(kk) : 0u;
+            const uint32_t o = static_cast<uint32_t>(row * Cfg::A_ROW_BYTES + (a_ch % Cfg::A_CPA) * 16);
+            cp_async_16(sA + a_base + swz<Cfg::A_MASK>(o), acol + k * lda32, ok ? mbytes : 0u);
           }
-          const uint32_t o = static_cast<uint32_t>(row * Cfg::A_ROW_BYTES + (ch % Cfg::A_CPA) * 16);
-          cp_async_16(abase + swz<Cfg::A_MASK>(o), acol + static_cast<uint32_t>(k) * lda32,
-                      row < kvalid ? mbytes : 0u);
         }
       }
       cp_async_arrive_noinc(&full_bar[stage]);
@@ -308,10 +313,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         stage = 0;
         phase ^= 1;
       }
-      cur = nxt;
-      nxt = nn;
-      ci = di;
-      di = ei;
+    };
+    Pos P0 = cur, P1 = advance(P0), P2;
+    Idx X0 = load_idx(P0), X1 = load_idx(P1), X2;
+    while (true) {
+      if (P0.u >= units) break;
+      P2 = advance(P1);
+      X2 = load_idx(P2);
+      issue(P0, X0);
+      if (P1.u >= units) break;
+      P0 = advance(P2);
+      X0 = load_idx(P0);
+      issue(P1, X1);
+      if (P2.u >= units) break;
+      P1 = advance(P0);
+      X1 = load_idx(P1);
+      issue(P2, X2);
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
