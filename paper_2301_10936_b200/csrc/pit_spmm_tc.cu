@@ -72,6 +72,40 @@ __host__ __device__ constexpr uint32_t tmem_cols_pow2() {
   return N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : N <= 256 ? 256 : 512;
 }
 
+// One 32-row x 64-column output box of a warp's TMEM lane quarter -> C through a TMA tile store:
+// tcgen05.ld (two x32) -> bf16/fp16 -> 128B-swizzled shared staging (conflict-free 16-byte stores)
+// -> cp.async.bulk.tensor store of whole 128-byte lines. Two staging buffers per warp alternate; a
+// buffer is reused only after the store issued from it two boxes ago has read it. Rows / columns
+// past the tensor are clipped by the tensor map. have == false stores zeros (empty units).
+template <bool kBF16>
+__device__ __forceinline__ void epi_box_tma(uint32_t tsrc, bool have, uint32_t buf, const CUtensorMap* tmC,
+                                            bool do_store, int c0, int r0, int lane) {
+  uint32_t v[64];
+  if (have) {
+    tmem_ld32(tsrc, *reinterpret_cast<uint32_t(*)[32]>(v));
+    tmem_ld32(tsrc + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+    tmem_wait_ld();
+  } else {
+#pragma unroll
+    for (int i = 0; i < 64; ++i) v[i] = 0u;
+  }
+  if (lane == 0) bulk_wait_read<1>();
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    st_shared_v4(buf + lane * 128 + ((static_cast<uint32_t>(j) ^ static_cast<uint32_t>(lane & 7)) << 4),
+                 pack2(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]), kBF16),
+                 pack2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]), kBF16),
+                 pack2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]), kBF16),
+                 pack2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]), kBF16));
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0 && do_store) {
+    tma_store_2d(tmC, buf, c0, r0);
+    bulk_commit();
+  }
+}
+
 // =============================================================================================
 // spmm_gk: PIT axis k.
 //
@@ -94,7 +128,12 @@ struct GkCfg {
   static constexpr int B_BYTES = B_ATOMS * KS * 128;
   static constexpr int A_BYTES = A_ATOMS * KS * A_ROW_BYTES;
   static constexpr int STAGE_BYTES = ((B_BYTES + A_BYTES + 1023) / 1024) * 1024;
-  static constexpr int STAGES = (216 * 1024) / STAGE_BYTES > 16 ? 16 : (216 * 1024) / STAGE_BYTES;
+  // C goes out through TMA tile stores from shared staging: orientation N, 2 x 4 KB per epilogue
+  // warp (epi_box_tma); orientation T (GW <= 64), one [GW rows x 32 columns] box per warp
+  static constexpr int STG_T = GW <= 64 ? GW * 64 : 0;
+  static constexpr int STG_BYTES = kOrientN ? 4 * 2 * 4096 : 4 * STG_T;
+  static constexpr int STAGE_BUDGET = 232448 - 2048 - STG_BYTES;  // 227 KB opt-in minus barriers/align
+  static constexpr int STAGES = STAGE_BUDGET / STAGE_BYTES > 16 ? 16 : STAGE_BUDGET / STAGE_BYTES;
   static constexpr int ACC_COLS = kOrientN ? N_TILE : (N_TILE / 128) * GW;  // TMEM columns per buffer
   // accumulator ring: as many units in flight as TMEM holds (<= 8), so short units (few live k per
   // group) overlap their load, MMA and epilogue across units instead of serialising on 2 buffers
@@ -103,7 +142,8 @@ struct GkCfg {
 #endif
   static constexpr int NBUF = (512 / ACC_COLS) > PIT_GK_NBUF_MAX ? PIT_GK_NBUF_MAX : (512 / ACC_COLS);
   static constexpr int TMEM_COLS = tmem_cols_pow2<NBUF * ACC_COLS>();
-  static constexpr size_t SMEM = static_cast<size_t>(STAGES) * STAGE_BYTES + 1024 + 512;
+  static constexpr size_t SMEM = static_cast<size_t>(STAGES) * STAGE_BYTES + STG_BYTES + 2048;
+  static_assert(SMEM <= 232448, "shared memory over the sm_100 opt-in limit");
   static constexpr uint32_t A_SW = sw_layout_for_row(A_ROW_BYTES);
   static constexpr uint32_t A_MASK = A_ROW_BYTES == 128 ? 7 : A_ROW_BYTES == 64 ? 3 : A_ROW_BYTES == 32 ? 1 : 0;
   static constexpr int B_CPR = N_TILE / 8;       // 16-byte chunks per gathered B row
@@ -114,7 +154,7 @@ struct GkCfg {
 
 template <int GW, bool kOrientN, bool kBF16, int kKS, int kNT>
 __global__ void __launch_bounds__(kThreads, 1)
-    spmm_gk_kernel(const void* __restrict__ Bv, int64_t ldb, const void* __restrict__ Atv, int64_t lda,
+    spmm_gk_kernel(const __grid_constant__ CUtensorMap tmC, int use_tma_store, const void* __restrict__ Bv, int64_t ldb, const void* __restrict__ Atv, int64_t lda,
                    const int32_t* __restrict__ counts, const int32_t* __restrict__ slots, int64_t slot_stride,
                    int n_groups, int n_tiles, int M, int N, int K, void* __restrict__ Cv, int64_t ldc,
                    int grp_rows, int gpb, int64_t b_batch_stride) {
@@ -126,7 +166,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   using OT = OutT<kBF16>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint8_t* stg = smem + Cfg::STAGES * Cfg::STAGE_BYTES;  // epilogue staging (orientation N)
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(stg + Cfg::STG_BYTES);
   uint64_t* empty_bar = full_bar + Cfg::STAGES;
   uint64_t* tfull_bar = empty_bar + Cfg::STAGES;
   uint64_t* tempty_bar = tfull_bar + Cfg::NBUF;
@@ -386,6 +427,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     using T = typename OT::T;
     T* C = static_cast<T*>(Cv);
     const int q = warp & 3;  // TMEM lane quarter
+    const uint32_t stg_w = smem_u32(stg) + static_cast<uint32_t>(q * 2 * 4096);
+    int sbuf = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -397,7 +440,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * Cfg::ACC_COLS);
-      if constexpr (kOrientN) {
+      if (kOrientN && (use_tma_store & 1)) {
+        // lane = group row: 32-row x 64-column boxes through shared staging and TMA stores
+        const int wrow0 = m0 + q * 32;
+#pragma unroll 1
+        for (int bx = 0; bx < Cfg::N_TILE / 64; ++bx) {
+          epi_box_tma<kBF16>(tbase + static_cast<uint32_t>(bx * 64), cnt > 0, stg_w + static_cast<uint32_t>(sbuf * 4096),
+                             &tmC, wrow0 < m_end && n0 + bx * 64 < N, n0 + bx * 64, wrow0, lane);
+          sbuf ^= 1;
+        }
+      } else if constexpr (kOrientN) {
         // lane = group row, columns = n: 32 consecutive outputs per tcgen05.ld
         const int m = m0 + q * 32 + lane;
         const bool row_ok = m < m_end;
@@ -433,6 +485,44 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
+      } else if (!kOrientN && Cfg::STG_T > 0 && (use_tma_store & 1)) {
+        // lane = output column n, TMEM columns = group rows: 2-byte shared stores build the warp's
+        // [grp_rows x 32 columns] box (64-byte rows, conflict-free), one TMA store writes it
+        const uint32_t buf = smem_u32(stg) + static_cast<uint32_t>(q * Cfg::STG_T);
+#pragma unroll 1
+        for (int a = 0; a < Cfg::N_TILE / 128; ++a) {
+          const int ncol0 = n0 + a * 128 + q * 32;
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
+#pragma unroll
+          for (int c = 0; c < GW; c += 16) {
+            uint32_t v[16];
+            if (cnt > 0) {
+              tmem_ld16(tbase + static_cast<uint32_t>(a * GW + c), v);
+              tmem_wait_ld();
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v[i] = 0u;
+            }
+#pragma unroll
+            for (int i = 0; i < 16; i += 2) {
+              // rows c+i and c+i+1 of this column: one 2-byte store each
+              const T h0 = OT::cvt(__uint_as_float(v[i])), h1 = OT::cvt(__uint_as_float(v[i + 1]));
+              if (c + i < grp_rows)
+                asm volatile("st.shared.b16 [%0], %1;" ::"r"(buf + (c + i) * 64 + lane * 2),
+                             "h"(*reinterpret_cast<const uint16_t*>(&h0)) : "memory");
+              if (c + i + 1 < grp_rows)
+                asm volatile("st.shared.b16 [%0], %1;" ::"r"(buf + (c + i + 1) * 64 + lane * 2),
+                             "h"(*reinterpret_cast<const uint16_t*>(&h1)) : "memory");
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0 && ncol0 < N) {
+            tma_store_2d(&tmC, buf, ncol0, m0);
+            bulk_commit();
+          }
+        }
       } else {
         // lane = output column n, columns = group rows
 #pragma unroll
@@ -448,7 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int i = 0; i < 16; ++i) v[i] = 0u;
             }
-            if (n < N) {
+            if (n < N && !(use_tma_store & 2)) {
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
                 const int m = m0 + c + i;
@@ -465,6 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc_phase ^= 1;
       }
     }
+    if ((use_tma_store & 1) && lane == 0) bulk_wait<0>();  // staging outlives its stores
   }
 
   tc_fence_before();
@@ -796,31 +887,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool warp_rows = wrow0 < m_end;
 #pragma unroll 1
         for (int bx = 0; bx < Cfg::N_TILE / 64; ++bx) {
-          uint32_t v[64];
-          if (cnt > 0) {
-            tmem_ld32(tbase + static_cast<uint32_t>(bx * 64), *reinterpret_cast<uint32_t(*)[32]>(v));
-            tmem_ld32(tbase + static_cast<uint32_t>(bx * 64 + 32), *reinterpret_cast<uint32_t(*)[32]>(v + 32));
-            tmem_wait_ld();
-          } else {
-#pragma unroll
-            for (int i = 0; i < 64; ++i) v[i] = 0u;
-          }
-          const uint32_t buf = stg_w + static_cast<uint32_t>(sbuf * 4096);
-          if (lane == 0) bulk_wait_read<1>();  // the store issued from this buffer two boxes ago read it
-          __syncwarp();
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            st_shared_v4(buf + lane * 128 + ((static_cast<uint32_t>(j) ^ static_cast<uint32_t>(lane & 7)) << 4),
-                         pack2(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]), kBF16),
-                         pack2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]), kBF16),
-                         pack2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]), kBF16),
-                         pack2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]), kBF16));
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0 && warp_rows && n0 + bx * 64 < N) {
-            tma_store_2d(&tmC, buf, n0 + bx * 64, wrow0);
-            bulk_commit();
-          }
+          epi_box_tma<kBF16>(tbase + static_cast<uint32_t>(bx * 64), cnt > 0, stg_w + static_cast<uint32_t>(sbuf * 4096),
+                             &tmC, warp_rows && n0 + bx * 64 < N, n0 + bx * 64, wrow0, lane);
           sbuf ^= 1;
         }
       } else {
@@ -1276,11 +1344,24 @@ int num_sms() {
   return g_num_sms;
 }
 
-CUtensorMapSwizzle swizzle_enum(int row_bytes) {
-  return row_bytes >= 128 ? CU_TENSOR_MAP_SWIZZLE_128B
-         : row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
-         : row_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
-                           : CU_TENSOR_MAP_SWIZZLE_NONE;
+
+int tma_store_enabled() {  // PIT_TMA_STORE=0: per-thread row stores (A/B knob)
+  static int v = [] {
+    const char* e = getenv("PIT_TMA_STORE");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
+// Diagnostic knob (PIT_GK2_DIAG): bit 0 skips the MMAs, bit 1 the operand copies, bit 2 the C
+// stores, bit 4 records the CTA-pair stage timeline — isolates the gather pipeline, the tensor pipe
+// and the epilogue when profiling. Results are wrong with any of bits 0-2 set.
+int gk2_diag() {
+  static int v = [] {
+    const char* e = getenv("PIT_GK2_DIAG");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
 }
 
 template <int GW, bool kOrientN, bool kBF16, int kKS = 64, int kNT = 0>
@@ -1293,8 +1374,28 @@ int run_gk(const SpmmArgs& a, cudaStream_t s) {
   auto kern = spmm_gk_kernel<GW, kOrientN, kBF16, kKS, kNT>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::SMEM));
   const int grid = static_cast<int>(units < num_sms() ? units : num_sms());
+  // orientation N: C through TMA stores when whole 32-row warp blocks stay inside a group
+  CUtensorMap tmC;
+  memset(&tmC, 0, sizeof(tmC));
+  int epi = 0;
+  const bool c_ok = (reinterpret_cast<uintptr_t>(a.C) & 15) == 0 && (a.ldc * 2) % 16 == 0 && tma_store_enabled();
+  const CUtensorMapDataType cdt = kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  if (kOrientN && a.t0 % 32 == 0 && c_ok) {
+    if (encode_tensor_map_2d(&tmC, cdt, a.C, static_cast<uint64_t>(a.N), static_cast<uint64_t>(a.M),
+                             static_cast<uint64_t>(a.ldc) * 2, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B) != CUDA_SUCCESS)
+      return kErrCuda;
+    epi |= 1;
+  } else if (!kOrientN && Cfg::STG_T > 0 && c_ok) {
+    // orientation T: box = the group's rows x one warp's 32 columns (64-byte rows, no swizzle)
+    if (encode_tensor_map_2d(&tmC, cdt, a.C, static_cast<uint64_t>(a.N), static_cast<uint64_t>(a.M),
+                             static_cast<uint64_t>(a.ldc) * 2, 32, static_cast<uint32_t>(a.t0),
+                             CU_TENSOR_MAP_SWIZZLE_NONE) != CUDA_SUCCESS)
+      return kErrCuda;
+    epi |= 1;
+  }
+  if (gk2_diag() & 4) epi |= 2;  // diagnostic: no C stores (orientation T)
   // A column-major: A^T is row-major [K, M] with pitch sak
-  kern<<<grid, kThreads, Cfg::SMEM, s>>>(a.B, a.ldb, a.A, a.sak, a.counts, a.slots, a.slot_stride,
+  kern<<<grid, kThreads, Cfg::SMEM, s>>>(tmC, epi, a.B, a.ldb, a.A, a.sak, a.counts, a.slots, a.slot_stride,
                                          static_cast<int>(a.n_groups), n_tiles, static_cast<int>(a.M),
                                          static_cast<int>(a.N), static_cast<int>(a.K), a.C, a.ldc,
                                          static_cast<int>(a.t0),
@@ -1302,24 +1403,6 @@ int run_gk(const SpmmArgs& a, cudaStream_t s) {
                                          a.batch > 1 ? a.b_batch_stride : 0);
   note_launch();
   return cuda_status();
-}
-
-// Diagnostic knob (PIT_GK2_DIAG): bit 0 skips the MMAs, bit 1 the operand copies — isolates the
-// gather pipeline from the tensor pipe when profiling. Results are wrong with either bit set.
-int gk2_diag() {
-  static int v = [] {
-    const char* e = getenv("PIT_GK2_DIAG");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
-int tma_store_enabled() {  // PIT_TMA_STORE=0: per-thread row stores (A/B knob)
-  static int v = [] {
-    const char* e = getenv("PIT_TMA_STORE");
-    return e ? atoi(e) : 1;
-  }();
-  return v;
 }
 
 // CTA-pair gathered-K launch: one pair per co-resident cluster slot (persistent).
