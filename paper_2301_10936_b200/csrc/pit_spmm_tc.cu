@@ -987,13 +987,18 @@ struct GmCfg {
   static constexpr int A_BYTES = BM * A_ROW_BYTES;
   static constexpr int B_BYTES = (BN / 64) * KS * 128;  // MN-major, 4 atoms of 64 n
   static constexpr int STAGE_BYTES = ((A_BYTES + B_BYTES + 1023) / 1024) * 1024;
-  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+  // epilogue staging: one 32-row x 64-column box (4 KB) per epilogue warp
+  static constexpr int STG_BYTES = 4 * 4096;
+  static constexpr int STATIC_SMEM = 512 * 5 * 4 + 1024 / 8;  // tile_occ + kb_live below
+  static constexpr int STAGE_BUDGET = 232448 - 2048 - STG_BYTES - STATIC_SMEM;
+  static constexpr int STAGES = STAGE_BUDGET / STAGE_BYTES > 8 ? 8 : STAGE_BUDGET / STAGE_BYTES;
   static constexpr int TMEM_COLS = tmem_cols_pow2<2 * BN>();  // 2 accumulators
   // occupancy words of the current row tile for every K-group (contiguous-row units): 5 words per
   // group cover 128 rows at any 32-row alignment
   static constexpr int OCC_MAX_GROUPS = 512;   // static shared: 5 words per K-group
   static constexpr int KB_MAX = 1024;          // static shared: live-K-block bitmask
-  static constexpr size_t SMEM = static_cast<size_t>(STAGES) * STAGE_BYTES + 1024 + 512;
+  static constexpr size_t SMEM = static_cast<size_t>(STAGES) * STAGE_BYTES + STG_BYTES + 2048;
+  static_assert(SMEM + STATIC_SMEM <= 232448, "shared memory over the sm_100 opt-in limit");
   static constexpr uint32_t A_SW = sw_layout_for_row(A_ROW_BYTES);
 };
 
@@ -1040,7 +1045,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   using Cfg = GmCfg<KS, kBN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint8_t* stg = smem + Cfg::STAGES * Cfg::STAGE_BYTES;  // epilogue staging
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(stg + Cfg::STG_BYTES);
   uint64_t* empty_bar = full_bar + Cfg::STAGES;
   uint64_t* tfull_bar = empty_bar + Cfg::STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -1265,6 +1271,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= kEpiWarp0) {
     // ------------------------------------------------------------ epilogue: row scatter (SWrite)
+    using T = typename OutT<kBF16>::T;
     const int q = warp & 3;
     const bool vec_ok = (p.ldc % 8) == 0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0;
     int acc = 0;
@@ -1278,6 +1285,58 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const bool have = acc_live[acc] != 0;
+      if (vec_ok) {
+        // Staged, coalesced row scatter: the warp's 32 rows x 64 columns go through a swizzled shared
+        // box and leave as 128-byte row segments (8 lanes per row, 4 rows per instruction) instead of
+        // 16-byte pieces at a row stride per lane, which clog the LSU the producers' gathers share.
+        const uint32_t box = smem_u32(stg) + static_cast<uint32_t>(q * 4096);
+        T* C = static_cast<T*>(p.C);
+#pragma unroll 1
+        for (int bx = 0; bx < Cfg::BN / 64; ++bx) {
+          uint32_t v[64];
+          if (have) {
+            const uint32_t ta = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * Cfg::BN + bx * 64);
+            tmem_ld32(ta, *reinterpret_cast<uint32_t(*)[32]>(v));
+            tmem_ld32(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+            tmem_wait_ld();
+          } else {
+#pragma unroll
+            for (int j = 0; j < 64; ++j) v[j] = 0u;
+          }
+          __syncwarp();  // the previous box's copy-out has read the staging
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float f[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              float x = __uint_as_float(v[8 * j + e]);
+              if (p.act == 1) x = fmaxf(x, 0.0f);
+              f[e] = x * scale;
+            }
+            st_shared_v4(box + lane * 128 + ((static_cast<uint32_t>(j) ^ static_cast<uint32_t>(lane & 7)) << 4),
+                         pack2(f[0], f[1], kBF16), pack2(f[2], f[3], kBF16), pack2(f[4], f[5], kBF16),
+                         pack2(f[6], f[7], kBF16));
+          }
+          __syncwarp();
+          const int ch = lane & 7;
+          const int col = n0 + bx * 64 + ch * 8;
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int r = it * 4 + (lane >> 3);
+            const int drow = __shfl_sync(0xffffffffu, row, r);
+            const uint4 w = ld_shared_v4(box + r * 128 + ((static_cast<uint32_t>(ch) ^ static_cast<uint32_t>(r & 7)) << 4));
+            if (drow >= 0 && col < p.N) {
+              T* dst = C + static_cast<int64_t>(drow) * p.ldc + col;
+              if (col + 8 <= p.N) {
+                *reinterpret_cast<uint4*>(dst) = w;
+              } else {
+                const T* h = reinterpret_cast<const T*>(&w);
+                for (int e = 0; e < p.N - col; ++e) dst[e] = h[e];
+              }
+            }
+          }
+        }
+      } else {
       uint8_t* crow = row >= 0 ? static_cast<uint8_t*>(p.C) + (static_cast<int64_t>(row) * p.ldc) * 2 : nullptr;
 #pragma unroll 1
       for (int c = 0; c < Cfg::BN; c += 32) {
@@ -1316,6 +1375,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (nb + j < p.N) dst[nb + j] = OutT<kBF16>::cvt(f[j]);
           }
         }
+      }
       }
       tc_fence_before();
       mbar_arrive(&tempty_bar[acc]);
