@@ -977,6 +977,7 @@ struct RowGemmParams {
   int t1;
   int max_tiles;            // host bound on the total number of row tiles
   int uniform_rows;         // cnt == nullptr && G > 1: every group is this many consecutive rows
+  int a_tma;                // A tiles by TMA (rows contiguous: no row_src, no liveness); else cp.async
 };
 
 template <int KS, int kBN = 256>
@@ -1041,7 +1042,8 @@ __device__ __forceinline__ int tile_dst_row(const RowGemmParams& p, const RowTil
 
 template <int KS, bool kBF16, int kBN>
 __global__ void __launch_bounds__(kThreads, 1)
-    rowgemm_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ RowGemmParams p, int n_tiles) {
+    rowgemm_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmA,
+                   const __grid_constant__ RowGemmParams p, int n_tiles) {
   using Cfg = GmCfg<KS, kBN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1182,13 +1184,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* sB = sAp + Cfg::A_BYTES;
         if (tp == 0) {
           stage_live[stage] = 1;
-          mbar_expect_tx_only(&full_bar[stage], Cfg::B_BYTES);
+          mbar_expect_tx_only(&full_bar[stage], Cfg::B_BYTES + (p.a_tma ? Cfg::A_BYTES : 0));
 #pragma unroll
           for (int a = 0; a < Cfg::BN / 64; ++a)
             tma_load_3d(sB + a * KS * 128, &tmB, &full_bar[stage], n0 + a * 64, k0, rt.g);
+          // contiguous rows: the whole [128 rows x KS] A tile is one swizzled TMA box (rows past the
+          // tile belong to no output row of this unit and are never stored; past the tensor, zeros)
+          if (p.a_tma) tma_load_2d(sAp, &tmA, &full_bar[stage], k0, rt.base);
           mbar_arrive(&full_bar[stage]);  // publishes stage_live
         }
-        {
+        if (p.a_tma) {
+          cp_async_arrive_noinc(&full_bar[stage]);
+        } else {
           const int kc = k0 + ch * 8;
           const uint32_t kbytes = kc < p.K ? static_cast<uint32_t>(min(16, (p.K - kc) * 2)) : 0u;
 #pragma unroll
@@ -1516,6 +1523,14 @@ int run_gk2(const SpmmArgs& a, cudaStream_t s) {
   return cuda_status();
 }
 
+int a_tma_enabled() {  // PIT_A_TMA=0: cp.async row copies for contiguous A as well (A/B knob)
+  static int v = [] {
+    const char* e = getenv("PIT_A_TMA");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 template <int KS, bool kBF16, int kBN>
 int run_rowgemm(const RowGemmParams& p, const void* B, int64_t ldb, int64_t group_stride, cudaStream_t s) {
   using Cfg = GmCfg<KS, kBN>;
@@ -1530,10 +1545,24 @@ int run_rowgemm(const RowGemmParams& p, const void* B, int64_t ldb, int64_t grou
   const int64_t units = static_cast<int64_t>(p.max_tiles) * n_tiles;
   if (units == 0) return kOk;
   if (units >= (1ll << 31)) return kErrShape;
+  // A by TMA when every tile is 128 consecutive source rows (dense, batched slices, packed groups)
+  CUtensorMap tmA;
+  memset(&tmA, 0, sizeof(tmA));
+  RowGemmParams q = p;
+  q.a_tma = 0;
+  if (p.row_src == nullptr && p.occ == nullptr && (p.lda * 2) % 16 == 0 &&
+      (reinterpret_cast<uintptr_t>(p.A) & 15) == 0 && a_tma_enabled()) {
+    if (encode_tensor_map_2d(&tmA, dt, p.A, static_cast<uint64_t>(p.K), static_cast<uint64_t>(p.M),
+                             static_cast<uint64_t>(p.lda) * 2, KS, 128,
+                             KS * 2 >= 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                             : KS * 2 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B) != CUDA_SUCCESS)
+      return kErrCuda;
+    q.a_tma = 1;
+  }
   auto kern = rowgemm_kernel<KS, kBF16, kBN>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::SMEM));
   const int grid = static_cast<int>(units < num_sms() ? units : num_sms());
-  kern<<<grid, kThreads, Cfg::SMEM, s>>>(tmB, p, n_tiles);
+  kern<<<grid, kThreads, Cfg::SMEM, s>>>(tmB, tmA, q, n_tiles);
   note_launch();
   return cuda_status();
 }
