@@ -53,7 +53,7 @@ WORKLOADS = {
 }
 DEFAULT_WORKLOAD = "pitk_c1_8192"
 FLUSH_BYTES = 256 << 20
-L2_GATHER_CEILING_GBPS = 9425.0  # measured L2->SM gather ceiling (cp.async, 148 SMs, 1965 MHz)
+L2_GATHER_CEILING_GBPS = 11145.6  # best measured L2->SM cp.async gather rate (profiles/r1/copy_probe_l2_patterns.txt)
 
 
 # ----------------------------------------------------------------------------------- helpers
@@ -279,7 +279,7 @@ def run_ours(args, w):
         feed = gathered / (spmm_avg * 1e-3) / 1e9
         operand_feed = {"bytes_per_launch": gathered, "achieved_GBps": round(feed, 1),
                         "ceiling_GBps": L2_GATHER_CEILING_GBPS, "frac": round(feed / L2_GATHER_CEILING_GBPS, 4),
-                        "ceiling_source": "measured cp.async gather, scripts/probe/copy_probe.cu (profiles/r1/copy_probe.txt)"}
+                        "ceiling_source": "best measured cp.async gather rate, scripts/probe/copy_probe.cu (profiles/r1/copy_probe_l2_patterns.txt)"}
     roofline = {
         "bound": "tensor", "kernel": ("spmm_gk2" if axis == "k" and micro[0] > 128 and w["N"] > 128 and os.environ.get("PIT_GK2", "1") != "0" else "spmm_gk") if axis == "k" else "spmm_gm",
         "achieved": round(achieved, 2), "peak": peaks["bf16"], "unit": "TFLOP/s",
@@ -310,6 +310,11 @@ def run_ours(args, w):
 
     if not args.no_index_bench:
         result["index_build"] = index_build_bench(dev, peaks)
+    if not args.no_sweep:
+        try:
+            result["sparsity_sweep"] = sparsity_sweep_bench(args, dev, peaks)
+        except Exception as e:
+            result["sparsity_sweep"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     if not args.no_attn:
         try:
             result["attention"] = attention_bench(args, dev, peaks)
@@ -384,6 +389,55 @@ def moe_bench(args, world, rank, dev, peaks, tokens_per_gpu=16384, n_experts=128
                        "tokens_per_gpu": tokens_per_gpu, "routing": "top-1 argmax, Gaussian logits, dropless",
                        "parallelism": f"ep{world}" if world > 1 else "single GPU", "received_rank0": int(received)},
             "gpu_launches_per_layer": (_lib.kernel_launches() - launches0) // steps}
+
+
+def sparsity_sweep_bench(args, dev, peaks, side=8192, micros=((32, 1), (128, 1), (256, 1)),
+                         zeros=(0.5, 0.9, 0.95, 0.99), reps=5):
+    """"Effective TFLOP/s vs sparsity" (BASELINE metric) for the pit:k product at 8192^3 bf16: every
+    micro-tile height the tcgen05 kernels tile natively (32x1 = C1's, 128x1, 256x1 on CTA pairs),
+    random micro-tile sparsity 50..99%. SpMM kernel time alone (CUDA events on the launching stream,
+    L2 flushed before each call; the index is built once per configuration, outside the timing),
+    and the index build from values (detect + compaction) beside it."""
+    import torch
+
+    import paper_2301_10936_b200 as pit
+
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    out = {}
+    for micro in micros:
+        for zero in zeros:
+            w = dict(M=side, K=side, N=side, micro=micro, axis="k", zero=zero, tile=(micro[0], 64, 256),
+                     name=f"sweep_{micro[0]}x{micro[1]}_{zero}")
+            A, B, live = make_operands(w, seed=99, device=dev)
+            plan = make_plan(w)
+            flops = 2.0 * side * live
+            idx = pit.build_index_from_tensor(A, micro, "k")
+            for _ in range(2):
+                pit.run_matmul_with_index(plan, pit.DenseTensor(A), pit.DenseTensor(B), idx)
+            ev = []
+            for _ in range(reps):
+                flush.zero_()
+                e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                e0.record(stream)
+                idx = pit.build_index_from_tensor(A, micro, "k")
+                e1.record(stream)
+                pit.run_matmul_with_index(plan, pit.DenseTensor(A), pit.DenseTensor(B), idx)
+                e2.record(stream)
+                ev.append((e0, e1, e2))
+            torch.cuda.synchronize()
+            det = statistics.median(a.elapsed_time(b) for a, b, _ in ev)
+            mm = statistics.median(b.elapsed_time(c) for _, b, c in ev)
+            tf = flops / (mm * 1e-3) / 1e12
+            kern = "spmm_gk2 (CTA pair)" if micro[0] > 128 else "spmm_gk"
+            out[f"{micro[0]}x{micro[1]}@{zero}"] = {
+                "kernel": kern, "spmm_ms": round(mm, 4), "effective_TFLOPs": round(tf, 1),
+                "frac_bf16_peak": round(tf / peaks["bf16"], 4), "live_fraction": round(live / side / side, 4),
+                "index_build_ms": round(det, 4),
+                "index_build_GBps": round(A.numel() * 2 / (det * 1e-3) / 1e9, 1)}
+            del A, B, idx
+    return {"workload": f"pit:k SpMM {side}^3 bf16, random micro-tile sparsity, online index from values",
+            "peak_TFLOPs": peaks["bf16"], "by_microtile_and_zero_ratio": out}
 
 
 def index_build_bench(dev, peaks, side=16384, reps=20):
@@ -755,6 +809,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-index-bench", action="store_true")
     ap.add_argument("--no-moe", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the micro-tile x sparsity sweep")
     ap.add_argument("--no-attn", action="store_true", help="skip the C3 block-sparse attention section")
     ap.add_argument("--no-opt", action="store_true", help="skip the C4 OPT FFN2 section")
     ap.add_argument("--no-graph", action="store_true", help="time eager API calls instead of the captured step")

@@ -1631,8 +1631,8 @@ int run_gm_batched(const SpmmArgs& a, int ks, cudaStream_t s) {
   return rowgemm_dispatch<kBF16>(p, a.B, a.ldb, ks, s, a.b_batch_stride);
 }
 
-// Tuning knob: PIT_GK_KS=64|128 overrides the gathered-K stage depth (defaults: 128 for 16/32-row
-// groups up to 128 rows, 64 for 256-row groups — measured on B200).
+// Tuning knob: PIT_GK_KS=64|128 overrides the gathered-K stage depth (defaults: 128, and 128 for the
+// CTA-pair 256-row kernel; the single-CTA 256-row fallback runs 64 — measured on B200).
 int gk_ks_override() {
   static int v = [] {
     const char* e = getenv("PIT_GK_KS");
@@ -1663,7 +1663,7 @@ int dispatch_gk(const SpmmArgs& a, int gw, cudaStream_t s) {
       return ks64 ? run_gk<128, true, kBF16, 64, kNT>(a, s) : run_gk<128, true, kBF16, 128, kNT>(a, s);
     case 256:
       // N tiles of 256 columns: the CTA-pair kernel (PIT_GK2=0 selects the single-CTA one)
-      if (kNT == 0 && gk2_enabled()) return gk_ks_override() == 128 ? run_gk2<kBF16, 128>(a, s) : run_gk2<kBF16, 64>(a, s);
+      if (kNT == 0 && gk2_enabled()) return gk_ks_override() == 64 ? run_gk2<kBF16, 64>(a, s) : run_gk2<kBF16, 128>(a, s);
       return run_gk<256, false, kBF16, 64, 128>(a, s);
     default:
       return kErrUnsupported;

@@ -4,7 +4,7 @@ OUT=gpurun_out; mkdir -p $OUT
 W=${GK_W:-pitk_c1_8192}
 for cfg in ${GK_CFGS:-"X=0"}; do
   cfg=${cfg//,/ }
-  env $cfg timeout 300 python bench.py --workload $W --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --no-index-bench --no-moe --no-attn --no-opt > $OUT/knob.json 2>$OUT/knob.err
+  env $cfg timeout 300 python bench.py --workload $W --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --no-index-bench --no-moe --no-attn --no-opt --no-sweep > $OUT/knob.json 2>$OUT/knob.err
   python -c "
 import json,sys
 d=json.load(open('$OUT/knob.json')); r=d['roofline']
