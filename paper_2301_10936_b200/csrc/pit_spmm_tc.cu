@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (p.u < units) {
         const int r0 = p.kb + RW * warp;
         const int32_t* ps = slots + static_cast<int64_t>(p.g) * slot_stride + r0;
-        if (vec_idx && r0 + RW <= p.cnt) {
+        if (vec_idx && r0 + RW <= slot_stride) {  // in bounds; entries past cnt are masked by the copy
 #pragma unroll
           for (int q = 0; q < RW / 4; ++q) {
             const int4 t = __ldg(reinterpret_cast<const int4*>(ps) + q);
@@ -703,7 +703,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (p.u < units) {
         const int r0 = p.kb + RW * warp;
         const int32_t* ps = slots + static_cast<int64_t>(p.g) * slot_stride + r0;
-        if (vec_idx && r0 + RW <= p.cnt) {
+        if (vec_idx && r0 + RW <= slot_stride) {  // in bounds; entries past cnt are masked by the copy
 #pragma unroll
           for (int q = 0; q < RW / 4; ++q) {
             const int4 t = __ldg(reinterpret_cast<const int4*>(ps) + q);
