@@ -72,6 +72,14 @@ __host__ __device__ constexpr uint32_t tmem_cols_pow2() {
   return N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : N <= 256 ? 256 : 512;
 }
 
+// Diagnostic timeline (PIT_GK2_DIAG bit 4): globaltimer stamps of CTA (pair) 0's first 128 stages / units.
+__device__ unsigned long long g_gk2_trace[8 * 128];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // One 32-row x 64-column output box of a warp's TMEM lane quarter -> C through a TMA tile store:
 // tcgen05.ld (two x32) -> bf16/fp16 -> 128B-swizzled shared staging (conflict-free 16-byte stores)
 // -> cp.async.bulk.tensor store of whole 128-byte lines. Two staging buffers per warp alternate; a
@@ -298,6 +306,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int a_sub = lane / Cfg::A_CPR;
     const int a_ch = lane % Cfg::A_CPR;
     const uint32_t a_base = static_cast<uint32_t>((a_ch / Cfg::A_CPA) * (Cfg::KS * Cfg::A_ROW_BYTES));
+    int tj = 0;
     auto issue = [&](const Pos& p, const Idx& x) {
       const int kvalid = min(Cfg::KS, p.cnt - p.kb);
       const int kpad = (kvalid + 15) & ~15;
@@ -305,8 +314,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m0 = p.g * grp_rows;
       const int m_end = min(M, m0 + grp_rows);
       mbar_wait(&empty_bar[stage], phase ^ 1);
+      if ((use_tma_store & 16) && blockIdx.x == 0 && threadIdx.x == 0 && tj < 128) g_gk2_trace[tj] = gtimer();
+      ++tj;
       const int r0 = RW * warp;
-      if (r0 < kpad) {  // a warp's RW rows are all below kpad or all above it
+      if (r0 < kpad && !(use_tma_store & 8)) {  // a warp's RW rows are all below kpad or all above it
         const uint32_t sB = smem_u32(smem + stage * Cfg::STAGE_BYTES);
         const uint32_t sA = sB + Cfg::B_BYTES;
         // ---- B rows
@@ -379,20 +390,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const bool tr = (use_tma_store & 16) && blockIdx.x == 0 && lane == 0;
+    int tj = 0, ui = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++ui) {
       const int cnt = __ldg(counts + u % n_groups);
       mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc_fence_after();
+      if (tr && ui < 128) g_gk2_trace[3 * 128 + ui] = gtimer();
       for (int kb = 0; kb < cnt; kb += Cfg::KS) {
         const int ksteps = (min(Cfg::KS, cnt - kb) + 15) >> 4;
         mbar_wait(&full_bar[stage], phase);
         fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05.mma reads
         tc_fence_after();
+        if (tr && tj < 128) g_gk2_trace[128 + tj] = gtimer();
         if (lane == 0) {
           const uint32_t sB = smem_u32(smem + stage * Cfg::STAGE_BYTES);
           const uint32_t sA = sB + Cfg::B_BYTES;
           const uint32_t dbase = tmem_base + static_cast<uint32_t>(acc * Cfg::ACC_COLS);
-          for (int ks = 0; ks < ksteps; ++ks) {
+          for (int ks = 0; ks < ((use_tma_store & 4) ? 0 : ksteps); ++ks) {
             const uint32_t acc_flag = (kb > 0 || ks > 0) ? 1u : 0u;
             const uint64_t a_strip = smem_desc(sA + ks * 16 * Cfg::A_ROW_BYTES, Cfg::KS * Cfg::A_ROW_BYTES,
                                                8 * Cfg::A_ROW_BYTES, Cfg::A_SW);
@@ -408,7 +423,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           umma_commit(&empty_bar[stage]);
+          if (tr && tj < 128) g_gk2_trace[2 * 128 + tj] = gtimer();
         }
+        ++tj;
         __syncwarp();
         if (++stage == Cfg::STAGES) {
           stage = 0;
@@ -429,6 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;  // TMEM lane quarter
     const uint32_t stg_w = smem_u32(stg) + static_cast<uint32_t>(q * 2 * 4096);
     int sbuf = 0;
+    int ui = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -439,6 +457,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int cnt = __ldg(counts + g);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
+      const bool tre = (use_tma_store & 16) && blockIdx.x == 0 && threadIdx.x == kEpiWarp0 * 32 && ui < 128;
+      if (tre) g_gk2_trace[4 * 128 + ui] = gtimer();
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * Cfg::ACC_COLS);
       if (kOrientN && (use_tma_store & 1)) {
         // lane = group row: 32-row x 64-column boxes through shared staging and TMA stores
@@ -548,6 +568,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      if (tre) g_gk2_trace[5 * 128 + ui] = gtimer();
+      ++ui;
       tc_fence_before();
       mbar_arrive(&tempty_bar[acc]);
       if (++acc == Cfg::NBUF) {
@@ -596,13 +618,6 @@ struct Gk2Cfg {
   static constexpr size_t SMEM = static_cast<size_t>(STAGES) * STAGE_BYTES + STG_BYTES + 1024 + 1024;
 };
 constexpr int kRelayWarp = 10;
-// Diagnostic timeline (PIT_GK2_DIAG bit 4): globaltimer stamps of pair 0's first 128 stages.
-__device__ unsigned long long g_gk2_trace[8 * 128];
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 
 template <bool kBF16, int kKS>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -1461,6 +1476,9 @@ int run_gk(const SpmmArgs& a, cudaStream_t s) {
     epi |= 1;
   }
   if (gk2_diag() & 4) epi |= 2;  // diagnostic: no C stores (orientation T)
+  if (gk2_diag() & 1) epi |= 4;  // diagnostic: no MMAs
+  if (gk2_diag() & 2) epi |= 8;  // diagnostic: no operand copies
+  if (gk2_diag() & 16) epi |= 16;  // diagnostic: stage / unit timeline of CTA 0
   // A column-major: A^T is row-major [K, M] with pitch sak
   kern<<<grid, kThreads, Cfg::SMEM, s>>>(tmC, epi, a.B, a.ldb, a.A, a.sak, a.counts, a.slots, a.slot_stride,
                                          static_cast<int>(a.n_groups), n_tiles, static_cast<int>(a.M),
