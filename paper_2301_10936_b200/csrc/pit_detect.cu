@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kRaWarps * 32, 4) detect_rows_vec_kernel(const
                                                                           int64_t tiles) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const bool is_start = (lane % V) == 0;
+  const bool is_start = (lane % (V < 32 ? V : 32)) == 0;
   const uint32_t vmask = V >= 32 ? 0xffffffffu : ((1u << V) - 1u);
   // persistent: tile = (row block of 32 micro-rows, group of kRaWarps 512-byte column segments)
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
@@ -133,7 +133,13 @@ __global__ void __launch_bounds__(kRaWarps * 32, 4) detect_rows_vec_kernel(const
     }
     if (is_start && col_ok) {
       const int64_t j = vec / V;
-      if (j < GC) occ[j * WG + rb] = bits;
+      // V > 32: a micro-column spans several 512-byte segments (warps); they OR into a zeroed word
+      if (j < GC) {
+        if (V <= 32)
+          occ[j * WG + rb] = bits;
+        else if (bits)
+          atomicOr(&occ[j * WG + rb], bits);
+      }
     }
   }
 }
@@ -399,7 +405,11 @@ int launch_detect_values(const DetectValuesArgs& a, cudaStream_t s) {
   const bool aligned = (reinterpret_cast<uintptr_t>(a.x) % 16 == 0) && (ld_bytes % 16 == 0) && (row_bytes % 16 == 0);
   const bool pow2 = vec_per_micro >= 1 && vec_per_micro <= 32 && (vec_per_micro & (vec_per_micro - 1)) == 0 &&
                     (static_cast<int64_t>(a.tc) * eb) % 16 == 0;
-  if (a.pit_phys == 0 && aligned && pow2) {
+  // wide micro-columns (e.g. BERT's (1, 768) row micro-tiles): whole 512-byte segments per micro-column
+  const bool wide = vec_per_micro > 32 && vec_per_micro % 32 == 0 && (static_cast<int64_t>(a.tc) * eb) % 16 == 0;
+  if (a.pit_phys == 0 && aligned && (pow2 || wide)) {
+    if (wide && cudaMemsetAsync(a.occ, 0, static_cast<size_t>(n_groups * WG) * sizeof(uint32_t), s) != cudaSuccess)
+      return cuda_status();
     const int64_t segs = ceil_div(row_bytes, 512);
     const int64_t seg_groups = ceil_div(segs, kRaWarps);
     const int64_t tiles = seg_groups * ceil_div(GR, 32);

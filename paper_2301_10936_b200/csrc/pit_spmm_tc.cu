@@ -1619,7 +1619,9 @@ int run_gm(const SpmmArgs& a, int ks, cudaStream_t s) {
   p.n_rows = dense ? nullptr : a.n_rows;
   p.row_src = dense ? nullptr : a.rows;
   p.row_dst = dense ? nullptr : a.rows;
-  p.occ = dense ? nullptr : a.occ;
+  // one K-group (micro-tile spans all of K, e.g. BERT's row-uniform (1, K)): every union row is live
+  // in every K-block, so no per-row liveness lookups or per-stage votes
+  p.occ = (dense || ceil_div(a.K, a.t1) == 1) ? nullptr : a.occ;
   p.WG = a.WG;
   p.t1 = dense ? 1 : a.t1;
   p.max_tiles = static_cast<int>(ceil_div(dense ? a.M : a.n_rows_host, 128));
