@@ -382,9 +382,20 @@ def moe_bench(args, world, rank, dev, peaks, tokens_per_gpu=16384, n_experts=128
         dist.barrier()
     toks = world * tokens_per_gpu / (ms * 1e-3)
     flops = switch_flops(world * tokens_per_gpu, d_model, d_ff) / (ms * 1e-3) / 1e12
+    # HBM roofline of one rank's layer: its experts' weights are streamed once (2 matrices x El x
+    # d_model x d_ff bf16) plus the token rows read / written (x, hidden, output; pack / combine
+    # buffers not counted). At 128 tokens per expert this, not the tensor pipe, bounds the layer.
+    hbm_bytes = 2 * El * d_model * d_ff * 2 + received * (d_model * 2 * 2 + d_ff * 2 * 2) + tokens_per_gpu * d_model * 2 * 2
+    hbm_gbps = hbm_bytes / (ms * 1e-3) / 1e9
     return {"metric": "MoE layer tokens/s", "value": round(toks, 1), "unit": "tokens/s", "n_gpus": world,
             "ms_per_layer": round(ms, 4), "expert_tflops_per_gpu": round(flops / world, 2),
             "frac_bf16_peak": round(flops / world / peaks["bf16"], 4),
+            "roofline": {"bound": "hbm", "achieved": round(hbm_gbps, 1), "peak": peaks["hbm"], "unit": "GB/s",
+                         "frac": round(hbm_gbps / peaks["hbm"], 4), "traffic": None,
+                         "algorithmic_bytes_per_layer": int(hbm_bytes),
+                         "note": "expert weights streamed once per layer dominate; tensor-time floor "
+                                 f"{switch_flops(tokens_per_gpu, d_model, d_ff) / peaks['bf16'] / 1e9:.3f} ms vs HBM floor "
+                                 f"{hbm_bytes / peaks['hbm'] / 1e6:.3f} ms"},
             "config": {"experts": E, "experts_per_gpu": El, "d_model": d_model, "d_ff": d_ff,
                        "tokens_per_gpu": tokens_per_gpu, "routing": "top-1 argmax, Gaussian logits, dropless",
                        "parallelism": f"ep{world}" if world > 1 else "single GPU", "received_rank0": int(received)},
