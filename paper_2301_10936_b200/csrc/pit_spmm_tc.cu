@@ -1414,6 +1414,264 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// =============================================================================================
+// rowgemm2: the dense / contiguous-row cases of rowgemm (no per-row liveness, single group or
+// uniform batched slices) on CTA pairs — tcgen05 cta_group::2, 256 x 256 tiles. CTA r holds rows
+// [128 r, 128 r + 128) of the pair tile and columns [128 r, 128 r + 128) of the B tile, so each
+// CTA moves 32 KB per 64-deep K-block for a 128 x 256 x 64 share of the MMA (131 FLOP per byte,
+// against 87 for the single-CTA 128 x 256 tile whose operand feed bounds it near 1 PFLOP/s).
+// Pipeline as spmm_gk2: local full barrier (TMA bytes + cp.async arrivals) -> relay -> even CTA's
+// pair barrier -> pair MMA -> multicast commits; each CTA drains and stores its own 128 rows.
+// =============================================================================================
+struct Rg2Cfg {
+  static constexpr int KS = 64;
+  static constexpr int BN = 256;
+  static constexpr int A_BYTES = 128 * KS * 2;        // K-major rows, 128B swizzle
+  static constexpr int B_BYTES = 2 * KS * 128;        // the CTA's 128-column half: 2 MN-major atoms
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STG_BYTES = 4 * 4096;
+  static constexpr int STAGE_BUDGET = 232448 - 2048 - STG_BYTES;
+  static constexpr int STAGES = STAGE_BUDGET / STAGE_BYTES > 8 ? 8 : STAGE_BUDGET / STAGE_BYTES;
+  static constexpr size_t SMEM = static_cast<size_t>(STAGES) * STAGE_BYTES + STG_BYTES + 2048;
+};
+
+// CTA r's 128-row tile of pair tile pt (rows may be <= 0: a partial pair, nothing stored)
+__device__ __forceinline__ RowTile decode_pair_tile(const RowGemmParams& p, int pt, int r, int single_rows) {
+  if (p.uniform_rows) {
+    const int tpg = (p.uniform_rows + 255) >> 8;
+    const int g = pt / tpg, start = (pt - g * tpg) * 256 + 128 * r;
+    return {g, g * p.uniform_rows + start, min(128, p.uniform_rows - start)};
+  }
+  const int base = pt * 256 + 128 * r;
+  return {0, base, min(128, single_rows - base)};
+}
+
+template <bool kBF16>
+__global__ void __launch_bounds__(kThreads, 1)
+    rowgemm2_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmA,
+                    const __grid_constant__ RowGemmParams p, int n_tiles, int pair_tiles) {
+  using Cfg = Rg2Cfg;
+  constexpr int KS = Cfg::KS;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stg = smem + Cfg::STAGES * Cfg::STAGE_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(stg + Cfg::STG_BYTES);
+  uint64_t* pair_full = full_bar + Cfg::STAGES;
+  uint64_t* empty_bar = pair_full + Cfg::STAGES;
+  uint64_t* tfull_bar = empty_bar + Cfg::STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = static_cast<int>(blockIdx.x >> 1);
+  const int npairs = static_cast<int>(gridDim.x >> 1);
+  const int single_rows = p.n_rows ? *p.n_rows : p.M;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < Cfg::STAGES; ++i) {
+      mbar_init(&full_bar[i], kProdThreads + 1);
+      mbar_init(&pair_full[i], 2);
+      mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull_bar[i], 1);
+      mbar_init(&tempty_bar[i], 8);  // 4 epilogue warps x 2 CTAs
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == kAllocWarp) tmem_alloc2<512>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int units = pair_tiles * n_tiles;
+  const int kblocks = (p.K + KS - 1) / KS;
+
+  if (warp < kProdWarps) {
+    // ------------------------------------------------------------ producers
+    constexpr int CPR = KS * 2 / 16;               // 16-byte chunks per A row
+    constexpr int RPT = 128 * CPR / kProdThreads;  // A rows per producer thread (gathered rows)
+    constexpr int RSTEP = kProdThreads / CPR;
+    const int tp = threadIdx.x;
+    const int ch = tp % CPR;
+    using T = typename OutT<kBF16>::T;
+    const T* Ap = static_cast<const T*>(p.A);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = pair; u < units; u += npairs) {
+      const RowTile rt = decode_pair_tile(p, u / n_tiles, static_cast<int>(rank), single_rows);
+      const int n0 = (u % n_tiles) * Cfg::BN + 128 * static_cast<int>(rank);
+      int rid[RPT];
+      if (!p.a_tma) {
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+          const int i = tp / CPR + j * RSTEP;
+          rid[j] = i < rt.rows ? tile_src_row(p, rt, i) : -1;
+        }
+      }
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const int k0 = kb * KS;
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        uint8_t* sAp = smem + stage * Cfg::STAGE_BYTES;
+        uint8_t* sB = sAp + Cfg::A_BYTES;
+        if (tp == 0) {
+          mbar_expect_tx_only(&full_bar[stage], Cfg::B_BYTES + (p.a_tma ? Cfg::A_BYTES : 0));
+          tma_load_3d(sB, &tmB, &full_bar[stage], n0, k0, rt.g);
+          tma_load_3d(sB + KS * 128, &tmB, &full_bar[stage], n0 + 64, k0, rt.g);
+          if (p.a_tma) tma_load_2d(sAp, &tmA, &full_bar[stage], k0, rt.base);
+          mbar_arrive(&full_bar[stage]);
+        }
+        if (!p.a_tma) {
+          const uint32_t sA = smem_u32(sAp);
+          const int kc = k0 + ch * 8;
+          const uint32_t kbytes = kc < p.K ? static_cast<uint32_t>(min(16, (p.K - kc) * 2)) : 0u;
+#pragma unroll
+          for (int j = 0; j < RPT; ++j) {
+            const int row = tp / CPR + j * RSTEP;
+            const uint32_t bytes = rid[j] >= 0 ? kbytes : 0u;
+            const T* src = bytes ? Ap + static_cast<int64_t>(rid[j]) * p.lda + kc : Ap;
+            cp_async_16(sA + swz<7>(static_cast<uint32_t>(row * 128 + ch * 16)), src, bytes);
+          }
+        }
+        cp_async_arrive_noinc(&full_bar[stage]);
+        if (++stage == Cfg::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == kRelayWarp) {
+    // ------------------------------------------------------------ relay: local full -> pair full
+    if (lane == 0) {
+      const uint32_t leader_pf = mapa_shared(smem_u32(pair_full), 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = pair; u < units; u += npairs) {
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          fence_proxy_async_smem();
+          mbar_arrive_cluster(leader_pf + stage * 8);
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ------------------------------------------------------------ MMA issuer (even CTA)
+    if (rank == 0) {
+      constexpr uint32_t idesc = idesc_f16(256, Cfg::BN, kBF16, false, true);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = pair; u < units; u += npairs) {
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&pair_full[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t sA = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+            const uint32_t sB = sA + Cfg::A_BYTES;
+#pragma unroll
+            for (int ks = 0; ks < KS / 16; ++ks) {
+              const uint64_t adesc = smem_desc(sA + ks * 32, 16, 8 * 128, kSw128);
+              const uint64_t bdesc = smem_desc(sB + ks * 2048, KS * 128, 1024, kSw128);
+              umma2_f16(tmem_base + static_cast<uint32_t>(acc * Cfg::BN), adesc, bdesc, idesc,
+                        (kb > 0 || ks > 0) ? 1u : 0u);
+            }
+            umma2_commit_mc(&empty_bar[stage], 3);
+          }
+          __syncwarp();
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (lane == 0) umma2_commit_mc(&tfull_bar[acc], 3);
+        __syncwarp();
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= kEpiWarp0) {
+    // ------------------------------------------------------------ epilogue: this CTA's 128 rows
+    using T = typename OutT<kBF16>::T;
+    const int q = warp & 3;
+    const uint32_t leader_te = mapa_shared(smem_u32(tempty_bar), 0);
+    const uint32_t box = smem_u32(stg) + static_cast<uint32_t>(q * 4096);
+    T* C = static_cast<T*>(p.C);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = pair; u < units; u += npairs) {
+      const RowTile rt = decode_pair_tile(p, u / n_tiles, static_cast<int>(rank), single_rows);
+      const int n0 = (u % n_tiles) * Cfg::BN;
+      const int i = q * 32 + lane;
+      const int row = i < rt.rows ? tile_dst_row(p, rt, i) : -1;
+      const float scale = (row >= 0 && p.row_scale) ? __ldg(p.row_scale + row) : 1.0f;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+#pragma unroll 1
+      for (int bx = 0; bx < Cfg::BN / 64; ++bx) {
+        uint32_t v[64];
+        const uint32_t ta = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * Cfg::BN + bx * 64);
+        tmem_ld32(ta, *reinterpret_cast<uint32_t(*)[32]>(v));
+        tmem_ld32(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+        tmem_wait_ld();
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float f[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            float x = __uint_as_float(v[8 * j + e]);
+            if (p.act == 1) x = fmaxf(x, 0.0f);
+            f[e] = x * scale;
+          }
+          st_shared_v4(box + lane * 128 + ((static_cast<uint32_t>(j) ^ static_cast<uint32_t>(lane & 7)) << 4),
+                       pack2(f[0], f[1], kBF16), pack2(f[2], f[3], kBF16), pack2(f[4], f[5], kBF16),
+                       pack2(f[6], f[7], kBF16));
+        }
+        __syncwarp();
+        const int ch = lane & 7;
+        const int col = n0 + bx * 64 + ch * 8;
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int r = it * 4 + (lane >> 3);
+          const int drow = __shfl_sync(0xffffffffu, row, r);
+          const uint4 w = ld_shared_v4(box + r * 128 + ((static_cast<uint32_t>(ch) ^ static_cast<uint32_t>(r & 7)) << 4));
+          if (drow >= 0 && col < p.N) {
+            T* dst = C + static_cast<int64_t>(drow) * p.ldc + col;
+            if (col + 8 <= p.N) {
+              *reinterpret_cast<uint4*>(dst) = w;
+            } else {
+              const T* h = reinterpret_cast<const T*>(&w);
+              for (int e = 0; e < p.N - col; ++e) dst[e] = h[e];
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_te + acc * 8);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == kAllocWarp) {
+    tc_fence_after();
+    tmem_dealloc2<512>(tmem_base);
+  }
+}
+
 int g_num_sms = 0;
 
 int num_sms() {
@@ -1585,9 +1843,78 @@ int run_rowgemm(const RowGemmParams& p, const void* B, int64_t ldb, int64_t grou
   return cuda_status();
 }
 
+int rg2_enabled() {  // PIT_RG2=0: single-CTA rowgemm for the dense / contiguous-row cases too
+  static int v = [] {
+    const char* e = getenv("PIT_RG2");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
+// CTA-pair launch of the dense / contiguous-row rowgemm cases (see rowgemm2_kernel).
+template <bool kBF16>
+int run_rowgemm2(const RowGemmParams& p, const void* B, int64_t ldb, int64_t group_stride, cudaStream_t s) {
+  using Cfg = Rg2Cfg;
+  constexpr int KS = Cfg::KS;
+  const CUtensorMapDataType dt = kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  CUtensorMap tmB, tmA;
+  memset(&tmA, 0, sizeof(tmA));
+  const uint64_t gstride = static_cast<uint64_t>(group_stride > 0 ? group_stride : ldb * p.K) * 2;
+  if (encode_tensor_map_3d(&tmB, dt, B, p.N, p.K, p.G, ldb * 2, gstride, 64, KS, CU_TENSOR_MAP_SWIZZLE_128B) !=
+      CUDA_SUCCESS)
+    return kErrCuda;
+  RowGemmParams q = p;
+  q.a_tma = 0;
+  if (p.row_src == nullptr && (p.lda * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(p.A) & 15) == 0 &&
+      a_tma_enabled()) {
+    if (encode_tensor_map_2d(&tmA, dt, p.A, static_cast<uint64_t>(p.K), static_cast<uint64_t>(p.M),
+                             static_cast<uint64_t>(p.lda) * 2, KS, 128, CU_TENSOR_MAP_SWIZZLE_128B) != CUDA_SUCCESS)
+      return kErrCuda;
+    q.a_tma = 1;
+  }
+  const int rows = p.uniform_rows ? p.uniform_rows : p.max_tiles * 128;
+  const int pair_tiles = static_cast<int>(p.uniform_rows ? p.G * ceil_div(p.uniform_rows, 256) : ceil_div(rows, 256));
+  const int n_tiles = static_cast<int>(ceil_div(p.N, Cfg::BN));
+  const int64_t units = static_cast<int64_t>(pair_tiles) * n_tiles;
+  if (units == 0) return kOk;
+  if (units >= (1ll << 31)) return kErrShape;
+  auto kern = rowgemm2_kernel<kBF16>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::SMEM));
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  static int max_pairs = 0;
+  if (max_pairs == 0) {
+    cfg.gridDim = dim3(static_cast<unsigned>(num_sms() & ~1));
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) != cudaSuccess || nc <= 0) {
+      cudaGetLastError();
+      nc = num_sms() / 2;
+    }
+    max_pairs = nc;
+  }
+  const int pairs = static_cast<int>(units < max_pairs ? units : max_pairs);
+  cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
+  cudaLaunchKernelEx(&cfg, kern, tmB, tmA, q, n_tiles, pair_tiles);
+  note_launch();
+  return cuda_status();
+}
+
 template <bool kBF16>
 int rowgemm_dispatch(const RowGemmParams& p, const void* B, int64_t ldb, int ks, cudaStream_t s,
                      int64_t group_stride = 0) {
+  // dense / contiguous-row cases (no liveness, one group or uniform slices, N > 128) on CTA pairs
+  if (ks == 64 && p.N > 128 && p.occ == nullptr && p.cnt == nullptr && (p.ldc % 8) == 0 &&
+      (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && rg2_enabled())
+    return run_rowgemm2<kBF16>(p, B, ldb, group_stride, s);
   if (p.N <= 64) {  // narrow products: 64-column units, no zero-filled B atoms or idle MMA columns
     if (ks == 64) return run_rowgemm<64, kBF16, 64>(p, B, ldb, group_stride, s);
     if (ks == 32) return run_rowgemm<32, kBF16, 64>(p, B, ldb, group_stride, s);
