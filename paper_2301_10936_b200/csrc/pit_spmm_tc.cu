@@ -1423,6 +1423,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Pipeline as spmm_gk2: local full barrier (TMA bytes + cp.async arrivals) -> relay -> even CTA's
 // pair barrier -> pair MMA -> multicast commits; each CTA drains and stores its own 128 rows.
 // =============================================================================================
+constexpr int kRg2MaxGroups = 1024;
+
 struct Rg2Cfg {
   static constexpr int KS = 64;
   static constexpr int BN = 256;
@@ -1435,8 +1437,19 @@ struct Rg2Cfg {
   static constexpr size_t SMEM = static_cast<size_t>(STAGES) * STAGE_BYTES + STG_BYTES + 2048;
 };
 
-// CTA r's 128-row tile of pair tile pt (rows may be <= 0: a partial pair, nothing stored)
-__device__ __forceinline__ RowTile decode_pair_tile(const RowGemmParams& p, int pt, int r, int single_rows) {
+// CTA r's 128-row tile of pair tile pt (rows may be <= 0: a partial pair, nothing stored).
+// Grouped (MoE experts): pto = shared prefix of ceil(cnt[g] / 256) over the groups.
+__device__ __forceinline__ RowTile decode_pair_tile(const RowGemmParams& p, int pt, int r, int single_rows,
+                                                    const int* pto) {
+  if (p.cnt != nullptr) {
+    int lo = 0, hi = p.G;  // last g with pto[g] <= pt
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (pto[mid] <= pt) lo = mid; else hi = mid;
+    }
+    const int start = (pt - pto[lo]) * 256 + 128 * r;
+    return {lo, __ldg(p.off + lo) + start, min(128, __ldg(p.cnt + lo) - start)};
+  }
   if (p.uniform_rows) {
     const int tpg = (p.uniform_rows + 255) >> 8;
     const int g = pt / tpg, start = (pt - g * tpg) * 256 + 128 * r;
@@ -1468,6 +1481,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int pair = static_cast<int>(blockIdx.x >> 1);
   const int npairs = static_cast<int>(gridDim.x >> 1);
   const int single_rows = p.n_rows ? *p.n_rows : p.M;
+  __shared__ int pto[kRg2MaxGroups + 1];  // grouped: prefix of pair tiles per group
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < Cfg::STAGES; ++i) {
@@ -1483,11 +1497,30 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmB);
   }
   if (warp == kAllocWarp) tmem_alloc2<512>(tmem_slot);
+  if (p.cnt != nullptr && warp == kRelayWarp + 1) {
+    // warp 11: pair tiles per group, scanned (each lane a contiguous run of groups)
+    const int per = (p.G + 31) / 32;
+    const int g0 = lane * per;
+    int run = 0;
+    for (int g = g0; g < min(p.G, g0 + per); ++g) run += (__ldg(p.cnt + g) + 255) >> 8;
+    int incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int acc = incl - run;
+    for (int g = g0; g < min(p.G, g0 + per); ++g) {
+      pto[g] = acc;
+      acc += (__ldg(p.cnt + g) + 255) >> 8;
+    }
+    if (lane == 31) pto[p.G] = incl;
+  }
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int units = pair_tiles * n_tiles;
+  const int units = (p.cnt != nullptr ? min(pair_tiles, pto[p.G]) : pair_tiles) * n_tiles;
   const int kblocks = (p.K + KS - 1) / KS;
 
   if (warp < kProdWarps) {
@@ -1502,7 +1535,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int u = pair; u < units; u += npairs) {
-      const RowTile rt = decode_pair_tile(p, u / n_tiles, static_cast<int>(rank), single_rows);
+      const RowTile rt = decode_pair_tile(p, u / n_tiles, static_cast<int>(rank), single_rows, pto);
       const int n0 = (u % n_tiles) * Cfg::BN + 128 * static_cast<int>(rank);
       int rid[RPT];
       if (!p.a_tma) {
@@ -1609,7 +1642,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = pair; u < units; u += npairs) {
-      const RowTile rt = decode_pair_tile(p, u / n_tiles, static_cast<int>(rank), single_rows);
+      const RowTile rt = decode_pair_tile(p, u / n_tiles, static_cast<int>(rank), single_rows, pto);
       const int n0 = (u % n_tiles) * Cfg::BN;
       const int i = q * 32 + lane;
       const int row = i < rt.rows ? tile_dst_row(p, rt, i) : -1;
@@ -1851,6 +1884,14 @@ int rg2_enabled() {  // PIT_RG2=0: single-CTA rowgemm for the dense / contiguous
   return v;
 }
 
+int rg2_grouped() {  // PIT_RG2_GROUPED=0: grouped (MoE) GEMMs stay on single-CTA 128-row tiles
+  static int v = [] {
+    const char* e = getenv("PIT_RG2_GROUPED");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 // CTA-pair launch of the dense / contiguous-row rowgemm cases (see rowgemm2_kernel).
 template <bool kBF16>
 int run_rowgemm2(const RowGemmParams& p, const void* B, int64_t ldb, int64_t group_stride, cudaStream_t s) {
@@ -1873,7 +1914,9 @@ int run_rowgemm2(const RowGemmParams& p, const void* B, int64_t ldb, int64_t gro
     q.a_tma = 1;
   }
   const int rows = p.uniform_rows ? p.uniform_rows : p.max_tiles * 128;
-  const int pair_tiles = static_cast<int>(p.uniform_rows ? p.G * ceil_div(p.uniform_rows, 256) : ceil_div(rows, 256));
+  // grouped: the device prefix decides; max_tiles (128-row tiles) bounds the pair tiles
+  const int pair_tiles = static_cast<int>(p.cnt ? p.max_tiles
+                                          : p.uniform_rows ? p.G * ceil_div(p.uniform_rows, 256) : ceil_div(rows, 256));
   const int n_tiles = static_cast<int>(ceil_div(p.N, Cfg::BN));
   const int64_t units = static_cast<int64_t>(pair_tiles) * n_tiles;
   if (units == 0) return kOk;
@@ -1912,8 +1955,8 @@ template <bool kBF16>
 int rowgemm_dispatch(const RowGemmParams& p, const void* B, int64_t ldb, int ks, cudaStream_t s,
                      int64_t group_stride = 0) {
   // dense / contiguous-row cases (no liveness, one group or uniform slices, N > 128) on CTA pairs
-  if (ks == 64 && p.N > 128 && p.occ == nullptr && p.cnt == nullptr && (p.ldc % 8) == 0 &&
-      (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && rg2_enabled())
+  if (ks == 64 && p.N > 128 && p.occ == nullptr && (p.cnt == nullptr || (p.G <= kRg2MaxGroups && rg2_grouped())) &&
+      (p.ldc % 8) == 0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && rg2_enabled())
     return run_rowgemm2<kBF16>(p, B, ldb, group_stride, s);
   if (p.N <= 64) {  // narrow products: 64-column units, no zero-filled B atoms or idle MMA columns
     if (ks == 64) return run_rowgemm<64, kBF16, 64>(p, B, ldb, group_stride, s);

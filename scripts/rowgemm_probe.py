@@ -56,3 +56,12 @@ layer = SwitchMoE(w1, w2, E)
 ms = timed(lambda: layer(x, logits))
 f = 2 * T * d * ff * 2
 print(f"moe layer T={T}: {ms:.4f} ms = {T / ms / 1e3:.0f} k tokens/s, {f / ms / 1e9:.1f} TFLOP/s (expert FLOPs / layer time)")
+
+# per-rank share of an 8-GPU expert-parallel layer: 16 local experts, 16384 received tokens
+E8 = 16
+w1b = (torch.randn((E8, d, ff), device=dev, generator=g) / d ** 0.5).to(torch.bfloat16)
+w2b = (torch.randn((E8, ff, d), device=dev, generator=g) / ff ** 0.5).to(torch.bfloat16)
+logits8 = torch.randn((T, E8), device=dev, dtype=torch.float32, generator=g)
+layer8 = SwitchMoE(w1b, w2b, E8)
+ms = timed(lambda: layer8(x, logits8))
+print(f"moe layer T={T} E={E8} (EP8 per-rank proxy): {ms:.4f} ms = {T / ms / 1e3:.0f} k tokens/s, {f / ms / 1e9:.1f} TFLOP/s")
