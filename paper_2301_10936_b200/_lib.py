@@ -7,10 +7,15 @@ operation raises. ``load()`` builds the library in-tree on first use when nvcc i
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
 _LIB_PATH = Path(__file__).resolve().parent / "libpit_b200.so"
+# A/B knob for kernel work: PIT_LIB_PATH points at an alternative build of the same library
+# (e.g. an older revision built into build_alt/); the product always ships the in-tree build.
+if os.environ.get("PIT_LIB_PATH"):
+    _LIB_PATH = Path(os.environ["PIT_LIB_PATH"])
 _lock = threading.Lock()
 _lib = None
 

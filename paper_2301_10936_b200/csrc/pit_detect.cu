@@ -349,10 +349,23 @@ __global__ void __launch_bounds__(kCompactThreads) compact_kernel(const uint32_t
       total += v;
     }
     int pos = base + wbase + incl - c;
-    while (word) {
-      const int b = __ffs(word) - 1;
-      word &= word - 1;
-      out[pos++] = static_cast<int32_t>(w * 32 + b);
+    // dense words (e.g. attention windows): a lane walking its own word's 32 bits serialises the
+    // warp and scatters 4-byte stores; instead the warp expands one word at a time, lane = bit,
+    // stores coalesced. Sparse words keep the per-lane walk (fewer iterations than 32).
+    const int maxc = __reduce_max_sync(0xffffffffu, c);
+    if (maxc > 8) {
+      const uint32_t below = (1u << lane) - 1u;
+      for (int j = 0; j < 32; ++j) {
+        const uint32_t wj = __shfl_sync(0xffffffffu, word, j);
+        const int pj = __shfl_sync(0xffffffffu, pos, j);
+        if ((wj >> lane) & 1u) out[pj + __popc(wj & below)] = static_cast<int32_t>((w - lane + j) * 32 + lane);
+      }
+    } else {
+      while (word) {
+        const int b = __ffs(word) - 1;
+        word &= word - 1;
+        out[pos++] = static_cast<int32_t>(w * 32 + b);
+      }
     }
     base += total;
     __syncthreads();

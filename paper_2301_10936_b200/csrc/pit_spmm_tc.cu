@@ -72,14 +72,6 @@ __host__ __device__ constexpr uint32_t tmem_cols_pow2() {
   return N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : N <= 256 ? 256 : 512;
 }
 
-// Diagnostic timeline (PIT_GK2_DIAG bit 4): globaltimer stamps of CTA (pair) 0's first 128 stages / units.
-__device__ unsigned long long g_gk2_trace[8 * 128];
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
 // One 32-row x 64-column output box of a warp's TMEM lane quarter -> C through a TMA tile store:
 // tcgen05.ld (two x32) -> bf16/fp16 -> 128B-swizzled shared staging (conflict-free 16-byte stores)
 // -> cp.async.bulk.tensor store of whole 128-byte lines. Two staging buffers per warp alternate; a
@@ -306,7 +298,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int a_sub = lane / Cfg::A_CPR;
     const int a_ch = lane % Cfg::A_CPR;
     const uint32_t a_base = static_cast<uint32_t>((a_ch / Cfg::A_CPA) * (Cfg::KS * Cfg::A_ROW_BYTES));
-    int tj = 0;
     auto issue = [&](const Pos& p, const Idx& x) {
       const int kvalid = min(Cfg::KS, p.cnt - p.kb);
       const int kpad = (kvalid + 15) & ~15;
@@ -314,10 +305,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m0 = p.g * grp_rows;
       const int m_end = min(M, m0 + grp_rows);
       mbar_wait(&empty_bar[stage], phase ^ 1);
-      if ((use_tma_store & 16) && blockIdx.x == 0 && threadIdx.x == 0 && tj < 128) g_gk2_trace[tj] = gtimer();
-      ++tj;
       const int r0 = RW * warp;
-      if (r0 < kpad && !(use_tma_store & 8)) {  // a warp's RW rows are all below kpad or all above it
+      if (r0 < kpad) {  // a warp's RW rows are all below kpad or all above it
         const uint32_t sB = smem_u32(smem + stage * Cfg::STAGE_BYTES);
         const uint32_t sA = sB + Cfg::B_BYTES;
         // ---- B rows
@@ -390,24 +379,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    const bool tr = (use_tma_store & 16) && blockIdx.x == 0 && lane == 0;
-    int tj = 0, ui = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++ui) {
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int cnt = __ldg(counts + u % n_groups);
       mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc_fence_after();
-      if (tr && ui < 128) g_gk2_trace[3 * 128 + ui] = gtimer();
       for (int kb = 0; kb < cnt; kb += Cfg::KS) {
         const int ksteps = (min(Cfg::KS, cnt - kb) + 15) >> 4;
         mbar_wait(&full_bar[stage], phase);
         fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05.mma reads
         tc_fence_after();
-        if (tr && tj < 128) g_gk2_trace[128 + tj] = gtimer();
         if (lane == 0) {
           const uint32_t sB = smem_u32(smem + stage * Cfg::STAGE_BYTES);
           const uint32_t sA = sB + Cfg::B_BYTES;
           const uint32_t dbase = tmem_base + static_cast<uint32_t>(acc * Cfg::ACC_COLS);
-          for (int ks = 0; ks < ((use_tma_store & 4) ? 0 : ksteps); ++ks) {
+          for (int ks = 0; ks < ksteps; ++ks) {
             const uint32_t acc_flag = (kb > 0 || ks > 0) ? 1u : 0u;
             const uint64_t a_strip = smem_desc(sA + ks * 16 * Cfg::A_ROW_BYTES, Cfg::KS * Cfg::A_ROW_BYTES,
                                                8 * Cfg::A_ROW_BYTES, Cfg::A_SW);
@@ -423,9 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           umma_commit(&empty_bar[stage]);
-          if (tr && tj < 128) g_gk2_trace[2 * 128 + tj] = gtimer();
         }
-        ++tj;
         __syncwarp();
         if (++stage == Cfg::STAGES) {
           stage = 0;
@@ -446,7 +429,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;  // TMEM lane quarter
     const uint32_t stg_w = smem_u32(stg) + static_cast<uint32_t>(q * 2 * 4096);
     int sbuf = 0;
-    int ui = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -457,8 +439,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int cnt = __ldg(counts + g);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
-      const bool tre = (use_tma_store & 16) && blockIdx.x == 0 && threadIdx.x == kEpiWarp0 * 32 && ui < 128;
-      if (tre) g_gk2_trace[4 * 128 + ui] = gtimer();
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * Cfg::ACC_COLS);
       if (kOrientN && (use_tma_store & 1)) {
         // lane = group row: 32-row x 64-column boxes through shared staging and TMA stores
@@ -568,8 +548,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (tre) g_gk2_trace[5 * 128 + ui] = gtimer();
-      ++ui;
       tc_fence_before();
       mbar_arrive(&tempty_bar[acc]);
       if (++acc == Cfg::NBUF) {
@@ -618,6 +596,18 @@ struct Gk2Cfg {
   static constexpr size_t SMEM = static_cast<size_t>(STAGES) * STAGE_BYTES + STG_BYTES + 1024 + 1024;
 };
 constexpr int kRelayWarp = 10;
+// Diagnostics (compiled in with -DPIT_DIAG=1 only: `PIT_DIAG=1 python -m paper_2301_10936_b200._build
+// --force`): PIT_GK2_DIAG bits 0-2 drop the MMAs / copies / C stores of spmm_gk2, bit 4 records its
+// stage timeline (globaltimer stamps of pair 0's first 128 stages, scripts/gk2_trace.py).
+#ifndef PIT_DIAG
+#define PIT_DIAG 0
+#endif
+__device__ unsigned long long g_gk2_trace[8 * 128];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 template <bool kBF16, int kKS>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -768,11 +758,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         src = static_cast<const T*>(Bv) + p.b * b_batch_stride + (nbytes ? n : 0);
       }
       mbar_wait(&empty_bar[stage], phase ^ 1);
-      if ((diag & 16) && pair == 0 && threadIdx.x == 0 && trace_j < 128) g_gk2_trace[rank * 128 + trace_j] = gtimer();
+      if ((PIT_DIAG && (diag & 16)) && pair == 0 && threadIdx.x == 0 && trace_j < 128) g_gk2_trace[rank * 128 + trace_j] = gtimer();
       ++trace_j;
       // rows [kvalid, kpad) are zero-filled; a warp's RW rows are all below kpad or all above it
       const int r0 = RW * warp;
-      if (r0 < kpad && !(diag & 2)) {
+      if (r0 < kpad && !(PIT_DIAG && (diag & 2))) {
         const uint32_t dst = smem_u32(smem + stage * Cfg::STAGE_BYTES) + lane_off;
 #pragma unroll
         for (int i = 0; i < RW; ++i) {
@@ -816,7 +806,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int cnt = __ldg(counts + u % n_groups);
         for (int kb = 0; kb < cnt; kb += Cfg::KS) {
           mbar_wait(&full_bar[stage], phase);
-          if ((diag & 16) && pair == 0 && tj < 128) g_gk2_trace[(2 + rank) * 128 + tj] = gtimer();
+          if ((PIT_DIAG && (diag & 16)) && pair == 0 && tj < 128) g_gk2_trace[(2 + rank) * 128 + tj] = gtimer();
           ++tj;
           fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05.mma reads
           mbar_arrive_cluster(leader_pf + stage * 8);
@@ -844,18 +834,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int ksteps = (min(Cfg::KS, cnt - kb) + 15) >> 4;
           mbar_wait(&pair_full[stage], phase);
           tc_fence_after();
-          if ((diag & 16) && pair == 0 && lane == 0 && tj < 128) g_gk2_trace[4 * 128 + tj] = gtimer();
+          if ((PIT_DIAG && (diag & 16)) && pair == 0 && lane == 0 && tj < 128) g_gk2_trace[4 * 128 + tj] = gtimer();
           if (lane == 0) {
             const uint32_t sA = smem_u32(smem + stage * Cfg::STAGE_BYTES);
             const uint32_t sB = sA + Cfg::OP_BYTES;
             const uint32_t d = tmem_base + static_cast<uint32_t>(acc * Cfg::ACC_COLS);
-            for (int ks = 0; ks < ((diag & 1) ? 0 : ksteps); ++ks) {
+            for (int ks = 0; ks < ((PIT_DIAG && (diag & 1)) ? 0 : ksteps); ++ks) {
               const uint64_t adesc = smem_desc(sA + ks * 2048, Cfg::KS * 128, 1024, kSw128);
               const uint64_t bdesc = smem_desc(sB + ks * 2048, Cfg::KS * 128, 1024, kSw128);
               umma2_f16(d, adesc, bdesc, idesc, (kb > 0 || ks > 0) ? 1u : 0u);
             }
             umma2_commit_mc(&empty_bar[stage], 3);
-            if ((diag & 16) && pair == 0 && tj < 128) g_gk2_trace[5 * 128 + tj] = gtimer();
+            if ((PIT_DIAG && (diag & 16)) && pair == 0 && tj < 128) g_gk2_trace[5 * 128 + tj] = gtimer();
           }
           ++tj;
           __syncwarp();
@@ -919,7 +909,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < 32; ++i) v[i] = 0u;
           }
           const int nb = n0 + cc;
-          if (row_ok && nb < N && !(diag & 4)) {
+          if (row_ok && nb < N && !(PIT_DIAG && (diag & 4))) {
             if (vec_ok && nb + 32 <= N) {
               uint4* dstp = reinterpret_cast<uint4*>(crow + static_cast<int64_t>(nb) * 2);
 #pragma unroll
@@ -1767,9 +1757,6 @@ int run_gk(const SpmmArgs& a, cudaStream_t s) {
     epi |= 1;
   }
   if (gk2_diag() & 4) epi |= 2;  // diagnostic: no C stores (orientation T)
-  if (gk2_diag() & 1) epi |= 4;  // diagnostic: no MMAs
-  if (gk2_diag() & 2) epi |= 8;  // diagnostic: no operand copies
-  if (gk2_diag() & 16) epi |= 16;  // diagnostic: stage / unit timeline of CTA 0
   // A column-major: A^T is row-major [K, M] with pitch sak
   kern<<<grid, kThreads, Cfg::SMEM, s>>>(tmC, epi, a.B, a.ldb, a.A, a.sak, a.counts, a.slots, a.slot_stride,
                                          static_cast<int>(a.n_groups), n_tiles, static_cast<int>(a.M),

@@ -1,4 +1,5 @@
 #!/bin/bash
+# needs a diagnostic build: PIT_DIAG=1 python -m paper_2301_10936_b200._build --force
 OUT=gpurun_out; mkdir -p $OUT
 for cfg in ${GK2_CFGS:-"PIT_GK_KS=128" "PIT_GK_KS=128 PIT_GK2_DIAG=1" "PIT_GK_KS=128 PIT_GK2_DIAG=2" "PIT_GK_KS=128 PIT_GK2_DIAG=3"}; do
   cfg=${cfg//,/ }

@@ -1,4 +1,5 @@
-"""Stage timeline of the CTA-pair gathered-K kernel (pair 0), from PIT_GK2_DIAG bit 4 stamps.
+"""Stage timeline of the CTA-pair gathered-K kernel (pair 0), from PIT_GK2_DIAG bit 4 stamps (needs a
+diagnostic build: PIT_DIAG=1 python -m paper_2301_10936_b200._build --force).
 
     PIT_GK2_DIAG=16 python scripts/gk2_trace.py      (add 1/2/4 to drop MMA / copies / stores)
 """
