@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(kCompactThreads) compact_kernel(const uint32_t
     // warp and scatters 4-byte stores; instead the warp expands one word at a time, lane = bit,
     // stores coalesced. Sparse words keep the per-lane walk (fewer iterations than 32).
     const int maxc = __reduce_max_sync(0xffffffffu, c);
-    if (maxc > 8) {
+    if (maxc > 20) {
       const uint32_t below = (1u << lane) - 1u;
       for (int j = 0; j < 32; ++j) {
         const uint32_t wj = __shfl_sync(0xffffffffu, word, j);

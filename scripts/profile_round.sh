@@ -15,6 +15,8 @@ cap gk32 spmm_gk_kernel pitk_c1_8192
 cap gk128 spmm_gk_kernel pitk_128_8192
 cap gk2 spmm_gk2 pitk_256_8192
 cap detect detect pitk_c1_8192
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:rowgemm -s 4 -c 1 -o $OUT/prof_rowgemm \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:rowgemm2 -s 0 -c 1 -o $OUT/prof_rowgemm2 \
   python scripts/rowgemm_probe.py --ncu > $OUT/ncu_rowgemm.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+  --log-file $OUT/launches_moe.csv python scripts/rowgemm_probe.py --ncu > /dev/null 2>&1
 ls -la $OUT/*.ncu-rep
