@@ -1414,6 +1414,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // pair barrier -> pair MMA -> multicast commits; each CTA drains and stores its own 128 rows.
 // =============================================================================================
 constexpr int kRg2MaxGroups = 1024;
+constexpr int kRg2Band = 8;  // pair row tiles per raster band (dense)
 
 struct Rg2Cfg {
   static constexpr int KS = 64;
@@ -1511,6 +1512,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int units = (p.cnt != nullptr ? min(pair_tiles, pto[p.G]) : pair_tiles) * n_tiles;
+  // unit -> (pair row tile, n tile). One group (dense, BERT): rasterised in bands of kRg2Band pair
+  // row tiles, n tile outer within a band, so the pairs running together share B n-tile slabs and
+  // an A row band in L2 (row-tile-major order re-streamed all of B for every wave of row tiles).
+  const bool banded = p.cnt == nullptr && p.uniform_rows == 0 && units >= 8 * npairs;
+  auto unit_pt = [&](int u) {
+    if (!banded) return u / n_tiles;
+    const int band = u / (kRg2Band * n_tiles), in = u - band * kRg2Band * n_tiles;
+    const int bh = min(kRg2Band, pair_tiles - band * kRg2Band);
+    return band * kRg2Band + in % bh;
+  };
+  auto unit_nt = [&](int u) {
+    if (!banded) return u % n_tiles;
+    const int band = u / (kRg2Band * n_tiles), in = u - band * kRg2Band * n_tiles;
+    const int bh = min(kRg2Band, pair_tiles - band * kRg2Band);
+    return in / bh;
+  };
   const int kblocks = (p.K + KS - 1) / KS;
 
   if (warp < kProdWarps) {
@@ -1525,8 +1542,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int u = pair; u < units; u += npairs) {
-      const RowTile rt = decode_pair_tile(p, u / n_tiles, static_cast<int>(rank), single_rows, pto);
-      const int n0 = (u % n_tiles) * Cfg::BN + 128 * static_cast<int>(rank);
+      const RowTile rt = decode_pair_tile(p, unit_pt(u), static_cast<int>(rank), single_rows, pto);
+      const int n0 = unit_nt(u) * Cfg::BN + 128 * static_cast<int>(rank);
       int rid[RPT];
       if (!p.a_tma) {
 #pragma unroll
@@ -1632,8 +1649,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = pair; u < units; u += npairs) {
-      const RowTile rt = decode_pair_tile(p, u / n_tiles, static_cast<int>(rank), single_rows, pto);
-      const int n0 = (u % n_tiles) * Cfg::BN;
+      const RowTile rt = decode_pair_tile(p, unit_pt(u), static_cast<int>(rank), single_rows, pto);
+      const int n0 = unit_nt(u) * Cfg::BN;
       const int i = q * 32 + lane;
       const int row = i < rt.rows ? tile_dst_row(p, rt, i) : -1;
       const float scale = (row >= 0 && p.row_scale) ? __ldg(p.row_scale + row) : 1.0f;
