@@ -30,7 +30,7 @@ def _tile_for(reg, t0):
     return tile
 
 
-@pytest.mark.parametrize("t0", [8, 32, 128])
+@pytest.mark.parametrize("t0", [8, 32, 128, 256])
 @pytest.mark.parametrize("n", [64, 100, 300])
 def test_batched_pit_k_bf16_matches_per_slice_oracle(t0, n):
     import torch
@@ -172,3 +172,25 @@ def test_pit_m_narrow_n_two_d():
     ref = orc.run_sparse_matmul(At.float().cpu().numpy(), Bt.float().cpu().numpy(),
                                 (ann.tensor_shape, ann.granularity, ann.packed), "m", (16, 32, 128), np.float64)
     assert orc.max_rel_error(C, ref) <= BF16_TOL
+
+
+@pytest.mark.parametrize("m,n", [(200, 300), (512, 264), (96, 520)])
+def test_batched_dense_bf16_cta_pairs(m, n):
+    """Dense batched slices run on CTA pairs (rowgemm2, 256-row pair tiles): slice heights that are
+    not a multiple of 256 leave partial and empty pair halves; every slice must equal its product."""
+    import torch
+
+    pit = _pit()
+    batch, k = 3, 192
+    reg = pit.register_builtin_kernels()
+    tile = (128, 64, 256)
+    if reg.get("matmul", tile) is None:
+        reg.register(pit.TileKernelDescriptor("matmul", tile, "d128"))
+    plan = pit.forced_plan(_bound(m, k, n), "dense", reg, tile_shape=tile)
+    rng = np.random.default_rng(m + n)
+    A = torch.from_numpy(rng.standard_normal((batch, m, k)).astype(np.float32)).to(torch.bfloat16).cuda()
+    B = torch.from_numpy(rng.standard_normal((batch, k, n)).astype(np.float32)).to(torch.bfloat16).cuda()
+    C = pit.run_sparse_batched_matmul(plan, pit.stack_slices(A, plan), B, None)
+    ref = torch.bmm(A.double(), B.double())
+    for b in range(batch):
+        assert orc.max_rel_error(C[b].float().cpu().numpy(), ref[b].cpu().numpy()) <= BF16_TOL, b
