@@ -569,6 +569,14 @@ def attention_bench(args, dev, peaks, heads=12, seq=4096, hd=64):
     del P
     variants["pit:k (32,1) column-major P"] = timed(
         lambda: pit.run_batched_matmul_with_index(plan_k, A3k, V, pit.build_index(ann_dev, (32, 1), "k")))
+    # B200-native wider query groups: micro-tile (128,1) covers four 32-query block rows (the union of
+    # their keys; Longformer windows of adjacent query blocks overlap), 4x the MMA width per key
+    tile128 = (128, 64, 256)
+    if reg.get("matmul", tile128) is None:
+        reg.register(pit.TileKernelDescriptor("matmul", tile128, "attn128"))
+    plan_k128 = pit.forced_plan(expr, "k", reg, tile_shape=tile128)
+    variants["pit:k (128,1) column-major P"] = timed(
+        lambda: pit.run_batched_matmul_with_index(plan_k128, A3k, V, pit.build_index(ann_dev, (128, 1), "k")))
     # online detection from the P values instead of the mask (K1 over the stacked 402 MB operand)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     pit.build_batched_index_from_tensor(A3k, (32, 1), "k")
