@@ -1712,6 +1712,292 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// =============================================================================================
+// rowgemm2t: grouped GEMMs (MoE experts) with the operand roles swapped — D^T = W^T . X^T on CTA
+// pairs. The expert weights are the MMA's M side (256 output features per pair, MN-major straight
+// from the [G, K, N] stack by TMA) and the group's tokens its N side (up to 256, in steps of 16:
+// K-major rows, gathered by cp.async or one TMA box when packed). A group of ~128 tokens then costs
+// one M=256 x N=128(+15) MMA chain instead of 1.5 row tiles of 128 (the token axis is quantised to
+// 16, not 128), and each expert's weights are streamed once per 256 of its tokens.
+// Epilogue: TMEM lane = output feature, column = token: per token, the warp's 32 features leave as
+// one 64-byte row segment (ReLU / gate scale fused; destination row per token = SWrite).
+// =============================================================================================
+struct Rg2tCfg {
+  static constexpr int KS = 64;
+  static constexpr int W_BYTES = 2 * KS * 128;   // weights: the CTA's 128 features, 2 MN-major atoms
+  static constexpr int X_BYTES = 128 * KS * 2;   // tokens: up to 128 K-major rows per CTA
+  static constexpr int STAGE_BYTES = W_BYTES + X_BYTES;
+  static constexpr int STAGE_BUDGET = 232448 - 2048 - 4 * 1025 * 4;
+  static constexpr int STAGES = STAGE_BUDGET / STAGE_BYTES > 8 ? 8 : STAGE_BUDGET / STAGE_BYTES;
+  static constexpr int STG_BYTES = 4 * 2048;  // per epilogue warp: [32 tokens x 32 features] bf16
+  static constexpr size_t SMEM = static_cast<size_t>(STAGES) * STAGE_BYTES + STG_BYTES + 2048;
+};
+
+template <bool kBF16>
+__global__ void __launch_bounds__(kThreads, 1)
+    rowgemm2t_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                     const __grid_constant__ RowGemmParams p, int out_tiles, int max_tok_tiles) {
+  using Cfg = Rg2tCfg;
+  constexpr int KS = Cfg::KS;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stg = smem + Cfg::STAGES * Cfg::STAGE_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(stg + Cfg::STG_BYTES);
+  uint64_t* pair_full = full_bar + Cfg::STAGES;
+  uint64_t* empty_bar = pair_full + Cfg::STAGES;
+  uint64_t* tfull_bar = empty_bar + Cfg::STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  __shared__ int pto[kRg2MaxGroups + 1];  // prefix of 256-token tiles per group
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = static_cast<int>(blockIdx.x >> 1);
+  const int npairs = static_cast<int>(gridDim.x >> 1);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < Cfg::STAGES; ++i) {
+      mbar_init(&full_bar[i], kProdThreads + 1);
+      mbar_init(&pair_full[i], 2);
+      mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull_bar[i], 1);
+      mbar_init(&tempty_bar[i], 8);
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&tmW);
+  }
+  if (warp == kAllocWarp) tmem_alloc2<512>(tmem_slot);
+  if (warp == kRelayWarp + 1) {
+    const int per = (p.G + 31) / 32;
+    const int g0 = lane * per;
+    int run = 0;
+    for (int g = g0; g < min(p.G, g0 + per); ++g) run += (__ldg(p.cnt + g) + 255) >> 8;
+    int incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int acc = incl - run;
+    for (int g = g0; g < min(p.G, g0 + per); ++g) {
+      pto[g] = acc;
+      acc += (__ldg(p.cnt + g) + 255) >> 8;
+    }
+    if (lane == 31) pto[p.G] = incl;
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int units = min(max_tok_tiles, pto[p.G]) * out_tiles;
+  const int kblocks = (p.K + KS - 1) / KS;
+  // unit -> (group g, token range [start, start + ntok) of g, output-feature tile ot)
+  struct TokTile {
+    int g, start, ntok, nmma;
+  };
+  auto decode = [&](int u) {
+    const int pt = u / out_tiles;
+    int lo = 0, hi = p.G;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (pto[mid] <= pt) lo = mid; else hi = mid;
+    }
+    const int start = (pt - pto[lo]) * 256;
+    const int ntok = min(256, __ldg(p.cnt + lo) - start);
+    return TokTile{lo, start, ntok, (ntok + 15) & ~15};
+  };
+
+  if (warp < kProdWarps) {
+    // ------------------------------------------------------------ producers
+    constexpr int CPR = KS * 2 / 16;
+    constexpr int RPT = 128 * CPR / kProdThreads;
+    constexpr int RSTEP = kProdThreads / CPR;
+    const int tp = threadIdx.x;
+    const int ch = tp % CPR;
+    using T = typename OutT<kBF16>::T;
+    const T* Xp = static_cast<const T*>(p.A);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = pair; u < units; u += npairs) {
+      const TokTile tt = decode(u);
+      const int o0 = (u % out_tiles) * 256 + 128 * static_cast<int>(rank);
+      const int half = tt.nmma >> 1;                                 // token rows this CTA feeds
+      const int t0 = tt.start + static_cast<int>(rank) * half;      // first token (group-relative)
+      const int tcnt = max(0, min(half, tt.ntok - static_cast<int>(rank) * half));
+      int rid[RPT];
+      if (!p.a_tma) {
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+          const int i = tp / CPR + j * RSTEP;
+          rid[j] = i < tcnt ? __ldg(p.row_src + static_cast<int64_t>(tt.g) * p.src_stride + t0 + i) : -1;
+        }
+      }
+      const int xbase = __ldg(p.off + tt.g) + t0;  // packed token rows (TMA path)
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const int k0 = kb * KS;
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        uint8_t* sW = smem + stage * Cfg::STAGE_BYTES;
+        uint8_t* sX = sW + Cfg::W_BYTES;
+        if (tp == 0) {
+          mbar_expect_tx_only(&full_bar[stage], Cfg::W_BYTES + (p.a_tma ? Cfg::X_BYTES : 0));
+          tma_load_3d(sW, &tmW, &full_bar[stage], o0, k0, tt.g);
+          tma_load_3d(sW + KS * 128, &tmW, &full_bar[stage], o0 + 64, k0, tt.g);
+          if (p.a_tma) tma_load_2d(sX, &tmX, &full_bar[stage], k0, xbase);
+          mbar_arrive(&full_bar[stage]);
+        }
+        if (!p.a_tma) {
+          const uint32_t sx = smem_u32(sX);
+          const int kc = k0 + ch * 8;
+          const uint32_t kbytes = kc < p.K ? static_cast<uint32_t>(min(16, (p.K - kc) * 2)) : 0u;
+#pragma unroll
+          for (int j = 0; j < RPT; ++j) {
+            const int row = tp / CPR + j * RSTEP;
+            if (row >= half) continue;  // rows past N/2 are never read by the MMA
+            const uint32_t bytes = rid[j] >= 0 ? kbytes : 0u;
+            const T* src = bytes ? Xp + static_cast<int64_t>(rid[j]) * p.lda + kc : Xp;
+            cp_async_16(sx + swz<7>(static_cast<uint32_t>(row * 128 + ch * 16)), src, bytes);
+          }
+        }
+        cp_async_arrive_noinc(&full_bar[stage]);
+        if (++stage == Cfg::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == kRelayWarp) {
+    if (lane == 0) {
+      const uint32_t leader_pf = mapa_shared(smem_u32(pair_full), 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = pair; u < units; u += npairs) {
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          fence_proxy_async_smem();
+          mbar_arrive_cluster(leader_pf + stage * 8);
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    if (rank == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = pair; u < units; u += npairs) {
+        const TokTile tt = decode(u);
+        const uint32_t idesc = idesc_f16(256, tt.nmma, kBF16, true, false);
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&pair_full[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t sW = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+            const uint32_t sX = sW + Cfg::W_BYTES;
+#pragma unroll
+            for (int ks = 0; ks < KS / 16; ++ks) {
+              const uint64_t wdesc = smem_desc(sW + ks * 2048, KS * 128, 1024, kSw128);
+              const uint64_t xdesc = smem_desc(sX + ks * 32, 16, 8 * 128, kSw128);
+              umma2_f16(tmem_base + static_cast<uint32_t>(acc * 256), wdesc, xdesc, idesc, (kb > 0 || ks > 0) ? 1u : 0u);
+            }
+            umma2_commit_mc(&empty_bar[stage], 3);
+          }
+          __syncwarp();
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (lane == 0) umma2_commit_mc(&tfull_bar[acc], 3);
+        __syncwarp();
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= kEpiWarp0) {
+    // ------------------------------------------------------------ epilogue: lane = output feature
+    using T = typename OutT<kBF16>::T;
+    const int q = warp & 3;
+    const uint32_t leader_te = mapa_shared(smem_u32(tempty_bar), 0);
+    T* C = static_cast<T*>(p.C);
+    const uint32_t stg_w = smem_u32(stg) + static_cast<uint32_t>(q * 2048);
+    const bool vec_ok = (p.ldc % 8) == 0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = pair; u < units; u += npairs) {
+      const TokTile tt = decode(u);
+      const int ocw = (u % out_tiles) * 256 + 128 * static_cast<int>(rank) + q * 32;  // warp's features
+      const int gbase = __ldg(p.off + tt.g);
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < tt.ntok; c += 32) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * 256 + c), v);
+        tmem_wait_ld();
+        // destination row and scale of token c + lane
+        const int within = tt.start + c + lane;
+        int my_row = -1;
+        float my_scale = 1.0f;
+        if (c + lane < tt.ntok) {
+          my_row = p.row_dst ? __ldg(p.row_dst + static_cast<int64_t>(tt.g) * p.dst_stride + within) : gbase + within;
+          if (p.row_scale) my_scale = __ldg(p.row_scale + my_row);
+        }
+        // transpose through shared memory: [token][32 features] rows of 64 bytes, then 8 tokens x
+        // 64 bytes per store instruction (4 lanes per token row)
+        __syncwarp();  // the previous block's read-back is done
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float sc = __shfl_sync(0xffffffffu, my_scale, j);
+          float x = __uint_as_float(v[j]);
+          if (p.act == 1) x = fmaxf(x, 0.0f);
+          const T h = OutT<kBF16>::cvt(x * sc);
+          asm volatile("st.shared.b16 [%0], %1;" ::"r"(stg_w + j * 64 + lane * 2),
+                       "h"(*reinterpret_cast<const uint16_t*>(&h)) : "memory");
+        }
+        __syncwarp();
+        const int sub = lane & 3;       // 16-byte quarter of the 64-byte feature segment
+        const int col = ocw + sub * 8;  // first feature of this lane's quarter
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int t = it * 8 + (lane >> 2);
+          const int row = __shfl_sync(0xffffffffu, my_row, t);
+          const uint4 w = ld_shared_v4(stg_w + t * 64 + sub * 16);
+          if (row >= 0 && col < p.N) {
+            T* dst = C + static_cast<int64_t>(row) * p.ldc + col;
+            if (col + 8 <= p.N && vec_ok) {
+              *reinterpret_cast<uint4*>(dst) = w;
+            } else {
+              const T* hh = reinterpret_cast<const T*>(&w);
+              for (int e2 = 0; e2 < 8 && col + e2 < p.N; ++e2) dst[e2] = hh[e2];
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_te + acc * 8);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == kAllocWarp) {
+    tc_fence_after();
+    tmem_dealloc2<512>(tmem_base);
+  }
+}
+
 int g_num_sms = 0;
 
 int num_sms() {
@@ -2109,6 +2395,68 @@ bool spmm_tc_supported(const SpmmArgs& a) {
   return a.t1 % 64 == 0 || a.t1 == 32 || a.t1 == 16;
 }
 
+int rg2t_enabled() {  // PIT_RG2T=0: grouped GEMMs keep tokens on the M side (rowgemm2 / rowgemm)
+  static int v = [] {
+    const char* e = getenv("PIT_RG2T");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
+// Grouped GEMM with swapped roles (see rowgemm2t_kernel): weights on M, tokens on N.
+template <bool kBF16>
+int run_rowgemm2t(const RowGemmParams& p, const void* B, int64_t ldb, cudaStream_t s) {
+  using Cfg = Rg2tCfg;
+  constexpr int KS = Cfg::KS;
+  const CUtensorMapDataType dt = kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  CUtensorMap tmW, tmX;
+  memset(&tmX, 0, sizeof(tmX));
+  if (encode_tensor_map_3d(&tmW, dt, B, p.N, p.K, p.G, ldb * 2, static_cast<uint64_t>(ldb * p.K) * 2, 64, KS,
+                           CU_TENSOR_MAP_SWIZZLE_128B) != CUDA_SUCCESS)
+    return kErrCuda;
+  RowGemmParams q = p;
+  q.a_tma = 0;
+  if (p.row_src == nullptr && (p.lda * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(p.A) & 15) == 0 &&
+      a_tma_enabled()) {
+    if (encode_tensor_map_2d(&tmX, dt, p.A, static_cast<uint64_t>(p.K), static_cast<uint64_t>(p.M),
+                             static_cast<uint64_t>(p.lda) * 2, KS, 128, CU_TENSOR_MAP_SWIZZLE_128B) != CUDA_SUCCESS)
+      return kErrCuda;
+    q.a_tma = 1;
+  }
+  const int out_tiles = static_cast<int>(ceil_div(p.N, 256));
+  const int64_t units = static_cast<int64_t>(p.max_tiles) * out_tiles;
+  if (units == 0) return kOk;
+  if (units >= (1ll << 31)) return kErrShape;
+  auto kern = rowgemm2t_kernel<kBF16>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::SMEM));
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  static int max_pairs = 0;
+  if (max_pairs == 0) {
+    cfg.gridDim = dim3(static_cast<unsigned>(num_sms() & ~1));
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) != cudaSuccess || nc <= 0) {
+      cudaGetLastError();
+      nc = num_sms() / 2;
+    }
+    max_pairs = nc;
+  }
+  const int pairs = static_cast<int>(units < max_pairs ? units : max_pairs);
+  cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
+  cudaLaunchKernelEx(&cfg, kern, tmW, tmX, q, out_tiles, p.max_tiles);
+  note_launch();
+  return cuda_status();
+}
+
 int launch_rowgemm(const GroupedGemmArgs& g, cudaStream_t s) {
   if (g.dtype != kDtypeBF16 && g.dtype != kDtypeF16) return kErrUnsupported;
   if (reinterpret_cast<uintptr_t>(g.A) % 16 || reinterpret_cast<uintptr_t>(g.B) % 16) return kErrUnsupported;
@@ -2134,6 +2482,11 @@ int launch_rowgemm(const GroupedGemmArgs& g, cudaStream_t s) {
   p.t1 = 1;
   p.max_tiles = static_cast<int>(g.max_tiles);
   const int ks = g.K % 64 == 0 || g.K > 64 ? 64 : g.K % 32 == 0 ? 32 : 16;
+  // small groups (MoE at ~128 tokens per expert): tokens on the MMA's N side, quantised to 16 rows
+  // instead of 128 (rowgemm2t); large groups fill 256-row tiles anyway and keep rowgemm2's epilogue
+  const bool small_groups = g.rows_a < 256 * g.G;
+  if (ks == 64 && p.G <= kRg2MaxGroups && rg2t_enabled() && p.N >= 64 && small_groups)
+    return g.dtype == kDtypeBF16 ? run_rowgemm2t<true>(p, g.B, g.ldb, s) : run_rowgemm2t<false>(p, g.B, g.ldb, s);
   return g.dtype == kDtypeBF16 ? rowgemm_dispatch<true>(p, g.B, g.ldb, ks, s) : rowgemm_dispatch<false>(p, g.B, g.ldb, ks, s);
 }
 
