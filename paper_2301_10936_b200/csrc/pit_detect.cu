@@ -204,6 +204,12 @@ __global__ void __launch_bounds__(kGenThreads) detect_generic_kernel(const uint8
 // Power-of-two geometry (the common PIT case: micro-tiles and block granularities like 1, 32, 64):
 // one THREAD per occupancy word, all index math in shifts, the word's 32 coordinates tested in a
 // register loop against L1-resident annotation bytes.
+// bits [a, b) of a word, 0 <= a < b <= 32
+__device__ __forceinline__ uint32_t range_mask(int a, int b) {
+  const uint32_t hi = b >= 32 ? 0xffffffffu : ((1u << b) - 1u);
+  return hi & ~((1u << a) - 1u);
+}
+
 template <typename I>
 __global__ void detect_bits_pow2_kernel(const uint8_t* __restrict__ packed, I s0, I s1, int lg0, int lg1, int lt0,
                                         int lt1, int pit_dim, I n_groups, I pit_grid, I WG,
@@ -221,6 +227,25 @@ __global__ void detect_bits_pow2_kernel(const uint8_t* __restrict__ packed, I s0
     const I ghi = (min((g + 1) << lgt, gs) + (I(1) << lgg) - 1) >> lgg;
     uint32_t word = 0;
     const I c_end = min(w * 32 + 32, pit_grid);
+    if (lcg >= lct + 5) {
+      // a coordinate block spans >= 32 coordinates (e.g. 64-key blocks, (t0,1) micro-tiles): the
+      // word's 32 coordinates fall in at most two blocks, so test each block once (OR over the
+      // group's blocks) and set its coordinates by mask — not 32 x (group blocks) bit loads
+      const int sh = lcg - lct;  // log2(coordinates per block)
+      for (I cb = (w * 32) >> sh; cb <= (c_end - 1) >> sh; ++cb) {
+        bool live = false;
+        for (I gb = glo; gb < ghi && !live; ++gb) {
+          const I f = pit_dim == 0 ? cb * bg1 + gb : gb * bg1 + cb;
+          live = (__ldg(packed + (f >> 3)) >> (7 - (f & 7))) & 1;
+        }
+        if (live) {
+          const I lo = max(cb << sh, w * 32), hi = min((cb + 1) << sh, c_end);
+          word |= range_mask(static_cast<int>(lo - w * 32), static_cast<int>(hi - w * 32));
+        }
+      }
+      occ[static_cast<int64_t>(g) * WG + w] = word;
+      continue;
+    }
     for (I c = w * 32; c < c_end; ++c) {
       const I clo = (c << lct) >> lcg;
       const I chi = (min((c + 1) << lct, cs) + (I(1) << lcg) - 1) >> lcg;
