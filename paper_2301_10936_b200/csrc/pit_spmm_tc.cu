@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const T* Ap = static_cast<const T*>(Atv);
     const uint32_t ldb32 = static_cast<uint32_t>(ldb);  // host guarantees K * pitch < 2^32 elements
     const uint32_t lda32 = static_cast<uint32_t>(lda);
-    // B: B_RPI rows per warp instruction (1 at N_TILE 256, 2 at 128), lane -> (row sub, chunk)
+    // B: B_RPI rows per warp instruction (1 at N_TILE 256, 2 at 128, 4 at 64), lane -> (row sub, chunk)
     constexpr int B_RPI = Cfg::B_CPR >= 32 ? 1 : 32 / Cfg::B_CPR;
     constexpr int B_IPR = Cfg::B_CPR >= 32 ? Cfg::B_CPR / 32 : 1;  // instructions per row
     const int b_sub = B_RPI > 1 ? lane / Cfg::B_CPR : 0;
@@ -320,7 +320,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < RW; i += B_RPI) {
             int kk = x.v[i];
-            if constexpr (B_RPI == 2) kk = b_sub ? x.v[i + 1] : kk;
+#pragma unroll
+            for (int r = 1; r < B_RPI; ++r) kk = b_sub == r ? x.v[i + r] : kk;
             const int row = i + b_sub;  // within the warp's rows; (r0 + row) & 7 == row & 7
             const bool ok = r0 + row < kvalid;
             const uint32_t k = ok ? static_cast<uint32_t>(kk) : 0u;
@@ -2360,6 +2361,12 @@ int dispatch_tc(const SpmmArgs& a, cudaStream_t s) {
       const char* e = getenv("PIT_GK_NT");
       return e ? atoi(e) : 0;
     }();
+    // 128-row groups (orientation N, N_mma = the n tile) with N <= 64 (attention P.V, head dim 64):
+    // 64-column units — no zero-filled half tile, half the MMA columns
+    if (gw == 128 && a.N <= 64 && nt_override != 128) {
+      const bool ks64 = gk_ks_override() == 64;
+      return ks64 ? run_gk<128, true, kBF16, 64, 64>(a, s) : run_gk<128, true, kBF16, 128, 64>(a, s);
+    }
     return (a.N <= 128 || nt_override == 128) ? dispatch_gk<kBF16, 128>(a, gw, s) : dispatch_gk<kBF16, 0>(a, gw, s);
   }
   const int t1 = a.plan == kPlanDense ? 64 : a.t1;
