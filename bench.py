@@ -223,6 +223,32 @@ def run_ours(args, w):
     torch.cuda.synchronize()
     det_ms = [a.elapsed_time(b) for a, b in det_ms]
     spmm_ms = [a.elapsed_time(b) for a, b in spmm_ms]
+    # detection alone on the device (scan + compaction captured in a CUDA graph: no host dispatch
+    # between the two launches), L2 flushed before each replay
+    det_dev_ms = None
+    try:
+        side = torch.cuda.Stream()
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            pit.build_index_from_tensor(A, micro, axis)
+        stream.wait_stream(side)
+        torch.cuda.synchronize()
+        g_det = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_det):
+            pit.build_index_from_tensor(A, micro, axis)
+        ev = []
+        for _ in range(args.steps):
+            flush.zero_()
+            d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            d0.record(stream)
+            g_det.replay()
+            d1.record(stream)
+            ev.append((d0, d1))
+        torch.cuda.synchronize()
+        det_dev_ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+        del g_det
+    except Exception:  # graph capture is an optimisation of the measurement, never a failure
+        det_dev_ms = None
     # the step as a served layer runs it: detection + SpMM captured once in a CUDA graph, replayed
     captured = None
     if not args.no_graph:
@@ -287,10 +313,14 @@ def run_ours(args, w):
         "traffic": traffic, "algorithmic_flops": eff_flops,
         "kernel_ms": round(spmm_avg, 4), "operand_feed": operand_feed,
     }
+    det_t = det_dev_ms if det_dev_ms else det_avg
     detection = {
-        "kernel": "detect+compact (eager call incl. host dispatch)", "ms": round(det_avg, 4), "bytes_scanned": scanned,
-        "achieved_GBps": round(scanned / (det_avg * 1e-3) / 1e9, 1), "peak_GBps": peaks["hbm"],
-        "frac": round(scanned / (det_avg * 1e-3) / 1e9 / peaks["hbm"], 4),
+        "kernel": "detect+compact (" + ("CUDA graph of the public call, device time" if det_dev_ms else
+                                       "eager call incl. host dispatch") + ")",
+        "ms": round(det_t, 4), "bytes_scanned": scanned,
+        "achieved_GBps": round(scanned / (det_t * 1e-3) / 1e9, 1), "peak_GBps": peaks["hbm"],
+        "frac": round(scanned / (det_t * 1e-3) / 1e9 / peaks["hbm"], 4),
+        "eager_ms_incl_host_dispatch": round(det_avg, 4),
     }
 
     result = {
