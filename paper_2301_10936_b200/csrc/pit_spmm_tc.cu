@@ -984,6 +984,7 @@ struct RowGemmParams {
   int max_tiles;            // host bound on the total number of row tiles
   int uniform_rows;         // cnt == nullptr && G > 1: every group is this many consecutive rows
   int a_tma;                // A tiles by TMA (rows contiguous: no row_src, no liveness); else cp.async
+  int contig_pct;           // > 0 (single group, union rows): contiguous row tiles when *n_rows >= pct% of M
 };
 
 template <int KS, int kBN = 256>
@@ -1066,7 +1067,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int single_rows = p.cnt ? 0 : (p.n_rows ? *p.n_rows : p.M);
+  // union rows that cover (nearly) every row (scattered per-row K patterns): contiguous 128-row tiles
+  // with the occupancy staged per tile instead (decided on the device: no host round trip)
+  const bool contig = p.contig_pct > 0 && p.n_rows != nullptr &&
+                      static_cast<int64_t>(*p.n_rows) * 100 >= static_cast<int64_t>(p.M) * p.contig_pct;
+  const int32_t* row_src = contig ? nullptr : p.row_src;
+  const int32_t* row_dst = contig ? nullptr : p.row_dst;
+  const int single_rows = p.cnt ? 0 : contig ? p.M : (p.n_rows ? *p.n_rows : p.M);
   const int total_tiles = p.cnt ? __ldg(p.tile_off + p.G)
                          : p.uniform_rows ? p.G * ((p.uniform_rows + 127) / 128) : (single_rows + 127) / 128;
 
@@ -1110,7 +1117,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // staged in shared memory once per unit, so a K-block's liveness costs no L2 round trip and no
     // barrier (every producer derives the same stage verdict). Union-row tiles look bits up per row.
     const int nkg = p.occ ? (p.K + p.t1 - 1) / p.t1 : 0;
-    const bool staged = p.occ != nullptr && p.row_src == nullptr && nkg <= Cfg::OCC_MAX_GROUPS &&
+    const int lg_t1 = (p.t1 & (p.t1 - 1)) == 0 ? __ffs(p.t1) - 1 : -1;  // power-of-two widths: shifts
+    const bool staged = p.occ != nullptr && row_src == nullptr && nkg <= Cfg::OCC_MAX_GROUPS &&
                         kblocks <= Cfg::KB_MAX;
     // next live K-block after kb (staged units): dead K-blocks cost no producer work at all
     auto next_kb = [&](int kb) {
@@ -1131,7 +1139,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int j = 0; j < RPT; ++j) {
         const int i = tp / CPR + j * RSTEP;
-        rid[j] = i < rt.rows ? tile_src_row(p, rt, i) : -1;
+        rid[j] = i < rt.rows ? (row_src ? tile_src_row(p, rt, i) : rt.base + i) : -1;
       }
       const int w0 = rt.base >> 5, sh = rt.base & 31;
       if (staged) {
@@ -1147,11 +1155,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int kb = kb0 + (tp & 31);
           uint32_t anyw = 0;
           if (kb < kblocks) {
-            const uint32_t* wv = tile_occ + (kb * KS / p.t1) * 5;
+            // every K-group the K-block overlaps (KS > t1: e.g. two 32-wide micro-columns per block)
+            const int kg1 = min((kb * KS + KS - 1) / p.t1, nkg - 1);
+            for (int kg = kb * KS / p.t1; kg <= kg1; ++kg) {
+              const uint32_t* wv = tile_occ + kg * 5;
 #pragma unroll
-            for (int w = 0; w < 5; ++w) {
-              const int a = max(sh - 32 * w, 0), b = min(sh + rt.rows - 32 * w, 32);
-              if (b > a) anyw |= wv[w] & bit_range(a, b);
+              for (int w = 0; w < 5; ++w) {
+                const int a = max(sh - 32 * w, 0), b = min(sh + rt.rows - 32 * w, 32);
+                if (b > a) anyw |= wv[w] & bit_range(a, b);
+              }
             }
           }
           const uint32_t word = __ballot_sync(0xffffffffu, anyw != 0);
@@ -1163,8 +1175,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int k0 = kb * KS;
         bool live[RPT];
         bool stage_any = true;
+        // the K-group of this thread's 16-byte chunk (a K-block may span several when KS > t1)
+        const int kc8 = k0 + ch * 8;
+        const int kgc = p.occ ? min(lg_t1 >= 0 ? kc8 >> lg_t1 : kc8 / p.t1, nkg - 1) : 0;
         if (staged) {
-          const uint32_t* wv = tile_occ + (k0 / p.t1) * 5;
+          const uint32_t* wv = tile_occ + kgc * 5;
 #pragma unroll
           for (int j = 0; j < RPT; ++j) {
             const int r = rid[j] - (w0 << 5);
@@ -1176,7 +1191,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < RPT; ++j) {
             live[j] = rid[j] >= 0;
             if (live[j] && p.occ)
-              live[j] = (__ldg(p.occ + static_cast<int64_t>(k0 / p.t1) * p.WG + (rid[j] >> 5)) >> (rid[j] & 31)) & 1u;
+              live[j] = (__ldg(p.occ + static_cast<int64_t>(kgc) * p.WG + (rid[j] >> 5)) >> (rid[j] & 31)) & 1u;
             any |= live[j];
           }
           stage_any = p.occ ? bar_or(1, kProdThreads, any) : true;
@@ -1293,7 +1308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const RowTile rt = decode_tile(p, u / n_tiles, single_rows);
       const int n0 = (u % n_tiles) * Cfg::BN;
       const int i = q * 32 + lane;
-      const int row = i < rt.rows ? tile_dst_row(p, rt, i) : -1;
+      const int row = i < rt.rows ? (row_dst ? tile_dst_row(p, rt, i) : rt.base + i) : -1;
       const float scale = (row >= 0 && p.row_scale) ? __ldg(p.row_scale + row) : 1.0f;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
@@ -2261,6 +2276,14 @@ int rowgemm_dispatch(const RowGemmParams& p, const void* B, int64_t ldb, int ks,
   return kErrUnsupported;
 }
 
+int gm_contig_pct() {  // PIT_GM_CONTIG=P: pit:m runs on contiguous row tiles when the union holds >= P% of rows
+  static int v = [] {
+    const char* e = getenv("PIT_GM_CONTIG");
+    return e ? atoi(e) : 50;
+  }();
+  return v;
+}
+
 template <bool kBF16>
 int run_gm(const SpmmArgs& a, int ks, cudaStream_t s) {
   const int dense = a.plan == kPlanDense ? 1 : 0;
@@ -2286,6 +2309,18 @@ int run_gm(const SpmmArgs& a, int ks, cudaStream_t s) {
   p.WG = a.WG;
   p.t1 = dense ? 1 : a.t1;
   p.max_tiles = static_cast<int>(ceil_div(dense ? a.M : a.n_rows_host, 128));
+  // Scattered per-row K patterns (random (1,32) activation sparsity) make the union of live rows
+  // (nearly) every row: union-row tiles then buy nothing and cost a per-row, per-K-block global
+  // liveness lookup plus a block-wide vote per stage. The kernel switches (on the device, from the
+  // union size) to contiguous 128-row tiles: the tile's occupancy words are staged in shared memory
+  // once per unit, a dead (row, micro-column) chunk is zero-filled by its cp.async, K-blocks with no
+  // live row take no ring slot. 64-deep K-blocks cover two 32-wide (four 16-wide) micro-columns:
+  // liveness is per 16-byte chunk's K-group.
+  if (p.occ != nullptr && (a.t1 == 32 || a.t1 == 16) && a.n_rows_host == a.M &&
+      ceil_div(a.K, a.t1) <= GmCfg<64>::OCC_MAX_GROUPS && ceil_div(a.K, 64) <= GmCfg<64>::KB_MAX) {
+    p.contig_pct = gm_contig_pct();
+    if (p.contig_pct > 0) ks = 64;
+  }
   return rowgemm_dispatch<kBF16>(p, a.B, a.ldb, ks, s);
 }
 
@@ -2371,7 +2406,8 @@ int dispatch_tc(const SpmmArgs& a, cudaStream_t s) {
   }
   const int t1 = a.plan == kPlanDense ? 64 : a.t1;
   if (a.batch > 1) {
-    const int ks = t1 % 64 == 0 ? 64 : t1 == 32 ? 32 : t1 == 16 ? 16 : 0;
+    // 64-deep K-blocks for 16/32-wide micro-columns too: liveness is looked up per 16-byte chunk
+    const int ks = (t1 % 64 == 0 || t1 == 32 || t1 == 16) ? 64 : 0;
     return ks ? run_gm_batched<kBF16>(a, ks, s) : kErrUnsupported;
   }
   if (t1 % 64 == 0) return run_gm<kBF16>(a, 64, s);

@@ -137,6 +137,34 @@ def test_bf16_pit_m_tensor_cores(t1, shape):
     assert np.all(C[dead] == 0.0)
 
 
+@pytest.mark.parametrize("t1", [16, 32])
+@pytest.mark.parametrize("dead_rows", [0.0, 0.8])
+@pytest.mark.parametrize("shape", [(1024, 2048, 512), (700, 416, 264)])
+def test_bf16_pit_m_dead_micro_tiles_not_read(t1, dead_rows, shape):
+    """pit:m reads only live (row, micro-column) tiles (SRead, executor.py:170-208): A carries
+    non-zero data in every dead micro-tile. Scattered per-row patterns (union = ~all rows) run on
+    contiguous row tiles with 64-deep K-blocks spanning 2-4 micro-columns; mostly-dead rows keep
+    union-row tiles. Both must ignore the dead data."""
+    pit = _pkg()
+    m, k, n = shape
+    reg = pit.register_builtin_kernels()
+    tile = (128, t1, 256)
+    if reg.get("matmul", tile) is None:
+        reg.register(pit.TileKernelDescriptor("matmul", tile, f"m{t1}"))
+    rng = np.random.default_rng(t1 + m)
+    mask = np.repeat(rng.random((m, -(-k // t1))) >= 0.9, t1, axis=1)[:, :k]
+    mask[rng.random(m) < dead_rows] = False
+    ann = pit.from_mask(mask, (1, t1))
+    A = rng.standard_normal((m, k)).astype(np.float32)  # dense data: dead micro-tiles hold values too
+    B = rng.standard_normal((k, n)).astype(np.float32)
+    plan = pit.forced_plan(bound(m, k, n), "m", reg, tile_shape=tile)
+    C, Ar, Br = _run_bf16(plan, A, B, ann, col_major=False)
+    ref = orc.run_sparse_matmul(Ar, Br, (ann.tensor_shape, ann.granularity, ann.packed), "m", tile, np.float64)
+    assert orc.max_rel_error(C, ref) <= BF16_TOL
+    dead = ~mask.any(axis=1)
+    assert np.all(C[dead] == 0.0)
+
+
 def test_bf16_row_uniform_and_dense_bitwise():
     """Fully dense annotation through pit:m equals the dense plan bitwise (test_executor.py:178-186)."""
     pit = _pkg()
