@@ -136,9 +136,17 @@ typedef struct {
    * so M must be a multiple of t0) -- what one detection pass over the stacked A produces. */
   int64_t batch;
   int64_t b_batch_stride;
+  /* Caller-owned device scratch (may be NULL / 0): the gathered-K path for few, unequal groups
+   * (e.g. attention with global query rows) splits long groups over several CTAs and reduces their
+   * partial tiles; without scratch it runs unsplit. Size from pit_spmm_workspace_bytes. */
+  void* workspace;
+  int64_t workspace_bytes;
 } pit_spmm_args;
 
 PIT_API int pit_spmm(const pit_spmm_args* args, void* stream);
+
+/* Scratch bytes pit_spmm can use for these arguments (0: none needed). Host-only, no GPU work. */
+PIT_API int64_t pit_spmm_workspace_bytes(const pit_spmm_args* args);
 
 /* 1 if the tcgen05 tensor-core path covers these arguments, else 0 (CUDA-core path). */
 PIT_API int pit_spmm_uses_tensor_cores(const pit_spmm_args* args);

@@ -48,6 +48,7 @@ EXPORTS = (
     "pit_swrite",
     "pit_spmm",
     "pit_spmm_uses_tensor_cores",
+    "pit_spmm_workspace_bytes",
     "pit_dense_reference_f64",
     "pit_grouped_gemm",
     "pit_moe_route",
@@ -90,6 +91,8 @@ class SpmmArgs(C.Structure):
         ("force_simt", C.c_int),
         ("batch", C.c_int64),
         ("b_batch_stride", C.c_int64),
+        ("workspace", C.c_void_p),
+        ("workspace_bytes", C.c_int64),
     ]
 
 
@@ -138,6 +141,8 @@ def _declare(lib) -> None:
     lib.pit_swrite.argtypes = [vp, vp, i32, i64, i64, i64, i32, i64, i64, i32, i32, i32, i64, vp, i64, i32, vp]
     lib.pit_spmm.argtypes = [C.POINTER(SpmmArgs), vp]
     lib.pit_spmm_uses_tensor_cores.argtypes = [C.POINTER(SpmmArgs)]
+    lib.pit_spmm_workspace_bytes.argtypes = [C.POINTER(SpmmArgs)]
+    lib.pit_spmm_workspace_bytes.restype = i64
     lib.pit_dense_reference_f64.argtypes = [vp, i64, i64, vp, i64, vp, i64, i64, i64, vp]
     lib.pit_grouped_gemm.argtypes = [C.POINTER(GroupedGemmArgs), vp]
     lib.pit_moe_route.argtypes = [vp, i32, i64, i64, vp, vp, vp, vp, vp, vp]
@@ -148,7 +153,7 @@ def _declare(lib) -> None:
     lib.pit_copy2d_async.argtypes = [vp, i64, vp, i64, i64, i64, vp]
     lib.pit_reduce_rows.argtypes = [vp, i32, i64, i64, i64, vp, i64, i32, i32, vp, vp]
     for name in EXPORTS:
-        if name not in ("pit_last_error", "pit_abi_version", "pit_kernel_launches"):
+        if name not in ("pit_last_error", "pit_abi_version", "pit_kernel_launches", "pit_spmm_workspace_bytes"):
             getattr(lib, name).restype = i32
 
 

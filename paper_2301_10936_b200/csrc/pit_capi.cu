@@ -301,7 +301,15 @@ static SpmmArgs to_internal(const pit_spmm_args* p) {
   a.n_rows_host = p->n_rows_bound;
   a.batch = p->batch > 1 ? p->batch : 1;
   a.b_batch_stride = p->b_batch_stride;
+  a.ws = p->workspace;
+  a.ws_bytes = p->workspace ? p->workspace_bytes : 0;
   return a;
+}
+
+int64_t pit_spmm_workspace_bytes(const pit_spmm_args* p) {
+  if (!p || p->force_simt) return 0;
+  const SpmmArgs a = to_internal(p);
+  return spmm_tc_supported(a) ? spmm_tc_workspace_bytes(a) : 0;
 }
 
 int pit_spmm_uses_tensor_cores(const pit_spmm_args* p) {

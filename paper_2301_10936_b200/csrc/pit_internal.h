@@ -119,6 +119,8 @@ struct SpmmArgs {
   int64_t n_rows_host;      // upper bound used for the grid (<= M)
   int64_t batch = 1;        // pit:k slices stacked along M (see pit_spmm_args)
   int64_t b_batch_stride = 0;
+  void* ws = nullptr;       // caller scratch (split gathered-K units), may be null
+  int64_t ws_bytes = 0;
 };
 
 int launch_spmm_simt(const SpmmArgs& a, cudaStream_t s);
@@ -128,6 +130,7 @@ int launch_dense_ref_f64(const double* A, int64_t s0, int64_t s1, const double* 
                          int64_t N, int64_t K, cudaStream_t s);
 int launch_spmm_tc(const SpmmArgs& a, cudaStream_t s);  // bf16 / fp16 tcgen05 paths
 bool spmm_tc_supported(const SpmmArgs& a);
+int64_t spmm_tc_workspace_bytes(const SpmmArgs& a);  // scratch the tcgen05 path can use (0: none)
 int gk2_trace_read(unsigned long long* host);  // diagnostic timeline (PIT_GK2_DIAG bit 4)
 
 // Grouped gathered-row GEMM (MoE experts, batched per-slice plans): see rowgemm in pit_spmm_tc.cu.

@@ -117,6 +117,105 @@ __device__ __forceinline__ void epi_box_tma(uint32_t tsrc, bool have, uint32_t b
 // Both operands are MN-major 128B-swizzled gathers of k rows; only descriptors and the epilogue
 // differ between orientations.
 // =============================================================================================
+// ---------------------------------------------------------------------------------------------
+// Split gathered-K units (few, unequal groups). The persistent spmm_gk walk gives every CTA the
+// same number of units, so with only ~2-3 units per SM one long group sets the kernel's length:
+// Longformer's global query rows see every key (4096 live k against ~1100 for a windowed group) —
+// 46 us of a kernel whose work balances to ~30. Every CTA first derives the same plan from the
+// counts: a group longer than twice the mean becomes chunks of about the mean (multiples of KS),
+// virtual groups in group order; the CTA keeps its own units {group, first slot, count, partial}.
+// A chunk leaves an fp32 partial tile in caller scratch; the chunk that finishes its group last
+// (atomic counter) sums the tiles into C. Deterministic plan; the fp32 sum order of a split group
+// is fixed (chunk order), so results are reproducible.
+constexpr int kSplitParts = 255;     // partial tiles at most (8-bit index)
+constexpr int kSplitMaxGroups = 2048;
+constexpr int kSplitCtrBytes = 512;  // split-group arrival counters (<= 85 groups: >= 3 chunks each)
+
+// exclusive block scan (blockDim.x a multiple of 32, <= 1024); sh: >= 32 ints of shared scratch
+__device__ __forceinline__ int block_excl_scan(int v, int* sh, int& total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int z = lane < nw ? sh[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= o) z += y;
+    }
+    if (lane < nw) sh[lane] = z;
+  }
+  __syncthreads();
+  const int excl = x - v + (w ? sh[w - 1] : 0);
+  total = sh[nw - 1];
+  __syncthreads();
+  return excl;
+}
+
+// One CTA of 1024 threads (2 groups per thread, n_groups <= kSplitMaxGroups): the split plan as the
+// virtual-group table vtab[v] = {group, first slot, count, -1 or first partial | chunk << 8 |
+// split group << 16 | chunks << 24}, their number in *nv, and zeroed split-group counters.
+__global__ void __launch_bounds__(1024) gk_split_plan_kernel(const int32_t* __restrict__ counts, int n_groups, int ks,
+                                                             int4* __restrict__ vtab, int* __restrict__ nv,
+                                                             int* __restrict__ ctr) {
+  __shared__ int sc[32];
+  const int tid = threadIdx.x;
+  if (tid < kSplitCtrBytes / 4) ctr[tid] = 0;
+  int cnt[2], valid[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int g = 2 * tid + j;
+    valid[j] = g < n_groups;
+    cnt[j] = valid[j] ? __ldg(counts + g) : 0;
+  }
+  int tot;
+  block_excl_scan(cnt[0] + cnt[1], sc, tot);  // the total (live k of one index fits int32)
+  const int mean = (tot + n_groups - 1) / n_groups;
+  const int L = max((mean + ks - 1) / ks, 1) * ks;
+  int nch[2], want[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    nch[j] = cnt[j] > 2 * L ? (cnt[j] + L - 1) / L : 1;
+    want[j] = valid[j] && nch[j] > 1 && nch[j] <= 127 ? nch[j] : 0;
+  }
+  int t1, t2, t3;
+  const int pp = block_excl_scan(want[0] + want[1], sc, t1);
+  const int ppj[2] = {pp, pp + want[0]};
+  bool split[2];
+  int nf[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    split[j] = want[j] > 0 && ppj[j] + want[j] <= kSplitParts;
+    nf[j] = valid[j] ? (split[j] ? nch[j] : 1) : 0;
+  }
+  // virtual groups in group order (measured better than split chunks first); one scan carries both
+  // the virtual-group prefix (low 16 bits, <= n_groups + P) and the split-group prefix (high bits)
+  const int pk0 = nf[0] | (static_cast<int>(split[0]) << 16), pk1 = nf[1] | (static_cast<int>(split[1]) << 16);
+  int tpk;
+  const int pk = block_excl_scan(pk0 + pk1, sc, tpk);
+  t2 = tpk & 0xffff;
+  (void)t3;
+  const int vpj[2] = {pk & 0xffff, (pk & 0xffff) + nf[0]};
+  const int spj[2] = {pk >> 16, (pk >> 16) + static_cast<int>(split[0])};
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int g = 2 * tid + j;
+    const int len = split[j] ? ((cnt[j] + nch[j] - 1) / nch[j] + ks - 1) / ks * ks : cnt[j];
+    for (int c = 0; c < nf[j]; ++c) {
+      const int k0 = c * len;
+      vtab[vpj[j] + c] = make_int4(g, k0, min(len, cnt[j] - k0),
+                                   split[j] ? (ppj[j] | (c << 8) | (spj[j] << 16) | (nch[j] << 24)) : -1);
+    }
+  }
+  if (tid == 0) *nv = t2;
+}
+
 template <int GW, bool kOrientN, int kKS = 64, int kNT = 0>
 struct GkCfg {
   static constexpr int KS = kKS;  // gathered k per stage
@@ -152,12 +251,13 @@ struct GkCfg {
   static constexpr int A_RPW = 32 / A_CPR;       // A rows covered by one warp instruction
 };
 
-template <int GW, bool kOrientN, bool kBF16, int kKS, int kNT>
+template <int GW, bool kOrientN, bool kBF16, int kKS, int kNT, bool kSplit = false>
 __global__ void __launch_bounds__(kThreads, 1)
     spmm_gk_kernel(const __grid_constant__ CUtensorMap tmC, int use_tma_store, const void* __restrict__ Bv, int64_t ldb, const void* __restrict__ Atv, int64_t lda,
                    const int32_t* __restrict__ counts, const int32_t* __restrict__ slots, int64_t slot_stride,
                    int n_groups, int n_tiles, int M, int N, int K, void* __restrict__ Cv, int64_t ldc,
-                   int grp_rows, int gpb, int64_t b_batch_stride) {
+                   int grp_rows, int gpb, int64_t b_batch_stride, int* __restrict__ split_ctr,
+                   float* __restrict__ ws) {
   // grp_rows (<= GW, multiple of 8): rows per group. Micro-tiles narrower than the kernel's GW run
   // in it with the A^T strip's extra columns zero-filled and never stored.
   // Batched (prevalent axis, e.g. attention heads): slices are stacked along M in A and C (slice b
@@ -195,7 +295,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // Units are (n tile, group) pairs, n-tile major: the CTAs running concurrently share one
   // [K, N_TILE] slab of B, which stays L2-resident while every group gathers from it.
-  const int units = n_groups * n_tiles;
+  // kSplit: the walk runs over virtual groups (gk_split_plan_kernel): entry {group, first slot,
+  // count, partial tile or -1}; a long group's chunks go to different CTAs and leave fp32 partial
+  // tiles that gk_split_fixup_kernel sums into C.
+  static_assert(!kSplit || kOrientN, "split units are implemented for orientation N");
+  __shared__ int s_last;
+  const int4* vtab = reinterpret_cast<const int4*>(split_ctr + kSplitCtrBytes / 4);  // kSplit: after the counters
+  const int n_vg = kSplit ? __ldg(reinterpret_cast<const int*>(vtab) - 1) : n_groups;
+  const int units = n_vg * n_tiles;
+  auto vunit = [&](int g) { return __ldg(vtab + g); };
+  auto vcount = [&](int g) { return kSplit ? __ldg(&vtab[g].z) : __ldg(counts + g); };
 
   if (warp < kProdWarps) {
     // ------------------------------------------------------------ cp.async producers
@@ -213,22 +322,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       int u, g, t, kb, cnt;  // unit, its group and n tile (tracked without division), chunk, count
       int b;                 // batch slice of the group (one division per unit, not per stage)
       int ncnt;              // count of the CTA's next unit, loaded one unit ahead of its use
+      int rg, kbeg;          // kSplit: the virtual group's real group and first slot
     };
-    const int step_t = static_cast<int>(gridDim.x) / n_groups;
-    const int step_g = static_cast<int>(gridDim.x) % n_groups;
+    const int step_t = static_cast<int>(gridDim.x) / n_vg;
+    const int step_g = static_cast<int>(gridDim.x) % n_vg;
     auto next_unit = [&](Pos& q) {
       q.u += gridDim.x;
       q.g += step_g;
       q.t += step_t;
-      if (q.g >= n_groups) {
-        q.g -= n_groups;
+      if (q.g >= n_vg) {
+        q.g -= n_vg;
         ++q.t;
       }
     };
     auto prefetch_next = [&](Pos& q) {
       int gn = q.g + step_g;
-      if (gn >= n_groups) gn -= n_groups;
-      q.ncnt = q.u + static_cast<int>(gridDim.x) < units ? __ldg(counts + gn) : 0;
+      if (gn >= n_vg) gn -= n_vg;
+      q.ncnt = q.u + static_cast<int>(gridDim.x) < units ? vcount(gn) : 0;
+    };
+    auto locate = [&](Pos& q) {  // real group, first slot and batch slice of q's (virtual) group
+      if constexpr (kSplit) {
+        const int4 e = vunit(q.g);
+        q.rg = e.x;
+        q.kbeg = e.y;
+        q.b = e.x / gpb;
+      } else {
+        q.b = q.g / gpb;
+      }
     };
     auto advance = [&](Pos p) {
       Pos q = p;
@@ -239,10 +359,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         q.cnt = q.u < units ? p.ncnt : 0;  // prefetched: short units do not stall on the count
         while (q.u < units && q.cnt == 0) {
           next_unit(q);
-          q.cnt = q.u < units ? __ldg(counts + q.g) : 0;
+          q.cnt = q.u < units ? vcount(q.g) : 0;
         }
         prefetch_next(q);
-        q.b = q.g / gpb;
+        if (q.u < units) locate(q);
       }
       return q;
     };
@@ -258,8 +378,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int q = 0; q < RW; ++q) x.v[q] = 0;
       if (p.u < units) {
         const int r0 = p.kb + RW * warp;
-        const int32_t* ps = slots + static_cast<int64_t>(p.g) * slot_stride + r0;
-        if (vec_idx && r0 + RW <= slot_stride) {  // in bounds; entries past cnt are masked by the copy
+        const int kbase = kSplit ? p.kbeg : 0;
+        const int32_t* ps = slots + static_cast<int64_t>(kSplit ? p.rg : p.g) * slot_stride + kbase + r0;
+        if (vec_idx && kbase + r0 + RW <= slot_stride) {  // in bounds; entries past cnt are masked by the copy
 #pragma unroll
           for (int q = 0; q < RW / 4; ++q) {
             const int4 t = __ldg(reinterpret_cast<const int4*>(ps) + q);
@@ -276,10 +397,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       return x;
     };
-    Pos cur{static_cast<int>(blockIdx.x), static_cast<int>(blockIdx.x) % n_groups,
-            static_cast<int>(blockIdx.x) / n_groups, 0, 0, 0, 0};
-    cur.cnt = cur.u < units ? __ldg(counts + cur.g) : 0;
-    cur.b = cur.g / gpb;
+    Pos cur{static_cast<int>(blockIdx.x), static_cast<int>(blockIdx.x) % n_vg,
+            static_cast<int>(blockIdx.x) / n_vg, 0, 0, 0, 0, 0, 0};
+    cur.cnt = cur.u < units ? vcount(cur.g) : 0;
+    if (cur.u < units) locate(cur);
     prefetch_next(cur);
     if (cur.u < units && cur.cnt == 0) {
       cur.kb = Cfg::KS;  // force advance() past the empty unit
@@ -302,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int kvalid = min(Cfg::KS, p.cnt - p.kb);
       const int kpad = (kvalid + 15) & ~15;
       const int n0 = p.t * Cfg::N_TILE;
-      const int m0 = p.g * grp_rows;
+      const int m0 = (kSplit ? p.rg : p.g) * grp_rows;
       const int m_end = min(M, m0 + grp_rows);
       mbar_wait(&empty_bar[stage], phase ^ 1);
       const int r0 = RW * warp;
@@ -381,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int cnt = __ldg(counts + u % n_groups);
+      const int cnt = vcount(u % n_vg);
       mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc_fence_after();
       for (int kb = 0; kb < cnt; kb += Cfg::KS) {
@@ -433,15 +554,80 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int g = u % n_groups;
-      const int n0 = (u / n_groups) * Cfg::N_TILE;
+      int g = u % n_vg;
+      const int t = u / n_vg;
+      const int n0 = t * Cfg::N_TILE;
+      int cnt, part = -1;
+      if constexpr (kSplit) {
+        const int4 e = vunit(g);
+        g = e.x;
+        cnt = e.z;
+        part = e.w;  // -1, or first partial tile | chunk << 8 | split group << 16 | chunks << 24
+      } else {
+        cnt = __ldg(counts + g);
+      }
       const int m0 = g * grp_rows;
       const int m_end = min(M, m0 + grp_rows);
-      const int cnt = __ldg(counts + g);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * Cfg::ACC_COLS);
-      if (kOrientN && (use_tma_store & 1)) {
+      if (kSplit && part >= 0) {
+        // a chunk of a split group: its fp32 partial tile [128 rows x N_TILE] (lane = row) goes to
+        // scratch (a chunk always has live k). The chunk that completes its group last (counter in
+        // scratch, zeroed before the launch) sums every chunk's tile into C.
+        const int row = q * 32 + lane;
+        const int p0 = part & 255, ch = (part >> 8) & 255, sg = (part >> 16) & 255, nch = part >> 24;
+        float* wrow = ws + static_cast<int64_t>(p0 + ch) * 128 * Cfg::N_TILE + row * Cfg::N_TILE;
+#pragma unroll 1
+        for (int c = 0; c < Cfg::N_TILE; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(tbase + static_cast<uint32_t>(c), v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            reinterpret_cast<float4*>(wrow + c)[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                                                 __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+        }
+        if (!(use_tma_store & 8)) {
+        __threadfence();
+        bar_sync_named(3, 128);  // the 4 epilogue warps
+        if (row == 0) s_last = atomicAdd(split_ctr + sg, 1) == nch - 1;
+        bar_sync_named(3, 128);
+        }
+        if (s_last && !(use_tma_store & 12)) {
+          __threadfence();
+          // coalesced: thread t sums float4 t, t + 128, ... of the tile over the group's chunks
+          // (partial tiles p0 .. p0 + nch - 1), then writes 4 bf16 columns of one C row
+          constexpr int F4 = 128 * Cfg::N_TILE / 4, PER = F4 / 128, C4 = Cfg::N_TILE / 4;
+          float4 acc[PER];
+#pragma unroll
+          for (int j = 0; j < PER; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+          const float4* t4 = reinterpret_cast<const float4*>(ws + static_cast<int64_t>(p0) * 128 * Cfg::N_TILE);
+#pragma unroll 1
+          for (int h = 0; h < nch; ++h) {
+            float4 v4[PER];
+#pragma unroll
+            for (int j = 0; j < PER; ++j) v4[j] = __ldcg(t4 + static_cast<int64_t>(h) * F4 + row + 128 * j);
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+              acc[j].x += v4[j].x; acc[j].y += v4[j].y; acc[j].z += v4[j].z; acc[j].w += v4[j].w;
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < PER; ++j) {
+            const int e = row + 128 * j;
+            const int m = m0 + e / C4, n = n0 + (e % C4) * 4;
+            if (m >= m_end || n >= N) continue;
+            T* dst = C + static_cast<int64_t>(m) * ldc + n;
+            if (n + 4 <= N && (ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(Cv) & 7) == 0) {
+              *reinterpret_cast<uint2*>(dst) = make_uint2(pack2(acc[j].x, acc[j].y, kBF16), pack2(acc[j].z, acc[j].w, kBF16));
+            } else {
+              const float f[4] = {acc[j].x, acc[j].y, acc[j].z, acc[j].w};
+              for (int i = 0; i < 4 && n + i < N; ++i) dst[i] = OT::cvt(f[i]);
+            }
+          }
+        }
+      } else if (kOrientN && (use_tma_store & 1)) {
         // lane = group row: 32-row x 64-column boxes through shared staging and TMA stores
         const int wrow0 = m0 + q * 32;
 #pragma unroll 1
@@ -2046,6 +2232,49 @@ int gk2_diag() {
   return v;
 }
 
+int gk_split_enabled() {  // PIT_GK_SPLIT=0: no split units (A/B knob)
+  static int v = [] {
+    const char* e = getenv("PIT_GK_SPLIT");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
+// Scratch for split units (counters | partial tiles); 0 when the case does not use them: many units
+// balance by themselves, and the CTA's unit list must fit kSplitUnitsMax.
+template <int NT>
+int64_t gk_split_ws_bytes(int64_t n_groups, int n_tiles) {
+  if (!gk_split_enabled() || n_tiles != 1 || n_groups * n_tiles >= 4ll * num_sms() || n_groups > kSplitMaxGroups)
+    return 0;
+  return kSplitCtrBytes + (n_groups + kSplitParts) * 16 + static_cast<int64_t>(kSplitParts) * 128 * NT * 4;
+}
+
+template <int GW, bool kOrientN, bool kBF16, int kKS, int kNT>
+int run_gk_split(const SpmmArgs& a, cudaStream_t s, const CUtensorMap& tmC, int epi, int n_tiles) {
+  using Cfg = GkCfg<GW, kOrientN, kKS, kNT>;
+  // scratch: counters (the last int = number of virtual groups) | vtab | partial tiles
+  int* ctr = static_cast<int*>(a.ws);
+  int4* vtab = reinterpret_cast<int4*>(ctr + kSplitCtrBytes / 4);
+  float* parts = reinterpret_cast<float*>(vtab + a.n_groups + kSplitParts);
+  gk_split_plan_kernel<<<1, 1024, 0, s>>>(a.counts, static_cast<int>(a.n_groups), Cfg::KS, vtab,
+                                          ctr + kSplitCtrBytes / 4 - 1, ctr);
+  note_launch();
+  auto kern = spmm_gk_kernel<GW, kOrientN, kBF16, kKS, kNT, true>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::SMEM));
+  if (gk_split_enabled() >= 2) epi |= gk_split_enabled() == 2 ? 4 : 8;  // diagnostics: no reduce / no arrive
+  // virtual groups <= n_groups + P: enough CTAs for the longest walk; idle CTAs exit at once
+  const int64_t vunits = a.n_groups + kSplitParts;
+  const int grid = static_cast<int>(vunits < num_sms() ? vunits : num_sms());
+  kern<<<grid, kThreads, Cfg::SMEM, s>>>(tmC, epi, a.B, a.ldb, a.A, a.sak, a.counts, a.slots, a.slot_stride,
+                                         static_cast<int>(a.n_groups), n_tiles, static_cast<int>(a.M),
+                                         static_cast<int>(a.N), static_cast<int>(a.K), a.C, a.ldc,
+                                         static_cast<int>(a.t0),
+                                         static_cast<int>(a.batch > 1 ? a.n_groups / a.batch : a.n_groups),
+                                         a.batch > 1 ? a.b_batch_stride : 0, ctr, parts);
+  note_launch();
+  return cuda_status();
+}
+
 template <int GW, bool kOrientN, bool kBF16, int kKS = 64, int kNT = 0>
 int run_gk(const SpmmArgs& a, cudaStream_t s) {
   using Cfg = GkCfg<GW, kOrientN, kKS, kNT>;
@@ -2076,13 +2305,18 @@ int run_gk(const SpmmArgs& a, cudaStream_t s) {
     epi |= 1;
   }
   if (gk2_diag() & 4) epi |= 2;  // diagnostic: no C stores (orientation T)
+  if constexpr (kOrientN && kNT == 64) {
+    const int64_t need = gk_split_ws_bytes<Cfg::N_TILE>(a.n_groups, n_tiles);
+    if (need > 0 && a.ws != nullptr && a.ws_bytes >= need && (reinterpret_cast<uintptr_t>(a.ws) & 255) == 0)
+      return run_gk_split<GW, kOrientN, kBF16, kKS, kNT>(a, s, tmC, epi, n_tiles);
+  }
   // A column-major: A^T is row-major [K, M] with pitch sak
   kern<<<grid, kThreads, Cfg::SMEM, s>>>(tmC, epi, a.B, a.ldb, a.A, a.sak, a.counts, a.slots, a.slot_stride,
                                          static_cast<int>(a.n_groups), n_tiles, static_cast<int>(a.M),
                                          static_cast<int>(a.N), static_cast<int>(a.K), a.C, a.ldc,
                                          static_cast<int>(a.t0),
                                          static_cast<int>(a.batch > 1 ? a.n_groups / a.batch : a.n_groups),
-                                         a.batch > 1 ? a.b_batch_stride : 0);
+                                         a.batch > 1 ? a.b_batch_stride : 0, nullptr, nullptr);
   note_launch();
   return cuda_status();
 }
@@ -2531,6 +2765,14 @@ int launch_rowgemm(const GroupedGemmArgs& g, cudaStream_t s) {
   if (ks == 64 && p.G <= kRg2MaxGroups && rg2t_enabled() && p.N >= 64 && small_groups)
     return g.dtype == kDtypeBF16 ? run_rowgemm2t<true>(p, g.B, g.ldb, s) : run_rowgemm2t<false>(p, g.B, g.ldb, s);
   return g.dtype == kDtypeBF16 ? rowgemm_dispatch<true>(p, g.B, g.ldb, ks, s) : rowgemm_dispatch<false>(p, g.B, g.ldb, ks, s);
+}
+
+int64_t spmm_tc_workspace_bytes(const SpmmArgs& a) {
+  // mirrors dispatch_tc: only the 128-row gathered-K kernel on 64-column units splits groups
+  if (a.plan != kPlanPitK || a.t0 <= 64 || a.t0 > 128 || a.N > 64) return 0;
+  const char* e = getenv("PIT_GK_NT");
+  if (e && atoi(e) == 128) return 0;
+  return gk_split_ws_bytes<64>(a.n_groups, 1);
 }
 
 int launch_spmm_tc(const SpmmArgs& a, cudaStream_t s) {

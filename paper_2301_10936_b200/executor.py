@@ -358,6 +358,17 @@ def _check_matmul_operands(plan: SparseKernelPlan, A: DenseTensor, B: DenseTenso
 _PLAN_CODE = {"dense": _lib.PIT_PLAN_DENSE, "m": _lib.PIT_PLAN_PIT_M, "k": _lib.PIT_PLAN_PIT_K}
 
 
+def _attach_workspace(a, keep) -> None:
+    """Caller-owned scratch for pit_spmm (split gathered-K units): a stream-ordered torch allocation
+    per call, so concurrent streams never share it and CUDA-graph capture draws it from the graph's
+    pool."""
+    n = int(_lib.load().pit_spmm_workspace_bytes(C.byref(a)))
+    if n > 0:
+        buf = _torch().empty(n, dtype=_torch().uint8, device=_device.require_cuda())
+        a.workspace, a.workspace_bytes = buf.data_ptr(), n
+        keep.append(buf)
+
+
 def spmm_device(plan: SparseKernelPlan, Ad, Bd, idx: Optional[MicroTileIndex], out=None, force_simt: bool = False):
     """Launch the fused SpMM on device tensors (no validation beyond the C ABI's); returns C."""
     torch = _torch()
@@ -399,6 +410,7 @@ def spmm_device(plan: SparseKernelPlan, Ad, Bd, idx: Optional[MicroTileIndex], o
             a.rows, a.n_rows = rows.data_ptr(), n_rows.data_ptr()
             a.n_rows_bound = M
     a.force_simt = int(force_simt)
+    _attach_workspace(a, keep)
     lib = _lib.load()
     _device.check(lib.pit_spmm(C.byref(a), _device.stream_ptr()), ExecError)
     return C_
@@ -761,6 +773,7 @@ def run_batched_matmul_with_index(plan: SparseKernelPlan, A3, B3, idx: Optional[
             keep.append(occ)
             a.occ = occ.data_ptr()
             a.words_per_group = occ.shape[1]
+    _attach_workspace(a, keep)
     _device.check(_lib.load().pit_spmm(C.byref(a), _device.stream_ptr()), ExecError)
     if stats is not None:
         if plan.is_dense:

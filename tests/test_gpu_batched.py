@@ -194,3 +194,40 @@ def test_batched_dense_bf16_cta_pairs(m, n):
     ref = torch.bmm(A.double(), B.double())
     for b in range(batch):
         assert orc.max_rel_error(C[b].float().cpu().numpy(), ref[b].cpu().numpy()) <= BF16_TOL, b
+
+
+@pytest.mark.parametrize("batch,m,n", [(4, 1024, 64), (1, 1000, 40), (2, 512, 64)])
+def test_split_long_groups_narrow_n(batch, m, n):
+    """Few, unequal groups (attention with global query rows): 128-row gathered-K groups longer than
+    twice the mean are split over several CTAs and their fp32 partial tiles summed (split units).
+    Result must match the per-slice oracle; empty groups stay exact zeros."""
+    import torch
+
+    pit = _pit()
+    k, t0 = 4096, 128
+    reg = pit.register_builtin_kernels()
+    plan = pit.forced_plan(_bound(m, k, n), "k", reg, tile_shape=_tile_for(reg, t0))
+    rng = np.random.default_rng(m + n)
+    mask = np.repeat(rng.random((batch, -(-m // t0), k)) >= 0.9, t0, axis=1)[:, :m]
+    mask[:, :t0, :] = True                  # a global group per slice: every key live
+    mask[:, t0 : 2 * t0, :] = False          # and an empty one
+    A = rng.standard_normal((batch, m, k)).astype(np.float32) * mask
+    B = rng.standard_normal((batch, k, n)).astype(np.float32)
+    At = torch.from_numpy(A).to(torch.bfloat16).cuda()
+    B3 = torch.from_numpy(B).to(torch.bfloat16).cuda()
+    if batch > 1:
+        A3 = pit.stack_slices(At, plan)
+        idx = pit.build_batched_index_from_tensor(A3, (t0, 1), "k")
+        C3 = pit.run_batched_matmul_with_index(plan, A3, B3, idx).float().cpu().numpy()
+    else:
+        A2 = At[0].t().contiguous().t()
+        idx = pit.build_index_from_tensor(A2, (t0, 1), "k")
+        C3 = pit.run_matmul_with_index(plan, pit.DenseTensor(A2), pit.DenseTensor(B3[0]), idx).array
+        C3 = C3.float().cpu().numpy()[None]
+    Ar, Br = At.float().cpu().numpy(), B3.float().cpu().numpy()
+    for b in range(batch):
+        ref = orc.dense_reference_f64(Ar[b], Br[b])
+        assert orc.max_rel_error(C3[b], ref) <= BF16_TOL, b
+        assert np.all(C3[b, t0 : 2 * t0] == 0.0)
+    lib = pit._lib.load()
+    assert lib.pit_spmm_workspace_bytes is not None
