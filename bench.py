@@ -623,6 +623,15 @@ def attention_bench(args, dev, peaks, heads=12, seq=4096, hd=64):
            "ms_per_step": variants[best]["ms_per_step"], "variants": variants,
            "density": round(live / (heads * seq * seq), 4), "effective_flops": eff,
            "frac_bf16_peak": round(variants[best]["value"] / peaks["bf16"], 4),
+           # head dim 64: every gathered P value feeds 64 MACs, so the product is bound by reading the
+           # live P blocks (plus V once and C once), not by the tensor pipe
+           "roofline": {"bound": "hbm", "unit": "GB/s", "peak": peaks["hbm"],
+                        "algorithmic_bytes": live * 2 + 2 * heads * seq * hd * 2,
+                        "achieved": round((live * 2 + 2 * heads * seq * hd * 2)
+                                          / (variants[best]["ms_per_step"] * 1e-3) / 1e9, 1),
+                        "frac": round((live * 2 + 2 * heads * seq * hd * 2)
+                                      / (variants[best]["ms_per_step"] * 1e-3) / 1e9 / peaks["hbm"], 4),
+                        "note": "whole step (index build from the block mask + SpMM) against live P + V + C bytes"},
            "detect_from_values_ms": round(det_ms, 4),
            "detect_from_values_GBps": round(heads * seq * seq * 2 / (det_ms * 1e-3) / 1e9, 1),
            "execution": "CUDA graph: build_index(mask bits on device) + batched SpMM"}

@@ -1256,7 +1256,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // union rows that cover (nearly) every row (scattered per-row K patterns): contiguous 128-row tiles
   // with the occupancy staged per tile instead (decided on the device: no host round trip)
   const bool contig = p.contig_pct > 0 && p.n_rows != nullptr &&
-                      static_cast<int64_t>(*p.n_rows) * 100 >= static_cast<int64_t>(p.M) * p.contig_pct;
+                      static_cast<int64_t>(*p.n_rows) * 100 >= static_cast<int64_t>(p.M) * (p.contig_pct % 1000);
+  const bool diag_all_live = PIT_DIAG && p.contig_pct >= 1000;  // diagnostic builds: no zero-fill
   const int32_t* row_src = contig ? nullptr : p.row_src;
   const int32_t* row_dst = contig ? nullptr : p.row_dst;
   const int single_rows = p.cnt ? 0 : contig ? p.M : (p.n_rows ? *p.n_rows : p.M);
@@ -1330,6 +1331,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int w0 = rt.base >> 5, sh = rt.base & 31;
       if (staged) {
         bar_sync_named(2, kProdThreads);  // every producer is done with the previous unit's words
+        // independent loads, several in flight per thread (a K = 8192, t1 = 32 tile reads 1280 words)
+#pragma unroll 4
         for (int e = tp; e < nkg * 5; e += kProdThreads) {
           const int kg = e / 5;
           const int64_t word = static_cast<int64_t>(w0) + (e - kg * 5);
@@ -1408,7 +1411,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < RPT; ++j) {
             const int row = tp / CPR + j * RSTEP;
-            const uint32_t bytes = live[j] ? kbytes : 0u;
+            const uint32_t bytes = (live[j] || (diag_all_live && rid[j] >= 0)) ? kbytes : 0u;
             const T* src = bytes ? Ap + static_cast<int64_t>(rid[j]) * p.lda + kc : Ap;
             cp_async_16(sA + swz<MASK>(static_cast<uint32_t>(row * Cfg::A_ROW_BYTES + ch * 16)), src, bytes);
           }
