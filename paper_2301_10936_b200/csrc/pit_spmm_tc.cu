@@ -1171,6 +1171,9 @@ struct RowGemmParams {
   int uniform_rows;         // cnt == nullptr && G > 1: every group is this many consecutive rows
   int a_tma;                // A tiles by TMA (rows contiguous: no row_src, no liveness); else cp.async
   int contig_pct;           // > 0 (single group, union rows): contiguous row tiles when *n_rows >= pct% of M
+  int exit_if_contig;       // rowgemm: leave the contiguous case to the rowgemm2 launched beside it
+  int masked;               // rowgemm2: contiguous 128-row halves, per-chunk liveness from occ; runs only
+                            // when the union holds >= contig_pct% of the rows
 };
 
 template <int KS, int kBN = 256>
@@ -1258,6 +1261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool contig = p.contig_pct > 0 && p.n_rows != nullptr &&
                       static_cast<int64_t>(*p.n_rows) * 100 >= static_cast<int64_t>(p.M) * (p.contig_pct % 1000);
   const bool diag_all_live = PIT_DIAG && p.contig_pct >= 1000;  // diagnostic builds: no zero-fill
+  if (contig && p.exit_if_contig) return;  // rowgemm2 (masked) runs this product on CTA pairs
   const int32_t* row_src = contig ? nullptr : p.row_src;
   const int32_t* row_dst = contig ? nullptr : p.row_dst;
   const int single_rows = p.cnt ? 0 : contig ? p.M : (p.n_rows ? *p.n_rows : p.M);
@@ -1619,6 +1623,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // pair barrier -> pair MMA -> multicast commits; each CTA drains and stores its own 128 rows.
 // =============================================================================================
 constexpr int kRg2MaxGroups = 1024;
+constexpr int kRg2OccGroups = 512;  // masked mode: K-groups whose occupancy words fit shared memory
 constexpr int kRg2Band = 8;  // pair row tiles per raster band (dense)
 
 struct Rg2Cfg {
@@ -1676,8 +1681,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t rank = cluster_ctarank();
   const int pair = static_cast<int>(blockIdx.x >> 1);
   const int npairs = static_cast<int>(gridDim.x >> 1);
-  const int single_rows = p.n_rows ? *p.n_rows : p.M;
+  // masked (2-D pit:m with scattered per-row K patterns): decided on the device from the union size;
+  // when the union is small the union-row rowgemm launched beside this kernel runs the product
+  if (p.masked && p.n_rows != nullptr &&
+      static_cast<int64_t>(*p.n_rows) * 100 < static_cast<int64_t>(p.M) * p.contig_pct)
+    return;
+  const int single_rows = p.masked ? p.M : (p.n_rows ? *p.n_rows : p.M);
   __shared__ int pto[kRg2MaxGroups + 1];  // grouped: prefix of pair tiles per group
+  __shared__ uint32_t tile_occ[kRg2OccGroups * 4];  // masked: the CTA's 128 rows' words per K-group
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < Cfg::STAGES; ++i) {
@@ -1746,6 +1757,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const T* Ap = static_cast<const T*>(p.A);
     int stage = 0;
     uint32_t phase = 0;
+    const int nkg = p.masked ? (p.K + p.t1 - 1) / p.t1 : 0;
+    const int lg_t1 = p.masked ? __ffs(p.t1) - 1 : 0;  // masked: t1 in {16, 32}
     for (int u = pair; u < units; u += npairs) {
       const RowTile rt = decode_pair_tile(p, unit_pt(u), static_cast<int>(rank), single_rows, pto);
       const int n0 = unit_nt(u) * Cfg::BN + 128 * static_cast<int>(rank);
@@ -1756,6 +1769,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int i = tp / CPR + j * RSTEP;
           rid[j] = i < rt.rows ? tile_src_row(p, rt, i) : -1;
         }
+      }
+      if (p.masked) {
+        // the half tile's 128 rows start at a multiple of 128: 4 occupancy words per K-group
+        bar_sync_named(2, kProdThreads);  // every producer is done with the previous unit's words
+        const int64_t w0 = rt.base >> 5;
+#pragma unroll 4
+        for (int e = tp; e < nkg * 4; e += kProdThreads) {
+          const int64_t word = w0 + (e & 3);
+          tile_occ[e] = word < p.WG ? __ldg(p.occ + static_cast<int64_t>(e >> 2) * p.WG + word) : 0u;
+        }
+        bar_sync_named(2, kProdThreads);
       }
       for (int kb = 0; kb < kblocks; ++kb) {
         const int k0 = kb * KS;
@@ -1773,10 +1797,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t sA = smem_u32(sAp);
           const int kc = k0 + ch * 8;
           const uint32_t kbytes = kc < p.K ? static_cast<uint32_t>(min(16, (p.K - kc) * 2)) : 0u;
+          // masked: this thread's chunk lies in one K-group; a row dead there is zero-filled
+          const uint32_t* wv = tile_occ + min(kc >> lg_t1, nkg - 1) * 4;
 #pragma unroll
           for (int j = 0; j < RPT; ++j) {
             const int row = tp / CPR + j * RSTEP;
-            const uint32_t bytes = rid[j] >= 0 ? kbytes : 0u;
+            const bool live = rid[j] >= 0 && (!p.masked || ((wv[row >> 5] >> (row & 31)) & 1u));
+            const uint32_t bytes = live ? kbytes : 0u;
             const T* src = bytes ? Ap + static_cast<int64_t>(rid[j]) * p.lda + kc : Ap;
             cp_async_16(sA + swz<7>(static_cast<uint32_t>(row * 128 + ch * 16)), src, bytes);
           }
@@ -2449,7 +2476,7 @@ int run_rowgemm2(const RowGemmParams& p, const void* B, int64_t ldb, int64_t gro
     return kErrCuda;
   RowGemmParams q = p;
   q.a_tma = 0;
-  if (p.row_src == nullptr && (p.lda * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(p.A) & 15) == 0 &&
+  if (p.row_src == nullptr && !p.masked && (p.lda * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(p.A) & 15) == 0 &&
       a_tma_enabled()) {
     if (encode_tensor_map_2d(&tmA, dt, p.A, static_cast<uint64_t>(p.K), static_cast<uint64_t>(p.M),
                              static_cast<uint64_t>(p.lda) * 2, KS, 128, CU_TENSOR_MAP_SWIZZLE_128B) != CUDA_SUCCESS)
@@ -2513,6 +2540,14 @@ int rowgemm_dispatch(const RowGemmParams& p, const void* B, int64_t ldb, int ks,
   return kErrUnsupported;
 }
 
+int gm_pairs_enabled() {  // PIT_GM_PAIRS=0: contiguous pit:m stays on the single-CTA rowgemm
+  static int v = [] {
+    const char* e = getenv("PIT_GM_PAIRS");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 int gm_contig_pct() {  // PIT_GM_CONTIG=P: pit:m runs on contiguous row tiles when the union holds >= P% of rows
   static int v = [] {
     const char* e = getenv("PIT_GM_CONTIG");
@@ -2557,6 +2592,19 @@ int run_gm(const SpmmArgs& a, int ks, cudaStream_t s) {
       ceil_div(a.K, a.t1) <= GmCfg<64>::OCC_MAX_GROUPS && ceil_div(a.K, 64) <= GmCfg<64>::KB_MAX) {
     p.contig_pct = gm_contig_pct();
     if (p.contig_pct > 0) ks = 64;
+    // N > 128: the contiguous case runs on CTA pairs (rowgemm2, 256 x 256 tiles, every K-block, dead
+    // chunks zero-filled); both kernels are launched and each leaves on the device unless the union
+    // size selects it
+    if (p.contig_pct > 0 && a.N > 128 && rg2_enabled() && gm_pairs_enabled() && (a.ldc % 8) == 0 &&
+        (reinterpret_cast<uintptr_t>(a.C) & 15) == 0 && ceil_div(a.K, a.t1) <= kRg2OccGroups) {
+      RowGemmParams q = p;
+      q.masked = 1;
+      q.row_src = nullptr;
+      q.row_dst = nullptr;
+      q.max_tiles = static_cast<int>(ceil_div(a.M, 128));
+      if (int st = run_rowgemm2<kBF16>(q, a.B, a.ldb, 0, s)) return st;
+      p.exit_if_contig = 1;
+    }
   }
   return rowgemm_dispatch<kBF16>(p, a.B, a.ldb, ks, s);
 }
