@@ -1675,6 +1675,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull_bar = empty_bar + Cfg::STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* loaded_bar = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // masked + TMA A: operands landed
+  // masked with A by TMA: producer warp 0 (one lane) issues the TMA loads, warps 1-7 zero the dead
+  // (row, micro-column) chunks of each landed stage and then arrive on the full barrier
+  const bool mask_tma = p.masked && p.a_tma;
+  constexpr int kMaskers = kProdThreads - 32;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -1692,7 +1697,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < Cfg::STAGES; ++i) {
-      mbar_init(&full_bar[i], kProdThreads + 1);
+      mbar_init(&full_bar[i], mask_tma ? kMaskers : kProdThreads + 1);
+      mbar_init(&loaded_bar[i], 1);
       mbar_init(&pair_full[i], 2);
       mbar_init(&empty_bar[i], 1);
     }
@@ -1746,7 +1752,67 @@ __global__ void __launch_bounds__(kThreads, 1)
   };
   const int kblocks = (p.K + KS - 1) / KS;
 
-  if (warp < kProdWarps) {
+  if (warp < kProdWarps && mask_tma) {
+    // ------------------------------------------------------------ producers, masked + TMA A
+    const int nkg = (p.K + p.t1 - 1) / p.t1;
+    const int lg_t1 = __ffs(p.t1) - 1;  // t1 in {16, 32}
+    int stage = 0;
+    uint32_t phase = 0;
+    if (warp == 0) {
+      if (lane == 0) {
+        for (int u = pair; u < units; u += npairs) {
+          const RowTile rt = decode_pair_tile(p, unit_pt(u), static_cast<int>(rank), single_rows, pto);
+          const int n0 = unit_nt(u) * Cfg::BN + 128 * static_cast<int>(rank);
+          for (int kb = 0; kb < kblocks; ++kb) {
+            const int k0 = kb * KS;
+            mbar_wait(&empty_bar[stage], phase ^ 1);
+            uint8_t* sAp = smem + stage * Cfg::STAGE_BYTES;
+            uint8_t* sB = sAp + Cfg::A_BYTES;
+            mbar_expect_tx_only(&loaded_bar[stage], Cfg::B_BYTES + Cfg::A_BYTES);
+            tma_load_3d(sB, &tmB, &loaded_bar[stage], n0, k0, rt.g);
+            tma_load_3d(sB + KS * 128, &tmB, &loaded_bar[stage], n0 + 64, k0, rt.g);
+            tma_load_2d(sAp, &tmA, &loaded_bar[stage], k0, rt.base);
+            mbar_arrive(&loaded_bar[stage]);
+            if (++stage == Cfg::STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    } else {
+      const int tm = threadIdx.x - 32;  // 0 .. kMaskers-1
+      for (int u = pair; u < units; u += npairs) {
+        const RowTile rt = decode_pair_tile(p, unit_pt(u), static_cast<int>(rank), single_rows, pto);
+        bar_sync_named(2, kMaskers);  // every masker is done with the previous unit's words
+        const int64_t w0 = rt.base >> 5;
+#pragma unroll 4
+        for (int e = tm; e < nkg * 4; e += kMaskers) {
+          const int64_t word = w0 + (e & 3);
+          tile_occ[e] = word < p.WG ? __ldg(p.occ + static_cast<int64_t>(e >> 2) * p.WG + word) : 0u;
+        }
+        bar_sync_named(2, kMaskers);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          const int k0 = kb * KS;
+          mbar_wait(&loaded_bar[stage], phase);
+          const uint32_t sA = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+          // 1024 16-byte chunks (128 rows x 8): a chunk whose row is dead in its K-group is zeroed
+          for (int c = tm; c < 128 * 8; c += kMaskers) {
+            const int row = c >> 3, ch = c & 7;
+            const uint32_t w = tile_occ[min((k0 + ch * 8) >> lg_t1, nkg - 1) * 4 + (row >> 5)];
+            if (!((w >> (row & 31)) & 1u))
+              st_shared_v4(sA + swz<7>(static_cast<uint32_t>(row * 128 + ch * 16)), 0u, 0u, 0u, 0u);
+          }
+          fence_proxy_async_smem();  // generic zero stores -> tcgen05.mma reads
+          mbar_arrive(&full_bar[stage]);
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp < kProdWarps) {
     // ------------------------------------------------------------ producers
     constexpr int CPR = KS * 2 / 16;               // 16-byte chunks per A row
     constexpr int RPT = 128 * CPR / kProdThreads;  // A rows per producer thread (gathered rows)
@@ -2463,6 +2529,14 @@ int rg2_grouped() {  // PIT_RG2_GROUPED=0: grouped (MoE) GEMMs stay on single-CT
 }
 
 // CTA-pair launch of the dense / contiguous-row rowgemm cases (see rowgemm2_kernel).
+int gm_mask_tma_enabled() {  // PIT_GM_MASK_TMA=0: masked pit:m loads A by cp.async with zero-fill
+  static int v = [] {
+    const char* e = getenv("PIT_GM_MASK_TMA");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 template <bool kBF16>
 int run_rowgemm2(const RowGemmParams& p, const void* B, int64_t ldb, int64_t group_stride, cudaStream_t s) {
   using Cfg = Rg2Cfg;
@@ -2476,8 +2550,8 @@ int run_rowgemm2(const RowGemmParams& p, const void* B, int64_t ldb, int64_t gro
     return kErrCuda;
   RowGemmParams q = p;
   q.a_tma = 0;
-  if (p.row_src == nullptr && !p.masked && (p.lda * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(p.A) & 15) == 0 &&
-      a_tma_enabled()) {
+  if (p.row_src == nullptr && (p.lda * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(p.A) & 15) == 0 &&
+      a_tma_enabled() && (!p.masked || gm_mask_tma_enabled())) {
     if (encode_tensor_map_2d(&tmA, dt, p.A, static_cast<uint64_t>(p.K), static_cast<uint64_t>(p.M),
                              static_cast<uint64_t>(p.lda) * 2, KS, 128, CU_TENSOR_MAP_SWIZZLE_128B) != CUDA_SUCCESS)
       return kErrCuda;
