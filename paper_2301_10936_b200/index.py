@@ -175,6 +175,11 @@ class MicroTileIndex:
 
         if self._union is not None and not self._host_authoritative:
             return self._union
+        if self._n_groups == 1 and not self._host_authoritative:
+            # one group (row-uniform micro-tiles spanning K, e.g. BERT's (1, 768)): the union is that
+            # group's ascending coordinates — no union / compaction launches
+            self._union = (self._slots_dev[0], self._counts_dev[:1])
+            return self._union
         dev = _device.require_cuda()
         occ = self.occupancy_words()
         wg = -(-self.pit_grid // 32)
