@@ -76,6 +76,38 @@ __device__ __forceinline__ bool elem_live(const uint8_t* p, int dtype) {
 // ---------------------------------------------------------------------------
 constexpr int kRaWarps = 8;
 
+// ---------------------------------------------------------------------------
+// Pass 1, whole-row micro-tiles (1, >= C) — BERT's (1, 768) padding rows: one group, one bit per
+// row. A 256-thread block owns 32 rows: its threads read the rows' 16-byte vectors coalesced (every
+// load in flight at once), OR a per-row bit into a 32-bit register mask, and the block's OR-reduced
+// mask is the group's bitmap word — stored directly (no memset, no atomics).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) detect_row_any_kernel(const uint8_t* __restrict__ x, int64_t R, int64_t row_bytes,
+                                                             int64_t ld_bytes, LiveMask lm, uint32_t* __restrict__ occ) {
+  __shared__ uint32_t wm[8];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int rows = R - r0 < 32 ? static_cast<int>(R - r0) : 32;
+  const int vpr = static_cast<int>(row_bytes >> 4);  // 16-byte vectors per row
+  const int nv = rows * vpr;
+  uint32_t mask = 0;
+#pragma unroll 4
+  for (int v = threadIdx.x; v < nv; v += 256) {
+    const int r = v / vpr, c = v - r * vpr;
+    const uint4 q = __ldg(reinterpret_cast<const uint4*>(x + (r0 + r) * ld_bytes) + c);
+    const bool live = ((q.x & lm.even) | (q.y & lm.odd) | (q.z & lm.even) | (q.w & lm.odd)) != 0;
+    mask |= static_cast<uint32_t>(live) << r;
+  }
+  mask = __reduce_or_sync(0xffffffffu, mask);
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = mask;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) m |= wm[w];
+    occ[blockIdx.x] = m;
+  }
+}
+
 __global__ void __launch_bounds__(kRaWarps * 32, 4) detect_rows_vec_kernel(const uint8_t* __restrict__ x, int64_t R,
                                                                           int64_t row_bytes, int64_t ld_bytes, int tr,
                                                                           int V, int64_t GR, int64_t GC,
@@ -430,6 +462,8 @@ __global__ void slots_to_occ_kernel(const int32_t* __restrict__ counts, const in
 }  // namespace
 
 // ---------------------------------------------------------------------------- launchers
+static bool R_fits_grid(int64_t GR) { return GR / 32 + 1 < (1ll << 31); }
+
 int launch_detect_values(const DetectValuesArgs& a, cudaStream_t s) {
   const int eb = dtype_bytes(a.dtype);
   const int64_t GR = ceil_div(a.R, a.tr), GC = ceil_div(a.C, a.tc);
@@ -445,6 +479,12 @@ int launch_detect_values(const DetectValuesArgs& a, cudaStream_t s) {
                     (static_cast<int64_t>(a.tc) * eb) % 16 == 0;
   // wide micro-columns (e.g. BERT's (1, 768) row micro-tiles): whole 512-byte segments per micro-column
   const bool wide = vec_per_micro > 32 && vec_per_micro % 32 == 0 && (static_cast<int64_t>(a.tc) * eb) % 16 == 0;
+  if (a.pit_phys == 0 && aligned && a.tr == 1 && GC == 1 && R_fits_grid(GR)) {
+    detect_row_any_kernel<<<static_cast<unsigned>(GR / 32 + (GR % 32 != 0)), 256, 0, s>>>(
+        static_cast<const uint8_t*>(a.x), a.R, row_bytes, ld_bytes, live_mask_for(a.dtype), a.occ);
+    note_launch();
+    return cuda_status();
+  }
   if (a.pit_phys == 0 && aligned && (pow2 || wide)) {
     if (wide && cudaMemsetAsync(a.occ, 0, static_cast<size_t>(n_groups * WG) * sizeof(uint32_t), s) != cudaSuccess)
       return cuda_status();

@@ -174,3 +174,23 @@ def test_device_from_mask_matches_host():
         dev = pit.from_mask(torch.from_numpy(m).cuda(), gran)
         host = pit.from_mask(m, gran)
         np.testing.assert_array_equal(dev.packed, host.packed)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("shape,micro", [((4096, 768), (1, 768)), ((1000, 200), (1, 200)), ((77, 64), (1, 512)),
+                                         ((33, 8), (1, 8))])
+def test_whole_row_micro_tiles_match_oracle(dtype, shape, micro):
+    """(1, >= C) micro-tiles (BERT padding rows): one group, one bit per row, stored per 32-row
+    block without atomics. Rows mix zeros, -0.0 and (for floats) denormals / NaN."""
+    pit = _pkg()
+    rng = np.random.default_rng(shape[0] + micro[1])
+    v = _values(shape, 0.002, rng)
+    v[rng.random(shape[0]) < 0.3] = 0.0
+    if dtype in ("float32", "float64"):
+        v[3, 1] = -0.0
+        v[5, 2] = np.float32(1e-45)
+        v[shape[0] - 1, shape[1] - 1] = np.nan
+    t = _torch_values(v, dtype, False)
+    idx = pit.build_index_from_tensor(t, micro, "m")
+    counts, groups = orc.build_index_from_values(v, micro, "m")
+    assert_same_index(idx, counts, groups)
