@@ -2598,9 +2598,13 @@ int run_rowgemm2(const RowGemmParams& p, const void* B, int64_t ldb, int64_t gro
 template <bool kBF16>
 int rowgemm_dispatch(const RowGemmParams& p, const void* B, int64_t ldb, int ks, cudaStream_t s,
                      int64_t group_stride = 0) {
-  // dense / contiguous-row cases (no liveness, one group or uniform slices, N > 128) on CTA pairs
+  // dense / contiguous-row cases (no liveness, one group or uniform slices, N > 128) on CTA pairs.
+  // A single product with fewer than 4 pair units per cluster slot (BERT FFN1: 4096 x 768 x 3072)
+  // is latency-bound either way and measured faster on the single-CTA tiles (2x the units).
+  const int64_t pair_units = ceil_div(static_cast<int64_t>(p.max_tiles) * 128, 256) * ceil_div(p.N, 256);
+  const bool small_single = p.cnt == nullptr && p.uniform_rows == 0 && pair_units < 2ll * num_sms();
   if (ks == 64 && p.N > 128 && p.occ == nullptr && (p.cnt == nullptr || (p.G <= kRg2MaxGroups && rg2_grouped())) &&
-      (p.ldc % 8) == 0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && rg2_enabled())
+      (p.ldc % 8) == 0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && rg2_enabled() && !small_single)
     return run_rowgemm2<kBF16>(p, B, ldb, group_stride, s);
   if (p.N <= 64) {  // narrow products: 64-column units, no zero-filled B atoms or idle MMA columns
     if (ks == 64) return run_rowgemm<64, kBF16, 64>(p, B, ldb, group_stride, s);
