@@ -119,7 +119,7 @@ typedef struct {
   void* C; /* row-major [M,N], pitch ldc; every element is written */
   int64_t ldc;
   int t0, t1; /* plan micro-tile */
-  const int32_t* counts;
+  const int32_t* counts; /* pit:k: required; pit:m: optional (enables global dead-K-block skipping) */
   const int32_t* slots;
   int64_t slot_stride; /* = pit_grid */
   int64_t n_groups;

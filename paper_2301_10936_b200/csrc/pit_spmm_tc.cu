@@ -1174,6 +1174,7 @@ struct RowGemmParams {
   int exit_if_contig;       // rowgemm: leave the contiguous case to the rowgemm2 launched beside it
   int masked;               // rowgemm2: contiguous 128-row halves, per-chunk liveness from occ; runs only
                             // when the union holds >= contig_pct% of the rows
+  const int32_t* kg_cnt;    // masked: live rows per K-group (the pit:m index counts)
 };
 
 template <int KS, int kBN = 256>
@@ -1729,11 +1730,47 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (lane == 31) pto[p.G] = incl;
   }
+  // masked: K-blocks in which no row of the whole operand is live (dead neurons: column-structured
+  // activation sparsity) are skipped by every role of both CTAs — a global property, so the pair
+  // agrees without exchanging anything
+  __shared__ uint32_t kbl[32];
+  if (p.masked) {
+    const int nkb = (p.K + KS - 1) / KS, nkg = (p.K + p.t1 - 1) / p.t1;
+    for (int kb0 = warp * 32; kb0 < nkb; kb0 += (kThreads / 32) * 32) {
+      const int kb = kb0 + lane;
+      bool live = false;
+      if (kb < nkb) {
+        const int kg1 = min((kb * KS + KS - 1) / p.t1, nkg - 1);
+        for (int kg = kb * KS / p.t1; kg <= kg1; ++kg) live |= __ldg(p.kg_cnt + kg) > 0;
+      }
+      const uint32_t word = __ballot_sync(0xffffffffu, live);
+      if (lane == 0) kbl[kb0 >> 5] = word;
+    }
+  }
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int units = (p.cnt != nullptr ? min(pair_tiles, pto[p.G]) : pair_tiles) * n_tiles;
+  const int kblocks = (p.K + KS - 1) / KS;
+  auto next_kb = [&](int kb) {  // masked: next live K-block after kb (kblocks: none)
+    if (!p.masked) return kb + 1;
+    int w = (kb + 1) >> 5;
+    if (w * 32 >= kblocks) return kblocks;
+    uint32_t bits = kbl[w] & (0xffffffffu << ((kb + 1) & 31));
+    while (!bits) {
+      if (++w * 32 >= kblocks) return kblocks;
+      bits = kbl[w];
+    }
+    return min(w * 32 + __ffs(bits) - 1, kblocks);
+  };
+  const int kb_first = next_kb(-1);  // 0 unless masked
+  int nlive_kb = kblocks;
+  if (p.masked) {
+    nlive_kb = 0;
+    for (int w = 0; w < (kblocks + 31) / 32; ++w) nlive_kb += __popc(kbl[w]);
+  }
+  const bool all_kb = nlive_kb == kblocks;  // the common case keeps the plain K-block loop
   // unit -> (pair row tile, n tile). One group (dense, BERT): rasterised in bands of kRg2Band pair
   // row tiles, n tile outer within a band, so the pairs running together share B n-tile slabs and
   // an A row band in L2 (row-tile-major order re-streamed all of B for every wave of row tiles).
@@ -1750,7 +1787,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int bh = min(kRg2Band, pair_tiles - band * kRg2Band);
     return in / bh;
   };
-  const int kblocks = (p.K + KS - 1) / KS;
 
   if (warp < kProdWarps && mask_tma) {
     // ------------------------------------------------------------ producers, masked + TMA A
@@ -1763,7 +1799,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int u = pair; u < units; u += npairs) {
           const RowTile rt = decode_pair_tile(p, unit_pt(u), static_cast<int>(rank), single_rows, pto);
           const int n0 = unit_nt(u) * Cfg::BN + 128 * static_cast<int>(rank);
-          for (int kb = 0; kb < kblocks; ++kb) {
+          for (int kb = kb_first; kb < kblocks; kb = all_kb ? kb + 1 : next_kb(kb)) {
             const int k0 = kb * KS;
             mbar_wait(&empty_bar[stage], phase ^ 1);
             uint8_t* sAp = smem + stage * Cfg::STAGE_BYTES;
@@ -1792,7 +1828,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tile_occ[e] = word < p.WG ? __ldg(p.occ + static_cast<int64_t>(e >> 2) * p.WG + word) : 0u;
         }
         bar_sync_named(2, kMaskers);
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = kb_first; kb < kblocks; kb = all_kb ? kb + 1 : next_kb(kb)) {
           const int k0 = kb * KS;
           mbar_wait(&loaded_bar[stage], phase);
           const uint32_t sA = smem_u32(smem + stage * Cfg::STAGE_BYTES);
@@ -1847,7 +1883,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         bar_sync_named(2, kProdThreads);
       }
-      for (int kb = 0; kb < kblocks; ++kb) {
+      for (int kb = kb_first; kb < kblocks; kb = all_kb ? kb + 1 : next_kb(kb)) {
         const int k0 = kb * KS;
         mbar_wait(&empty_bar[stage], phase ^ 1);
         uint8_t* sAp = smem + stage * Cfg::STAGE_BYTES;
@@ -1888,7 +1924,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int u = pair; u < units; u += npairs) {
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = kb_first; kb < kblocks; kb = all_kb ? kb + 1 : next_kb(kb)) {
           mbar_wait(&full_bar[stage], phase);
           fence_proxy_async_smem();
           mbar_arrive_cluster(leader_pf + stage * 8);
@@ -1910,7 +1946,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int u = pair; u < units; u += npairs) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = kb_first; kb < kblocks; kb = all_kb ? kb + 1 : next_kb(kb)) {
           mbar_wait(&pair_full[stage], phase);
           tc_fence_after();
           if (lane == 0) {
@@ -1921,7 +1957,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint64_t adesc = smem_desc(sA + ks * 32, 16, 8 * 128, kSw128);
               const uint64_t bdesc = smem_desc(sB + ks * 2048, KS * 128, 1024, kSw128);
               umma2_f16(tmem_base + static_cast<uint32_t>(acc * Cfg::BN), adesc, bdesc, idesc,
-                        (kb > 0 || ks > 0) ? 1u : 0u);
+                        (kb > kb_first || ks > 0) ? 1u : 0u);
             }
             umma2_commit_mc(&empty_bar[stage], 3);
           }
@@ -1958,9 +1994,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int bx = 0; bx < Cfg::BN / 64; ++bx) {
         uint32_t v[64];
         const uint32_t ta = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * Cfg::BN + bx * 64);
-        tmem_ld32(ta, *reinterpret_cast<uint32_t(*)[32]>(v));
-        tmem_ld32(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
-        tmem_wait_ld();
+        if (kb_first < kblocks) {
+          tmem_ld32(ta, *reinterpret_cast<uint32_t(*)[32]>(v));
+          tmem_ld32(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+          tmem_wait_ld();
+        } else {  // masked with no live K-block anywhere: C is zero
+#pragma unroll
+          for (int j = 0; j < 64; ++j) v[j] = 0u;
+        }
         __syncwarp();
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -2673,10 +2714,11 @@ int run_gm(const SpmmArgs& a, int ks, cudaStream_t s) {
     // N > 128: the contiguous case runs on CTA pairs (rowgemm2, 256 x 256 tiles, every K-block, dead
     // chunks zero-filled); both kernels are launched and each leaves on the device unless the union
     // size selects it
-    if (p.contig_pct > 0 && a.N > 128 && rg2_enabled() && gm_pairs_enabled() && (a.ldc % 8) == 0 &&
+    if (p.contig_pct > 0 && a.N > 128 && a.counts != nullptr && rg2_enabled() && gm_pairs_enabled() && (a.ldc % 8) == 0 &&
         (reinterpret_cast<uintptr_t>(a.C) & 15) == 0 && ceil_div(a.K, a.t1) <= kRg2OccGroups) {
       RowGemmParams q = p;
       q.masked = 1;
+      q.kg_cnt = a.counts;
       q.row_src = nullptr;
       q.row_dst = nullptr;
       q.max_tiles = static_cast<int>(ceil_div(a.M, 128));

@@ -405,6 +405,8 @@ def spmm_device(plan: SparseKernelPlan, Ad, Bd, idx: Optional[MicroTileIndex], o
             occ = idx.occupancy_words()
             rows, n_rows = idx.union_coords()
             keep += [occ, rows, n_rows]
+            a.counts, _, alive = idx.device_ptrs()  # live rows per K-group (globally dead K-blocks)
+            keep += list(alive)
             a.occ = occ.data_ptr()
             a.words_per_group = occ.shape[1]
             a.rows, a.n_rows = rows.data_ptr(), n_rows.data_ptr()

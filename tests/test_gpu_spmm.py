@@ -165,6 +165,31 @@ def test_bf16_pit_m_dead_micro_tiles_not_read(t1, dead_rows, shape):
     assert np.all(C[dead] == 0.0)
 
 
+@pytest.mark.parametrize("t1", [16, 32])
+def test_bf16_pit_m_dead_neurons_skipped(t1):
+    """Column-structured activation sparsity (dead neurons): only ~10% of the micro-columns hold any
+    live row, but every row is live somewhere (union = all rows -> contiguous masked tiles on CTA
+    pairs). Globally dead K-blocks are skipped; dead micro-tiles still hold data and must not count."""
+    pit = _pkg()
+    m, k, n = 1024, 4096, 512
+    reg = pit.register_builtin_kernels()
+    tile = (128, t1, 256)
+    if reg.get("matmul", tile) is None:
+        reg.register(pit.TileKernelDescriptor("matmul", tile, f"m{t1}"))
+    rng = np.random.default_rng(77 + t1)
+    cols = rng.random(k // t1) < 0.1
+    cols[0] = True
+    mask = np.repeat((rng.random((m, k // t1)) < 0.5) & cols[None, :], t1, axis=1)
+    mask[:, :t1] = True  # every row live in the first micro-column
+    ann = pit.from_mask(mask, (1, t1))
+    A = rng.standard_normal((m, k)).astype(np.float32)
+    B = rng.standard_normal((k, n)).astype(np.float32)
+    plan = pit.forced_plan(bound(m, k, n), "m", reg, tile_shape=tile)
+    C, Ar, Br = _run_bf16(plan, A, B, ann, col_major=False)
+    ref = orc.run_sparse_matmul(Ar, Br, (ann.tensor_shape, ann.granularity, ann.packed), "m", tile, np.float64)
+    assert orc.max_rel_error(C, ref) <= BF16_TOL
+
+
 def test_bf16_row_uniform_and_dense_bitwise():
     """Fully dense annotation through pit:m equals the dense plan bitwise (test_executor.py:178-186)."""
     pit = _pkg()
