@@ -57,7 +57,7 @@ def test_route_index_is_bit_exact():
 
 @pytest.mark.parametrize("T,E,d,F,skew", [(1000, 8, 256, 512, 0.0), (4096, 128, 768, 3072, 0.0),
                                           (3000, 16, 128, 256, 3.0), (5, 4, 64, 128, 0.0),
-                                          (4100, 4, 192, 320, 1.0)])
+                                          (4100, 4, 192, 320, 1.0), (4096, 4, 256, 384, 0.0)])
 def test_switch_layer_single_gpu_matches_oracle(T, E, d, F, skew):
     # small groups (< 256 tokens per expert on average) run the swapped-role rowgemm2t, large ones
     # the 256-row pair tiles of rowgemm2 (the last case: ~1025 tokens per expert, ragged tails)
