@@ -345,6 +345,11 @@ def run_ours(args, w):
             result["sparsity_sweep"] = sparsity_sweep_bench(args, dev, peaks)
         except Exception as e:
             result["sparsity_sweep"] = {"error": f"{type(e).__name__}: {e}"[:300]}
+    if not args.no_bert and w["name"] != "bert_ffn1":
+        try:
+            result["bert_ffn1"] = bert_bench(args, dev, peaks)
+        except Exception as e:
+            result["bert_ffn1"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     if not args.no_attn:
         try:
             result["attention"] = attention_bench(args, dev, peaks)
@@ -369,6 +374,39 @@ def run_ours(args, w):
     if world > 1:
         dist.destroy_process_group()
     return result if rank == 0 else None
+
+
+def bert_bench(args, dev, peaks):
+    """C2 (BASELINE configs[1]): BERT-base FFN1 over a variable-length batch (32 sequences of
+    U[16,128] tokens padded to 128), padding removed via pit:m with row-uniform (1, 768) micro-tiles:
+    online detection from the activations + the gathered-row GEMM, one CUDA graph, L2 flushed.
+    Effective FLOPs = 2 * 3072 * live elements (padding excluded)."""
+    import torch
+
+    from paper_2301_10936_b200.graph import CapturedSparseMatmul
+
+    w = dict(WORKLOADS["bert_ffn1"], name="bert_ffn1")
+    A, B, live = make_operands(w, seed=1234, device=dev)  # the --workload bert_ffn1 operands
+    eff = 2.0 * w["N"] * live
+    captured = CapturedSparseMatmul(make_plan(w), A, B)
+    for _ in range(max(3, args.warmup)):
+        captured.replay()
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    ev = []
+    for _ in range(max(5, args.steps)):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        captured.replay()
+        e1.record(stream)
+        ev.append((e0, e1))
+    torch.cuda.synchronize()
+    ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+    return {"workload": w["desc"], "value": round(eff / (ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s (effective)",
+            "ms_per_step": round(ms, 4), "live_rows": int(live // w["K"]), "rows": w["M"],
+            "frac_bf16_peak": round(eff / (ms * 1e-3) / 1e12 / peaks["bf16"], 4),
+            "execution": "CUDA graph: build_index_from_tensor (1, 768) + run_matmul_with_index (pit:m)"}
 
 
 def moe_bench(args, world, rank, dev, peaks, tokens_per_gpu=16384, n_experts=128, d_model=768, d_ff=3072):
@@ -871,6 +909,7 @@ def main():
     ap.add_argument("--no-moe", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the micro-tile x sparsity sweep")
     ap.add_argument("--no-attn", action="store_true", help="skip the C3 block-sparse attention section")
+    ap.add_argument("--no-bert", action="store_true", help="skip the C2 BERT varlen FFN1 section")
     ap.add_argument("--no-opt", action="store_true", help="skip the C4 OPT FFN2 section")
     ap.add_argument("--no-graph", action="store_true", help="time eager API calls instead of the captured step")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
