@@ -30,6 +30,7 @@ def _plan(m, k, n, axis, tile):
     ("k", (128, 1), (128, 64, 256)),   # spmm_gk, orientation N
     ("k", (256, 1), (256, 64, 256)),   # spmm_gk2, CTA pairs
     ("m", (1, 64), (128, 64, 256)),    # rowgemm, union rows
+    ("m", (1, 32), (128, 32, 256)),    # rowgemm2 masked mode (union ~86% of rows), CTA pairs
     ("dense", None, (128, 64, 256)),   # rowgemm2, CTA pairs
 ])
 def test_fp16_plans_match_oracle(axis, micro, tile):
@@ -79,3 +80,24 @@ def test_fp16_moe_layer(T, E):
     ref = orc.switch_forward(r16(x), logits, r16(w1), r16(w2),
                              round_hidden=lambda h: torch.from_numpy(h).to(torch.float16).float().numpy())
     assert orc.max_rel_error(out, ref) <= TOL
+
+
+def test_fp16_split_gathered_k_units():
+    """Split units (few, unequal 128-row groups, N <= 64) in fp16: a global group sees every key."""
+    import torch
+
+    pit = _pit()
+    m, k, n = 1024, 4096, 64
+    plan = _plan(m, k, n, "k", (128, 64, 256))
+    rng = np.random.default_rng(11)
+    mask = np.repeat(rng.random((m // 128, k)) >= 0.9, 128, axis=0)
+    mask[:128] = True
+    A = rng.standard_normal((m, k)).astype(np.float32) * mask
+    B = rng.standard_normal((k, n)).astype(np.float32)
+    At = torch.from_numpy(A).to(torch.float16).cuda().t().contiguous().t()
+    Bt = torch.from_numpy(B).to(torch.float16).cuda()
+    idx = pit.build_index_from_tensor(At, (128, 1), "k")
+    C = pit.run_matmul_with_index(plan, pit.DenseTensor(At), pit.DenseTensor(Bt), idx).array
+    assert C.dtype == torch.float16
+    ref = orc.dense_reference_f64(At.float().cpu().numpy(), Bt.float().cpu().numpy())
+    assert orc.max_rel_error(C.float().cpu().numpy(), ref) <= TOL
