@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include "pit_internal.h"
+#include <type_traits>
 #include "pit_ptx.cuh"
 
 namespace pit {
@@ -1832,13 +1833,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int k0 = kb * KS;
           mbar_wait(&loaded_bar[stage], phase);
           const uint32_t sA = smem_u32(smem + stage * Cfg::STAGE_BYTES);
-          // 1024 16-byte chunks (128 rows x 8): a chunk whose row is dead in its K-group is zeroed
-          for (int c = tm; c < 128 * 8; c += kMaskers) {
-            const int row = c >> 3, ch = c & 7;
-            const uint32_t w = tile_occ[min((k0 + ch * 8) >> lg_t1, nkg - 1) * 4 + (row >> 5)];
-            if (!((w >> (row & 31)) & 1u))
-              st_shared_v4(sA + swz<7>(static_cast<uint32_t>(row * 128 + ch * 16)), 0u, 0u, 0u, 0u);
-          }
+          // (row, micro-column) items: one liveness lookup per item, a dead item's 16-byte chunks
+          // (4 for t1 = 32, 2 for t1 = 16) are zeroed
+          const int kg0 = k0 >> lg_t1;
+          auto mask_items = [&](auto cpk_tag) {
+            constexpr int CPK = decltype(cpk_tag)::value;  // chunks per micro-column
+            constexpr int PARTS = 8 / CPK;                 // micro-columns per 64-deep K-block
+#pragma unroll 2
+            for (int it = tm; it < 128 * PARTS; it += kMaskers) {
+              const int row = it / PARTS, part = it % PARTS;
+              const uint32_t w = tile_occ[min(kg0 + part, nkg - 1) * 4 + (row >> 5)];
+              if (!((w >> (row & 31)) & 1u)) {
+#pragma unroll
+                for (int c = 0; c < CPK; ++c)
+                  st_shared_v4(sA + swz<7>(static_cast<uint32_t>(row * 128 + (part * CPK + c) * 16)), 0u, 0u, 0u, 0u);
+              }
+            }
+          };
+          if (lg_t1 == 5) mask_items(std::integral_constant<int, 4>{});
+          else mask_items(std::integral_constant<int, 2>{});
           fence_proxy_async_smem();  // generic zero stores -> tcgen05.mma reads
           mbar_arrive(&full_bar[stage]);
           if (++stage == Cfg::STAGES) {
