@@ -1678,10 +1678,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   uint64_t* loaded_bar = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // masked + TMA A: operands landed
-  // masked with A by TMA: producer warp 0 (one lane) issues the TMA loads, warps 1-7 zero the dead
-  // (row, micro-column) chunks of each landed stage and then arrive on the full barrier
+  // masked with A by TMA: warp 11 (one lane) issues the TMA loads, the 8 producer warps zero the dead
+  // (row, micro-column) items of each landed stage (one item per thread at t1 = 32) and then arrive
+  // on the full barrier
   const bool mask_tma = p.masked && p.a_tma;
-  constexpr int kMaskers = kProdThreads - 32;
+  constexpr int kMaskers = kProdThreads;
+  constexpr int kIssuerWarp = kRelayWarp + 1;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -1789,13 +1791,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     return in / bh;
   };
 
-  if (warp < kProdWarps && mask_tma) {
+  if ((warp < kProdWarps || warp == kIssuerWarp) && mask_tma) {
     // ------------------------------------------------------------ producers, masked + TMA A
     const int nkg = (p.K + p.t1 - 1) / p.t1;
     const int lg_t1 = __ffs(p.t1) - 1;  // t1 in {16, 32}
     int stage = 0;
     uint32_t phase = 0;
-    if (warp == 0) {
+    if (warp == kIssuerWarp) {
       if (lane == 0) {
         for (int u = pair; u < units; u += npairs) {
           const RowTile rt = decode_pair_tile(p, unit_pt(u), static_cast<int>(rank), single_rows, pto);
@@ -1818,7 +1820,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     } else {
-      const int tm = threadIdx.x - 32;  // 0 .. kMaskers-1
+      const int tm = threadIdx.x;  // 0 .. kMaskers-1 (warps 0-7)
       for (int u = pair; u < units; u += npairs) {
         const RowTile rt = decode_pair_tile(p, unit_pt(u), static_cast<int>(rank), single_rows, pto);
         bar_sync_named(2, kMaskers);  // every masker is done with the previous unit's words
