@@ -1701,7 +1701,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < Cfg::STAGES; ++i) {
-      mbar_init(&full_bar[i], mask_tma ? kMaskers : kProdThreads + 1);
+      // every operand by TMA (dense, packed rows): the issuing thread's arrival alone
+      mbar_init(&full_bar[i], mask_tma ? kMaskers : (p.a_tma ? 1 : kProdThreads + 1));
       mbar_init(&loaded_bar[i], 1);
       mbar_init(&pair_full[i], 2);
       mbar_init(&empty_bar[i], 1);
@@ -1876,7 +1877,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t phase = 0;
     const int nkg = p.masked ? (p.K + p.t1 - 1) / p.t1 : 0;
     const int lg_t1 = p.masked ? __ffs(p.t1) - 1 : 0;  // masked: t1 in {16, 32}
-    for (int u = pair; u < units; u += npairs) {
+    // A and B both by TMA: one thread runs the ring (255 per-stage arrivals were pure overhead)
+    const int u_first = (p.a_tma && tp != 0) ? units : pair;
+    for (int u = u_first; u < units; u += npairs) {
       const RowTile rt = decode_pair_tile(p, unit_pt(u), static_cast<int>(rank), single_rows, pto);
       const int n0 = unit_nt(u) * Cfg::BN + 128 * static_cast<int>(rank);
       int rid[RPT];
@@ -1925,7 +1928,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             cp_async_16(sA + swz<7>(static_cast<uint32_t>(row * 128 + ch * 16)), src, bytes);
           }
         }
-        cp_async_arrive_noinc(&full_bar[stage]);
+        if (!p.a_tma) cp_async_arrive_noinc(&full_bar[stage]);
         if (++stage == Cfg::STAGES) {
           stage = 0;
           phase ^= 1;
