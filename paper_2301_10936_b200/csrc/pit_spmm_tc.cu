@@ -1272,7 +1272,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < Cfg::STAGES; ++i) {
-      mbar_init(&full_bar[i], kProdThreads + 1);
+      mbar_init(&full_bar[i], p.a_tma ? 1 : kProdThreads + 1);
       mbar_init(&empty_bar[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -1325,7 +1325,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       return min(w * 32 + __ffs(bits) - 1, kblocks);
     };
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    for (int u = (p.a_tma && tp != 0) ? units : static_cast<int>(blockIdx.x); u < units; u += gridDim.x) {
       const RowTile rt = decode_tile(p, u / n_tiles, single_rows);
       const int n0 = (u % n_tiles) * Cfg::BN;
       int rid[RPT];  // this thread's rows: tp / CPR + j * RSTEP
@@ -1410,7 +1410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive(&full_bar[stage]);  // publishes stage_live
         }
         if (p.a_tma) {
-          cp_async_arrive_noinc(&full_bar[stage]);
+          // A and B by TMA: the issuing thread alone runs the ring (its arrive above)
         } else {
           const int kc = k0 + ch * 8;
           const uint32_t kbytes = kc < p.K ? static_cast<uint32_t>(min(16, (p.K - kc) * 2)) : 0u;
@@ -2115,7 +2115,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < Cfg::STAGES; ++i) {
-      mbar_init(&full_bar[i], kProdThreads + 1);
+      mbar_init(&full_bar[i], p.a_tma ? 1 : kProdThreads + 1);
       mbar_init(&pair_full[i], 2);
       mbar_init(&empty_bar[i], 1);
     }
@@ -2178,7 +2178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const T* Xp = static_cast<const T*>(p.A);
     int stage = 0;
     uint32_t phase = 0;
-    for (int u = pair; u < units; u += npairs) {
+    for (int u = (p.a_tma && tp != 0) ? units : pair; u < units; u += npairs) {
       const TokTile tt = decode(u);
       const int o0 = (u % out_tiles) * 256 + 128 * static_cast<int>(rank);
       const int half = tt.nmma >> 1;                                 // token rows this CTA feeds
@@ -2218,7 +2218,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             cp_async_16(sx + swz<7>(static_cast<uint32_t>(row * 128 + ch * 16)), src, bytes);
           }
         }
-        cp_async_arrive_noinc(&full_bar[stage]);
+        if (!p.a_tma) cp_async_arrive_noinc(&full_bar[stage]);  // TMA-only stages: one arrival
         if (++stage == Cfg::STAGES) {
           stage = 0;
           phase ^= 1;
