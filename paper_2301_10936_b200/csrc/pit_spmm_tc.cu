@@ -2654,6 +2654,14 @@ int run_rowgemm2(const RowGemmParams& p, const void* B, int64_t ldb, int64_t gro
   return cuda_status();
 }
 
+int small_single_enabled() {  // PIT_SMALL_SINGLE=0: small gathered-row products stay on CTA pairs
+  static int v = [] {
+    const char* e = getenv("PIT_SMALL_SINGLE");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 template <bool kBF16>
 int rowgemm_dispatch(const RowGemmParams& p, const void* B, int64_t ldb, int ks, cudaStream_t s,
                      int64_t group_stride = 0) {
@@ -2661,7 +2669,8 @@ int rowgemm_dispatch(const RowGemmParams& p, const void* B, int64_t ldb, int ks,
   // A single product with fewer than 4 pair units per cluster slot (BERT FFN1: 4096 x 768 x 3072)
   // is latency-bound either way and measured faster on the single-CTA tiles (2x the units).
   const int64_t pair_units = ceil_div(static_cast<int64_t>(p.max_tiles) * 128, 256) * ceil_div(p.N, 256);
-  const bool small_single = p.cnt == nullptr && p.uniform_rows == 0 && pair_units < 2ll * num_sms();
+  const bool small_single = p.cnt == nullptr && p.uniform_rows == 0 && p.row_src != nullptr &&
+                            pair_units < 2ll * num_sms() && small_single_enabled();
   if (ks == 64 && p.N > 128 && p.occ == nullptr && (p.cnt == nullptr || (p.G <= kRg2MaxGroups && rg2_grouped())) &&
       (p.ldc % 8) == 0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && rg2_enabled() && !small_single)
     return run_rowgemm2<kBF16>(p, B, ldb, group_stride, s);
