@@ -2686,6 +2686,16 @@ int rowgemm_dispatch(const RowGemmParams& p, const void* B, int64_t ldb, int ks,
   return kErrUnsupported;
 }
 
+// Clears the C rows whose bit in a single-group pit:m bitmap is 0 (a warp per row, 16-byte stores).
+__global__ void __launch_bounds__(256) zero_dead_rows_kernel(const uint32_t* __restrict__ occ, int64_t M,
+                                                             uint8_t* __restrict__ C, int64_t ld_bytes,
+                                                             int64_t row_bytes) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (row >= M || ((__ldg(occ + (row >> 5)) >> (row & 31)) & 1u)) return;
+  uint4* dst = reinterpret_cast<uint4*>(C + row * ld_bytes);
+  for (int64_t i = threadIdx.x & 31; i < row_bytes / 16; i += 32) dst[i] = make_uint4(0u, 0u, 0u, 0u);
+}
+
 int gm_pairs_enabled() {  // PIT_GM_PAIRS=0: contiguous pit:m stays on the single-CTA rowgemm
   static int v = [] {
     const char* e = getenv("PIT_GM_PAIRS");
@@ -2706,8 +2716,16 @@ template <bool kBF16>
 int run_gm(const SpmmArgs& a, int ks, cudaStream_t s) {
   const int dense = a.plan == kPlanDense ? 1 : 0;
   if (!dense) {
-    // rows named by no group stay exactly zero
-    if (cudaMemset2DAsync(a.C, a.ldc * 2, 0, a.N * 2, a.M, s) != cudaSuccess) return cuda_status();
+    // rows named by no group stay exactly zero. One K-group (BERT's row-uniform micro-tiles): only
+    // the dead rows are written (the union is that group's bitmap); otherwise all of C is cleared.
+    if (ceil_div(a.K, a.t1) == 1 && a.occ != nullptr && (a.ldc % 8) == 0 && (a.N % 8) == 0 &&
+        (reinterpret_cast<uintptr_t>(a.C) & 15) == 0) {
+      zero_dead_rows_kernel<<<static_cast<unsigned>(ceil_div(a.M, 8)), 256, 0, s>>>(
+          a.occ, a.M, static_cast<uint8_t*>(a.C), a.ldc * 2, a.N * 2);
+      note_launch();
+    } else if (cudaMemset2DAsync(a.C, a.ldc * 2, 0, a.N * 2, a.M, s) != cudaSuccess) {
+      return cuda_status();
+    }
   }
   RowGemmParams p{};
   p.A = a.A;
