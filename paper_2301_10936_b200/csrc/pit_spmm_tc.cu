@@ -2696,6 +2696,20 @@ __global__ void __launch_bounds__(256) zero_dead_rows_kernel(const uint32_t* __r
   for (int64_t i = threadIdx.x & 31; i < row_bytes / 16; i += 32) dst[i] = make_uint4(0u, 0u, 0u, 0u);
 }
 
+// Clears C unless the union covers >= pct% of the rows (then the contiguous-tile kernel writes every
+// row itself): the decision is the kernels' own, read on the device.
+__global__ void __launch_bounds__(256) zero_unless_contig_kernel(const int32_t* __restrict__ n_rows, int pct,
+                                                                 int64_t M, uint8_t* __restrict__ C, int64_t ld_bytes,
+                                                                 int64_t chunks_per_row) {
+  if (static_cast<int64_t>(*n_rows) * 100 >= M * pct) return;
+  const int64_t total = M * chunks_per_row;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / chunks_per_row, c = i - r * chunks_per_row;
+    reinterpret_cast<uint4*>(C + r * ld_bytes)[c] = make_uint4(0u, 0u, 0u, 0u);
+  }
+}
+
 int gm_pairs_enabled() {  // PIT_GM_PAIRS=0: contiguous pit:m stays on the single-CTA rowgemm
   static int v = [] {
     const char* e = getenv("PIT_GM_PAIRS");
@@ -2712,6 +2726,14 @@ int gm_contig_pct() {  // PIT_GM_CONTIG=P: pit:m runs on contiguous row tiles wh
   return v;
 }
 
+// 2-D pit:m cases whose kernels switch to contiguous row tiles on the device when the union holds
+// >= PIT_GM_CONTIG % of the rows (scattered per-row K patterns over 16/32-wide micro-columns)
+bool gm_contig_capable(const SpmmArgs& a) {
+  return a.plan == kPlanPitM && a.occ != nullptr && a.n_rows != nullptr && (a.t1 == 32 || a.t1 == 16) &&
+         ceil_div(a.K, a.t1) > 1 && a.n_rows_host == a.M && ceil_div(a.K, a.t1) <= GmCfg<64>::OCC_MAX_GROUPS &&
+         ceil_div(a.K, 64) <= GmCfg<64>::KB_MAX && gm_contig_pct() > 0;
+}
+
 template <bool kBF16>
 int run_gm(const SpmmArgs& a, int ks, cudaStream_t s) {
   const int dense = a.plan == kPlanDense ? 1 : 0;
@@ -2722,6 +2744,15 @@ int run_gm(const SpmmArgs& a, int ks, cudaStream_t s) {
         (reinterpret_cast<uintptr_t>(a.C) & 15) == 0) {
       zero_dead_rows_kernel<<<static_cast<unsigned>(ceil_div(a.M, 8)), 256, 0, s>>>(
           a.occ, a.M, static_cast<uint8_t*>(a.C), a.ldc * 2, a.N * 2);
+      note_launch();
+    } else if (gm_contig_capable(a) && (a.ldc % 8) == 0 && (a.N % 8) == 0 &&
+               (reinterpret_cast<uintptr_t>(a.C) & 15) == 0) {
+      // the contiguous-tile kernels write every row: clear C only if the union-row kernel runs
+      const int64_t chunks = a.M * (a.N / 8);
+      const int64_t blocks = ceil_div(chunks, 256);
+      const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
+      zero_unless_contig_kernel<<<static_cast<unsigned>(blocks < cap ? blocks : cap), 256, 0, s>>>(
+          a.n_rows, gm_contig_pct(), a.M, static_cast<uint8_t*>(a.C), a.ldc * 2, a.N / 8);
       note_launch();
     } else if (cudaMemset2DAsync(a.C, a.ldc * 2, 0, a.N * 2, a.M, s) != cudaSuccess) {
       return cuda_status();
@@ -2752,10 +2783,9 @@ int run_gm(const SpmmArgs& a, int ks, cudaStream_t s) {
   // once per unit, a dead (row, micro-column) chunk is zero-filled by its cp.async, K-blocks with no
   // live row take no ring slot. 64-deep K-blocks cover two 32-wide (four 16-wide) micro-columns:
   // liveness is per 16-byte chunk's K-group.
-  if (p.occ != nullptr && (a.t1 == 32 || a.t1 == 16) && a.n_rows_host == a.M &&
-      ceil_div(a.K, a.t1) <= GmCfg<64>::OCC_MAX_GROUPS && ceil_div(a.K, 64) <= GmCfg<64>::KB_MAX) {
+  if (gm_contig_capable(a)) {
     p.contig_pct = gm_contig_pct();
-    if (p.contig_pct > 0) ks = 64;
+    ks = 64;
     // N > 128: the contiguous case runs on CTA pairs (rowgemm2, 256 x 256 tiles, every K-block, dead
     // chunks zero-filled); both kernels are launched and each leaves on the device unless the union
     // size selects it
