@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(1024) gk_split_plan_kernel(const int32_t* __re
     cnt[j] = valid[j] ? __ldg(counts + g) : 0;
   }
   int tot;
-  block_excl_scan(cnt[0] + cnt[1], sc, tot);  // the total (live k of one index fits int32)
+  block_excl_scan(cnt[0] + cnt[1], sc, tot);  // total live k (the host keeps n_groups * pit_grid < 2^31)
   const int mean = (tot + n_groups - 1) / n_groups;
   const int L = max((mean + ks - 1) / ks, 1) * ks;
   int nch[2], want[2];
@@ -185,8 +185,8 @@ __global__ void __launch_bounds__(1024) gk_split_plan_kernel(const int32_t* __re
     nch[j] = cnt[j] > 2 * L ? (cnt[j] + L - 1) / L : 1;
     want[j] = valid[j] && nch[j] > 1 && nch[j] <= 127 ? nch[j] : 0;
   }
-  int t1, t2, t3;
-  const int pp = block_excl_scan(want[0] + want[1], sc, t1);
+  int twant;
+  const int pp = block_excl_scan(want[0] + want[1], sc, twant);
   const int ppj[2] = {pp, pp + want[0]};
   bool split[2];
   int nf[2];
@@ -200,8 +200,6 @@ __global__ void __launch_bounds__(1024) gk_split_plan_kernel(const int32_t* __re
   const int pk0 = nf[0] | (static_cast<int>(split[0]) << 16), pk1 = nf[1] | (static_cast<int>(split[1]) << 16);
   int tpk;
   const int pk = block_excl_scan(pk0 + pk1, sc, tpk);
-  t2 = tpk & 0xffff;
-  (void)t3;
   const int vpj[2] = {pk & 0xffff, (pk & 0xffff) + nf[0]};
   const int spj[2] = {pk >> 16, (pk >> 16) + static_cast<int>(split[0])};
 #pragma unroll
@@ -214,7 +212,7 @@ __global__ void __launch_bounds__(1024) gk_split_plan_kernel(const int32_t* __re
                                    split[j] ? (ppj[j] | (c << 8) | (spj[j] << 16) | (nch[j] << 24)) : -1);
     }
   }
-  if (tid == 0) *nv = t2;
+  if (tid == 0) *nv = tpk & 0xffff;
 }
 
 template <int GW, bool kOrientN, int kKS = 64, int kNT = 0>
@@ -2462,7 +2460,8 @@ int run_gk(const SpmmArgs& a, cudaStream_t s) {
   if (gk2_diag() & 4) epi |= 2;  // diagnostic: no C stores (orientation T)
   if constexpr (kOrientN && kNT == 64) {
     const int64_t need = gk_split_ws_bytes<Cfg::N_TILE>(a.n_groups, n_tiles);
-    if (need > 0 && a.ws != nullptr && a.ws_bytes >= need && (reinterpret_cast<uintptr_t>(a.ws) & 255) == 0)
+    if (need > 0 && a.ws != nullptr && a.ws_bytes >= need && (reinterpret_cast<uintptr_t>(a.ws) & 255) == 0 &&
+        a.n_groups * a.slot_stride < (1ll << 31))
       return run_gk_split<GW, kOrientN, kBF16, kKS, kNT>(a, s, tmC, epi, n_tiles);
   }
   // A column-major: A^T is row-major [K, M] with pitch sak
