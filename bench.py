@@ -279,6 +279,8 @@ def run_ours(args, w):
         torch.cuda.synchronize()
     launches = (captured.kernels_per_replay * args.steps) if captured is not None else \
         (_lib.kernel_launches() - launches0)
+    # the timed replays must compute what the eager public calls compute (deterministic kernels)
+    replay_ok = bool(torch.equal(captured.C, C0.array)) if captured is not None else None
     total_ms = sum(a.elapsed_time(b) for a, b in step_ev)
     if world > 1:
         t = torch.tensor([total_ms], device=dev)
@@ -336,6 +338,7 @@ def run_ours(args, w):
                    else "eager API calls"},
         "roofline": roofline, "detection": detection,
         "clocks": clocks.summary(), "gpu_launches": int(launches),
+        "graph_replay_equals_eager": replay_ok,
     }
 
     if not args.no_index_bench:
@@ -376,6 +379,14 @@ def run_ours(args, w):
     return result if rank == 0 else None
 
 
+def pit_run(plan, A, B, w):
+    """The eager public calls of one step (reference output for a captured graph)."""
+    import paper_2301_10936_b200 as pit
+
+    idx = pit.build_index_from_tensor(A, w["micro"], w["axis"])
+    return pit.run_matmul_with_index(plan, pit.DenseTensor(A), pit.DenseTensor(B), idx).array
+
+
 def bert_bench(args, dev, peaks):
     """C2 (BASELINE configs[1]): BERT-base FFN1 over a variable-length batch (32 sequences of
     U[16,128] tokens padded to 128), padding removed via pit:m with row-uniform (1, 768) micro-tiles:
@@ -388,7 +399,9 @@ def bert_bench(args, dev, peaks):
     w = dict(WORKLOADS["bert_ffn1"], name="bert_ffn1")
     A, B, live = make_operands(w, seed=1234, device=dev)  # the --workload bert_ffn1 operands
     eff = 2.0 * w["N"] * live
-    captured = CapturedSparseMatmul(make_plan(w), A, B)
+    plan = make_plan(w)
+    eager = pit_run(plan, A, B, w)
+    captured = CapturedSparseMatmul(plan, A, B)
     for _ in range(max(3, args.warmup)):
         captured.replay()
     flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
@@ -406,6 +419,7 @@ def bert_bench(args, dev, peaks):
     return {"workload": w["desc"], "value": round(eff / (ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s (effective)",
             "ms_per_step": round(ms, 4), "live_rows": int(live // w["K"]), "rows": w["M"],
             "frac_bf16_peak": round(eff / (ms * 1e-3) / 1e12 / peaks["bf16"], 4),
+            "graph_replay_equals_eager": bool(torch.equal(captured.C, eager)),
             "execution": "CUDA graph: build_index_from_tensor (1, 768) + run_matmul_with_index (pit:m)"}
 
 
@@ -611,7 +625,7 @@ def attention_bench(args, dev, peaks, heads=12, seq=4096, hd=64):
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
-            step()
+            O_g = step()
         for _ in range(args.warmup):
             graph.replay()
         ev = []
@@ -625,7 +639,7 @@ def attention_bench(args, dev, peaks, heads=12, seq=4096, hd=64):
         torch.cuda.synchronize()
         ms = statistics.median(a.elapsed_time(b) for a, b in ev)
         return {"ms_per_step": round(ms, 4), "value": round(eff / (ms * 1e-3) / 1e12, 2),
-                "max_rel_err_head0_vs_f64": err}
+                "max_rel_err_head0_vs_f64": err, "graph_replay_equals_eager": bool(torch.equal(O_g, O))}
 
     variants = {}
     plan_m = pit.forced_plan(expr, "m", reg, tile_shape=(128, 64, 256))
@@ -729,7 +743,7 @@ def opt_bench(args, dev, peaks, tokens=4096, d_model=2048, d_ff=8192, zeros=(0.9
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
-            step()
+            O_g = step()
         for _ in range(args.warmup):
             graph.replay()
         ev = []
@@ -758,7 +772,8 @@ def opt_bench(args, dev, peaks, tokens=4096, d_model=2048, d_ff=8192, zeros=(0.9
                 live / (tokens * d_ff), 4),
             "fwd_pit_m_TFLOPs": round(eff / 2 / (split[0] * 1e-3) / 1e12, 1),
             "bwd_pit_k_TFLOPs": round(eff / 2 / (split[1] * 1e-3) / 1e12, 1),
-            "max_rel_err_vs_f64": err}
+            "max_rel_err_vs_f64": err,
+            "graph_replay_equals_eager": bool(torch.equal(O_g[0], Y) and torch.equal(O_g[1], dW2))}
         del H, keep
     first = out["by_zero_ratio"][str(zeros[0])]
     out["value"], out["ms_per_step"] = first["value"], first["ms_per_step"]
