@@ -1174,6 +1174,7 @@ struct RowGemmParams {
   int masked;               // rowgemm2: contiguous 128-row halves, per-chunk liveness from occ; runs only
                             // when the union holds >= contig_pct% of the rows
   const int32_t* kg_cnt;    // masked: live rows per K-group (the pit:m index counts)
+  int mask_tma;             // rowgemm, staged contiguous rows: A tiles by TMA + dead micro-tiles zeroed
 };
 
 template <int KS, int kBN = 256>
@@ -1251,6 +1252,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   int32_t* acc_live = reinterpret_cast<int32_t*>(tmem_slot + 2);    // per accumulator: 0 = no MMA (all zero)
   int32_t* stage_live = reinterpret_cast<int32_t*>(tmem_slot + 4);  // per stage: 1 = MMA, 0 = skipped
+  uint64_t* loaded_bar = reinterpret_cast<uint64_t*>(tmem_slot + 4 + 8);  // mask mode: TMA landed
   __shared__ uint32_t tile_occ[Cfg::OCC_MAX_GROUPS * 5];  // the row tile's occupancy words per K-group
   __shared__ uint32_t kb_live[Cfg::KB_MAX / 32];            // bit kb: some row of the tile is live
 
@@ -1267,11 +1269,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int single_rows = p.cnt ? 0 : contig ? p.M : (p.n_rows ? *p.n_rows : p.M);
   const int total_tiles = p.cnt ? __ldg(p.tile_off + p.G)
                          : p.uniform_rows ? p.G * ((p.uniform_rows + 127) / 128) : (single_rows + 127) / 128;
+  // mask mode (contiguous rows with staged occupancy, A by TMA): warp 11 issues the A/B tiles, the 8
+  // producer warps zero each landed stage's dead (row, micro-column) items, then arrive
+  const bool mask_mode = p.mask_tma && p.occ != nullptr && row_src == nullptr && (p.t1 & (p.t1 - 1)) == 0 &&
+                         (p.K + p.t1 - 1) / p.t1 <= Cfg::OCC_MAX_GROUPS && (p.K + KS - 1) / KS <= Cfg::KB_MAX;
+  constexpr int kIssuerWarp = kRelayWarp + 1;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < Cfg::STAGES; ++i) {
-      mbar_init(&full_bar[i], p.a_tma ? 1 : kProdThreads + 1);
+      mbar_init(&full_bar[i], mask_mode ? kProdThreads : p.a_tma ? 1 : kProdThreads + 1);
       mbar_init(&empty_bar[i], 1);
+      mbar_init(&loaded_bar[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 2);  // MMA commit + the issuer's release of acc_live
@@ -1363,9 +1371,35 @@ __global__ void __launch_bounds__(kThreads, 1)
           if ((tp & 31) == 0) kb_live[kb0 >> 5] = word;
         }
         bar_sync_named(2, kProdThreads);
+        if (mask_mode) bar_sync_named(3, kProdThreads + 32);  // kb_live -> the TMA issuer (warp 11)
       }
       for (int kb = staged ? next_kb(-1) : 0; kb < kblocks; kb = staged ? next_kb(kb) : kb + 1) {
         const int k0 = kb * KS;
+        if (mask_mode) {
+          // the issuer's A tile has landed: zero its dead (row, micro-column) items
+          mbar_wait(&loaded_bar[stage], phase);
+          const uint32_t sA = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+          const int parts = p.t1 >= KS ? 1 : KS >> lg_t1;  // micro-columns per K-block
+          const int cpk = CPR / parts;                      // 16-byte chunks per micro-column
+          const int kg0 = k0 >> lg_t1;
+          for (int it = tp; it < 128 * parts; it += kProdThreads) {
+            const int row = it / parts, part = it - row * parts;
+            const int rr = sh + row;
+            const uint32_t w = tile_occ[min(kg0 + part, nkg - 1) * 5 + (rr >> 5)];
+            if (!((w >> (rr & 31)) & 1u)) {
+              for (int c = 0; c < cpk; ++c)
+                st_shared_v4(sA + swz<MASK>(static_cast<uint32_t>(row * Cfg::A_ROW_BYTES + (part * cpk + c) * 16)), 0u,
+                             0u, 0u, 0u);
+            }
+          }
+          fence_proxy_async_smem();  // generic zero stores -> tcgen05.mma reads
+          mbar_arrive(&full_bar[stage]);
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+          continue;
+        }
         bool live[RPT];
         bool stage_any = true;
         // the K-group of this thread's 16-byte chunk (a K-block may span several when KS > t1)
@@ -1426,7 +1460,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           phase ^= 1;
         }
       }
-      if (p.occ) {  // END marker: closes the unit for the MMA issuer
+      if (p.occ && mask_mode) {  // END marker from the issuer
+        mbar_wait(&loaded_bar[stage], phase);
+        mbar_arrive(&full_bar[stage]);
+        if (++stage == Cfg::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      } else if (p.occ) {  // END marker: closes the unit for the MMA issuer
         mbar_wait(&empty_bar[stage], phase ^ 1);
         if (tp == 0) {
           stage_live[stage] = 2;
@@ -1438,6 +1479,53 @@ __global__ void __launch_bounds__(kThreads, 1)
           phase ^= 1;
         }
       }
+    }
+  } else if (mask_mode && warp == kIssuerWarp) {
+    // ------------------------------------------------------------ mask mode: TMA issuer
+    int stage = 0;
+    uint32_t phase = 0;
+    auto next_live = [&](int kb) {
+      int start = kb + 1;
+      int w = start >> 5;
+      if (w * 32 >= kblocks) return kblocks;
+      uint32_t bits = kb_live[w] & (0xffffffffu << (start & 31));
+      while (!bits) {
+        if (++w * 32 >= kblocks) return kblocks;
+        bits = kb_live[w];
+      }
+      return min(w * 32 + __ffs(bits) - 1, kblocks);
+    };
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const RowTile rt = decode_tile(p, u / n_tiles, single_rows);
+      const int n0 = (u % n_tiles) * Cfg::BN;
+      bar_sync_named(3, kProdThreads + 32);  // the producers staged this unit's kb_live
+      if (lane == 0) {
+        for (int kb = next_live(-1); kb < kblocks; kb = next_live(kb)) {
+          const int k0 = kb * KS;
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sAp = smem + stage * Cfg::STAGE_BYTES;
+          uint8_t* sB = sAp + Cfg::A_BYTES;
+          stage_live[stage] = 1;
+          mbar_expect_tx_only(&loaded_bar[stage], Cfg::B_BYTES + Cfg::A_BYTES);
+#pragma unroll
+          for (int a = 0; a < Cfg::BN / 64; ++a)
+            tma_load_3d(sB + a * KS * 128, &tmB, &loaded_bar[stage], n0 + a * 64, k0, rt.g);
+          tma_load_2d(sAp, &tmA, &loaded_bar[stage], k0, rt.base);
+          mbar_arrive(&loaded_bar[stage]);
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mbar_wait(&empty_bar[stage], phase ^ 1);  // END marker
+        stage_live[stage] = 2;
+        mbar_arrive(&loaded_bar[stage]);
+        if (++stage == Cfg::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      __syncwarp();
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
@@ -2534,6 +2622,14 @@ int a_tma_enabled() {  // PIT_A_TMA=0: cp.async row copies for contiguous A as w
   return v;
 }
 
+int gm_mask_tma_enabled() {  // PIT_GM_MASK_TMA=0: masked pit:m loads A by cp.async with zero-fill
+  static int v = [] {
+    const char* e = getenv("PIT_GM_MASK_TMA");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 template <int KS, bool kBF16, int kBN>
 int run_rowgemm(const RowGemmParams& p, const void* B, int64_t ldb, int64_t group_stride, cudaStream_t s) {
   using Cfg = GmCfg<KS, kBN>;
@@ -2553,7 +2649,19 @@ int run_rowgemm(const RowGemmParams& p, const void* B, int64_t ldb, int64_t grou
   memset(&tmA, 0, sizeof(tmA));
   RowGemmParams q = p;
   q.a_tma = 0;
-  if (p.row_src == nullptr && p.occ == nullptr && (p.lda * 2) % 16 == 0 &&
+  q.mask_tma = 0;
+  // staged contiguous rows (batched pit:m, or 2-D pit:m that goes contiguous on the device): A tiles
+  // by TMA with the dead micro-tiles zeroed in shared memory (mask mode)
+  const bool mask_ok = p.occ != nullptr && (p.row_src == nullptr || p.contig_pct > 0) && (p.lda * 2) % 16 == 0 &&
+                       (reinterpret_cast<uintptr_t>(p.A) & 15) == 0 && gm_mask_tma_enabled() && a_tma_enabled();
+  if (mask_ok) {
+    if (encode_tensor_map_2d(&tmA, dt, p.A, static_cast<uint64_t>(p.K), static_cast<uint64_t>(p.M),
+                             static_cast<uint64_t>(p.lda) * 2, KS, 128,
+                             KS * 2 >= 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                             : KS * 2 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B) != CUDA_SUCCESS)
+      return kErrCuda;
+    q.mask_tma = 1;
+  } else if (p.row_src == nullptr && p.occ == nullptr && (p.lda * 2) % 16 == 0 &&
       (reinterpret_cast<uintptr_t>(p.A) & 15) == 0 && a_tma_enabled()) {
     if (encode_tensor_map_2d(&tmA, dt, p.A, static_cast<uint64_t>(p.K), static_cast<uint64_t>(p.M),
                              static_cast<uint64_t>(p.lda) * 2, KS, 128,
@@ -2587,13 +2695,6 @@ int rg2_grouped() {  // PIT_RG2_GROUPED=0: grouped (MoE) GEMMs stay on single-CT
 }
 
 // CTA-pair launch of the dense / contiguous-row rowgemm cases (see rowgemm2_kernel).
-int gm_mask_tma_enabled() {  // PIT_GM_MASK_TMA=0: masked pit:m loads A by cp.async with zero-fill
-  static int v = [] {
-    const char* e = getenv("PIT_GM_MASK_TMA");
-    return e ? atoi(e) : 1;
-  }();
-  return v;
-}
 
 template <bool kBF16>
 int run_rowgemm2(const RowGemmParams& p, const void* B, int64_t ldb, int64_t group_stride, cudaStream_t s) {
