@@ -69,6 +69,28 @@ def test_geometry_and_validation_without_gpu(lib):
     assert lib.pit_kernel_launches() == 0
 
 
+def test_workspace_query_without_gpu(lib):
+    """pit_spmm_workspace_bytes is a host-only query: scratch only for the split gathered-K case (few
+    128-row groups, N <= 64), none for C1-style launches or the CUDA-core path."""
+    from paper_2301_10936_b200 import _lib
+
+    def args(t0, n, groups):
+        a = _lib.SpmmArgs()
+        a.plan, a.dtype = _lib.PIT_PLAN_PIT_K, _lib.PIT_BF16
+        a.M, a.N, a.K = groups * t0, n, 4096
+        a.A = a.B = a.C = 1 << 20  # aligned placeholders: never dereferenced
+        a.sam, a.sak, a.ldb, a.ldc = 1, groups * t0, n, n
+        a.t0, a.t1, a.n_groups, a.slot_stride = t0, 1, groups, 4096
+        return a
+
+    attn = args(128, 64, 384)
+    assert lib.pit_spmm_workspace_bytes(C.byref(attn)) > 0
+    assert lib.pit_spmm_workspace_bytes(C.byref(args(128, 8192, 384))) == 0
+    assert lib.pit_spmm_workspace_bytes(C.byref(args(32, 64, 384))) == 0
+    attn.force_simt = 1
+    assert lib.pit_spmm_workspace_bytes(C.byref(attn)) == 0
+
+
 def test_spmm_args_struct_matches_header():
     """Field order of the ctypes mirror equals the C struct's."""
     from paper_2301_10936_b200 import _lib
