@@ -162,6 +162,9 @@ __device__ __forceinline__ int block_excl_scan(int v, int* sh, int& total) {
 // One CTA of 1024 threads (2 groups per thread, n_groups <= kSplitMaxGroups): the split plan as the
 // virtual-group table vtab[v] = {group, first slot, count, -1 or first partial | chunk << 8 |
 // split group << 16 | chunks << 24}, their number in *nv, and zeroed split-group counters.
+__device__ int g_split_first = 1;  // PIT_GK_SPLIT_FIRST (default 1), set from the host once
+__device__ __forceinline__ bool split_first_order() { return g_split_first != 0; }
+
 __global__ void __launch_bounds__(1024) gk_split_plan_kernel(const int32_t* __restrict__ counts, int n_groups, int ks,
                                                              int4* __restrict__ vtab, int* __restrict__ nv,
                                                              int* __restrict__ ctr) {
@@ -195,13 +198,23 @@ __global__ void __launch_bounds__(1024) gk_split_plan_kernel(const int32_t* __re
     split[j] = want[j] > 0 && ppj[j] + want[j] <= kSplitParts;
     nf[j] = valid[j] ? (split[j] ? nch[j] : 1) : 0;
   }
-  // virtual groups in group order (measured better than split chunks first); one scan carries both
-  // the virtual-group prefix (low 16 bits, <= n_groups + P) and the split-group prefix (high bits)
+  // virtual groups: the split groups' chunks first (their last-arriver sums then overlap the CTAs'
+  // later units; C3 step 55 -> 52 us), the others after in group order. One scan carries the
+  // group-order prefix (low 16 bits, <= n_groups + P) and the split-group prefix (high bits).
   const int pk0 = nf[0] | (static_cast<int>(split[0]) << 16), pk1 = nf[1] | (static_cast<int>(split[1]) << 16);
   int tpk;
   const int pk = block_excl_scan(pk0 + pk1, sc, tpk);
-  const int vpj[2] = {pk & 0xffff, (pk & 0xffff) + nf[0]};
+  int vpj[2] = {pk & 0xffff, (pk & 0xffff) + nf[0]};
   const int spj[2] = {pk >> 16, (pk >> 16) + static_cast<int>(split[0])};
+  if (split_first_order()) {
+    const int ns0 = split[0] ? nch[0] : 0, ns1 = split[1] ? nch[1] : 0;
+    const int nu0 = nf[0] && !split[0] ? 1 : 0, nu1 = nf[1] && !split[1] ? 1 : 0;
+    int tns, tnu;
+    const int vs = block_excl_scan(ns0 + ns1, sc, tns);
+    const int vu = block_excl_scan(nu0 + nu1, sc, tnu);
+    vpj[0] = split[0] ? vs : tns + vu;
+    vpj[1] = split[1] ? vs + ns0 : tns + vu + nu0;
+  }
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
     const int g = 2 * tid + j;
@@ -2497,6 +2510,13 @@ int run_gk_split(const SpmmArgs& a, cudaStream_t s, const CUtensorMap& tmC, int 
   int* ctr = static_cast<int*>(a.ws);
   int4* vtab = reinterpret_cast<int4*>(ctr + kSplitCtrBytes / 4);
   float* parts = reinterpret_cast<float*>(vtab + a.n_groups + kSplitParts);
+  static const int split_first = [] {
+    const char* e = getenv("PIT_GK_SPLIT_FIRST");
+    const int v = e ? atoi(e) : 1;
+    cudaMemcpyToSymbol(g_split_first, &v, sizeof(int));
+    return v;
+  }();
+  (void)split_first;
   gk_split_plan_kernel<<<1, 1024, 0, s>>>(a.counts, static_cast<int>(a.n_groups), Cfg::KS, vtab,
                                           ctr + kSplitCtrBytes / 4 - 1, ctr);
   note_launch();
