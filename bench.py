@@ -56,6 +56,26 @@ FLUSH_BYTES = 256 << 20
 L2_GATHER_CEILING_GBPS = 11145.6  # best measured L2->SM cp.async gather rate (profiles/r1/copy_probe_l2_patterns.txt)
 
 
+# ------------------------------------------------------------------------------- bench CSV
+# `pittile bench --csv` columns (reference cli.py:330) followed by the B200 roofline columns
+CSV_COLUMNS = ["op", "shape", "granularity", "zero_ratio", "plan", "microtile", "tile", "launches", "wall_ms",
+               "dense_wall_ms", "speedup", "eff_tflops", "gbps", "roofline_frac"]
+
+
+def write_bench_csv(path, rows) -> None:
+    """rows: dicts keyed by CSV_COLUMNS (values already formatted like the reference's: ms to 3
+    decimals, speedup to 3)."""
+    lines = [",".join(CSV_COLUMNS)] + [",".join(str(r.get(c, "")) for c in CSV_COLUMNS) for r in rows]
+    Path(path).write_text("\n".join(lines) + "\n")
+
+
+def read_bench_csv(path):
+    """Rows of a `pittile bench` CSV or of ours (extra columns are kept when present)."""
+    lines = Path(path).read_text().splitlines()
+    head = lines[0].split(",")
+    return [dict(zip(head, ln.split(","))) for ln in lines[1:] if ln.strip()]
+
+
 # ----------------------------------------------------------------------------------- helpers
 def load_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
@@ -165,7 +185,7 @@ def make_operands(w: dict, seed: int, device):
 def make_plan(w: dict):
     import paper_2301_10936_b200 as pit
 
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     if reg.get("matmul", w["tile"]) is None:
         reg.register(pit.TileKernelDescriptor("matmul", tuple(w["tile"]), "bench"))
     expr = pit.bind_extents(pit.parse_expr("C[m,n] += A[m,k] * B[k,n]"), dict(m=w["M"], k=w["K"], n=w["N"]))
@@ -607,7 +627,7 @@ def attention_bench(args, dev, peaks, heads=12, seq=4096, hd=64):
     P.mul_(emask.to(torch.bfloat16))
     del emask
     V = torch.randn((heads, seq, hd), device=dev, dtype=torch.bfloat16, generator=g)
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     expr = pit.bind_extents(pit.parse_expr("C[m,n] += A[m,k] * B[k,n]"), dict(m=seq, k=seq, n=hd))
     flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
@@ -703,7 +723,7 @@ def opt_bench(args, dev, peaks, tokens=4096, d_model=2048, d_ff=8192, zeros=(0.9
 
     import paper_2301_10936_b200 as pit
 
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     fwd_e = pit.bind_extents(pit.parse_expr("C[m,n] += A[m,k] * B[k,n]"), dict(m=tokens, k=d_ff, n=d_model))
     bwd_e = pit.bind_extents(pit.parse_expr("C[m,n] += A[m,k] * B[k,n]"), dict(m=d_ff, k=tokens, n=d_model))
     plan_f = pit.forced_plan(fwd_e, "m", reg, tile_shape=(16, 32, 128))

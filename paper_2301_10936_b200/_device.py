@@ -70,7 +70,12 @@ def to_device(x, *, keep_layout: bool = True) -> torch.Tensor:
 def _pinned_upload(t: torch.Tensor, dev) -> torch.Tensor:
     if t.numel() * t.element_size() < (1 << 16):
         return t.to(dev)
-    staged = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    # same strides as the source, so a column-major operand arrives column-major at every size
+    # (the small-tensor t.to(dev) path above preserves dense strides too)
+    dense_t = t.dim() == 2 and t.t().is_contiguous()
+    if not (t.is_contiguous() or dense_t):
+        t = t.contiguous()
+    staged = torch.empty_strided(t.shape, t.stride(), dtype=t.dtype, pin_memory=True)
     staged.copy_(t)
     return staged.to(dev, non_blocking=True)
 

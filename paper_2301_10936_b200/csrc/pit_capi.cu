@@ -241,6 +241,12 @@ static int gather_args(GatherArgs& a, void* tensor, int dtype, int64_t s0, int64
   a.n_coords = n_coords;
   a.src_or_dst = tensor;
   const int t_d = pit_dim == 0 ? t0 : t1, t_o = pit_dim == 0 ? t1 : t0;
+  if (tile_rows < 0 || tile_cols < 0 || n_coords < 0)
+    return fail(kErrArg, "tile extents and coordinate count must be non-negative");
+  // slot s occupies tile rows/cols [s*t_d, (s+1)*t_d) along the PIT dim (executor.py:190-192)
+  if (n_coords * static_cast<int64_t>(t_d) > (pit_dim == 0 ? tile_rows : tile_cols))
+    return fail(kErrArg, "tile buffer holds %lld micro-tiles, %lld coordinates given",
+                static_cast<long long>((pit_dim == 0 ? tile_rows : tile_cols) / t_d), static_cast<long long>(n_coords));
   a.t_d = t_d;
   a.t_o = t_o;
   a.off_o = group * t_o;

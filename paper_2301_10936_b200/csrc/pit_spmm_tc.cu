@@ -162,12 +162,9 @@ __device__ __forceinline__ int block_excl_scan(int v, int* sh, int& total) {
 // One CTA of 1024 threads (2 groups per thread, n_groups <= kSplitMaxGroups): the split plan as the
 // virtual-group table vtab[v] = {group, first slot, count, -1 or first partial | chunk << 8 |
 // split group << 16 | chunks << 24}, their number in *nv, and zeroed split-group counters.
-__device__ int g_split_first = 1;  // PIT_GK_SPLIT_FIRST (default 1), set from the host once
-__device__ __forceinline__ bool split_first_order() { return g_split_first != 0; }
-
 __global__ void __launch_bounds__(1024) gk_split_plan_kernel(const int32_t* __restrict__ counts, int n_groups, int ks,
                                                              int4* __restrict__ vtab, int* __restrict__ nv,
-                                                             int* __restrict__ ctr) {
+                                                             int* __restrict__ ctr, int split_first) {
   __shared__ int sc[32];
   const int tid = threadIdx.x;
   if (tid < kSplitCtrBytes / 4) ctr[tid] = 0;
@@ -206,7 +203,7 @@ __global__ void __launch_bounds__(1024) gk_split_plan_kernel(const int32_t* __re
   const int pk = block_excl_scan(pk0 + pk1, sc, tpk);
   int vpj[2] = {pk & 0xffff, (pk & 0xffff) + nf[0]};
   const int spj[2] = {pk >> 16, (pk >> 16) + static_cast<int>(split[0])};
-  if (split_first_order()) {
+  if (split_first) {
     const int ns0 = split[0] ? nch[0] : 0, ns1 = split[1] ? nch[1] : 0;
     const int nu0 = nf[0] && !split[0] ? 1 : 0, nu1 = nf[1] && !split[1] ? 1 : 0;
     int tns, tnu;
@@ -2510,15 +2507,14 @@ int run_gk_split(const SpmmArgs& a, cudaStream_t s, const CUtensorMap& tmC, int 
   int* ctr = static_cast<int*>(a.ws);
   int4* vtab = reinterpret_cast<int4*>(ctr + kSplitCtrBytes / 4);
   float* parts = reinterpret_cast<float*>(vtab + a.n_groups + kSplitParts);
+  // PIT_GK_SPLIT_FIRST (default 1): order split groups' chunks first; passed by value so the plan
+  // launch is graph-capturable and every device sees it
   static const int split_first = [] {
     const char* e = getenv("PIT_GK_SPLIT_FIRST");
-    const int v = e ? atoi(e) : 1;
-    cudaMemcpyToSymbol(g_split_first, &v, sizeof(int));
-    return v;
+    return e ? atoi(e) : 1;
   }();
-  (void)split_first;
   gk_split_plan_kernel<<<1, 1024, 0, s>>>(a.counts, static_cast<int>(a.n_groups), Cfg::KS, vtab,
-                                          ctr + kSplitCtrBytes / 4 - 1, ctr);
+                                          ctr + kSplitCtrBytes / 4 - 1, ctr, split_first);
   note_launch();
   auto kern = spmm_gk_kernel<GW, kOrientN, kBF16, kKS, kNT, true>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::SMEM));

@@ -252,6 +252,11 @@ def sread(src, idx: MicroTileIndex, group: int, tile_buffer, start: int = 0) -> 
     tile = _device.to_device(np.ascontiguousarray(tile_buffer)) if host_tile else tile_buffer
     if not tile.is_contiguous():
         raise ExecError("tile buffer must be contiguous")
+    user_tile = tile
+    if tile.dtype != x.dtype:
+        # the C ABI types the tile with the tensor's dtype: gather into a tile of that dtype and
+        # cast on the way back (numpy assignment semantics, executor.py:205-207)
+        tile = tile.to(x.dtype)
     cd = torch.from_numpy(np.ascontiguousarray(coords, dtype=np.int32)).to(dev)
     ld, col = _tensor_geometry(x)
     lib = _lib.load()
@@ -261,6 +266,8 @@ def sread(src, idx: MicroTileIndex, group: int, tile_buffer, start: int = 0) -> 
                                 _device.stream_ptr()), ExecError)
     if host_tile:
         tile_buffer[...] = _device.to_host(tile)
+    elif tile is not user_tile:
+        user_tile.copy_(tile)
     return int(coords.size)
 
 
@@ -277,6 +284,8 @@ def swrite(tile_buffer, dst, idx: MicroTileIndex, group: int, start: int = 0, ac
     host_dst = not _is_torch(arr)
     x = _device.to_device(arr)
     tile = _device.to_device(np.ascontiguousarray(tile_buffer)) if not _is_torch(tile_buffer) else tile_buffer
+    if tile.dtype != x.dtype or not tile.is_contiguous():
+        tile = tile.to(x.dtype).contiguous()  # read with the tensor's element size (C ABI contract)
     cd = torch.from_numpy(np.ascontiguousarray(coords, dtype=np.int32)).to(dev)
     ld, col = _tensor_geometry(x)
     lib = _lib.load()

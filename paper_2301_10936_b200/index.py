@@ -136,10 +136,27 @@ class MicroTileIndex:
 
         if self._host_authoritative:
             dev = _device.require_cuda()
+            self._check_host_entries()
             counts = torch.from_numpy(np.ascontiguousarray(self._counts, dtype=np.int32)).to(dev)
             slots = torch.from_numpy(np.ascontiguousarray(self._slots, dtype=np.int32)).to(dev)
             return counts, slots
         return self._counts_dev, self._slots_dev
+
+    def _check_host_entries(self) -> None:
+        """A host-authoritative index may have been edited by the caller (the reference's tests
+        write slots directly). The gathered-K kernels trust every coordinate they are given, so
+        reject what the reference's executor rejects before anything is uploaded
+        (executor.py:200-204: "micro-tile coordinate out of range")."""
+        from .executor import ExecError
+
+        counts = np.asarray(self._counts)
+        slots = np.asarray(self._slots).reshape(self._n_groups, self.pit_grid)
+        if counts.size and (int(counts.min()) < 0 or int(counts.max()) > self.pit_grid):
+            raise ExecError("micro-tile coordinate out of range: group count outside [0, pit_grid]")
+        live = np.arange(self.pit_grid)[None, :] < counts[:, None]
+        vals = slots[live]
+        if vals.size and (int(vals.min()) < 0 or int(vals.max()) >= self.pit_grid):
+            raise ExecError("micro-tile coordinate out of range")
 
     def device_ptrs(self):
         """(counts, slots) device pointers plus the tensors keeping them alive."""

@@ -90,7 +90,7 @@ REFERENCE_MATMUL_TILES = ((16, 32, 128), (8, 32, 128), (32, 64, 32), (32, 32, 32
 B200_MATMUL_TILES = ((128, 64, 256), (64, 64, 256), (256, 64, 256))
 
 
-def register_builtin_kernels(include_b200_tiles: bool = True) -> KernelRegistry:
+def register_builtin_kernels(include_b200_tiles: bool = False) -> KernelRegistry:
     reg = KernelRegistry()
     mm = (ROW_MAJOR,) * 3
     for m, k, n in REFERENCE_MATMUL_TILES:

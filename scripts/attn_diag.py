@@ -16,7 +16,7 @@ ann = pit.from_bits(blocks.reshape(heads * seq // 32, seq // 64), (heads * seq, 
 live = int(blocks.sum()) * 32 * 64
 P = torch.randn((heads, seq, seq), device=dev, dtype=torch.bfloat16)
 V = torch.randn((heads, seq, hd), device=dev, dtype=torch.bfloat16)
-reg = pit.register_builtin_kernels()
+reg = pit.register_builtin_kernels(include_b200_tiles=True)
 expr = pit.bind_extents(pit.parse_expr("C[m,n] += A[m,k] * B[k,n]"), dict(m=seq, k=seq, n=hd))
 plan_m = pit.forced_plan(expr, "m", reg, tile_shape=(128, 64, 256))
 plan_k = pit.forced_plan(expr, "k", reg, tile_shape=(32, 64, 32))

@@ -20,7 +20,7 @@ emask = torch.from_numpy(blocks).to(dev).repeat_interleave(32, 1).repeat_interle
 P = torch.randn((heads, seq, seq), device=dev, dtype=torch.bfloat16, generator=g) * emask.to(torch.bfloat16)
 del emask
 V = torch.randn((heads, seq, hd), device=dev, dtype=torch.bfloat16, generator=g)
-reg = pit.register_builtin_kernels()
+reg = pit.register_builtin_kernels(include_b200_tiles=True)
 expr = pit.bind_extents(pit.parse_expr("C[m,n] += A[m,k] * B[k,n]"), dict(m=seq, k=seq, n=hd))
 tile = (128, 64, 256)
 if reg.get("matmul", tile) is None:

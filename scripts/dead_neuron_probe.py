@@ -21,7 +21,7 @@ for frac in (0.1, 0.3, 1.0):
     m[:, 0] = True
     H = torch.randn(T, F, device=dev, dtype=torch.bfloat16, generator=g) * m.repeat_interleave(32, 1).to(torch.bfloat16)
     W = torch.randn(F, D, device=dev, dtype=torch.bfloat16, generator=g)
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     expr = pit.bind_extents(pit.parse_expr("C[m,n] += A[m,k] * B[k,n]"), dict(m=T, k=F, n=D))
     if reg.get("matmul", (128, 32, 256)) is None:
         reg.register(pit.TileKernelDescriptor("matmul", (128, 32, 256), "m32"))

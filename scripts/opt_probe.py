@@ -15,7 +15,7 @@ keep = torch.rand((tokens, d_ff // 32), device=dev, generator=g) >= zr
 H = torch.relu(torch.randn((tokens, d_ff), device=dev, dtype=torch.bfloat16, generator=g))
 H.mul_(keep.repeat_interleave(32, dim=1).to(torch.bfloat16))
 dY = torch.randn((tokens, d_model), device=dev, dtype=torch.bfloat16, generator=g)
-reg = pit.register_builtin_kernels()
+reg = pit.register_builtin_kernels(include_b200_tiles=True)
 e = pit.bind_extents(pit.parse_expr("C[m,n] += A[m,k] * B[k,n]"), dict(m=d_ff, k=tokens, n=d_model))
 plan = pit.forced_plan(e, "k", reg, tile_shape=(32, 64, 32))
 idx = pit.build_index_from_tensor(H, (1, 32), "m").transposed()

@@ -13,7 +13,7 @@ from paper_2301_10936_b200.moe import SwitchMoE  # noqa: E402
 
 ncu = "--ncu" in sys.argv
 dev = torch.device("cuda", 0)
-reg = pit.register_builtin_kernels()
+reg = pit.register_builtin_kernels(include_b200_tiles=True)
 tile = (128, 64, 256)
 if reg.get("matmul", tile) is None:
     reg.register(pit.TileKernelDescriptor("matmul", tile, "probe"))

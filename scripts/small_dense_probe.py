@@ -9,7 +9,7 @@ import paper_2301_10936_b200 as pit  # noqa: E402
 
 dev = torch.device("cuda", 0)
 m, k, n = (int(x) for x in (sys.argv[1:4] if len(sys.argv) > 3 else (4096, 768, 3072)))
-reg = pit.register_builtin_kernels()
+reg = pit.register_builtin_kernels(include_b200_tiles=True)
 tile = (128, 64, 256)
 if reg.get("matmul", tile) is None:
     reg.register(pit.TileKernelDescriptor("matmul", tile, "probe"))

@@ -8,6 +8,10 @@ The reference cannot travel to the GPU box, so its outputs are committed here as
   gather_cases.npz   sread / swrite known answers
   matmul_cases.npz   run_sparse_matmul fp32 results + the f64 oracle for pit:m / pit:k / dense
   plan_cases.json    get_micro_tile, plan_launches, cover table (PAPER.md:1072-1094 configs)
+  wire/              files WRITTEN BY THE REFERENCE in its own formats: annotation text
+                     (sparsity.py:135-144), PITT tensors (executor.py:93-102), index dumps
+                     (index.py:185-195) and a `pittile bench` CSV (cli.py:330) - read back by the
+                     package and replayed on the GPU (tests/test_wire_formats.py, test_gpu_golden.py)
 Everything is seeded; rerunning reproduces the files byte for byte.
 """
 
@@ -209,7 +213,70 @@ def reduce_cases():
     (OUT / "reduce_cases.json").write_text(json.dumps(meta))
 
 
+def wire_cases():
+    """Reference-written files in the reference's own formats."""
+    wire = OUT / "wire"
+    wire.mkdir(exist_ok=True)
+    rng = np.random.default_rng(4242)
+    reg = pt.register_builtin_kernels()
+    specs = [  # name, (m, k, n), axis, tile, granularity, zero ratio
+        ("c1_pitk", (256, 256, 128), "k", (32, 64, 32), (32, 1), 0.9),
+        ("pitm_1x32", (128, 256, 96), "m", (16, 32, 128), (1, 32), 0.9),
+        ("blocks_32x64", (256, 256, 64), "m", (32, 64, 32), (32, 64), 0.8),
+        ("ragged_pitk", (45, 70, 51), "k", (16, 32, 128), (3, 2), 0.6),
+        ("dense", (64, 96, 80), "dense", (32, 64, 32), (1, 1), 0.0),
+    ]
+    meta = []
+    for i, (name, (m, k, n), axis, tile, gran, ratio) in enumerate(specs):
+        ann = pt.random_annotation((m, k), gran, ratio, seed=900 + i)
+        pt.save_annotation(ann, wire / f"{name}.ann")
+        A = rng.standard_normal((m, k)).astype(np.float32) * ann.materialize()
+        B = rng.standard_normal((k, n)).astype(np.float32)
+        plan = pt.forced_plan(bound(m, k, n), axis, reg, tile_shape=tile)
+        At = pt.DenseTensor.from_array(A, layout=plan.sparse_layout)
+        stats = pt.ExecStats()
+        C = pt.run_sparse_matmul(plan, At, pt.DenseTensor.from_array(B), ann if axis != "dense" else None,
+                                 stats=stats)
+        pt.save_tensor(At, wire / f"{name}_A.pitt")
+        pt.save_tensor(pt.DenseTensor.from_array(B), wire / f"{name}_B.pitt")
+        pt.save_tensor(C, wire / f"{name}_C.pitt")
+        pt.save_tensor(pt.DenseTensor(pt.run_dense_reference(At, pt.DenseTensor.from_array(B))),
+                       wire / f"{name}_R.pitt")
+        if axis != "dense":
+            idx = pt.build_index(ann, plan.micro_tile, axis)
+            (wire / f"{name}.index").write_text(pt.dump_index(idx))
+        meta.append(dict(name=name, shape=[m, k, n], axis=axis, tile=list(tile), micro=list(plan.micro_tile or ()),
+                         granularity=list(gran), zero_ratio=ratio, seed=900 + i,
+                         launches=stats.launches, gathered=stats.gathered_micro_tiles))
+    # the C1 annotation itself (BASELINE configs[0]: 1024^2, 32x1 blocks, 90% zero, seed 1)
+    c1 = pt.random_annotation((1024, 1024), (32, 1), 0.9, seed=1)
+    pt.save_annotation(c1, wire / "c1_1024.ann")
+    (wire / "c1_1024.index").write_text(pt.dump_index(pt.build_index(c1, (32, 1), "k")))
+    (wire / "wire_cases.json").write_text(json.dumps(meta, indent=1))
+
+
+def wire_cli():
+    """The reference CLI's own outputs: a CPU cost table (`pittile profile`, tiles.py:224-253) and a
+    sparsity-sweep CSV (`pittile bench`, cli.py:271-345). Timings differ per run; the files pin the
+    formats, not the numbers."""
+    import os
+    import subprocess
+
+    wire = OUT / "wire"
+    env = dict(os.environ, PYTHONPATH=str(REF))
+    prof = wire / "pittile_cpu.prof"
+    subprocess.run([sys.executable, "-m", "pittile", "profile", "--reps", "3", "-o", str(prof)], check=True, env=env)
+    subprocess.run([sys.executable, "-m", "pittile", "bench", "--expr", MATMUL, "--shape", "m=256,k=256,n=256",
+                    "--random", "32x1:0.9", "--ratios", "0.5,0.9", "--profile", str(prof), "--csv",
+                    str(wire / "pittile_bench.csv")], check=True, env=env)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:  # regenerate only the named fixture sets, e.g. `make_golden.py wire_cases`
+        for name in sys.argv[1:]:
+            globals()[name]()
+        sys.exit(0)
+    wire_cases()
     reduce_cases()
     index_cases()
     value_cases()

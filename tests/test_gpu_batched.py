@@ -37,7 +37,7 @@ def test_batched_pit_k_bf16_matches_per_slice_oracle(t0, n):
 
     pit = _pit()
     batch, m, k = 3, 256, 384
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     plan = pit.forced_plan(_bound(m, k, n), "k", reg, tile_shape=_tile_for(reg, t0))
     anns = [pit.random_annotation((m, k), (t0, 1), 0.85, seed=10 * t0 + b) for b in range(batch)]
     rng = np.random.default_rng(t0 + n)
@@ -60,7 +60,8 @@ def test_batched_pit_k_bf16_matches_per_slice_oracle(t0, n):
     # one detection pass over the stacked operand gives the same stacked index
     idx = pit.build_batched_index_from_tensor(A3, plan.micro_tile, "k")
     ref_idx = pit.build_batched_index(anns, plan.micro_tile, "k")
-    assert pit.dump_index(idx) == pit.dump_index(ref_idx) or idx.total <= ref_idx.total
+    # standard-normal values inside live blocks are never exactly 0: the dumps must be equal
+    assert pit.dump_index(idx) == pit.dump_index(ref_idx)
 
 
 def test_batched_fp32_and_dense_slices():
@@ -68,7 +69,7 @@ def test_batched_fp32_and_dense_slices():
 
     pit = _pit()
     batch, m, k, n = 2, 64, 96, 40
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     rng = np.random.default_rng(5)
     anns = [pit.random_annotation((m, k), (32, 1), 0.7, seed=b) for b in range(batch)]
     A = np.stack([rng.standard_normal((m, k)).astype(np.float32) * a.materialize() for a in anns])
@@ -87,7 +88,7 @@ def test_batched_layout_is_never_converted_silently():
     import torch
 
     pit = _pit()
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     plan = pit.forced_plan(_bound(64, 64, 64), "k", reg, tile_shape=(32, 64, 32))
     A3 = torch.zeros((2, 64, 64), device="cuda")  # row-major slices, not stacked col-major
     with pytest.raises(pit.LayoutError, match="stack_slices"):
@@ -102,7 +103,7 @@ def test_narrow_n_units(t0, n):
 
     pit = _pit()
     m, k = 512, 1024
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     plan = pit.forced_plan(_bound(m, k, n), "k", reg, tile_shape=_tile_for(reg, t0))
     ann = pit.random_annotation((m, k), (t0, 1), 0.9, seed=t0 + n)
     rng = np.random.default_rng(n)
@@ -125,7 +126,7 @@ def test_batched_pit_m_bf16_matches_per_slice_oracle(t1, n):
 
     pit = _pit()
     batch, m, k = 3, 320, 256
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     tile = (16, t1, 128)
     if reg.get("matmul", tile) is None:
         reg.register(pit.TileKernelDescriptor("matmul", tile, f"m{t1}"))
@@ -160,7 +161,7 @@ def test_pit_m_narrow_n_two_d():
 
     pit = _pit()
     m, k, n = 1000, 512, 48
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     plan = pit.forced_plan(_bound(m, k, n), "m", reg, tile_shape=(16, 32, 128))
     ann = pit.random_annotation((m, k), (1, 32), 0.9, seed=2)
     rng = np.random.default_rng(2)
@@ -182,7 +183,7 @@ def test_batched_dense_bf16_cta_pairs(m, n):
 
     pit = _pit()
     batch, k = 3, 192
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     tile = (128, 64, 256)
     if reg.get("matmul", tile) is None:
         reg.register(pit.TileKernelDescriptor("matmul", tile, "d128"))
@@ -205,7 +206,7 @@ def test_split_long_groups_narrow_n(batch, m, n):
 
     pit = _pit()
     k, t0 = 4096, 128
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     plan = pit.forced_plan(_bound(m, k, n), "k", reg, tile_shape=_tile_for(reg, t0))
     rng = np.random.default_rng(m + n)
     mask = np.repeat(rng.random((batch, -(-m // t0), k)) >= 0.9, t0, axis=1)[:, :m]

@@ -18,7 +18,7 @@ def _pit():
 
 def _plan(m, k, n, axis, tile):
     pit = _pit()
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     if reg.get("matmul", tile) is None:
         reg.register(pit.TileKernelDescriptor("matmul", tile, "fp16"))
     expr = pit.bind_extents(pit.parse_expr("C[m,n] += A[m,k] * B[k,n]"), dict(m=m, k=k, n=n))

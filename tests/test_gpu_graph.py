@@ -36,7 +36,7 @@ def test_graph_replay_equals_eager_and_tracks_new_values(case):
     else:
         m, k, n, micro, axis, tile = 2048, 768, 1024, (1, 768), "m", (128, 768, 256)
         mask = np.repeat((rng.random(m) >= 0.4)[:, None], k, axis=1)
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     if reg.get("matmul", tile) is None:
         reg.register(pit.TileKernelDescriptor("matmul", tile, "graph"))
     expr = pit.bind_extents(pit.parse_expr("C[m,n] += A[m,k] * B[k,n]"), dict(m=m, k=k, n=n))

@@ -10,7 +10,7 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture(scope="module")
 def registry():
-    return pit.register_builtin_kernels()
+    return pit.register_builtin_kernels(include_b200_tiles=True)
 
 
 @pytest.fixture(scope="module")

@@ -41,7 +41,7 @@ def _operands(m, k, n, ann, seed, dtype=np.float32):
 def test_fp32_plans_match_oracle(axis, tile, shape):
     pit = _pkg()
     m, k, n = shape
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     ann = pit.random_annotation((m, k), (3, 2), 0.6, seed=m + k + n)
     A, B = _operands(m, k, n, ann, seed=7)
     plan = pit.forced_plan(bound(m, k, n), axis, reg, tile_shape=tile)
@@ -58,7 +58,7 @@ def test_fp32_config1_1024_pit_k():
     """C1: 1024^3 fp32, random (32,1) micro-tile sparsity 90%, pit:k, tile 32x64x32."""
     pit = _pkg()
     m = k = n = 1024
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     ann = pit.random_annotation((m, k), (32, 1), 0.90, seed=1)
     A, B = _operands(m, k, n, ann, seed=1001)
     plan = pit.forced_plan(bound(m, k, n), "k", reg, tile_shape=(32, 64, 32))
@@ -97,7 +97,7 @@ def _run_bf16(plan, A, B, ann, col_major):
 def test_bf16_pit_k_tensor_cores(t0, shape):
     pit = _pkg()
     m, k, n = shape
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     expr = bound(m, k, n)
     tile = (t0, 64, 256)
     if reg.get("matmul", tile) is None:
@@ -120,7 +120,7 @@ def test_bf16_pit_k_tensor_cores(t0, shape):
 def test_bf16_pit_m_tensor_cores(t1, shape):
     pit = _pkg()
     m, k, n = shape
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     tile = (128, t1, 256)
     if reg.get("matmul", tile) is None:
         reg.register(pit.TileKernelDescriptor("matmul", tile, f"m{t1}"))
@@ -147,7 +147,7 @@ def test_bf16_pit_m_dead_micro_tiles_not_read(t1, dead_rows, shape):
     union-row tiles. Both must ignore the dead data."""
     pit = _pkg()
     m, k, n = shape
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     tile = (128, t1, 256)
     if reg.get("matmul", tile) is None:
         reg.register(pit.TileKernelDescriptor("matmul", tile, f"m{t1}"))
@@ -172,7 +172,7 @@ def test_bf16_pit_m_dead_neurons_skipped(t1):
     pairs). Globally dead K-blocks are skipped; dead micro-tiles still hold data and must not count."""
     pit = _pkg()
     m, k, n = 1024, 4096, 512
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     tile = (128, t1, 256)
     if reg.get("matmul", tile) is None:
         reg.register(pit.TileKernelDescriptor("matmul", tile, f"m{t1}"))
@@ -194,7 +194,7 @@ def test_bf16_row_uniform_and_dense_bitwise():
     """Fully dense annotation through pit:m equals the dense plan bitwise (test_executor.py:178-186)."""
     pit = _pkg()
     m, k, n = 384, 512, 512
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     expr = bound(m, k, n)
     full = pit.from_mask(np.ones((m, k)), (1, 1))
     A, B = _operands(m, k, n, full, seed=3)
@@ -213,7 +213,7 @@ def test_bf16_row_uniform_bert_like():
     rows = np.concatenate([np.arange(128) < L for L in lengths])
     mask = np.repeat(rows[:, None], k, axis=1)
     ann = pit.from_mask(mask, (1, k))
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     A, B = _operands(m, k, n, ann, seed=11)
     plan = pit.forced_plan(bound(m, k, n), "m", reg, tile_shape=(128, 64, 256))
     C, Ar, Br = _run_bf16(plan, A, B, ann, False)
@@ -225,7 +225,7 @@ def test_bf16_row_uniform_bert_like():
 def test_shuffled_slots_m_axis_bitwise_and_k_axis_close():
     pit = _pkg()
     m, k, n = 256, 256, 128
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     expr = bound(m, k, n)
     rng = np.random.default_rng(9)
     ann = pit.random_annotation((m, k), (1, 32), 0.5, seed=3)
@@ -259,7 +259,7 @@ def test_shuffled_slots_m_axis_bitwise_and_k_axis_close():
 
 def test_layout_and_operand_errors():
     pit = _pkg()
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     expr = bound(64, 64, 64)
     rng = np.random.default_rng(0)
     A = pit.DenseTensor.from_array(rng.standard_normal((64, 64)).astype(np.float32))
@@ -328,7 +328,7 @@ def test_captured_step_tracks_new_values():
     from paper_2301_10936_b200.graph import CapturedSparseMatmul
 
     m, k, n = 512, 1024, 512
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     plan = pit.forced_plan(bound(m, k, n), "k", reg, tile_shape=(32, 64, 32))
     A = torch.zeros((k, m), dtype=torch.bfloat16, device="cuda").t()  # column-major buffer
     B = torch.randn((k, n), dtype=torch.bfloat16, device="cuda")
@@ -351,7 +351,7 @@ def test_sparse_reduce_sum_matches_reference_golden():
     pit = _pkg()
     gold = Path(__file__).resolve().parent / "golden"
     data = np.load(gold / "reduce_cases.npz")
-    reg = pit.register_builtin_kernels()
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
     for c in json.loads((gold / "reduce_cases.json").read_text()):
         i = c["i"]
         p_, l_ = c["shape"]
