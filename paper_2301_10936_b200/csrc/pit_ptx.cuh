@@ -130,6 +130,23 @@ __device__ __forceinline__ void cp_async_16(uint32_t dst_smem, const void* src, 
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst_smem), "l"(src), "r"(src_bytes) : "memory");
 }
 
+// Full 16-byte copy, or 16 zero bytes when `ignore` (the ignore-src form: one predicate on the
+// LDGSTS instead of the src-size form's per-copy size arithmetic folded into the address).
+__device__ __forceinline__ void cp_async_16_ign(uint32_t dst_smem, const void* src, bool ignore) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
+      "cp.async.cg.shared.global [%0], [%1], 16, p;\n\t}" ::"r"(dst_smem),
+      "l"(src), "r"(static_cast<uint32_t>(ignore))
+      : "memory");
+}
+
+// base + k * pitch_bytes as one IMAD.WIDE.U32 (row address of a gathered row)
+__device__ __forceinline__ const void* row_addr(const void* base, uint32_t k, uint32_t pitch_bytes) {
+  uint64_t r;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(k), "r"(pitch_bytes), "l"(reinterpret_cast<uint64_t>(base)));
+  return reinterpret_cast<const void*>(r);
+}
+
 // Arrive on `bar` once all of this thread's prior cp.async copies have landed (no pending-count bump:
 // the barrier's expected count must include this arrival).
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {

@@ -420,6 +420,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const T* Ap = static_cast<const T*>(Atv);
     const uint32_t ldb32 = static_cast<uint32_t>(ldb);  // host guarantees K * pitch < 2^32 elements
     const uint32_t lda32 = static_cast<uint32_t>(lda);
+    const bool aligned8 = (N & 7) == 0 && (M & 7) == 0 && (grp_rows & 7) == 0;
+    const uint32_t ldb_bytes = ldb32 * static_cast<uint32_t>(sizeof(T));  // K * pitch * 2 < 2^32 (host check)
+    const uint32_t lda_bytes = lda32 * static_cast<uint32_t>(sizeof(T));
     // B: B_RPI rows per warp instruction (1 at N_TILE 256, 2 at 128, 4 at 64), lane -> (row sub, chunk)
     constexpr int B_RPI = Cfg::B_CPR >= 32 ? 1 : 32 / Cfg::B_CPR;
     constexpr int B_IPR = Cfg::B_CPR >= 32 ? Cfg::B_CPR / 32 : 1;  // instructions per row
@@ -436,7 +439,62 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m_end = min(M, m0 + grp_rows);
       mbar_wait(&empty_bar[stage], phase ^ 1);
       const int r0 = RW * warp;
-      if (r0 < kpad) {  // a warp's RW rows are all below kpad or all above it
+      if (r0 < kpad && aligned8) {
+        // 16-byte chunks are whole or absent (N, M, group rows multiples of 8): ignore-src copies,
+        // one predicate per copy — per B row one address multiply-add and the LDGSTS
+        const uint32_t sB = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+        const uint32_t sA = sB + Cfg::B_BYTES;
+        const bool all_rows = r0 + RW <= kvalid;  // every row of the warp live (all but a unit's last stage)
+#pragma unroll
+        for (int cb = 0; cb < B_IPR; ++cb) {
+          const int ch = cb * 32 + (B_RPI > 1 ? lane % Cfg::B_CPR : lane);
+          const int n = n0 + ch * 8;
+          const bool n_ok = n < N;
+          const T* bcol = Bp + p.b * b_batch_stride + (n_ok ? n : 0);
+          const uint32_t cbase = sB + (ch >> 3) * (Cfg::KS * 128) + r0 * 128;
+          if (B_RPI == 1 && all_rows) {
+            // row 8a + r lands at cbase + 1024 a + t[r]: eight per-lane swizzled offsets, the rest
+            // in the LDGSTS immediate; the source is one IMAD.WIDE per row
+            uint32_t t[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+              t[r] = cbase + r * 128 + ((static_cast<uint32_t>(ch & 7) ^ static_cast<uint32_t>(r)) << 4);
+#pragma unroll
+            for (int i = 0; i < RW; ++i)
+              cp_async_16_ign(t[i & 7] + (i >> 3) * 1024, row_addr(bcol, static_cast<uint32_t>(x.v[i]), ldb_bytes),
+                              !n_ok);
+            continue;
+          }
+#pragma unroll
+          for (int i = 0; i < RW; i += B_RPI) {
+            int kk = x.v[i];
+#pragma unroll
+            for (int r = 1; r < B_RPI; ++r) kk = b_sub == r ? x.v[i + r] : kk;
+            const int row = i + b_sub;
+            const bool ok = r0 + row < kvalid;
+            cp_async_16_ign(cbase + row * 128 + ((static_cast<uint32_t>(ch & 7) ^ static_cast<uint32_t>(row & 7)) << 4),
+                            row_addr(bcol, static_cast<uint32_t>(ok ? kk : 0), ldb_bytes), !(ok && n_ok));
+          }
+        }
+        {
+          const int m = m0 + a_ch * 8;
+          const bool m_ok = m < m_end;
+          const T* acol = Ap + (m_ok ? m : 0);
+#pragma unroll
+          for (int j = 0; j < RW; j += Cfg::A_RPW) {
+            int kk = x.v[j];
+#pragma unroll
+            for (int r = 1; r < Cfg::A_RPW; ++r)
+              if (j + r < RW) kk = a_sub == r ? x.v[j + r] : kk;
+            if (Cfg::A_RPW > RW && a_sub >= RW) continue;
+            const int row = r0 + j + a_sub;
+            const bool ok = row < kvalid;
+            const uint32_t o = static_cast<uint32_t>(row * Cfg::A_ROW_BYTES + (a_ch % Cfg::A_CPA) * 16);
+            cp_async_16_ign(sA + a_base + swz<Cfg::A_MASK>(o), row_addr(acol, static_cast<uint32_t>(ok ? kk : 0), lda_bytes),
+                            !(ok && m_ok));
+          }
+        }
+      } else if (r0 < kpad) {  // a warp's RW rows are all below kpad or all above it
         const uint32_t sB = smem_u32(smem + stage * Cfg::STAGE_BYTES);
         const uint32_t sA = sB + Cfg::B_BYTES;
         // ---- B rows
@@ -3026,7 +3084,7 @@ bool spmm_tc_supported(const SpmmArgs& a) {
   if ((a.ldb * 2) % 16) return false;
   if (a.plan == kPlanPitK) {
     if (a.sam != 1 || (a.sak * 2) % 16) return false;  // A column-major
-    if (a.K * a.ldb >= (1ll << 32) || a.K * a.sak >= (1ll << 32)) return false;  // 32-bit element offsets
+    if (a.K * a.ldb >= (1ll << 31) || a.K * a.sak >= (1ll << 31)) return false;  // 32-bit byte offsets (2-byte elements)
     return a.t0 % 8 == 0 && a.t0 <= 256;  // narrower groups run in the next wider kernel
   }
   if (a.sak != 1 || (a.sam * 2) % 16) return false;  // A row-major
