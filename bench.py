@@ -323,6 +323,8 @@ def run_ours(args, w):
         gw = micro[0]
         pair = gw > 128 and w["N"] > 128 and os.environ.get("PIT_GK2", "1") != "0"  # spmm_gk2 (CTA pairs)
         n_tile = 256 if (gw < 256 or pair) else 128
+        if gw <= 32 and w["N"] >= 1024 and os.environ.get("PIT_GK_NT") not in ("128", "256"):
+            n_tile = 512  # 16/32-row groups over wide N: 512-column units (csrc dispatch_tc)
         gathered = idx0.total * (-(-w["N"] // n_tile)) * (n_tile + gw) * 2
         feed = gathered / (spmm_avg * 1e-3) / 1e9
         operand_feed = {"bytes_per_launch": gathered, "achieved_GBps": round(feed, 1),

@@ -69,6 +69,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         objs.append(obj)
         if force or _stale(obj, [src] + headers):
             extra = ["-DPIT_DIAG=1"] if os.environ.get("PIT_DIAG") == "1" else []  # diagnostic builds only
+            extra += os.environ.get("PIT_NVCC_DEFS", "").split()  # A/B builds (scripts/build_alt.sh) only
             cmd = [cc, *ARCH, *NVCC_FLAGS, *extra, f"-I{INCLUDE}", f"-I{CSRC}", "-c", str(src), "-o", str(obj)]
             jobs.append((src, cmd))
 

@@ -140,6 +140,11 @@ __device__ __forceinline__ void cp_async_16_ign(uint32_t dst_smem, const void* s
       : "memory");
 }
 
+// L2 prefetch of a contiguous range (bulk engine; no shared memory, no completion tracking)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(src)), "r"(bytes) : "memory");
+}
+
 // base + k * pitch_bytes as one IMAD.WIDE.U32 (row address of a gathered row)
 __device__ __forceinline__ const void* row_addr(const void* base, uint32_t k, uint32_t pitch_bytes) {
   uint64_t r;

@@ -240,8 +240,16 @@ struct GkCfg {
   // warp (epi_box_tma); orientation T (GW <= 64), one [GW rows x 32 columns] box per warp
   static constexpr int STG_T = GW <= 64 ? GW * 64 : 0;
   static constexpr int STG_BYTES = kOrientN ? 4 * 2 * 4096 : 4 * STG_T;
-  static constexpr int STAGE_BUDGET = 232448 - 2048 - STG_BYTES;  // 227 KB opt-in minus barriers/align
-  static constexpr int STAGES = STAGE_BUDGET / STAGE_BYTES > 16 ? 16 : STAGE_BUDGET / STAGE_BYTES;
+  // 227 KB opt-in minus 1 KB alignment slack, the TMEM barriers / slot, the staging; every stage also
+  // carries 8 full + 8 empty barriers (one pair per producer warp)
+  // producer warps are split into BAR_GROUPS groups with their own full / empty barrier per stage
+  // (the MMA starts on a group's rows once they land and releases each group's slot separately)
+#ifndef PIT_GK_BG
+#define PIT_GK_BG 1
+#endif
+  static constexpr int BAR_GROUPS = (KS / PIT_GK_BG) % 16 == 0 ? PIT_GK_BG : 1;
+  static constexpr int STAGE_BUDGET = 232448 - 1024 - 256 - STG_BYTES;
+  static constexpr int STAGES = STAGE_BUDGET / (STAGE_BYTES + 128) > 16 ? 16 : STAGE_BUDGET / (STAGE_BYTES + 128);
   static constexpr int ACC_COLS = kOrientN ? N_TILE : (N_TILE / 128) * GW;  // TMEM columns per buffer
   // accumulator ring: as many units in flight as TMEM holds (<= 8), so short units (few live k per
   // group) overlap their load, MMA and epilogue across units instead of serialising on 2 buffers
@@ -250,7 +258,7 @@ struct GkCfg {
 #endif
   static constexpr int NBUF = (512 / ACC_COLS) > PIT_GK_NBUF_MAX ? PIT_GK_NBUF_MAX : (512 / ACC_COLS);
   static constexpr int TMEM_COLS = tmem_cols_pow2<NBUF * ACC_COLS>();
-  static constexpr size_t SMEM = static_cast<size_t>(STAGES) * STAGE_BYTES + STG_BYTES + 2048;
+  static constexpr size_t SMEM = static_cast<size_t>(STAGES) * (STAGE_BYTES + 128) + STG_BYTES + 1024 + 256;
   static_assert(SMEM <= 232448, "shared memory over the sm_100 opt-in limit");
   static constexpr uint32_t A_SW = sw_layout_for_row(A_ROW_BYTES);
   static constexpr uint32_t A_MASK = A_ROW_BYTES == 128 ? 7 : A_ROW_BYTES == 64 ? 3 : A_ROW_BYTES == 32 ? 1 : 0;
@@ -276,9 +284,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stg = smem + Cfg::STAGES * Cfg::STAGE_BYTES;  // epilogue staging (orientation N)
+  // per (stage, producer-warp group) full / empty barriers: the MMA starts on a group's rows as soon
+  // as they land and hands each group its slot back as soon as the MMAs reading it complete
+  constexpr int BG = Cfg::BAR_GROUPS, WPG = kProdWarps / BG;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(stg + Cfg::STG_BYTES);
-  uint64_t* empty_bar = full_bar + Cfg::STAGES;
-  uint64_t* tfull_bar = empty_bar + Cfg::STAGES;
+  uint64_t* empty_bar = full_bar + Cfg::STAGES * kProdWarps;
+  uint64_t* tfull_bar = empty_bar + Cfg::STAGES * kProdWarps;
   uint64_t* tempty_bar = tfull_bar + Cfg::NBUF;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + Cfg::NBUF);
 
@@ -286,8 +297,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < Cfg::STAGES; ++i) {
-      mbar_init(&full_bar[i], kProdThreads);
+    for (int i = 0; i < Cfg::STAGES * kProdWarps; ++i) {
+      mbar_init(&full_bar[i], 32 * WPG);
       mbar_init(&empty_bar[i], 1);
     }
     for (int i = 0; i < Cfg::NBUF; ++i) {
@@ -437,7 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int n0 = p.t * Cfg::N_TILE;
       const int m0 = (kSplit ? p.rg : p.g) * grp_rows;
       const int m_end = min(M, m0 + grp_rows);
-      mbar_wait(&empty_bar[stage], phase ^ 1);
+      mbar_wait(&empty_bar[stage * kProdWarps + warp / WPG], phase ^ 1);
       const int r0 = RW * warp;
       if (r0 < kpad && aligned8) {
         // 16-byte chunks are whole or absent (N, M, group rows multiples of 8): ignore-src copies,
@@ -538,7 +549,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      cp_async_arrive_noinc(&full_bar[stage]);
+      cp_async_arrive_noinc(&full_bar[stage * kProdWarps + warp / WPG]);
       if (++stage == Cfg::STAGES) {
         stage = 0;
         phase ^= 1;
@@ -568,37 +579,52 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
+    const bool elected = lane == 0;
+    const uint32_t sB0 = smem_u32(smem);
+    const uint64_t a_desc0 = smem_desc(sB0 + Cfg::B_BYTES, Cfg::KS * Cfg::A_ROW_BYTES, 8 * Cfg::A_ROW_BYTES, Cfg::A_SW);
+    const uint64_t b_desc0 = smem_desc(sB0, Cfg::KS * 128, 1024, kSw128);
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int cnt = vcount(u % n_vg);
       mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc_fence_after();
       for (int kb = 0; kb < cnt; kb += Cfg::KS) {
         const int ksteps = (min(Cfg::KS, cnt - kb) + 15) >> 4;
-        mbar_wait(&full_bar[stage], phase);
-        fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05.mma reads
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t sB = smem_u32(smem + stage * Cfg::STAGE_BYTES);
-          const uint32_t sA = sB + Cfg::B_BYTES;
-          const uint32_t dbase = tmem_base + static_cast<uint32_t>(acc * Cfg::ACC_COLS);
-          for (int ks = 0; ks < ksteps; ++ks) {
-            const uint32_t acc_flag = (kb > 0 || ks > 0) ? 1u : 0u;
-            const uint64_t a_strip = smem_desc(sA + ks * 16 * Cfg::A_ROW_BYTES, Cfg::KS * Cfg::A_ROW_BYTES,
-                                               8 * Cfg::A_ROW_BYTES, Cfg::A_SW);
-            if constexpr (kOrientN) {
-              const uint64_t b_strip = smem_desc(sB + ks * 2048, Cfg::KS * 128, 1024, kSw128);
-              umma_f16(dbase, a_strip, b_strip, idesc, acc_flag);
-            } else {
+        constexpr int KSG = Cfg::KS / 16 / BG;  // k-steps per barrier group
+        // descriptors of this stage: the stage-0 descriptors plus the stage offset (>> 4, the start
+        // address field; smem addresses < 256 KB never carry out of it); k-step / n-half offsets are
+        // compile-time immediates
+        const uint64_t soff = static_cast<uint64_t>((stage * Cfg::STAGE_BYTES) >> 4);
+        const uint64_t dA = a_desc0 + soff, dB = b_desc0 + soff;
+        const uint32_t dbase = tmem_base + static_cast<uint32_t>(acc * Cfg::ACC_COLS);
+        // every group's barrier is waited in every stage (phases stay in lock step); MMAs only for
+        // live k-steps; a group's slot is released after its last k-step
 #pragma unroll
-              for (int a = 0; a < Cfg::N_TILE / 128; ++a) {
-                const uint64_t b_half = smem_desc(sB + a * 2 * Cfg::KS * 128 + ks * 2048, Cfg::KS * 128, 1024, kSw128);
-                umma_f16(dbase + static_cast<uint32_t>(a * GW), b_half, a_strip, idesc, acc_flag);
+        for (int gi = 0; gi < BG; ++gi) {
+          mbar_wait(&full_bar[stage * kProdWarps + gi], phase);
+          fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05.mma reads
+          tc_fence_after();
+          if (elected) {
+#pragma unroll
+            for (int j = 0; j < KSG; ++j) {
+              const int ks = gi * KSG + j;
+              if (ks < ksteps) {
+                const uint32_t acc_flag = (kb > 0 || ks > 0) ? 1u : 0u;
+                const uint64_t a_strip = dA + static_cast<uint64_t>((ks * 16 * Cfg::A_ROW_BYTES) >> 4);
+                if constexpr (kOrientN) {
+                  umma_f16(dbase, a_strip, dB + static_cast<uint64_t>((ks * 2048) >> 4), idesc, acc_flag);
+                } else {
+#pragma unroll
+                  for (int a = 0; a < Cfg::N_TILE / 128; ++a)
+                    umma_f16(dbase + static_cast<uint32_t>(a * GW),
+                             dB + static_cast<uint64_t>((a * 2 * Cfg::KS * 128 + ks * 2048) >> 4), a_strip, idesc,
+                             acc_flag);
+                }
               }
             }
+            umma_commit(&empty_bar[stage * kProdWarps + gi]);
           }
-          umma_commit(&empty_bar[stage]);
+          __syncwarp();
         }
-        __syncwarp();
         if (++stage == Cfg::STAGES) {
           stage = 0;
           phase ^= 1;
@@ -2620,6 +2646,7 @@ int run_gk(const SpmmArgs& a, cudaStream_t s) {
     epi |= 1;
   }
   if (gk2_diag() & 4) epi |= 2;  // diagnostic: no C stores (orientation T)
+
   if constexpr (kOrientN && kNT == 64) {
     const int64_t need = gk_split_ws_bytes<Cfg::N_TILE>(a.n_groups, n_tiles);
     if (need > 0 && a.ws != nullptr && a.ws_bytes >= need && (reinterpret_cast<uintptr_t>(a.ws) & 255) == 0 &&
@@ -3055,6 +3082,12 @@ int dispatch_tc(const SpmmArgs& a, cudaStream_t s) {
     if (gw == 128 && a.N <= 64 && nt_override != 128) {
       const bool ks64 = gk_ks_override() == 64;
       return ks64 ? run_gk<128, true, kBF16, 64, 64>(a, s) : run_gk<128, true, kBF16, 128, 64>(a, s);
+    }
+    // 16/32-row groups with wide N: 512-column units (64-deep stages). Each gathered k row brings
+    // 1 KB of B for 64 B of A^T: 30.1 FLOP per gathered byte against 28.4 at 256 columns, and the
+    // gather feed (L2 -> SM) is what bounds these micro-tiles (PIT_GK_NT=256 keeps 256)
+    if ((gw == 16 || gw == 32) && a.N >= 1024 && nt_override != 256 && nt_override != 128) {
+      return gw == 16 ? run_gk<16, false, kBF16, 64, 512>(a, s) : run_gk<32, false, kBF16, 64, 512>(a, s);
     }
     return (a.N <= 128 || nt_override == 128) ? dispatch_gk<kBF16, 128>(a, gw, s) : dispatch_gk<kBF16, 0>(a, gw, s);
   }
