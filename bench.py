@@ -363,6 +363,10 @@ def run_ours(args, w):
         "graph_replay_equals_eager": replay_ok,
     }
 
+    if world > 1:
+        # N > 1: the single-operator sections are per-GPU replicas of the N=1 numbers (north_star reports
+        # them at 1 GPU); only the headline replica step and the expert-parallel MoE layer run
+        args.no_index_bench = args.no_sweep = args.no_bert = args.no_attn = args.no_opt = True
     if not args.no_index_bench:
         result["index_build"] = index_build_bench(dev, peaks)
     if not args.no_sweep:
@@ -445,11 +449,40 @@ def bert_bench(args, dev, peaks):
             "execution": "CUDA graph: build_index_from_tensor (1, 768) + run_matmul_with_index (pit:m)"}
 
 
+def _time_layer(fn, steps, dev, world):
+    """Median per-call device time of fn() (CUDA events on the current stream), max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    stream = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = []
+    for _ in range(steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        ev.append((e0, e1))
+    torch.cuda.synchronize()
+    ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
 def moe_bench(args, world, rank, dev, peaks, tokens_per_gpu=16384, n_experts=128, d_model=768, d_ff=3072):
     """C5: Switch-base-128 MoE layer (top-1, dropless), tokens sharded per GPU (weak scaling), experts
-    sharded over ranks (expert parallelism, NCCL all-to-all) when world > 1. Synthetic activations,
-    Gaussian router logits (imbalanced top-1), random bf16 expert weights. Layer time = route + index +
-    pack + all-to-all + FFN1(ReLU) + FFN2 + all-to-all + combine (router GEMM excluded). Max over ranks."""
+    sharded over ranks (expert parallelism) when world > 1. Synthetic activations, Gaussian router
+    logits (imbalanced top-1), random bf16 expert weights. Layer time = route + index + dispatch +
+    FFN1(ReLU) + FFN2 + combine (router GEMM excluded), one CUDA graph per layer, max over ranks.
+    world > 1: the product exchange is the peer-memory one (csrc/pit_ep.cu: dispatch stores token rows
+    into the expert rank's region over NVLink, combine pulls them back, no host sync); the NCCL
+    all-to-all-v orchestration is timed beside it as the baseline (eager: it needs a D2H of the
+    split sizes)."""
     import torch
     import torch.distributed as dist
 
@@ -462,48 +495,88 @@ def moe_bench(args, world, rank, dev, peaks, tokens_per_gpu=16384, n_experts=128
     logits = torch.randn((tokens_per_gpu, E), device=dev, dtype=torch.float32, generator=g)
     w1 = (torch.randn((El, d_model, d_ff), device=dev, generator=g) / d_model ** 0.5).to(torch.bfloat16)
     w2 = (torch.randn((El, d_ff, d_model), device=dev, generator=g) / d_ff ** 0.5).to(torch.bfloat16)
-    layer = SwitchMoE(w1, w2, E, group=dist.group.WORLD if world > 1 else None)
+    group = dist.group.WORLD if world > 1 else None
+    layer = SwitchMoE(w1, w2, E, group=group, capacity=tokens_per_gpu)
+    steps = max(5, args.steps)
     for _ in range(max(3, args.warmup)):
+        eager = layer(x, logits)
+    torch.cuda.synchronize()
+    # the layer as a served model runs it: one CUDA graph (no host round trip on either path)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
         layer(x, logits)
+    torch.cuda.current_stream().wait_stream(side)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    stream = torch.cuda.current_stream()
+    graph = torch.cuda.CUDAGraph()
     launches0 = _lib.kernel_launches()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    steps = max(5, args.steps)
-    e0.record(stream)
-    for _ in range(steps):
-        layer(x, logits)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / steps
-    received = layer.stats.received
+    with torch.cuda.graph(graph):
+        out_g = layer(x, logits)
+    launches_per_layer = _lib.kernel_launches() - launches0
+    for _ in range(max(3, args.warmup)):
+        graph.replay()
+    ms = _time_layer(graph.replay, steps, dev, world)
+    replay_ok = bool(torch.equal(out_g, eager))
+    ep_error = layer._peer.error() if layer._peer is not None else 0
+    baseline = None
     if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        nccl = SwitchMoE(w1, w2, E, group=group, exchange="nccl")
+        for _ in range(max(3, args.warmup)):
+            ref_out = nccl(x, logits)
+        nccl_ms = _time_layer(lambda: nccl(x, logits), steps, dev, world)
+        same = bool(torch.equal(ref_out, eager))
+        baseline = {"exchange": "NCCL all_to_all_single (counts) + D2H of split sizes + all-to-all-v x2, eager",
+                    "ms_per_layer": round(nccl_ms, 4),
+                    "tokens_per_s": round(world * tokens_per_gpu / (nccl_ms * 1e-3), 1),
+                    "output_equals_peer_path": same}
+    received = int(layer._peer.lcounts.sum().item()) if layer._peer is not None else tokens_per_gpu
+    peer_self = None
+    if world == 1:
+        # the peer-memory exchange kernels against this rank's own region (dispatch stores + combine
+        # pulls through the region instead of the fused gather / scaled-scatter GEMM epilogues)
+        selfx = SwitchMoE(w1, w2, E, exchange="peer", capacity=tokens_per_gpu)
+        for _ in range(max(3, args.warmup)):
+            so = selfx(x, logits)
+        ps_ms = _time_layer(lambda: selfx(x, logits), steps, dev, world)
+        peer_self = {"ms_per_layer": round(ps_ms, 4), "tokens_per_s": round(tokens_per_gpu / (ps_ms * 1e-3), 1),
+                     "max_abs_diff_vs_local": float((so.float() - eager.float()).abs().max()),
+                     "timeouts": selfx._peer.error(), "execution": "eager"}
+        selfx.close()
+    if world > 1:
+        layer.close()
         dist.barrier()
     toks = world * tokens_per_gpu / (ms * 1e-3)
     flops = switch_flops(world * tokens_per_gpu, d_model, d_ff) / (ms * 1e-3) / 1e12
     # HBM roofline of one rank's layer: its experts' weights are streamed once (2 matrices x El x
-    # d_model x d_ff bf16) plus the token rows read / written (x, hidden, output; pack / combine
-    # buffers not counted). At 128 tokens per expert this, not the tensor pipe, bounds the layer.
+    # d_model x d_ff bf16) plus the token rows read / written (x, hidden, output; exchange buffers
+    # not counted). At 128 tokens per expert this, not the tensor pipe, bounds the layer.
     hbm_bytes = 2 * El * d_model * d_ff * 2 + received * (d_model * 2 * 2 + d_ff * 2 * 2) + tokens_per_gpu * d_model * 2 * 2
     hbm_gbps = hbm_bytes / (ms * 1e-3) / 1e9
-    return {"metric": "MoE layer tokens/s", "value": round(toks, 1), "unit": "tokens/s", "n_gpus": world,
-            "ms_per_layer": round(ms, 4), "expert_tflops_per_gpu": round(flops / world, 2),
-            "frac_bf16_peak": round(flops / world / peaks["bf16"], 4),
-            "roofline": {"bound": "hbm", "achieved": round(hbm_gbps, 1), "peak": peaks["hbm"], "unit": "GB/s",
-                         "frac": round(hbm_gbps / peaks["hbm"], 4), "traffic": None,
-                         "algorithmic_bytes_per_layer": int(hbm_bytes),
-                         "note": "expert weights streamed once per layer dominate; tensor-time floor "
-                                 f"{switch_flops(tokens_per_gpu, d_model, d_ff) / peaks['bf16'] / 1e9:.3f} ms vs HBM floor "
-                                 f"{hbm_bytes / peaks['hbm'] / 1e6:.3f} ms"},
-            "config": {"experts": E, "experts_per_gpu": El, "d_model": d_model, "d_ff": d_ff,
-                       "tokens_per_gpu": tokens_per_gpu, "routing": "top-1 argmax, Gaussian logits, dropless",
-                       "parallelism": f"ep{world}" if world > 1 else "single GPU", "received_rank0": int(received)},
-            "gpu_launches_per_layer": (_lib.kernel_launches() - launches0) // steps}
+    out = {"metric": "MoE layer tokens/s", "value": round(toks, 1), "unit": "tokens/s", "n_gpus": world,
+           "ms_per_layer": round(ms, 4), "expert_tflops_per_gpu": round(flops / world, 2),
+           "frac_bf16_peak": round(flops / world / peaks["bf16"], 4),
+           "roofline": {"bound": "hbm", "achieved": round(hbm_gbps, 1), "peak": peaks["hbm"], "unit": "GB/s",
+                        "frac": round(hbm_gbps / peaks["hbm"], 4), "traffic": None,
+                        "algorithmic_bytes_per_layer": int(hbm_bytes),
+                        "note": "expert weights streamed once per layer dominate; tensor-time floor "
+                                f"{switch_flops(tokens_per_gpu, d_model, d_ff) / peaks['bf16'] / 1e9:.3f} ms vs HBM floor "
+                                f"{hbm_bytes / peaks['hbm'] / 1e6:.3f} ms"},
+           "config": {"experts": E, "experts_per_gpu": El, "d_model": d_model, "d_ff": d_ff,
+                      "tokens_per_gpu": tokens_per_gpu, "routing": "top-1 argmax, Gaussian logits, dropless",
+                      "parallelism": f"ep{world}" if world > 1 else "single GPU", "received_rank0": received,
+                      "exchange": layer.exchange, "execution": "CUDA graph of the whole layer"},
+           "gpu_launches_per_layer": int(launches_per_layer), "graph_replay_equals_eager": replay_ok,
+           "exchange_timeouts": int(ep_error)}
+    if world > 1:
+        # the exchange's own floor: every rank sends and receives its tokens twice over NVLink
+        xbytes = 2 * tokens_per_gpu * d_model * 2
+        out["exchange"] = {"bytes_per_rank_per_layer": xbytes, "nvlink_floor_ms": round(xbytes / 900e9 * 1e3, 4)}
+        out["baseline_nccl"] = baseline
+    else:
+        out["peer_exchange_one_rank"] = peer_self
+    return out
 
 
 def sparsity_sweep_bench(args, dev, peaks, side=8192, micros=((32, 1), (128, 1), (256, 1)),
@@ -952,6 +1025,17 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--ref-seconds", type=float, default=4.0)
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun (the driver may also launch it so)
+        import socket
+
+        sock = socket.socket()
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+        sock.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3  # timing rule: at least 3 warm-up steps
     w = dict(WORKLOADS[args.workload], name=args.workload)

@@ -48,7 +48,7 @@ typedef enum { PIT_PLAN_DENSE = 0, PIT_PLAN_PIT_M = 1, PIT_PLAN_PIT_K = 2 } pit_
 PIT_API const char* pit_last_error(void);
 
 /* ABI version (major*100 + minor). */
-PIT_API int pit_abi_version(void); /* 101: pit_spmm_args gained batch / b_batch_stride */
+PIT_API int pit_abi_version(void); /* 102: pit_grouped_gemm_args gained rows_hint; pit_ep_* / pit_moe_dispatch */
 
 /* Number of kernels this library has launched in the process (monotonic; for launch accounting). */
 PIT_API long long pit_kernel_launches(void);
@@ -177,6 +177,7 @@ typedef struct {
   const float* row_scale;
   int act;
   int64_t max_tiles; /* host upper bound on tile_offsets[G] (e.g. ceil(total_rows/128) + G) */
+  int64_t rows_hint; /* expected total rows when rows_a is only a capacity (0: rows_a); picks the kernel */
 } pit_grouped_gemm_args;
 
 PIT_API int pit_grouped_gemm(const pit_grouped_gemm_args* args, void* stream);
@@ -207,6 +208,53 @@ PIT_API int pit_gather_rows(const void* src, int64_t ld_src_bytes, const int32_t
 /* SWrite of whole rows with a per-destination-row scale (MoE combine): dst[rows[i]] = scale[rows[i]] * src[i]. */
 PIT_API int pit_scatter_rows_scaled(const void* src, int dtype, int64_t ld_src, const int32_t* rows, int64_t n,
                                     int64_t width, const float* scale, void* dst, int64_t ld_dst, void* stream);
+
+/*
+ * Expert-parallel MoE exchange over NVLink peer memory (SURVEY 8(b) pit_moe_dispatch, 8(e)). No reference
+ * counterpart: the reference has no multi-GPU code; this is the cross-GPU form of the SRead that packs an
+ * expert group's token rows and of the SWrite that scatters its outputs (index.py:102-173 routing index,
+ * executor.py:170-264 gather/scatter semantics). One region per rank (pit_ep_region_alloc), exported to the
+ * other ranks of the node through CUDA IPC; every call is stream-ordered with no host synchronisation
+ * (CUDA-graph capturable). Region layout (pit_ep_region_layout): header, dispatch flags[W], combine
+ * flags[W], counts[W][El] (received per source rank and local expert), recv[W*cap rows], y[W*cap rows]
+ * (row r of source s at s*cap + position).
+ */
+typedef struct {
+  int rank, world;
+  int64_t experts_local; /* El: experts per rank; global expert e lives on rank e / El */
+  int64_t capacity;      /* max tokens any rank sends per layer (its T) */
+  int64_t row_bytes;     /* d_model * element size, multiple of 16 */
+  void* local;           /* this rank's region */
+  void* const* peers;    /* DEVICE array [world] of region pointers as mapped in this process */
+} pit_ep_args;
+
+/* out[6] = byte offsets {dispatch flags, combine flags, counts, recv, y, total size}. */
+PIT_API int pit_ep_region_layout(int64_t world, int64_t experts_local, int64_t capacity, int64_t row_bytes,
+                                 int64_t* out);
+/* cudaMalloc + zero a region of `bytes` on the current device (flags and epochs start at 0). */
+PIT_API int pit_ep_region_alloc(int64_t bytes, void** out);
+PIT_API int pit_ep_region_free(void* region);
+/* CUDA IPC: 64-byte handle of a region; open a peer's handle in this process (close with pit_ep_ipc_close). */
+PIT_API int pit_ep_ipc_handle(void* region, void* handle64);
+PIT_API int pit_ep_ipc_open(const void* handle64, void** out);
+PIT_API int pit_ep_ipc_close(void* mapped);
+/* nonzero if a wait in this region timed out (a peer never arrived); synchronous read. */
+PIT_API int pit_ep_error(void* region, int* out);
+
+/* Dispatch = pack + send fused: token perm[i] (expert order, expert prefix offsets[E+1], E = world*El) is
+ * stored straight into rank (e/El)'s recv region over NVLink; counts[E] go to the peers' counts rows;
+ * the last block publishes this rank's epoch to every peer. x: [T, row] with row pitch ldx_bytes. */
+PIT_API int pit_moe_dispatch(const pit_ep_args* ep, const void* x, int64_t ldx_bytes, int64_t T, const int32_t* perm,
+                             const int32_t* offsets, const int32_t* counts, void* stream);
+/* Wait for every peer's dispatch of this epoch, then rows[e*stride + j] = recv row of local expert e's j-th
+ * token (source-rank order), counts[El]. */
+PIT_API int pit_moe_recv_plan_ep(const pit_ep_args* ep, int32_t* rows, int64_t stride, int32_t* counts, void* stream);
+/* Publish "y ready" (the expert outputs are in this rank's y region) to every peer. */
+PIT_API int pit_moe_signal(const pit_ep_args* ep, void* stream);
+/* Combine = pull + SWrite * gate fused: wait for every peer's y flag, then out[perm[i]] = gate[perm[i]] *
+ * y(rank e/El)[rank*cap + position]. dtype bf16 / f16 / f32. */
+PIT_API int pit_moe_combine(const pit_ep_args* ep, int dtype, int64_t T, const int32_t* perm, const int32_t* offsets,
+                            const float* gate, void* out, int64_t ldo_bytes, void* stream);
 
 /*
  * Sparse row reduction (run_sparse_reduce_sum, executor.py:540-613): out[r] = sum of A[r, l] (row-major,

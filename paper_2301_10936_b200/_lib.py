@@ -58,6 +58,17 @@ EXPORTS = (
     "pit_scatter_rows_scaled",
     "pit_copy2d_async",
     "pit_reduce_rows",
+    "pit_ep_region_layout",
+    "pit_ep_region_alloc",
+    "pit_ep_region_free",
+    "pit_ep_ipc_handle",
+    "pit_ep_ipc_open",
+    "pit_ep_ipc_close",
+    "pit_ep_error",
+    "pit_moe_dispatch",
+    "pit_moe_recv_plan_ep",
+    "pit_moe_signal",
+    "pit_moe_combine",
 )
 
 
@@ -121,6 +132,21 @@ class GroupedGemmArgs(C.Structure):
         ("row_scale", C.c_void_p),
         ("act", C.c_int),
         ("max_tiles", C.c_int64),
+        ("rows_hint", C.c_int64),
+    ]
+
+
+class EpArgs(C.Structure):
+    """Mirror of ``pit_ep_args``."""
+
+    _fields_ = [
+        ("rank", C.c_int),
+        ("world", C.c_int),
+        ("experts_local", C.c_int64),
+        ("capacity", C.c_int64),
+        ("row_bytes", C.c_int64),
+        ("local", C.c_void_p),
+        ("peers", C.c_void_p),
     ]
 
 
@@ -152,6 +178,18 @@ def _declare(lib) -> None:
     lib.pit_scatter_rows_scaled.argtypes = [vp, i32, i64, vp, i64, i64, vp, vp, i64, vp]
     lib.pit_copy2d_async.argtypes = [vp, i64, vp, i64, i64, i64, vp]
     lib.pit_reduce_rows.argtypes = [vp, i32, i64, i64, i64, vp, i64, i32, i32, vp, vp]
+    ep = C.POINTER(EpArgs)
+    lib.pit_ep_region_layout.argtypes = [i64, i64, i64, i64, C.POINTER(i64)]
+    lib.pit_ep_region_alloc.argtypes = [i64, C.POINTER(vp)]
+    lib.pit_ep_region_free.argtypes = [vp]
+    lib.pit_ep_ipc_handle.argtypes = [vp, vp]
+    lib.pit_ep_ipc_open.argtypes = [vp, C.POINTER(vp)]
+    lib.pit_ep_ipc_close.argtypes = [vp]
+    lib.pit_ep_error.argtypes = [vp, C.POINTER(i32)]
+    lib.pit_moe_dispatch.argtypes = [ep, vp, i64, i64, vp, vp, vp, vp]
+    lib.pit_moe_recv_plan_ep.argtypes = [ep, vp, i64, vp, vp]
+    lib.pit_moe_signal.argtypes = [ep, vp]
+    lib.pit_moe_combine.argtypes = [ep, i32, i64, vp, vp, vp, vp, i64, vp]
     for name in EXPORTS:
         if name not in ("pit_last_error", "pit_abi_version", "pit_kernel_launches", "pit_spmm_workspace_bytes"):
             getattr(lib, name).restype = i32

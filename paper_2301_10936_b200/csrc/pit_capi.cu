@@ -117,7 +117,7 @@ extern "C" {
 
 const char* pit_last_error(void) { return g_err.c_str(); }
 
-int pit_abi_version(void) { return 101; }
+int pit_abi_version(void) { return 102; }
 
 // Diagnostic (not part of include/pit_b200.h): the CTA-pair gathered-K kernel's stage timeline.
 PIT_API int pit_debug_gk2_trace(unsigned long long* host_out_1024) { return pit::gk2_trace_read(host_out_1024); }
@@ -417,6 +417,7 @@ int pit_grouped_gemm(const pit_grouped_gemm_args* a, void* stream) {
   g.row_scale = a->row_scale;
   g.act = a->act;
   g.max_tiles = a->max_tiles;
+  g.rows_hint = a->rows_hint;
   const int st = launch_rowgemm(g, static_cast<cudaStream_t>(stream));
   if (st == kErrUnsupported) return fail(st, "grouped GEMM needs bf16/fp16 with 16-byte aligned rows");
   return st;
@@ -462,6 +463,117 @@ int pit_scatter_rows_scaled(const void* src, int dtype, int64_t ld_src, const in
   const int st = launch_scatter_rows_scaled(src, dtype, ld_src, rows, n, width, scale, dst, ld_dst,
                                             static_cast<cudaStream_t>(stream));
   if (st == kErrUnsupported) return fail(st, "unsupported dtype code %d", dtype);
+  return st;
+}
+
+static int ep_check(const pit_ep_args* ep, pit::EpArgs* out) {
+  if (!ep) return fail(kErrArg, "null expert-parallel args");
+  if (ep->world <= 0 || ep->rank < 0 || ep->rank >= ep->world || ep->experts_local <= 0 || ep->capacity < 0)
+    return fail(kErrShape, "bad expert-parallel geometry (rank %d of %d, %lld local experts)", ep->rank, ep->world,
+                (long long)ep->experts_local);
+  if (ep->row_bytes <= 0 || ep->row_bytes % 16) return fail(kErrShape, "exchanged rows must be a multiple of 16 bytes");
+  if (!ep->local || !ep->peers) return fail(kErrArg, "null region pointer");
+  out->rank = ep->rank;
+  out->world = ep->world;
+  out->experts_local = ep->experts_local;
+  out->capacity = ep->capacity;
+  out->row_bytes = ep->row_bytes;
+  out->local = ep->local;
+  out->peers = ep->peers;
+  return kOk;
+}
+
+int pit_ep_region_layout(int64_t world, int64_t El, int64_t cap, int64_t row_bytes, int64_t* out) {
+  if (world <= 0 || El <= 0 || cap < 0 || row_bytes <= 0) return fail(kErrShape, "bad expert-parallel geometry");
+  if (!out) return fail(kErrArg, "null output");
+  pit::ep_region_layout(static_cast<int>(world), El, cap, row_bytes, out);
+  return kOk;
+}
+
+int pit_ep_region_alloc(int64_t bytes, void** out) {
+  if (bytes <= 0 || !out) return fail(kErrArg, "bad region request");
+  void* p = nullptr;
+  if (cudaMalloc(&p, static_cast<size_t>(bytes)) != cudaSuccess) return cuda_status();
+  if (cudaMemset(p, 0, static_cast<size_t>(bytes)) != cudaSuccess) {
+    cudaFree(p);
+    return cuda_status();
+  }
+  *out = p;
+  return kOk;
+}
+
+int pit_ep_region_free(void* region) {
+  if (region && cudaFree(region) != cudaSuccess) return cuda_status();
+  return kOk;
+}
+
+int pit_ep_ipc_handle(void* region, void* handle64) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  if (!region || !handle64) return fail(kErrArg, "null pointer");
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, region) != cudaSuccess) return cuda_status();
+  memcpy(handle64, &h, sizeof h);
+  return kOk;
+}
+
+int pit_ep_ipc_open(const void* handle64, void** out) {
+  if (!handle64 || !out) return fail(kErrArg, "null pointer");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof h);
+  if (cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return cuda_status();
+  return kOk;
+}
+
+int pit_ep_ipc_close(void* mapped) {
+  if (mapped && cudaIpcCloseMemHandle(mapped) != cudaSuccess) return cuda_status();
+  return kOk;
+}
+
+int pit_ep_error(void* region, int* out) {
+  if (!region || !out) return fail(kErrArg, "null pointer");
+  unsigned v = 0;
+  if (cudaMemcpy(&v, static_cast<uint8_t*>(region) + 12, sizeof v, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return cuda_status();
+  *out = static_cast<int>(v);
+  return kOk;
+}
+
+int pit_moe_dispatch(const pit_ep_args* ep, const void* x, int64_t ldx_bytes, int64_t T, const int32_t* perm,
+                     const int32_t* offsets, const int32_t* counts, void* stream) {
+  pit::EpArgs a;
+  if (int st = ep_check(ep, &a)) return st;
+  if (T < 0 || T > ep->capacity) return fail(kErrShape, "%lld tokens exceed the exchange capacity %lld", (long long)T,
+                                             (long long)ep->capacity);
+  if (ldx_bytes < ep->row_bytes || ldx_bytes % 16 || reinterpret_cast<uintptr_t>(x) % 16)
+    return fail(kErrLayout, "token rows must be 16-byte aligned with pitch >= row bytes");
+  if ((T && (!x || !perm)) || !offsets || !counts) return fail(kErrArg, "null device pointer");
+  return launch_ep_dispatch(a, x, ldx_bytes, T, perm, offsets, counts, static_cast<cudaStream_t>(stream));
+}
+
+int pit_moe_recv_plan_ep(const pit_ep_args* ep, int32_t* rows, int64_t stride, int32_t* counts, void* stream) {
+  pit::EpArgs a;
+  if (int st = ep_check(ep, &a)) return st;
+  if (!rows || !counts) return fail(kErrArg, "null device pointer");
+  if (stride < ep->world * ep->capacity) return fail(kErrShape, "row-list stride below world * capacity");
+  return launch_ep_recv_plan(a, rows, stride, counts, static_cast<cudaStream_t>(stream));
+}
+
+int pit_moe_signal(const pit_ep_args* ep, void* stream) {
+  pit::EpArgs a;
+  if (int st = ep_check(ep, &a)) return st;
+  return launch_ep_signal(a, static_cast<cudaStream_t>(stream));
+}
+
+int pit_moe_combine(const pit_ep_args* ep, int dtype, int64_t T, const int32_t* perm, const int32_t* offsets,
+                    const float* gate, void* out, int64_t ldo_bytes, void* stream) {
+  pit::EpArgs a;
+  if (int st = ep_check(ep, &a)) return st;
+  if (T < 0 || T > ep->capacity) return fail(kErrShape, "token count outside the exchange capacity");
+  if (ldo_bytes < ep->row_bytes || ldo_bytes % 16 || reinterpret_cast<uintptr_t>(out) % 16)
+    return fail(kErrLayout, "output rows must be 16-byte aligned with pitch >= row bytes");
+  if ((T && (!out || !perm)) || !offsets) return fail(kErrArg, "null device pointer");
+  const int st = launch_ep_combine(a, dtype, T, perm, offsets, gate, out, ldo_bytes, static_cast<cudaStream_t>(stream));
+  if (st == kErrUnsupported) return fail(st, "combine dtype must be bf16, f16 or f32");
   return st;
 }
 

@@ -153,6 +153,7 @@ struct GroupedGemmArgs {
   const float* row_scale;
   int act;
   int64_t max_tiles;
+  int64_t rows_hint;  // expected total rows (0: rows_a)
 };
 int launch_rowgemm(const GroupedGemmArgs& g, cudaStream_t s);
 
@@ -167,6 +168,21 @@ int launch_gather_rows(const void* src, int64_t ld_src_bytes, const int32_t* row
                        void* dst, int64_t ld_dst_bytes, cudaStream_t s);
 int launch_scatter_rows_scaled(const void* src, int dtype, int64_t ld_src, const int32_t* rows, int64_t n,
                                int64_t width, const float* scale, void* dst, int64_t ld_dst, cudaStream_t s);
+
+// ------------------------------------------- expert-parallel exchange over peer memory (pit_ep.cu)
+struct EpArgs {
+  int rank, world;
+  int64_t experts_local, capacity, row_bytes;
+  void* local;              // this rank's region
+  void* const* peers;       // device array [world]: every rank's region as mapped here (peers[rank] = local)
+};
+void ep_region_layout(int W, int64_t El, int64_t cap, int64_t row_bytes, int64_t out[6]);
+int launch_ep_dispatch(const EpArgs& a, const void* x, int64_t ldx_bytes, int64_t T, const int32_t* perm,
+                       const int32_t* offsets, const int32_t* counts, cudaStream_t s);
+int launch_ep_recv_plan(const EpArgs& a, int32_t* rows, int64_t stride, int32_t* counts, cudaStream_t s);
+int launch_ep_signal(const EpArgs& a, cudaStream_t s);
+int launch_ep_combine(const EpArgs& a, int dtype, int64_t T, const int32_t* perm, const int32_t* offsets,
+                      const float* gate, void* out, int64_t ldo_bytes, cudaStream_t s);
 
 // Driver entry point for cuTensorMapEncodeTiled (resolved through the runtime, no -lcuda).
 CUresult encode_tensor_map_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner,

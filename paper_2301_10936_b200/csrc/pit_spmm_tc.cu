@@ -3214,7 +3214,7 @@ int launch_rowgemm(const GroupedGemmArgs& g, cudaStream_t s) {
   const int ks = g.K % 64 == 0 || g.K > 64 ? 64 : g.K % 32 == 0 ? 32 : 16;
   // small groups (MoE at ~128 tokens per expert): tokens on the MMA's N side, quantised to 16 rows
   // instead of 128 (rowgemm2t); large groups fill 256-row tiles anyway and keep rowgemm2's epilogue
-  const bool small_groups = g.rows_a < 256 * g.G;
+  const bool small_groups = (g.rows_hint > 0 ? g.rows_hint : g.rows_a) < 256 * g.G;
   if (ks == 64 && p.G <= kRg2MaxGroups && rg2t_enabled() && p.N >= 64 && small_groups)
     return g.dtype == kDtypeBF16 ? run_rowgemm2t<true>(p, g.B, g.ldb, s) : run_rowgemm2t<false>(p, g.B, g.ldb, s);
   return g.dtype == kDtypeBF16 ? rowgemm_dispatch<true>(p, g.B, g.ldb, ks, s) : rowgemm_dispatch<false>(p, g.B, g.ldb, ks, s);

@@ -5,11 +5,16 @@ one-hot mask whose PIT index (groups = experts, coordinates = tokens) is built o
 FFNs are per-expert gathered-row GEMMs (SRead of the token rows fused into the mainloop), and the
 combine is an SWrite scaled by the gate. No capacity padding: every token is computed once.
 
-Expert parallelism over W ranks (rank r owns experts [r*E/W, (r+1)*E/W)):
-  route -> plan -> pack (SRead by expert order) -> all_to_all(counts) -> all_to_all(tokens)
-  -> receive plan -> FFN1 (ReLU) -> FFN2 -> all_to_all(back) -> combine (SWrite * gate)
+Expert parallelism over W ranks (rank r owns experts [r*E/W, (r+1)*E/W)), two exchanges:
+  "peer" (the product, `PeerExchange`): route -> plan -> dispatch (SRead pack fused with the send:
+      token rows stored straight into the owning rank's receive region over NVLink) -> receive
+      plan (waits on the peers' epoch flags) -> FFN1 (ReLU) -> FFN2 (into the y region) -> signal
+      -> combine (each token pulls its output row from the expert rank, SWrite * gate fused).
+      No host synchronisation: the whole layer is capturable in one CUDA graph.
+  "nccl" (baseline): pack -> all_to_all(counts) -> one D2H of the split sizes -> all_to_all_v(tokens)
+      -> receive plan -> FFN1 -> FFN2 -> all_to_all_v(back) -> combine.
 The orchestration is written against a backend: `CudaBackend` (libpit_b200.so kernels) is the
-product; the exchange logic is backend-agnostic so it can be exercised over gloo in tests.
+product; the NCCL-path exchange logic is backend-agnostic so it can be exercised over gloo in tests.
 """
 
 from __future__ import annotations
@@ -90,7 +95,7 @@ class CudaBackend:
         return out
 
     def grouped_gemm(self, A, W, counts, offsets, tiles, out, *, row_src=None, src_stride=0, row_dst=None,
-                     dst_stride=0, row_scale=None, act=0, max_tiles=None):
+                     dst_stride=0, row_scale=None, act=0, max_tiles=None, rows_hint=0):
         G, K, N = W.shape
         a = _lib.GroupedGemmArgs()
         a.dtype = _device.dtype_code(A)
@@ -106,8 +111,121 @@ class CudaBackend:
         a.row_scale = row_scale.data_ptr() if row_scale is not None else None
         a.act = act
         a.max_tiles = max_tiles if max_tiles is not None else -(-A.shape[0] // 128) + G
+        a.rows_hint = rows_hint
         _device.check(self.lib.pit_grouped_gemm(C.byref(a), self._stream()))
         return out
+
+
+def _raw_view(ptr: int, rows: int, cols: int, dtype, device):
+    """Zero-copy torch view [rows, cols] of raw device memory (a region allocated by the C library)."""
+    torch = _torch()
+    elem = torch.empty((), dtype=dtype).element_size()
+    carrier = {2: "<i2", 4: "<i4", 8: "<i8"}[elem]
+
+    class _CAI:
+        __cuda_array_interface__ = {"shape": (rows, cols), "typestr": carrier, "data": (ptr, False), "version": 3,
+                                    "strides": None}
+
+    raw = torch.as_tensor(_CAI(), device=device)
+    return raw.view(dtype)
+
+
+class PeerExchange:
+    """One exchange region per rank, mapped into every other rank through CUDA IPC (pit_ep_* in the C
+    ABI). `dispatch` / `recv_plan` / `signal` / `combine` are stream-ordered device calls with no host
+    synchronisation. `capacity` = the most tokens a rank sends per layer.
+
+    Collective: every rank of `group` constructs it (and closes it) together."""
+
+    def __init__(self, group, experts_local: int, capacity: int, d_model: int, dtype, device=None):
+        import torch.distributed as dist
+
+        torch = _torch()
+        self.lib = _lib.load()
+        self.group = group
+        self.world = dist.get_world_size(group) if group is not None else 1
+        self.rank = dist.get_rank(group) if group is not None else 0
+        self.El, self.cap, self.d_model, self.dtype = int(experts_local), int(capacity), int(d_model), dtype
+        self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        elem = torch.empty((), dtype=dtype).element_size()
+        self.row_bytes = self.d_model * elem
+        lay = (C.c_int64 * 6)()
+        _device.check(self.lib.pit_ep_region_layout(self.world, self.El, self.cap, self.row_bytes, lay))
+        self.layout = dict(zip(("flags_d", "flags_c", "counts", "recv", "y", "total"), list(lay)))
+        region = C.c_void_p()
+        _device.check(self.lib.pit_ep_region_alloc(self.layout["total"], C.byref(region)))
+        self.region = region.value
+        self._opened = []
+        peers = [0] * self.world
+        peers[self.rank] = self.region
+        if self.world > 1:
+            h = (C.c_char * 64)()
+            _device.check(self.lib.pit_ep_ipc_handle(self.region, h))
+            handles = [None] * self.world
+            dist.all_gather_object(handles, bytes(h), group=group)
+            for r in range(self.world):
+                if r == self.rank:
+                    continue
+                p = C.c_void_p()
+                _device.check(self.lib.pit_ep_ipc_open(C.create_string_buffer(handles[r], 64), C.byref(p)))
+                self._opened.append(p.value)
+                peers[r] = p.value
+        self.peers_dev = torch.tensor(peers, dtype=torch.int64, device=self.device)
+        self.args = _lib.EpArgs(self.rank, self.world, self.El, self.cap, self.row_bytes, self.region,
+                                self.peers_dev.data_ptr())
+        rows_total = self.world * self.cap
+        self.recv = _raw_view(self.region + self.layout["recv"], rows_total, self.d_model, dtype, self.device)
+        self.y = _raw_view(self.region + self.layout["y"], rows_total, self.d_model, dtype, self.device)
+        self.rows = torch.empty((self.El, max(rows_total, 1)), dtype=torch.int32, device=self.device)
+        self.lcounts = torch.empty(self.El, dtype=torch.int32, device=self.device)
+        if self.world > 1:
+            torch.cuda.synchronize(self.device)
+            dist.barrier(group)  # every rank mapped every region before anyone writes
+
+    def _s(self):
+        return _device.stream_ptr()
+
+    def dispatch(self, x, perm, offsets, counts):
+        _device.check(self.lib.pit_moe_dispatch(C.byref(self.args), x.data_ptr(), x.stride(0) * x.element_size(),
+                                                x.shape[0], perm.data_ptr(), offsets.data_ptr(), counts.data_ptr(),
+                                                self._s()))
+
+    def recv_plan(self):
+        _device.check(self.lib.pit_moe_recv_plan_ep(C.byref(self.args), self.rows.data_ptr(), self.rows.shape[1],
+                                                    self.lcounts.data_ptr(), self._s()))
+        return self.rows, self.lcounts
+
+    def signal(self):
+        _device.check(self.lib.pit_moe_signal(C.byref(self.args), self._s()))
+
+    def combine(self, perm, offsets, gate, out):
+        _device.check(self.lib.pit_moe_combine(C.byref(self.args), _device.dtype_code(out), out.shape[0],
+                                               perm.data_ptr(), offsets.data_ptr(),
+                                               gate.data_ptr() if gate is not None else None, out.data_ptr(),
+                                               out.stride(0) * out.element_size(), self._s()))
+        return out
+
+    def error(self) -> int:
+        v = C.c_int()
+        _device.check(self.lib.pit_ep_error(self.region, C.byref(v)))
+        return v.value
+
+    def close(self):
+        """Collective: unmap the peers' regions and free this rank's."""
+        if self.region is None:
+            return
+        torch = _torch()
+        torch.cuda.synchronize(self.device)
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.barrier(self.group)  # nobody still reads or writes a region
+        for p in self._opened:
+            self.lib.pit_ep_ipc_close(p)
+        self._opened = []
+        self.recv = self.y = None
+        self.lib.pit_ep_region_free(self.region)
+        self.region = None
 
 
 @dataclass
@@ -124,7 +242,8 @@ class SwitchMoE:
     With a process group of W ranks, E = W * E_local and tokens are exchanged with all-to-all.
     """
 
-    def __init__(self, w1, w2, n_experts: int, group=None, backend=None):
+    def __init__(self, w1, w2, n_experts: int, group=None, backend=None, exchange: Optional[str] = None,
+                 capacity: Optional[int] = None, exchange_factory=None):
         torch = _torch()
         self.w1 = w1.contiguous()
         self.w2 = w2.contiguous()
@@ -147,12 +266,57 @@ class SwitchMoE:
         self.backend = backend if backend is not None else CudaBackend()
         self.stats = MoEStats()
         self._torch = torch
+        # "peer": device-driven exchange over NVLink (default with W > 1); "nccl": all-to-all-v baseline;
+        # "local": single-GPU path (W == 1). "peer" at W == 1 runs the exchange kernels against itself.
+        self.exchange = exchange or ("local" if self.world == 1 else "peer")
+        if self.exchange not in ("local", "peer", "nccl"):
+            raise ValueError(f"unknown exchange {self.exchange!r}")
+        if self.exchange == "local" and self.world > 1:
+            raise ValueError("the local path runs on one rank")
+        self.capacity = capacity
+        self._peer = None
+        self._peer_factory = exchange_factory or PeerExchange
 
     # --------------------------------------------------------------------------- forward
     def forward(self, x, logits):
-        if self.world == 1:
+        if self.exchange == "local":
             return self._forward_local(x, logits)
+        if self.exchange == "peer":
+            return self._forward_peer(x, logits)
         return self._forward_ep(x, logits)
+
+    def close(self):
+        if self._peer is not None:
+            self._peer.close()
+            self._peer = None
+
+    def _forward_peer(self, x, logits):
+        torch = self._torch
+        be = self.backend
+        T = x.shape[0]
+        if self._peer is None:  # collective: the first call of every rank creates the regions
+            cap = self.capacity if self.capacity is not None else T
+            self._peer = self._peer_factory(self.group, self.El, cap, self.d_model, x.dtype, x.device)
+        ex = self._peer
+        if T > ex.cap:
+            raise ValueError(f"{T} tokens exceed the exchange capacity {ex.cap}")
+        expert, gate, counts, slots = be.route(logits)
+        offsets, _, perm = be.plan(counts, slots, slots.shape[1], T)
+        ex.dispatch(x, perm, offsets, counts)               # SRead pack + send over NVLink
+        rows, lcounts = ex.recv_plan()                      # waits for every peer's tokens
+        loff, ltiles, _ = be.plan(lcounts)
+        R = self.world * ex.cap
+        h = torch.empty((R, self.d_ff), dtype=x.dtype, device=x.device)
+        max_tiles = -(-R // 128) + self.El
+        be.grouped_gemm(ex.recv, self.w1, lcounts, loff, ltiles, h, row_src=rows, src_stride=rows.shape[1], act=1,
+                        max_tiles=max_tiles, rows_hint=T)
+        be.grouped_gemm(h, self.w2, lcounts, loff, ltiles, ex.y, row_dst=rows, dst_stride=rows.shape[1],
+                        max_tiles=max_tiles, rows_hint=T)
+        ex.signal()                                         # y ready for the peers' pulls
+        out = torch.empty((T, self.d_model), dtype=x.dtype, device=x.device)
+        ex.combine(perm, offsets, gate, out)                # pull + SWrite * gate
+        self.stats = MoEStats(tokens=T, sent=T, received=-1)
+        return out
 
     __call__ = forward
 

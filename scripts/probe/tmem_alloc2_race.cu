@@ -58,18 +58,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128) alloc2_kernel(i
   }
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) alloc2_dyn_kernel(uint32_t* out) {
+// variant bits: 1 = skip the mbarrier init, 2 = allocate from warp 0 instead of warp 9,
+//               4 = static shared slot instead of the dynamic-smem slot
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) alloc2_dyn_kernel(uint32_t* out, int variant) {
+  __shared__ uint32_t static_slot;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * 32768);
-  uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 6 * 4 + 4);
+  uint32_t* slot = (variant & 4) ? &static_slot : reinterpret_cast<uint32_t*>(bars + 6 * 4 + 4);
   const int warp = threadIdx.x / 32;
-  if (threadIdx.x == 0) {
+  const int alloc_warp = (variant & 2) ? 0 : 9;
+  if (threadIdx.x == 0 && !(variant & 1)) {
     for (int i = 0; i < 6 * 4 + 4; ++i)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bars + i)), "r"(1));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 9) {
+  if (warp == alloc_warp) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
@@ -80,7 +84,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) alloc2_dyn_k
   if (threadIdx.x == 0) out[blockIdx.x] = base;
   fence_before();
   cluster_sync();
-  if (warp == 9) {
+  if (warp == alloc_warp) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(base));
   }
@@ -90,10 +94,11 @@ int main(int argc, char** argv) {
   const int mode = argc > 1 ? atoi(argv[1]) : 0;
   uint32_t* d = nullptr;
   cudaMalloc(&d, 8 * sizeof(uint32_t));
-  if (mode == 3) {
+  if (mode >= 3) {
+    // modes 3..10: rowgemm2's prologue layout with variant = mode - 3 (see alloc2_dyn_kernel)
     const int smem = 6 * 32768 + 2048;
     cudaFuncSetAttribute(alloc2_dyn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    alloc2_dyn_kernel<<<8, 512, smem>>>(d);
+    alloc2_dyn_kernel<<<8, 512, smem>>>(d, mode - 3);
   } else {
     alloc2_kernel<<<8, 128>>>(mode, d);
   }

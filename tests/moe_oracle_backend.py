@@ -51,7 +51,7 @@ class OracleBackend:
         return out
 
     def grouped_gemm(self, A, W, counts, offsets, tiles, out, *, row_src=None, src_stride=0, row_dst=None,
-                     dst_stride=0, row_scale=None, act=0, max_tiles=None):
+                     dst_stride=0, row_scale=None, act=0, max_tiles=None, rows_hint=0):
         for g in range(W.shape[0]):
             c, o = int(counts[g]), int(offsets[g])
             if c == 0:
@@ -65,3 +65,79 @@ class OracleBackend:
                 y = y * row_scale[dst].double()[:, None]
             out[dst] = y.to(out.dtype)
         return out
+
+
+class EmulatedPeerExchange:
+    """CPU restatement of the peer-memory exchange protocol of csrc/pit_ep.cu over gloo.
+
+    Same region layout and row positions as the kernels: source rank s's rows for rank r land in
+    r's receive region at s * cap + (position among the tokens s sends to r, in expert order); the
+    per-expert counts land in r's counts[s]; the receive plan lists a local expert's rows in
+    source-rank order; combine pulls row rank * cap + position from the expert rank's y region.
+    A store into a peer region is emulated by all_to_all_single of the padded per-peer slabs."""
+
+    def __init__(self, group, experts_local, capacity, d_model, dtype, device=None):
+        import torch.distributed as dist
+
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.El, self.cap, self.d_model = experts_local, capacity, d_model
+        R = self.world * self.cap
+        self.recv = torch.zeros((R, d_model), dtype=dtype)
+        self.y = torch.zeros((R, d_model), dtype=dtype)
+        self.counts_in = torch.zeros((self.world, self.El), dtype=torch.int32)
+        self.rows = torch.zeros((self.El, max(R, 1)), dtype=torch.int32)
+        self.lcounts = torch.zeros(self.El, dtype=torch.int32)
+        self._pulled = None
+
+    def _a2a(self, send):
+        import torch.distributed as dist
+
+        recv = torch.empty_like(send)
+        dist.all_to_all_single(recv, send.contiguous(), group=self.group)
+        return recv
+
+    def dispatch(self, x, perm, offsets, counts):
+        W, El, cap = self.world, self.El, self.cap
+        off = offsets.numpy()
+        slab = torch.zeros((W, cap, self.d_model), dtype=x.dtype)
+        for i in range(int(off[-1])):
+            e = int(np.searchsorted(off, i, side="right") - 1)
+            r = e // El
+            slab[r, i - off[r * El]] = x[int(perm[i])]
+        got = self._a2a(slab)  # got[s] = what rank s stored into my region
+        for s in range(W):
+            self.recv[s * cap:(s + 1) * cap] = got[s]
+        self.counts_in = self._a2a(counts.view(W, El).to(torch.int32))
+
+    def recv_plan(self):
+        rc = self.counts_in.numpy()
+        for e in range(self.El):
+            out = 0
+            for s in range(self.world):
+                before, n = int(rc[s, :e].sum()), int(rc[s, e])
+                self.rows[e, out:out + n] = torch.arange(s * self.cap + before, s * self.cap + before + n)
+                out += n
+            self.lcounts[e] = out
+        return self.rows, self.lcounts
+
+    def signal(self):
+        # peer s will pull rows [s*cap, (s+1)*cap) of my y: emulate the pull by sending that slab
+        self._pulled = self._a2a(self.y.view(self.world, self.cap, self.d_model))
+
+    def combine(self, perm, offsets, gate, out):
+        off = offsets.numpy()
+        for i in range(int(off[-1])):
+            e = int(np.searchsorted(off, i, side="right") - 1)
+            r = e // self.El
+            t = int(perm[i])
+            g = float(gate[t]) if gate is not None else 1.0
+            out[t] = (self._pulled[r, i - off[r * self.El]].double() * g).to(out.dtype)
+        return out
+
+    def error(self):
+        return 0
+
+    def close(self):
+        pass

@@ -1,6 +1,8 @@
-"""CPU, world size 2 over gloo: the expert-parallel exchange of SwitchMoE (counts all-to-all,
-token all-to-all-v, receive plan, reverse all-to-all, gate-scaled combine) equals the
-single-process oracle. Compute runs in the test-only oracle backend."""
+"""CPU, world size 2 over gloo: the expert-parallel exchanges of SwitchMoE equal the single-process
+oracle. "nccl": counts all-to-all, token all-to-all-v, receive plan, reverse all-to-all, gate-scaled
+combine. "peer": the peer-memory protocol of csrc/pit_ep.cu (region positions, receive plan, pull
+combine) restated on CPU (tests/moe_oracle_backend.EmulatedPeerExchange). Compute runs in the
+test-only oracle backend."""
 
 import os
 import socket
@@ -31,12 +33,12 @@ def _problem(T, E, d, F, seed):
     return x, logits, w1, w2
 
 
-def _worker(rank, world, port, T, E, d, F, q):
+def _worker(rank, world, port, T, E, d, F, q, exchange="nccl"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from moe_oracle_backend import OracleBackend
+        from moe_oracle_backend import EmulatedPeerExchange, OracleBackend
         from paper_2301_10936_b200.moe import SwitchMoE
 
         x, logits, w1, w2 = _problem(T, E, d, F, seed=5)
@@ -44,20 +46,27 @@ def _worker(rank, world, port, T, E, d, F, q):
         sl = slice(rank * T, (rank + 1) * T)
         layer = SwitchMoE(torch.from_numpy(w1[rank * El : (rank + 1) * El]).double(),
                           torch.from_numpy(w2[rank * El : (rank + 1) * El]).double(), E, group=dist.group.WORLD,
-                          backend=OracleBackend())
+                          backend=OracleBackend(), exchange=exchange,
+                          exchange_factory=EmulatedPeerExchange if exchange == "peer" else None)
         out = layer(torch.from_numpy(x[sl]).double(), torch.from_numpy(logits[sl]))
-        q.put((rank, out.numpy(), layer.stats.received))
+        received = layer.stats.received
+        if exchange == "peer":
+            received = int(layer._peer.lcounts.sum())
+            out2 = layer(torch.from_numpy(x[sl]).double(), torch.from_numpy(logits[sl]))  # regions reused
+            assert torch.equal(out, out2)
+        q.put((rank, out.numpy(), received))
     finally:
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("exchange", ["nccl", "peer"])
 @pytest.mark.parametrize("E", [4, 8])
-def test_expert_parallel_exchange_matches_single_process(E):
+def test_expert_parallel_exchange_matches_single_process(E, exchange):
     T, d, F, world = 37, 16, 24, 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, T, E, d, F, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, T, E, d, F, q, exchange)) for r in range(world)]
     for p in procs:
         p.start()
     results = dict((r, (o, n)) for r, o, n in (q.get(timeout=120) for _ in range(world)))
