@@ -148,6 +148,16 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def max_over_ranks(v: float, dev) -> float:
+    """Max of a per-rank float over all ranks (NCCL on the device; a gloo rehearsal group on the host)."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
@@ -203,8 +213,15 @@ def run_ours(args, w):
     from paper_2301_10936_b200 import _lib
 
     rank, world, local = dist_env()
+    # PIT_BENCH_PG=gloo PIT_BENCH_DEVICE=0: rehearsal of the N-rank path with every rank on one GPU
+    # (functional check of the multi-rank code on a 1-GPU box; its timings are not scaling numbers)
+    if os.environ.get("PIT_BENCH_DEVICE") is not None:
+        local = int(os.environ["PIT_BENCH_DEVICE"])
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("PIT_BENCH_PG", "nccl") == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     _lib.load()
@@ -303,9 +320,7 @@ def run_ours(args, w):
     replay_ok = bool(torch.equal(captured.C, C0.array)) if captured is not None else None
     total_ms = sum(a.elapsed_time(b) for a, b in step_ev)
     if world > 1:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = max_over_ranks(total_ms, dev)
         dist.barrier()
     ms_per_step = total_ms / args.steps
     value = world * eff_flops * args.steps / (total_ms * 1e-3) / 1e12
@@ -468,9 +483,7 @@ def _time_layer(fn, steps, dev, world):
     torch.cuda.synchronize()
     ms = statistics.median(a.elapsed_time(b) for a, b in ev)
     if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms, dev)
     return ms
 
 
@@ -521,7 +534,7 @@ def moe_bench(args, world, rank, dev, peaks, tokens_per_gpu=16384, n_experts=128
     replay_ok = bool(torch.equal(out_g, eager))
     ep_error = layer._peer.error() if layer._peer is not None else 0
     baseline = None
-    if world > 1:
+    if world > 1 and dist.get_backend() == "nccl":
         nccl = SwitchMoE(w1, w2, E, group=group, exchange="nccl")
         for _ in range(max(3, args.warmup)):
             ref_out = nccl(x, logits)
@@ -764,6 +777,7 @@ def attention_bench(args, dev, peaks, heads=12, seq=4096, hd=64):
     torch.cuda.synchronize()
     det_ms = e0.elapsed_time(e1)
     best = max(variants, key=lambda k: variants[k]["value"])
+    scores = attention_scores_bench(args, dev, peaks, blocks, ann_dev, heads, seq, hd, flush)
     out = {"workload": f"Longformer-style P.V: {heads} heads, seq {seq}, head dim {hd}, 32x64 blocks "
                        f"(window +-256, global first block row/col, 2% random), one batched launch for all heads",
            "value": variants[best]["value"], "unit": "TFLOP/s (effective)", "plan": best,
@@ -781,9 +795,75 @@ def attention_bench(args, dev, peaks, heads=12, seq=4096, hd=64):
                         "note": "whole step (index build from the block mask + SpMM) against live P + V + C bytes"},
            "detect_from_values_ms": round(det_ms, 4),
            "detect_from_values_GBps": round(heads * seq * seq * 2 / (det_ms * 1e-3) / 1e9, 1),
-           "execution": "CUDA graph: build_index(mask bits on device) + batched SpMM"}
+           "execution": "CUDA graph: build_index(mask bits on device) + batched SpMM",
+           "scores_sddmm": scores}
     del A3k
     return out
+
+
+def attention_scores_bench(args, dev, peaks, blocks, ann_dev, heads, seq, hd, flush):
+    """C3 producer side: S = Q.K^T per head only inside the 32x64 block mask, all heads
+    in one output-sparse launch (csrc/pit_sddmm.cu), as a CUDA graph of the public call (both output
+    indexes built from the device mask + the SDDMM), L2 flushed. Roofline: HBM — algorithmic bytes =
+    live S written + Q + K read once. Dense cuBLAS Q.K^T (torch.bmm, every score) beside it."""
+    import torch
+
+    from paper_2301_10936_b200.sddmm import run_batched_sddmm
+
+    g = torch.Generator(device=dev).manual_seed(17)
+    Q = torch.randn((heads, seq, hd), device=dev, dtype=torch.bfloat16, generator=g)
+    Kt = torch.randn((heads, seq, hd), device=dev, dtype=torch.bfloat16, generator=g)
+    S = torch.zeros((heads, seq, seq), device=dev, dtype=torch.bfloat16)
+    live = int(blocks.sum()) * 32 * 64
+    stream = torch.cuda.current_stream()
+
+    def step():
+        return run_batched_sddmm(Q, Kt.transpose(1, 2), ann_dev, out=S)
+
+    step()
+    torch.cuda.synchronize()
+    m = torch.from_numpy(blocks[0]).to(dev).repeat_interleave(32, 0).repeat_interleave(64, 1)
+    ref = Q[0].double() @ Kt[0].double().t()
+    err = float((S[0].double()[m] - ref[m]).abs().max() / ref[m].abs().max())
+    eager = S.clone()
+    side = torch.cuda.Stream()
+    side.wait_stream(stream)
+    with torch.cuda.stream(side):
+        step()
+    stream.wait_stream(side)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        step()
+
+    def timed(fn, reps):
+        ev = []
+        for _ in range(reps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            ev.append((e0, e1))
+        torch.cuda.synchronize()
+        return statistics.median(a.elapsed_time(b) for a, b in ev)
+
+    for _ in range(3):
+        graph.replay()
+    ms = timed(graph.replay, max(args.steps, 5))
+    replay_ok = bool(torch.equal(S, eager))
+    Sd = torch.empty((heads, seq, seq), device=dev, dtype=torch.bfloat16)
+    dense_ms = timed(lambda: torch.bmm(Q, Kt.transpose(1, 2), out=Sd), max(args.steps, 5))
+    del Sd
+    nbytes = live * 2 + 2 * heads * seq * hd * 2
+    gbps = nbytes / (ms * 1e-3) / 1e9
+    return {"ms_per_step": round(ms, 4), "effective_TFLOPs": round(2.0 * hd * live / (ms * 1e-3) / 1e12, 2),
+            "roofline": {"bound": "hbm", "achieved": round(gbps, 1), "peak": peaks["hbm"], "unit": "GB/s",
+                         "frac": round(gbps / peaks["hbm"], 4), "algorithmic_bytes": nbytes,
+                         "note": "live S written + Q, K read once; step includes both output indexes built from the device mask"},
+            "dense_cublas_bmm_ms": round(dense_ms, 4), "speedup_vs_dense": round(dense_ms / ms, 2),
+            "max_rel_err_head0_vs_f64": err, "graph_replay_equals_eager": replay_ok,
+            "execution": "CUDA graph: output_indexes(mask bits on device) + run_batched_sddmm"}
 
 
 def opt_bench(args, dev, peaks, tokens=4096, d_model=2048, d_ff=8192, zeros=(0.9, 0.99)):

@@ -48,7 +48,7 @@ typedef enum { PIT_PLAN_DENSE = 0, PIT_PLAN_PIT_M = 1, PIT_PLAN_PIT_K = 2 } pit_
 PIT_API const char* pit_last_error(void);
 
 /* ABI version (major*100 + minor). */
-PIT_API int pit_abi_version(void); /* 102: pit_grouped_gemm_args gained rows_hint; pit_ep_* / pit_moe_dispatch */
+PIT_API int pit_abi_version(void); /* 103: pit_sddmm; 102: pit_grouped_gemm_args.rows_hint, pit_ep_* / pit_moe_dispatch */
 
 /* Number of kernels this library has launched in the process (monotonic; for launch accounting). */
 PIT_API long long pit_kernel_launches(void);
@@ -70,7 +70,7 @@ PIT_API int pit_build_index_from_tensor(const void* values, int dtype, int64_t s
 /*
  * Detection from a block annotation: packed = np.packbits of the row-major block grid (MSB first),
  * granularity (g0,g1). Replaces build_index (index.py:102-161) over a SparsityAnnotation
- * (sparsity.py:27-65).
+ * (sparsity.py:27-65). counts = slots = NULL: only the occupancy bitmap (no compaction launch).
  */
 PIT_API int pit_build_index(const uint8_t* packed, int64_t s0, int64_t s1, int g0, int g1, int t0, int t1, int pit_dim,
                     uint32_t* occ, int32_t* counts, int32_t* slots, void* stream);
@@ -208,6 +208,42 @@ PIT_API int pit_gather_rows(const void* src, int64_t ld_src_bytes, const int32_t
 /* SWrite of whole rows with a per-destination-row scale (MoE combine): dst[rows[i]] = scale[rows[i]] * src[i]. */
 PIT_API int pit_scatter_rows_scaled(const void* src, int dtype, int64_t ld_src, const int32_t* rows, int64_t n,
                                     int64_t width, const float* scale, void* dst, int64_t ld_dst, void* stream);
+
+/*
+ * Output-sparse matmul (SDDMM): C = A . B computed and stored only inside the live
+ * micro-tiles of C's annotation. No reference counterpart is wired: the reference documents the
+ * output-side (n-axis) plan as the mirror of pit:m and leaves it unimplemented (pkg/README.md:150-153,
+ * SPEC.md:496). A row-major [batch*M, K]; B column-major per slice, passed as B^T row-major
+ * [batch*N, K]; C row-major [batch*M, N]. unit_* = index of C's annotation at micro (128, 64) with the
+ * column axis permuted (build_index(ann, (128, 64), "k")); occ = its occupancy at micro (g0, g1) (the
+ * annotation granularity, g1 % 8 == 0). Elements of dead micro-tiles of C are never written. gate
+ * (optional, same layout as C): a stored element is zeroed where gate <= 0 (ReLU-masked gradient).
+ * bf16 / fp16; M % 128 == 0 when batch > 1; N, K, pitches multiples of 8. Workspace:
+ * pit_sddmm_workspace_bytes.
+ */
+typedef struct {
+  int dtype;
+  const void* A;
+  int64_t lda;
+  const void* B;
+  int64_t ldb;
+  void* C;
+  int64_t ldc;
+  int64_t M, N, K, batch;
+  const int32_t* unit_counts;
+  const int32_t* unit_slots;
+  int64_t unit_slot_stride, n_unit_groups;
+  const uint32_t* occ;
+  int64_t words_per_group;
+  int g0, g1;
+  const void* gate;
+  int64_t ldgate;
+  void* workspace;
+  int64_t workspace_bytes;
+} pit_sddmm_args;
+
+PIT_API int64_t pit_sddmm_workspace_bytes(const pit_sddmm_args* args);
+PIT_API int pit_sddmm(const pit_sddmm_args* args, void* stream);
 
 /*
  * Expert-parallel MoE exchange over NVLink peer memory (SURVEY 8(b) pit_moe_dispatch, 8(e)). No reference

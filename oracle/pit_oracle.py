@@ -336,3 +336,19 @@ def reduce_sum(A, ann, pit_axis, tile_shape, dtype=np.float32):
                 if seg.size:
                     C[r] += A[r, seg].sum()
     return C
+
+
+# ------------------------------------------------------------- output-sparse matmul (8(f)3)
+def sddmm(A, B, ann, out, gate=None):
+    """Output-sparse product: out[i, j] = (A . B)[i, j] (f64, k ascending like run_dense_reference,
+    executor.py:267-283) for every element whose annotation block of C is live (sparsity.py:61-65
+    materialize); elements of dead blocks keep their value. With `gate`, stored elements are 0 where
+    gate <= 0. The reference documents this plan (README.md:150-153) without executing
+    it; this is its definition, not a port."""
+    live = materialize(*ann, dtype=np.float64).astype(bool)
+    prod = dense_reference_f64(A, B)
+    if gate is not None:
+        prod = np.where(np.asarray(gate, np.float64) > 0, prod, 0.0)
+    res = np.array(out, dtype=np.float64, copy=True)
+    res[live] = prod[live]
+    return res, live

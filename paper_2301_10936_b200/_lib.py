@@ -69,6 +69,8 @@ EXPORTS = (
     "pit_moe_recv_plan_ep",
     "pit_moe_signal",
     "pit_moe_combine",
+    "pit_sddmm",
+    "pit_sddmm_workspace_bytes",
 )
 
 
@@ -136,6 +138,36 @@ class GroupedGemmArgs(C.Structure):
     ]
 
 
+class SddmmArgs(C.Structure):
+    """Mirror of ``pit_sddmm_args``."""
+
+    _fields_ = [
+        ("dtype", C.c_int),
+        ("A", C.c_void_p),
+        ("lda", C.c_int64),
+        ("B", C.c_void_p),
+        ("ldb", C.c_int64),
+        ("C", C.c_void_p),
+        ("ldc", C.c_int64),
+        ("M", C.c_int64),
+        ("N", C.c_int64),
+        ("K", C.c_int64),
+        ("batch", C.c_int64),
+        ("unit_counts", C.c_void_p),
+        ("unit_slots", C.c_void_p),
+        ("unit_slot_stride", C.c_int64),
+        ("n_unit_groups", C.c_int64),
+        ("occ", C.c_void_p),
+        ("words_per_group", C.c_int64),
+        ("g0", C.c_int),
+        ("g1", C.c_int),
+        ("gate", C.c_void_p),
+        ("ldgate", C.c_int64),
+        ("workspace", C.c_void_p),
+        ("workspace_bytes", C.c_int64),
+    ]
+
+
 class EpArgs(C.Structure):
     """Mirror of ``pit_ep_args``."""
 
@@ -190,8 +222,12 @@ def _declare(lib) -> None:
     lib.pit_moe_recv_plan_ep.argtypes = [ep, vp, i64, vp, vp]
     lib.pit_moe_signal.argtypes = [ep, vp]
     lib.pit_moe_combine.argtypes = [ep, i32, i64, vp, vp, vp, vp, i64, vp]
+    lib.pit_sddmm.argtypes = [C.POINTER(SddmmArgs), vp]
+    lib.pit_sddmm_workspace_bytes.argtypes = [C.POINTER(SddmmArgs)]
+    lib.pit_sddmm_workspace_bytes.restype = i64
     for name in EXPORTS:
-        if name not in ("pit_last_error", "pit_abi_version", "pit_kernel_launches", "pit_spmm_workspace_bytes"):
+        if name not in ("pit_last_error", "pit_abi_version", "pit_kernel_launches", "pit_spmm_workspace_bytes",
+                        "pit_sddmm_workspace_bytes"):
             getattr(lib, name).restype = i32
 
 

@@ -117,7 +117,7 @@ extern "C" {
 
 const char* pit_last_error(void) { return g_err.c_str(); }
 
-int pit_abi_version(void) { return 102; }
+int pit_abi_version(void) { return 103; }
 
 // Diagnostic (not part of include/pit_b200.h): the CTA-pair gathered-K kernel's stage timeline.
 PIT_API int pit_debug_gk2_trace(unsigned long long* host_out_1024) { return pit::gk2_trace_read(host_out_1024); }
@@ -171,10 +171,11 @@ int pit_build_index(const uint8_t* packed, int64_t s0, int64_t s1, int g0, int g
   if (int st = geometry(s0, s1, t0, t1, pit_dim, &ng, &pg, &wg)) return st;
   if (g0 <= 0 || g1 <= 0) return fail(kErrArg, "granularity must be positive, got (%d,%d)", g0, g1);
   if (ng == 0 || pg == 0) return kOk;
-  if (!packed || !occ || !counts || !slots) return fail(kErrArg, "null device pointer");
+  if (!packed || !occ || (!counts) != (!slots)) return fail(kErrArg, "null device pointer");
   DetectBitsArgs a{packed, s0, s1, g0, g1, t0, t1, pit_dim, occ};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (int st = launch_detect_bits(a, s)) return st;
+  if (!counts) return kOk;  // occupancy bitmap only
   return launch_compact(occ, ng, wg, counts, slots, pg, s);
 }
 
@@ -464,6 +465,64 @@ int pit_scatter_rows_scaled(const void* src, int dtype, int64_t ld_src, const in
                                             static_cast<cudaStream_t>(stream));
   if (st == kErrUnsupported) return fail(st, "unsupported dtype code %d", dtype);
   return st;
+}
+
+static void sddmm_copy(const pit_sddmm_args* a, pit::SddmmArgs* o) {
+  o->dtype = a->dtype;
+  o->A = a->A;
+  o->lda = a->lda;
+  o->B = a->B;
+  o->ldb = a->ldb;
+  o->C = a->C;
+  o->ldc = a->ldc;
+  o->M = a->M;
+  o->N = a->N;
+  o->K = a->K;
+  o->batch = a->batch;
+  o->unit_counts = a->unit_counts;
+  o->unit_slots = a->unit_slots;
+  o->unit_slot_stride = a->unit_slot_stride;
+  o->n_unit_groups = a->n_unit_groups;
+  o->occ = a->occ;
+  o->words_per_group = a->words_per_group;
+  o->g0 = a->g0;
+  o->g1 = a->g1;
+  o->gate = a->gate;
+  o->ldgate = a->ldgate;
+  o->workspace = a->workspace;
+  o->workspace_bytes = a->workspace_bytes;
+}
+
+int64_t pit_sddmm_workspace_bytes(const pit_sddmm_args* a) {
+  if (!a) return -1;
+  pit::SddmmArgs s{};
+  sddmm_copy(a, &s);
+  return pit::sddmm_workspace_bytes(s);
+}
+
+int pit_sddmm(const pit_sddmm_args* a, void* stream) {
+  if (!a) return fail(kErrArg, "null args");
+  if (a->M < 0 || a->N < 0 || a->K < 0 || a->batch <= 0) return fail(kErrShape, "shape mismatch: bad SDDMM extents");
+  if (a->M == 0 || a->N == 0) return kOk;
+  if (a->dtype != kDtypeBF16 && a->dtype != kDtypeF16) return fail(kErrUnsupported, "SDDMM needs bf16 or fp16 operands");
+  if (!a->A || !a->B || !a->C || !a->unit_counts || !a->unit_slots || !a->occ)
+    return fail(kErrArg, "null device pointer");
+  if (a->N % 8 || a->K % 8 || a->lda % 8 || a->ldb % 8 || a->ldc % 8 || (a->gate && a->ldgate % 8))
+    return fail(kErrLayout, "SDDMM needs N, K and every pitch to be multiples of 8 elements");
+  if (a->lda < a->K || a->ldb < a->K || a->ldc < a->N) return fail(kErrLayout, "pitch smaller than the row");
+  if ((reinterpret_cast<uintptr_t>(a->A) | reinterpret_cast<uintptr_t>(a->B) | reinterpret_cast<uintptr_t>(a->C) |
+       reinterpret_cast<uintptr_t>(a->gate)) % 16)
+    return fail(kErrLayout, "SDDMM operands must be 16-byte aligned");
+  if (a->g0 <= 0 || a->g1 <= 0 || a->g1 % 8) return fail(kErrShape, "output micro-tile width must be a multiple of 8");
+  if (a->batch > 1 && a->M % 128) return fail(kErrShape, "batched SDDMM needs M to be a multiple of 128");
+  if (a->n_unit_groups != a->batch * ((a->M + 127) / 128))
+    return fail(kErrShape, "unit index does not match C (expected micro-tile (128, 64) with the column axis permuted)");
+  if (a->unit_slot_stride < (a->N + 63) / 64) return fail(kErrShape, "unit index stride below the column-block grid");
+  pit::SddmmArgs s{};
+  sddmm_copy(a, &s);
+  if (a->workspace_bytes < pit::sddmm_workspace_bytes(s) || !a->workspace)
+    return fail(kErrArg, "SDDMM workspace too small (%lld bytes needed)", (long long)pit::sddmm_workspace_bytes(s));
+  return pit::launch_sddmm(s, static_cast<cudaStream_t>(stream));
 }
 
 static int ep_check(const pit_ep_args* ep, pit::EpArgs* out) {

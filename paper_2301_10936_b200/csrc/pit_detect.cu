@@ -297,6 +297,41 @@ __global__ void detect_bits_pow2_kernel(const uint8_t* __restrict__ packed, I s0
   }
 }
 
+// Same geometry as detect_bits_pow2_kernel when a coordinate block is narrower than a word: a warp per
+// (group, word), a lane per coordinate, the word assembled with one ballot. The per-word loop walked
+// 32 coordinates x the group's block rows with dependent loads (a (128, 64) index of a 32x64 block
+// mask: 20 us for 12 KB of bits); here every lane issues its few loads at once.
+template <typename I>
+__global__ void detect_bits_pow2_lane_kernel(const uint8_t* __restrict__ packed, I s0, I s1, int lg0, int lg1,
+                                             int lt0, int lt1, int pit_dim, I n_groups, I pit_grid, I WG,
+                                             uint32_t* __restrict__ occ) {
+  const I bg1 = (s1 + (I(1) << lg1) - 1) >> lg1;
+  const I gs = pit_dim == 0 ? s1 : s0, cs = pit_dim == 0 ? s0 : s1;
+  const int lgt = pit_dim == 0 ? lt1 : lt0, lgg = pit_dim == 0 ? lg1 : lg0;
+  const int lct = pit_dim == 0 ? lt0 : lt1, lcg = pit_dim == 0 ? lg0 : lg1;
+  const int lane = threadIdx.x & 31;
+  const I n_items = n_groups * WG;
+  const I warps = static_cast<I>(gridDim.x) * (blockDim.x >> 5);
+  for (I item = static_cast<I>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); item < n_items; item += warps) {
+    const I g = item / WG, w = item - g * WG;
+    const I glo = (g << lgt) >> lgg;
+    const I ghi = (min((g + 1) << lgt, gs) + (I(1) << lgg) - 1) >> lgg;
+    const I c = w * 32 + lane;
+    bool live = false;
+    if (c < pit_grid) {
+      const I clo = (c << lct) >> lcg;
+      const I chi = (min((c + 1) << lct, cs) + (I(1) << lcg) - 1) >> lcg;
+      for (I gb = glo; gb < ghi && !live; ++gb)
+        for (I cb = clo; cb < chi && !live; ++cb) {
+          const I f = pit_dim == 0 ? cb * bg1 + gb : gb * bg1 + cb;
+          live = (__ldg(packed + (f >> 3)) >> (7 - (f & 7))) & 1;
+        }
+    }
+    const uint32_t word = __ballot_sync(0xffffffffu, live);
+    if (lane == 0) occ[static_cast<int64_t>(g) * WG + w] = word;
+  }
+}
+
 // kPow2: micro-tile and granularity along the coordinate axis are powers of two (lct / lcg their
 // log2), so the coordinate's block range needs shifts, not divisions — the common PIT geometry.
 template <typename I, bool kPow2>
@@ -535,7 +570,14 @@ int launch_detect_bits(const DetectBitsArgs& a, cudaStream_t s) {
   const int lcg = pow2 ? __builtin_ctz(static_cast<unsigned>(cg)) : 0;
   const bool all_pow2 = pow2 && (a.t0 & (a.t0 - 1)) == 0 && (a.t1 & (a.t1 - 1)) == 0 && (a.g0 & (a.g0 - 1)) == 0 &&
                         (a.g1 & (a.g1 - 1)) == 0;
-  if (fits32 && all_pow2) {
+  if (fits32 && all_pow2 && lcg < lct + 5) {
+    const unsigned b3 = static_cast<unsigned>(needed < wave ? needed : wave);  // a warp per (group, word)
+    detect_bits_pow2_lane_kernel<int32_t><<<b3, threads, 0, s>>>(
+        a.packed, static_cast<int32_t>(a.s0), static_cast<int32_t>(a.s1), __builtin_ctz(static_cast<unsigned>(a.g0)),
+        __builtin_ctz(static_cast<unsigned>(a.g1)), __builtin_ctz(static_cast<unsigned>(a.t0)),
+        __builtin_ctz(static_cast<unsigned>(a.t1)), a.pit_dim, static_cast<int32_t>(n_groups),
+        static_cast<int32_t>(pit_grid), static_cast<int32_t>(WG), a.occ);
+  } else if (fits32 && all_pow2) {
     const int64_t items = n_groups * WG;
     const int64_t need = ceil_div(items, threads);
     const unsigned b2 = static_cast<unsigned>(need < wave ? need : wave);

@@ -184,6 +184,30 @@ int launch_ep_signal(const EpArgs& a, cudaStream_t s);
 int launch_ep_combine(const EpArgs& a, int dtype, int64_t T, const int32_t* perm, const int32_t* offsets,
                       const float* gate, void* out, int64_t ldo_bytes, cudaStream_t s);
 
+// ------------------------------------------------------- output-sparse matmul (pit_sddmm.cu)
+struct SddmmArgs {
+  int dtype;
+  const void* A;  // [batch * M, K] row-major, pitch lda
+  int64_t lda;
+  const void* B;  // B^T [batch * N, K] row-major (B column-major per slice), pitch ldb
+  int64_t ldb;
+  void* C;        // [batch * M, N] row-major, pitch ldc
+  int64_t ldc;
+  int64_t M, N, K, batch;
+  const int32_t* unit_counts;  // index of C at micro (128, 64), pit axis = columns
+  const int32_t* unit_slots;
+  int64_t unit_slot_stride, n_unit_groups;
+  const uint32_t* occ;  // C's annotation occupancy at micro (g0, g1), groups = row blocks
+  int64_t words_per_group;
+  int g0, g1;
+  const void* gate;  // optional [batch * M, N], pitch ldgate: stored elements zeroed where gate <= 0
+  int64_t ldgate;
+  void* workspace;
+  int64_t workspace_bytes;
+};
+int64_t sddmm_workspace_bytes(const SddmmArgs& a);
+int launch_sddmm(const SddmmArgs& a, cudaStream_t s);
+
 // Driver entry point for cuTensorMapEncodeTiled (resolved through the runtime, no -lcuda).
 CUresult encode_tensor_map_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner,
                               uint64_t outer, uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_outer,

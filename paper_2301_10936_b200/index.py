@@ -269,6 +269,28 @@ def build_index(ann: SparsityAnnotation, micro_tile, pit_axis: Union[str, int], 
     return idx
 
 
+def build_occupancy(ann: SparsityAnnotation, micro_tile, pit_axis: Union[str, int]):
+    """Only the group-major occupancy bitmap of ``build_index`` (int32 storage [n_groups, words]):
+    one detection launch, no compaction — for consumers that test liveness, not list coordinates
+    (the output-sparse epilogue)."""
+    import torch
+
+    micro = _micro(micro_tile)
+    dim = _pit_dim(pit_axis)
+    n_groups, pit_grid, wg = _geometry(ann.tensor_shape, micro, dim)
+    dev = _device.require_cuda()
+    occ = torch.empty((n_groups, max(wg, 1)), dtype=torch.int32, device=dev)
+    if isinstance(ann.packed, torch.Tensor):
+        packed = ann.packed
+    else:
+        packed = torch.from_numpy(np.ascontiguousarray(ann.packed, dtype=np.uint8)).to(dev)
+    s0, s1 = ann.tensor_shape
+    g0, g1 = ann.granularity
+    _device.check(_lib.load().pit_build_index(packed.data_ptr(), s0, s1, g0, g1, micro[0], micro[1], dim,
+                                              occ.data_ptr(), None, None, _device.stream_ptr()), IndexBuildError)
+    return occ
+
+
 def build_index_from_tensor(values, micro_tile, pit_axis: Union[str, int], workers: int = 1) -> MicroTileIndex:
     """Detection directly on raw values with the exact test ``value != 0.0`` (index.py:164-173).
 
