@@ -52,6 +52,9 @@ WORKLOADS = {
                       desc="BERT-base FFN1 varlen (batch 32 x 128, lengths U[16,128]), padding removed via pit:m"),
 }
 DEFAULT_WORKLOAD = "pitk_c1_8192"
+# BASELINE configs[0] itself: the reference's CPU case (fp32, TF32 off) -- the `c1_fp32_1024` section
+C1_1024 = dict(M=1024, K=1024, N=1024, micro=(32, 1), axis="k", zero=0.90, tile=(32, 64, 32),
+               desc="BASELINE configs[0]: pit:k SpMM 1024^3 fp32, random 32x1 micro-tiles, 90% zero")
 FLUSH_BYTES = 256 << 20
 L2_GATHER_CEILING_GBPS = 11145.6  # best measured L2->SM cp.async gather rate (profiles/r1/copy_probe_l2_patterns.txt)
 
@@ -367,9 +370,7 @@ def run_ours(args, w):
         "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": w["desc"], "name": w["name"], "M": w["M"], "K": w["K"], "N": w["N"],
-                   "micro_tile": list(micro), "pit_axis": axis, "zero_ratio": w["zero"],
-                   "plan_tile": list(w["tile"]), "parallelism": f"replica x{world} (per-GPU work fixed)",
+        "config": {**base_config(w), "parallelism": f"replica x{world} (per-GPU work fixed)",
                    "l2": "flushed (256 MiB write) before every step; inputs also exceed L2",
                    "execution": "CUDA graph of detect+SpMM (paper_2301_10936_b200.graph)" if not args.no_graph
                    else "eager API calls"},
@@ -413,8 +414,23 @@ def run_ours(args, w):
     # ---- end to end through the public API with host buffers
     if rank == 0 and not args.no_e2e:
         result["e2e"] = e2e_ours(args, w, A, B, plan, eff_flops)
+    if rank == 0 and not args.no_c1 and world == 1:
+        try:
+            result["c1_fp32_1024"] = c1_fp32_bench(args, dev, peaks)
+        except Exception as e:
+            result["c1_fp32_1024"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     if rank == 0 and not args.no_cpu_baseline and world == 1:
-        result["cpu_baseline"] = cpu_reference(w, target_s=args.cpu_seconds, procs=1)
+        # the reference's CPU path beside every section (1 core and all host cores, CPU model stated)
+        names = [w["name"]] + [s for s, key in (("c1_1024", "c1_fp32_1024"), ("bert_ffn1", "bert_ffn1"),
+                                                  ("attention", "attention"), ("opt_ffn2", "opt_ffn2"),
+                                                  ("moe", "moe")) if isinstance(result.get(key), dict)
+                                and "error" not in result[key]]
+        cpu = cpu_sections_subprocess(names, args.cpu_seconds)
+        result["cpu_baseline"] = cpu.pop(w["name"], {"error": "missing"})
+        for s, key in (("c1_1024", "c1_fp32_1024"), ("bert_ffn1", "bert_ffn1"), ("attention", "attention"),
+                       ("opt_ffn2", "opt_ffn2"), ("moe", "moe")):
+            if s in cpu:
+                result[key]["cpu_baseline"] = cpu[s]
     if world > 1:
         dist.destroy_process_group()
     return result if rank == 0 else None
@@ -955,6 +971,49 @@ def opt_bench(args, dev, peaks, tokens=4096, d_model=2048, d_ff=8192, zeros=(0.9
     return out
 
 
+def c1_fp32_bench(args, dev, peaks):
+    """BASELINE configs[0] on the GPU: 1024^3 fp32 (TF32 never used: K7 FFMA path, 1e-5 parity),
+    detection from values + SpMM as one CUDA graph, L2 flushed. The reference's own number for this
+    configuration is its CPU time (cpu_baseline, attached by run_ours)."""
+    import torch
+
+    from paper_2301_10936_b200.graph import CapturedSparseMatmul
+
+    w = dict(C1_1024, name="c1_fp32_1024")
+    g = torch.Generator(device=dev).manual_seed(3)
+    keep = torch.rand((w["K"], w["M"] // 32), device=dev, generator=g) >= w["zero"]
+    At = torch.randn((w["K"], w["M"]), device=dev, dtype=torch.float32, generator=g)
+    At.mul_(keep.repeat_interleave(32, dim=1).float())
+    A = At.t()
+    B = torch.randn((w["K"], w["N"]), device=dev, dtype=torch.float32, generator=g)
+    eff = 2.0 * w["N"] * int(keep.sum().item()) * 32
+    plan = make_plan(w)
+    eager = pit_run(plan, A, B, w)
+    ref = A.double() @ B.double()
+    err = float((eager.double() - ref).norm() / ref.norm())
+    captured = CapturedSparseMatmul(plan, A, B)
+    for _ in range(max(3, args.warmup)):
+        captured.replay()
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    ev = []
+    for _ in range(max(10, args.steps)):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        captured.replay()
+        e1.record(stream)
+        ev.append((e0, e1))
+    torch.cuda.synchronize()
+    ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+    return {"workload": w["desc"], "value": round(eff / (ms * 1e-3) / 1e12, 3), "unit": "TFLOP/s (effective)",
+            "ms_per_step": round(ms, 4), "dtype": "f32", "kernel": "spmm_simt (K7 FFMA, fp32, no TF32)",
+            "rel_err_normwise_vs_f64": err, "tolerance": 1e-5,
+            "graph_replay_equals_eager": bool(torch.equal(captured.C, eager)),
+            "gpu_launches_per_step": captured.kernels_per_replay,
+            "execution": "CUDA graph: build_index_from_tensor (32,1) + run_matmul_with_index (pit:k)"}
+
+
 def e2e_ours(args, w, A, B, plan, eff_flops):
     """Host pinned A, B -> H2D -> detection -> SpMM -> D2H of C, all inside the timed region."""
     import torch
@@ -993,95 +1052,277 @@ def e2e_ours(args, w, A, B, plan, eff_flops):
             "api": "build_index_from_tensor + run_matmul_with_index on pinned host buffers (B/C slabs pipelined)"}
 
 
-# ------------------------------------------------------------------ reference CPU restatement
+# --------------------------------------------------------------------------- CPU baselines
+# The reference's own CPU path, timed on the host cores beside the GPU numbers: `pittile` itself
+# from baseline/_ref (the unmodified reference, installed offline: kind "reference") or, when that
+# is absent, its restatement oracle/pit_oracle.py (kind "port"). Every sample runs in a fresh
+# process (`bench.py --cpu-sections ...`) that never touches CUDA, so its fork pool is safe; the
+# work is split over processes by independent units (M-block groups, sequences, heads' query
+# blocks, experts) with no reduction, and each process runs the reference single-threaded
+# (OPENBLAS_NUM_THREADS=1, workers=1: its fastest configuration).
+REF_SITE = ROOT / "baseline" / "_ref"
+MM_EXPR = "C[m,n] += A[m,k] * B[k,n]"
+REF_TILES = {(16, 32, 128), (8, 32, 128), (32, 64, 32), (32, 32, 32)}  # reference tiles.py:106-116
 _CPU = {}
 
 
-def _cpu_worker(groups):
-    from oracle import pit_oracle as orc
-
-    w = _CPU["w"]
-    t0 = w["micro"][0]
-    flops = 0.0
-    for g in groups:
-        A = _CPU["A"][g]                     # [t0, K] rows of one M-block (fp32)
-        ann = _CPU["ann"][g]                 # annotation restricted to the group's rows
-        counts, groups_k = orc.build_index(*ann, w["micro"], w["axis"])
-        orc.matmul_pit_k(A, _CPU["B"], groups_k, w["micro"], w["tile"])
-        flops += 2.0 * w["N"] * t0 * int(counts.sum())
-    return flops
-
-
-def _cpu_setup(w, n_groups, seed=7):
-    """Host operands for a bounded sample of M-block groups of the same workload (fp32: the
-    reference has no bf16, executor.py:40-41)."""
-    from oracle import pit_oracle as orc
-
-    rng = np.random.default_rng(seed)
-    t0 = w["micro"][0]
-    K, N = w["K"], w["N"]
-    _CPU["w"] = w
-    _CPU["B"] = rng.standard_normal((K, N), dtype=np.float32)
-    _CPU["A"], _CPU["ann"] = [], []
-    for g in range(n_groups):
-        ann = orc.random_ann((t0, K), w["micro"], w["zero"], seed=seed + g)
-        _CPU["A"].append(rng.standard_normal((t0, K), dtype=np.float32) * orc.materialize(*ann))
-        _CPU["ann"].append(ann)
+def ref_backend():
+    """pittile from baseline/_ref, or None."""
+    if "backend" not in _CPU:
+        P = None
+        if (REF_SITE / "pittile").is_dir():
+            sys.path.insert(0, str(REF_SITE))
+            try:
+                import pittile as P
+            except Exception:
+                P = None
+        _CPU["backend"] = P
+    return _CPU["backend"]
 
 
-def cpu_reference(w, target_s=8.0, procs=None):
-    """Time the reference algorithm (oracle port: detection + gather/tile-dot/scatter) on a bounded
-    sample of the workload; returns the cpu_baseline object."""
-    if w["axis"] != "k":
-        return {"value": None, "unit": "TFLOP/s", "note": "CPU sampler implemented for pit:k workloads"}
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+def host_cores() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+
+
+def ref_tile(axis: str, tile) -> tuple:
+    """The reference registry has no B200 tile shapes; those run on the reference tile of the same
+    PIT role (its default (32,64,32) for k and dense, (16,32,128) for m)."""
+    tile = tuple(tile)
+    if tile in REF_TILES:
+        return tile
+    return (16, 32, 128) if axis == "m" else (32, 64, 32)
+
+
+def cpu_mm(A, B, axis, tile):
+    """One product through the reference's public path: detection on the values
+    (build_index_from_tensor, index.py:164-173) + run_matmul_with_index (executor.py:464-516).
+    A must already be in the plan's layout (column-major for pit:k)."""
+    P = ref_backend()
+    if P is None:
+        from oracle import pit_oracle as orc
+
+        if axis == "dense":
+            return orc.matmul_dense(A, B, tile)
+        micro = (tile[0], 1) if axis == "k" else (1, tile[1])
+        _, groups = orc.build_index_from_values(A, micro, axis)
+        return (orc.matmul_pit_k if axis == "k" else orc.matmul_pit_m)(A, B, groups, micro, tile)
+    key = (A.shape, B.shape[1], axis, tile)
+    plan = _CPU.setdefault("plans", {}).get(key)
+    if plan is None:
+        expr = P.bind_extents(P.parse_expr(MM_EXPR), dict(m=A.shape[0], k=A.shape[1], n=B.shape[1]))
+        plan = _CPU["plans"][key] = P.forced_plan(expr, axis, P.register_builtin_kernels(), tile_shape=tile)
+    idx = None if axis == "dense" else P.build_index_from_tensor(A, plan.micro_tile, axis)
+    return P.run_matmul_with_index(plan, P.DenseTensor(A), P.DenseTensor(B), idx).array
+
+
+def _relu_mask(rng, shape, gran, zero):
+    keep = rng.random((shape[0] // gran[0], shape[1] // gran[1])) >= zero
+    return np.kron(keep, np.ones(gran, dtype=bool))
+
+
+def cpu_job(name: str, rng):
+    """(units_total, make_unit(i) -> unit data, run(unit) -> work, unit name, work unit, sample text)
+    for one section. Units are generated before the timed region."""
+    if name in WORKLOADS or name == "c1_1024":
+        w = dict(WORKLOADS.get(name, C1_1024), name=name)
+        M, K, N, t0 = w["M"], w["K"], w["N"], w["micro"][0]
+        tile = ref_tile(w["axis"], w["tile"])
+        B = rng.standard_normal((K, N), dtype=np.float32)
+        if w["axis"] == "k":
+            def make(i):
+                A = rng.standard_normal((t0, K), dtype=np.float32) * _relu_mask(rng, (t0, K), (t0, 1), w["zero"])
+                return np.asfortranarray(A)
+
+            total, what = M // t0, f"{t0}-row M-block groups (all K, all N)"
+        elif name.startswith("bert"):
+            def make(i):
+                A = rng.standard_normal((128, K), dtype=np.float32)
+                A[int(rng.integers(16, 129)):] = 0.0
+                return A
+
+            total, what = M // 128, "sequences (128 padded rows each)"
+        else:
+            def make(i):
+                return rng.standard_normal((128, K), dtype=np.float32) * _relu_mask(rng, (128, K), w["micro"], w["zero"])
+
+            total, what = M // 128, "128-row slabs (all K, all N)"
+
+        def run(A):
+            cpu_mm(A, B, w["axis"], tile)
+            return 2.0 * N * np.count_nonzero(A)
+
+        return total, make, run, "TFLOP/s", 1e12, f"{what} of {name}, fp32, plan tile {tile}"
+    if name == "attention":
+        heads, seq, hd = 12, 4096, 64
+        blocks = longformer_blocks(heads, seq, np.random.default_rng(5))  # [heads, seq/32, seq/64]
+        V = rng.standard_normal((seq, hd), dtype=np.float32)
+
+        def make(i):
+            h, qb = divmod(i, seq // 32)
+            live = np.repeat(blocks[h, qb], 64)
+            return np.asfortranarray(rng.random((32, seq), dtype=np.float32) * live)
+
+        def run(P):
+            cpu_mm(P, V, "k", (32, 64, 32))
+            return 2.0 * hd * np.count_nonzero(P)
+
+        return heads * seq // 32, make, run, "TFLOP/s", 1e12, \
+            "32-row query blocks of P.V (12 heads x 4096^2, 32x64 block mask), pit:k (32,1), fp32"
+    if name == "opt_ffn2":
+        tokens, d_ff, d_model, zero = 4096, 8192, 2048, 0.9
+        W2 = rng.standard_normal((d_ff, d_model), dtype=np.float32)
+        dY = rng.standard_normal((tokens, d_model), dtype=np.float32)
+
+        def make(i):
+            if i % 9 == 0:   # forward: 128 token rows of H, pit:m (1,32) -- 1/32 of the forward product
+                return ("m", rng.random((128, d_ff), dtype=np.float32) * _relu_mask(rng, (128, d_ff), (1, 32), zero))
+            # weight gradient: 32 neurons of H^T (all tokens), pit:k (32,1) on H^T column-major -- 1/256 of it
+            return ("k", np.asfortranarray(rng.random((32, tokens), dtype=np.float32) *
+                                           _relu_mask(rng, (tokens, 32), (1, 32), zero).T))
+
+        def run(u):
+            axis, A = u
+            if axis == "m":
+                cpu_mm(A, W2, "m", (16, 32, 128))
+            else:
+                cpu_mm(A, dY, "k", (32, 64, 32))
+            return 2.0 * d_model * np.count_nonzero(A)
+
+        return tokens // 128 + d_ff // 32, make, run, "TFLOP/s", 1e12, \
+            "units of the step (1 forward 128-token slab, pit:m (1,32) H.W2, per 8 weight-grad 32-neuron slabs, " \
+            "pit:k (32,1) H^T.dY: equal FLOPs), 90% zero, fp32"
+    if name == "moe":
+        d_model, d_ff, per_expert = 768, 3072, 128
+
+        def make(i):
+            return (rng.standard_normal((per_expert, d_model), dtype=np.float32),
+                    rng.standard_normal((d_model, d_ff), dtype=np.float32) * 0.03,
+                    rng.standard_normal((d_ff, d_model), dtype=np.float32) * 0.03)
+
+        def run(u):
+            x, w1, w2 = u
+            h = np.maximum(cpu_mm(x, w1, "dense", (32, 64, 32)), 0.0)
+            cpu_mm(np.ascontiguousarray(h, dtype=np.float32), w2, "dense", (32, 64, 32))
+            return float(per_expert)
+
+        return 128, make, run, "tokens/s", 1.0, \
+            "experts of the 128-expert layer (128 tokens each = 16384 tokens), FFN1+ReLU+FFN2 on the dense plan, fp32"
+    raise ValueError(name)
+
+
+def _cpu_run_units(ids):
+    run, units = _CPU["run"], _CPU["units"]
+    return sum(run(units[i]) for i in ids)
+
+
+def cpu_sample(name: str, procs: int, target_s: float, seed: int = 7) -> dict:
+    """Time the reference path on a bounded sample of one section's units with `procs` processes."""
     import multiprocessing as mp
 
-    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    procs = cores if procs is None else procs
-    _cpu_setup(w, 1)
+    rng = np.random.default_rng(seed)
+    total, make, run, unit, scale, what = cpu_job(name, rng)
+    _CPU["run"] = run
+    _CPU["units"] = [make(0)]
     t = time.perf_counter()
-    _cpu_worker([0])
-    per_group = time.perf_counter() - t
-    n = int(max(procs, min(4096, target_s * procs / max(per_group, 1e-3))))
-    n = min(n, w["M"] // w["micro"][0])
-    _cpu_setup(w, n)
-    chunks = [list(range(i, n, procs)) for i in range(procs)]
-    t = time.perf_counter()
+    _cpu_run_units([0])
+    per_unit = time.perf_counter() - t
+    n = int(min(total, max(procs, target_s * procs / max(per_unit, 1e-4))))
+    n = -(-n // procs) * procs if n >= procs else n
+    n = min(n, total)
+    _CPU["units"] = [make(i) for i in range(n)]
+    # small workloads: the whole unit set repeated until the sample is long enough to time
+    reps = max(1, int(target_s * procs / max(per_unit * n, 1e-6))) if n == total else 1
+    chunks = [[j % n for j in range(i, n * reps, procs)] for i in range(procs)]
     if procs == 1:
-        flops = _cpu_worker(chunks[0])
+        t = time.perf_counter()
+        work = _cpu_run_units(chunks[0])
     else:
         with mp.get_context("fork").Pool(procs) as pool:
+            pool.map(_cpu_run_units, [[0]] * procs)  # warm the workers (imports, BLAS init)
             t = time.perf_counter()
-            flops = sum(pool.map(_cpu_worker, chunks))
+            work = sum(pool.map(_cpu_run_units, chunks))
     secs = time.perf_counter() - t
-    return {"value": round(flops / secs / 1e12, 6), "unit": "TFLOP/s", "cores": procs, "kind": "port",
-            "seconds": round(secs, 2),
-            "sample": f"{n} of {w['M'] // w['micro'][0]} M-block groups (all K, all N) of {w['name']}, fp32, "
-                      f"detection + tile loop (oracle/pit_oracle.py), OPENBLAS_NUM_THREADS=1"}
+    _CPU["units"] = []
+    P = ref_backend()
+    return {"value": round(work / secs / scale, 6 if scale > 1 else 1), "unit": unit, "cores": procs,
+            "kind": "reference" if P is not None else "port", "seconds": round(secs, 2),
+            "sample": f"{n} of {total} {what}" + (f", x{reps} passes" if reps > 1 else ""),
+            "implementation": (f"pittile {P.__version__} (the reference, baseline/_ref) public API"
+                               if P is not None else "oracle/pit_oracle.py restatement"),
+            "cpu_model": cpu_model()}
+
+
+def cpu_sections(names, target_s: float) -> dict:
+    """Each section: the reference path on one core and on every host core."""
+    out = {}
+    cores = host_cores()
+    for name in names:
+        try:
+            one = cpu_sample(name, 1, target_s)
+            allc = cpu_sample(name, cores, target_s) if cores > 1 else one
+            out[name] = dict(allc, single_core=one)
+        except Exception as e:  # a CPU sample never costs the GPU line
+            out[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
+    return out
+
+
+def cpu_sections_subprocess(names, target_s: float, timeout: float = 600) -> dict:
+    """cpu_sections in a fresh interpreter (no CUDA context in the forking process)."""
+    import subprocess
+
+    r = subprocess.run([sys.executable, str(Path(__file__).resolve()), "--cpu-sections", ",".join(names),
+                        "--cpu-seconds", str(target_s)], capture_output=True, text=True, timeout=timeout,
+                       env=dict(os.environ, CUDA_VISIBLE_DEVICES=""))
+    try:
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    except (ValueError, IndexError):
+        return {n: {"error": (r.stderr or "no output")[-300:]} for n in names}
+
+
+def base_config(w: dict) -> dict:
+    return {"workload": w["desc"], "name": w["name"], "M": w["M"], "K": w["K"], "N": w["N"],
+            "micro_tile": list(w["micro"]), "pit_axis": w["axis"], "zero_ratio": w["zero"],
+            "plan_tile": list(w["tile"])}
 
 
 def run_reference(args, w):
+    """--impl reference: the reference's own CPU path on every host core, same workload/config."""
     rank, world, _ = dist_env()
     if rank != 0:
         return None
-    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    vals = []
-    base = None
+    cores = host_cores()
+    vals, base = [], None
     for i in range(args.warmup + args.steps):
-        r = cpu_reference(w, target_s=args.ref_seconds, procs=cores)
+        r = cpu_sample(w["name"], cores, args.ref_seconds, seed=7 + i)
         if i >= args.warmup:
             vals.append(r["value"])
             base = r
     value = statistics.mean(vals)
     # one step = the full workload (every M-block group); its expected effective FLOPs / the rate
     step_flops = 2.0 * w["M"] * w["K"] * w["N"] * (1.0 - (w["zero"] or 0.0))
+    cfg = dict(base_config(w), workload=w["desc"].replace("bf16", "fp32 (the reference has no bf16)"), execution=f"reference CPU path, {cores} processes x 1 thread, fp32 "
+                                         "(the reference has no bf16, executor.py:40-41)")
     return {
         "impl": "reference", "metric": "PIT sparse matmul effective TFLOP/s (online detection + SpMM)",
         "value": round(value, 6), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(step_flops / (value * 1e12) * 1e3, 1) if value > 0 else None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": {"workload": w["desc"], "name": w["name"]},
-        "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": base["cores"], "kind": "port",
-                         "sample": base["sample"]},
+        "ms_per_step": round(step_flops / (value * 1e12) * 1e3, 1) if value > 0 else None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": cfg,
+        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample", "implementation",
+                                               "cpu_model")} | {"value": round(value, 6)},
         "e2e": {"value": round(value, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -1102,9 +1343,14 @@ def main():
     ap.add_argument("--no-bert", action="store_true", help="skip the C2 BERT varlen FFN1 section")
     ap.add_argument("--no-opt", action="store_true", help="skip the C4 OPT FFN2 section")
     ap.add_argument("--no-graph", action="store_true", help="time eager API calls instead of the captured step")
-    ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--no-c1", action="store_true", help="skip the BASELINE configs[0] (1024^3 fp32) section")
+    ap.add_argument("--cpu-seconds", type=float, default=3.0, help="target seconds per CPU-baseline sample")
+    ap.add_argument("--cpu-sections", default=None, help=argparse.SUPPRESS)  # internal: CPU samples, no CUDA
     ap.add_argument("--ref-seconds", type=float, default=4.0)
     args = ap.parse_args()
+    if args.cpu_sections:
+        print(json.dumps(cpu_sections(args.cpu_sections.split(","), args.cpu_seconds)), flush=True)
+        return
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # one process per GPU: re-launch this command under torchrun (the driver may also launch it so)
         import socket

@@ -90,12 +90,23 @@ __global__ void __launch_bounds__(256) detect_row_any_kernel(const uint8_t* __re
   const int vpr = static_cast<int>(row_bytes >> 4);  // 16-byte vectors per row
   const int nv = rows * vpr;
   uint32_t mask = 0;
-#pragma unroll 4
-  for (int v = threadIdx.x; v < nv; v += 256) {
-    const int r = v / vpr, c = v - r * vpr;
-    const uint4 q = __ldg(reinterpret_cast<const uint4*>(x + (r0 + r) * ld_bytes) + c);
-    const bool live = ((q.x & lm.even) | (q.y & lm.odd) | (q.z & lm.even) | (q.w & lm.odd)) != 0;
-    mask |= static_cast<uint32_t>(live) << r;
+  // up to 16 vectors per thread in flight before any is tested (one DRAM round trip for a 32-row
+  // block of BERT's 1536-byte rows, instead of one per 4 loads)
+  constexpr int U = 16;
+  for (int v0 = threadIdx.x; v0 < nv; v0 += 256 * U) {
+    uint4 q[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int v = v0 + u * 256;
+      const int r = v / vpr, c = v - r * vpr;
+      q[u] = v < nv ? __ldg(reinterpret_cast<const uint4*>(x + (r0 + r) * ld_bytes) + c) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int v = v0 + u * 256;
+      const bool live = ((q[u].x & lm.even) | (q[u].y & lm.odd) | (q[u].z & lm.even) | (q[u].w & lm.odd)) != 0;
+      mask |= static_cast<uint32_t>(live && v < nv) << ((v / vpr) & 31);
+    }
   }
   mask = __reduce_or_sync(0xffffffffu, mask);
   if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = mask;

@@ -1269,6 +1269,10 @@ struct RowGemmParams {
                             // when the union holds >= contig_pct% of the rows
   const int32_t* kg_cnt;    // masked: live rows per K-group (the pit:m index counts)
   int mask_tma;             // rowgemm, staged contiguous rows: A tiles by TMA + dead micro-tiles zeroed
+  int a_rows;               // rows of A when it is not M (packed live rows); 0: M
+  int epi8;                 // rowgemm2: 8 epilogue warps when the producer warps 4-7 are idle
+  const uint32_t* zero_occ; // rowgemm2, one-K-group pit:m: live-row bitmap; its dead C rows [0, M) are
+                            // cleared by the otherwise idle warps 9 and 11 (no separate clearing launch)
 };
 
 template <int KS, int kBN = 256>
@@ -1814,11 +1818,20 @@ struct Rg2Cfg {
   static constexpr int A_BYTES = 128 * KS * 2;        // K-major rows, 128B swizzle
   static constexpr int B_BYTES = 2 * KS * 128;        // the CTA's 128-column half: 2 MN-major atoms
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STG_BYTES = 4 * 4096;
+  // one 32 x 64 staging box per epilogue warp: 8 warps when the producer warps 4-7 are idle
+  // (A and B by TMA from one thread), else 4
+  // (4-warp modes keep their per-mode tables in the upper half: grouped prefix, masked occupancy)
+  static constexpr int STG_BYTES = 8 * 4096;
+  static constexpr int PTO_OFF = 4 * 4096, OCC_OFF = PTO_OFF + 4352, KBL_OFF = OCC_OFF + 4 * 2048;
   static constexpr int STAGE_BUDGET = 232448 - 2048 - STG_BYTES;
   static constexpr int STAGES = STAGE_BUDGET / STAGE_BYTES > 8 ? 8 : STAGE_BUDGET / STAGE_BYTES;
   static constexpr size_t SMEM = static_cast<size_t>(STAGES) * STAGE_BYTES + STG_BYTES + 2048;
 };
+
+static_assert((kRg2MaxGroups + 1) * 4 <= Rg2Cfg::OCC_OFF - Rg2Cfg::PTO_OFF, "rowgemm2 group prefix");
+static_assert(kRg2OccGroups * 4 * 4 <= Rg2Cfg::KBL_OFF - Rg2Cfg::OCC_OFF, "rowgemm2 occupancy words");
+static_assert(Rg2Cfg::KBL_OFF + 128 <= Rg2Cfg::STG_BYTES, "rowgemm2 staging half");
+static_assert(Rg2Cfg::SMEM <= 232448, "rowgemm2 shared memory");
 
 // CTA r's 128-row tile of pair tile pt (rows may be <= 0: a partial pair, nothing stored).
 // Grouped (MoE experts): pto = shared prefix of ceil(cnt[g] / 256) over the groups.
@@ -1845,9 +1858,14 @@ __device__ __forceinline__ RowTile decode_pair_tile(const RowGemmParams& p, int 
 template <bool kBF16>
 __global__ void __launch_bounds__(kThreads, 1)
     rowgemm2_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmA,
-                    const __grid_constant__ RowGemmParams p, int n_tiles, int pair_tiles) {
+                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ RowGemmParams p, int n_tiles,
+                    int pair_tiles, int c_tma) {
   using Cfg = Rg2Cfg;
   constexpr int KS = Cfg::KS;
+  // diagnostic builds: globaltimer stamps of pair 0 (even CTA) into g_gk2_trace (scripts/rg2_trace.py):
+  // [0,128) producer stage issue, [128,256) relay full (odd CTA: [384,512)), [256,384) MMA pair_full, [512,576) MMA unit
+  // start, [576,640) epilogue TMEM full, [640,704) epilogue done, 767 setup done, [768,1024) CTA entry
+  if (PIT_DIAG && threadIdx.x == 0 && blockIdx.x < 256) g_gk2_trace[768 + blockIdx.x] = gtimer();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stg = smem + Cfg::STAGES * Cfg::STAGE_BYTES;
@@ -1868,28 +1886,65 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
+  // A and B by TMA from one thread (no masking): producer warps 4-7 drain columns 128-255 of each
+  // accumulator beside warps 12-15 (columns 0-127), halving the exposed epilogue
+  const bool epi8 = p.epi8 && p.a_tma && !p.masked && p.cnt == nullptr;
+  const bool epi_warp = warp >= kEpiWarp0 || (epi8 && warp >= 4 && warp < kProdWarps);
+
   const int pair = static_cast<int>(blockIdx.x >> 1);
   const int npairs = static_cast<int>(gridDim.x >> 1);
+  const bool trace = PIT_DIAG && pair == 0 && rank == 0;
+  int tj = 0, tu = 0;  // trace counters (diagnostic builds)
   // masked (2-D pit:m with scattered per-row K patterns): decided on the device from the union size;
   // when the union is small the union-row rowgemm launched beside this kernel runs the product
   if (p.masked && p.n_rows != nullptr &&
       static_cast<int64_t>(*p.n_rows) * 100 < static_cast<int64_t>(p.M) * p.contig_pct)
     return;
   const int single_rows = p.masked ? p.M : (p.n_rows ? *p.n_rows : p.M);
-  __shared__ int pto[kRg2MaxGroups + 1];  // grouped: prefix of pair tiles per group
-  __shared__ uint32_t tile_occ[kRg2OccGroups * 4];  // masked: the CTA's 128 rows' words per K-group
+  // pair row tiles that hold rows: one group of union rows from the device row count (the host sized
+  // the grid for every row of A); grouped: from the device prefix, after the setup barrier
+  int pt_live = pair_tiles;
+  if (p.cnt == nullptr && !p.masked && p.uniform_rows == 0 && p.n_rows != nullptr)
+    pt_live = min(pair_tiles, (single_rows + 255) >> 8);
+  int units = pt_live * n_tiles;
+  // unit -> (pair row tile, n tile). One group (dense, BERT): rasterised in bands of kRg2Band pair
+  // row tiles, n tile outer within a band, so the pairs running together share B n-tile slabs and
+  // an A row band in L2 (row-tile-major order re-streamed all of B for every wave of row tiles).
+  const bool banded = p.cnt == nullptr && p.uniform_rows == 0 && units >= 8 * npairs;  // (grouped: never)
+  auto unit_pt = [&](int u) {
+    if (!banded) return u / n_tiles;
+    const int band = u / (kRg2Band * n_tiles), in = u - band * kRg2Band * n_tiles;
+    const int bh = min(kRg2Band, pt_live - band * kRg2Band);
+    return band * kRg2Band + in % bh;
+  };
+  auto unit_nt = [&](int u) {
+    if (!banded) return u % n_tiles;
+    const int band = u / (kRg2Band * n_tiles), in = u - band * kRg2Band * n_tiles;
+    const int bh = min(kRg2Band, pt_live - band * kRg2Band);
+    return in / bh;
+  };
+  // the first unit's first stages are requested by warp 1 between the arrival on and the wait at the
+  // setup barrier (local shared memory and barriers only): their load latency overlaps the TMEM
+  // allocation and the cluster barrier; the producer thread skips them
+  int early = (p.a_tma && !p.masked && p.cnt == nullptr && pair < units) ? min(Cfg::STAGES, (p.K + KS - 1) / KS) : 0;
+  // grouped: prefix of pair tiles per group; masked: the CTA's 128 rows' words per K-group and the
+  // globally live K-blocks (both in the staging half the 4-warp epilogue leaves free)
+  int* pto = reinterpret_cast<int*>(stg + Cfg::PTO_OFF);
+  uint32_t* tile_occ = reinterpret_cast<uint32_t*>(stg + Cfg::OCC_OFF);
+  uint32_t* kbl = reinterpret_cast<uint32_t*>(stg + Cfg::KBL_OFF);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < Cfg::STAGES; ++i) {
       // every operand by TMA (dense, packed rows): the issuing thread's arrival alone
-      mbar_init(&full_bar[i], mask_tma ? kMaskers : (p.a_tma ? 1 : kProdThreads + 1));
+      // cp.async rows: one arrival per producer warp, kLag stages behind its copies (below)
+      mbar_init(&full_bar[i], mask_tma ? kMaskers : (p.a_tma ? 1 : kProdWarps + 1));
       mbar_init(&loaded_bar[i], 1);
       mbar_init(&pair_full[i], 2);
       mbar_init(&empty_bar[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
-      mbar_init(&tempty_bar[i], 8);  // 4 epilogue warps x 2 CTAs
+      mbar_init(&tempty_bar[i], epi8 ? 16 : 8);  // epilogue warps x 2 CTAs
     }
     fence_mbar_init();
     tma_prefetch_desc(&tmB);
@@ -1917,7 +1972,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   // masked: K-blocks in which no row of the whole operand is live (dead neurons: column-structured
   // activation sparsity) are skipped by every role of both CTAs — a global property, so the pair
   // agrees without exchanging anything
-  __shared__ uint32_t kbl[32];
   if (p.masked) {
     const int nkb = (p.K + KS - 1) / KS, nkg = (p.K + p.t1 - 1) / p.t1;
     for (int kb0 = warp * 32; kb0 < nkb; kb0 += (kThreads / 32) * 32) {
@@ -1932,10 +1986,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   tc_fence_before();
-  cluster_sync();
+  __syncthreads();  // the barrier inits are visible to warp 1
+  cluster_arrive();
+  if (warp == 1 && early > 0) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tmA);
+      const RowTile rt = decode_pair_tile(p, unit_pt(pair), static_cast<int>(rank), single_rows, pto);
+      const int n0 = unit_nt(pair) * Cfg::BN + 128 * static_cast<int>(rank);
+      for (int kb = 0; kb < early; ++kb) {
+        uint8_t* sAp = smem + kb * Cfg::STAGE_BYTES;
+        uint8_t* sB = sAp + Cfg::A_BYTES;
+        mbar_expect_tx_only(&full_bar[kb], Cfg::B_BYTES + Cfg::A_BYTES);
+        tma_load_3d(sB, &tmB, &full_bar[kb], n0, kb * KS, rt.g);
+        tma_load_3d(sB + KS * 128, &tmB, &full_bar[kb], n0 + 64, kb * KS, rt.g);
+        tma_load_2d(sAp, &tmA, &full_bar[kb], kb * KS, rt.base);
+        mbar_arrive(&full_bar[kb]);
+      }
+    }
+    __syncwarp();
+  }
+  cluster_wait();
   tc_fence_after();
+  if (trace && threadIdx.x == 0) g_gk2_trace[767] = gtimer();
   const uint32_t tmem_base = *tmem_slot;
-  const int units = (p.cnt != nullptr ? min(pair_tiles, pto[p.G]) : pair_tiles) * n_tiles;
+  if (p.cnt != nullptr) {  // grouped: pair row tiles from the device prefix
+    pt_live = min(pair_tiles, pto[p.G]);
+    units = pt_live * n_tiles;
+  }
   const int kblocks = (p.K + KS - 1) / KS;
   auto next_kb = [&](int kb) {  // masked: next live K-block after kb (kblocks: none)
     if (!p.masked) return kb + 1;
@@ -1955,24 +2032,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int w = 0; w < (kblocks + 31) / 32; ++w) nlive_kb += __popc(kbl[w]);
   }
   const bool all_kb = nlive_kb == kblocks;  // the common case keeps the plain K-block loop
-  // unit -> (pair row tile, n tile). One group (dense, BERT): rasterised in bands of kRg2Band pair
-  // row tiles, n tile outer within a band, so the pairs running together share B n-tile slabs and
-  // an A row band in L2 (row-tile-major order re-streamed all of B for every wave of row tiles).
-  const bool banded = p.cnt == nullptr && p.uniform_rows == 0 && units >= 8 * npairs;
-  auto unit_pt = [&](int u) {
-    if (!banded) return u / n_tiles;
-    const int band = u / (kRg2Band * n_tiles), in = u - band * kRg2Band * n_tiles;
-    const int bh = min(kRg2Band, pair_tiles - band * kRg2Band);
-    return band * kRg2Band + in % bh;
-  };
-  auto unit_nt = [&](int u) {
-    if (!banded) return u % n_tiles;
-    const int band = u / (kRg2Band * n_tiles), in = u - band * kRg2Band * n_tiles;
-    const int bh = min(kRg2Band, pair_tiles - band * kRg2Band);
-    return in / bh;
-  };
 
-  if ((warp < kProdWarps || warp == kIssuerWarp) && mask_tma) {
+
+  if (epi_warp) {
+    // handled below (epilogue)
+  } else if ((warp < kProdWarps || warp == kIssuerWarp) && mask_tma) {
     // ------------------------------------------------------------ producers, masked + TMA A
     const int nkg = (p.K + p.t1 - 1) / p.t1;
     const int lg_t1 = __ffs(p.t1) - 1;  // t1 in {16, 32}
@@ -2057,6 +2121,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t phase = 0;
     const int nkg = p.masked ? (p.K + p.t1 - 1) / p.t1 : 0;
     const int lg_t1 = p.masked ? __ffs(p.t1) - 1 : 0;  // masked: t1 in {16, 32}
+#ifndef PIT_RG2_LAG
+#define PIT_RG2_LAG 3
+#endif
+    constexpr int kLag = PIT_RG2_LAG;  // stages between a warp's copies and its arrival
+    int lagged = 0;  // stages whose copies this thread issued
     // A and B both by TMA: one thread runs the ring (255 per-stage arrivals were pure overhead)
     const int u_first = (p.a_tma && tp != 0) ? units : pair;
     for (int u = u_first; u < units; u += npairs) {
@@ -2083,10 +2152,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       for (int kb = kb_first; kb < kblocks; kb = all_kb ? kb + 1 : next_kb(kb)) {
         const int k0 = kb * KS;
+        if (early > 0) {  // issued before the setup barrier (thread 0 only; ring slots 0 .. early-1)
+          --early;
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+          continue;
+        }
         mbar_wait(&empty_bar[stage], phase ^ 1);
         uint8_t* sAp = smem + stage * Cfg::STAGE_BYTES;
         uint8_t* sB = sAp + Cfg::A_BYTES;
         if (tp == 0) {
+          if (trace && tj < 128) g_gk2_trace[tj++] = gtimer();
           mbar_expect_tx_only(&full_bar[stage], Cfg::B_BYTES + (p.a_tma ? Cfg::A_BYTES : 0));
           tma_load_3d(sB, &tmB, &full_bar[stage], n0, k0, rt.g);
           tma_load_3d(sB + KS * 128, &tmB, &full_bar[stage], n0 + 64, k0, rt.g);
@@ -2108,12 +2186,30 @@ __global__ void __launch_bounds__(kThreads, 1)
             cp_async_16(sA + swz<7>(static_cast<uint32_t>(row * 128 + ch * 16)), src, bytes);
           }
         }
-        if (!p.a_tma) cp_async_arrive_noinc(&full_bar[stage]);
+        if (!p.a_tma) {
+          // the warp's copies of this stage form one group; the group kLag stages older is waited
+          // for and signalled with one arrival per warp (256 per-thread cp.async arrivals on one
+          // barrier serialised the ring: 0.7 us per stage against 0.45 for TMA-fed A)
+          cp_async_commit();
+          if (++lagged > kLag) {
+            cp_async_wait<kLag>();
+            fence_proxy_async_smem();  // generic-proxy cp.async writes -> tcgen05.mma reads
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full_bar[(stage + Cfg::STAGES - kLag) % Cfg::STAGES]);
+          }
+        }
         if (++stage == Cfg::STAGES) {
           stage = 0;
           phase ^= 1;
         }
       }
+    }
+    if (!p.a_tma && lagged > 0) {  // the last kLag stages
+      cp_async_wait<0>();
+      fence_proxy_async_smem();
+      __syncwarp();
+      for (int j = min(lagged, kLag); j >= 1; --j)
+        if (lane == 0) mbar_arrive(&full_bar[(stage + Cfg::STAGES - j) % Cfg::STAGES]);
     }
   } else if (warp == kRelayWarp) {
     // ------------------------------------------------------------ relay: local full -> pair full
@@ -2124,6 +2220,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int u = pair; u < units; u += npairs) {
         for (int kb = kb_first; kb < kblocks; kb = all_kb ? kb + 1 : next_kb(kb)) {
           mbar_wait(&full_bar[stage], phase);
+          if (PIT_DIAG && pair == 0 && tj < 128) g_gk2_trace[(rank ? 384 : 128) + tj++] = gtimer();
           fence_proxy_async_smem();
           mbar_arrive_cluster(leader_pf + stage * 8);
           if (++stage == Cfg::STAGES) {
@@ -2144,9 +2241,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int u = pair; u < units; u += npairs) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
+        if (trace && lane == 0 && tu < 64) g_gk2_trace[512 + tu++] = gtimer();
         for (int kb = kb_first; kb < kblocks; kb = all_kb ? kb + 1 : next_kb(kb)) {
           mbar_wait(&pair_full[stage], phase);
           tc_fence_after();
+          if (trace && lane == 0 && tj < 128) g_gk2_trace[256 + tj++] = gtimer();
           if (lane == 0) {
             const uint32_t sA = smem_u32(smem + stage * Cfg::STAGE_BYTES);
             const uint32_t sB = sA + Cfg::A_BYTES;
@@ -2171,12 +2270,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (acc == 0) acc_phase ^= 1;
       }
     }
-  } else if (warp >= kEpiWarp0) {
+  } else if ((warp == kAllocWarp || warp == kIssuerWarp) && p.zero_occ != nullptr) {
+    // ------------------------------------------------------------ dead rows of C: exact zeros
+    // (rows no group names), a warp per row, 16-byte stores, beside the mainloop
+    const int zw = 2 * static_cast<int>(blockIdx.x) + (warp == kAllocWarp ? 0 : 1);
+    const int nzw = 2 * static_cast<int>(gridDim.x);
+    const int chunks = p.N >> 3;
+    for (int r = zw; r < p.M; r += nzw) {
+      if ((__ldg(p.zero_occ + (r >> 5)) >> (r & 31)) & 1u) continue;
+      uint4* dst = reinterpret_cast<uint4*>(static_cast<uint8_t*>(p.C) + static_cast<int64_t>(r) * p.ldc * 2);
+      for (int i = lane; i < chunks; i += 32) dst[i] = make_uint4(0u, 0u, 0u, 0u);
+    }
+  }
+  if (epi_warp) {
     // ------------------------------------------------------------ epilogue: this CTA's 128 rows
     using T = typename OutT<kBF16>::T;
     const int q = warp & 3;
+    const int half = (epi8 && warp < kProdWarps) ? 1 : 0;  // epi8: warps 4-7 take boxes 2-3
+    const int bx0 = epi8 ? 2 * half : 0, bx1 = epi8 ? 2 * half + 2 : Cfg::BN / 64;
     const uint32_t leader_te = mapa_shared(smem_u32(tempty_bar), 0);
-    const uint32_t box = smem_u32(stg) + static_cast<uint32_t>(q * 4096);
+    const uint32_t box = smem_u32(stg) + static_cast<uint32_t>((half * 4 + q) * 4096);
     T* C = static_cast<T*>(p.C);
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -2188,8 +2301,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float scale = (row >= 0 && p.row_scale) ? __ldg(p.row_scale + row) : 1.0f;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
+      if (trace && q == 0 && half == 0 && lane == 0 && tu < 64) g_gk2_trace[576 + tu] = gtimer();
+      // consecutive destination rows (dense, batched slices, masked pit:m): the warp's 32 x 64 boxes
+      // leave as TMA tile stores (clipped at the tensor's last row); a box that would cross into the
+      // next slice, and scattered rows, take the row-segment stores
+      bool box_tma = c_tma && rt.rows > q * 32 && (p.uniform_rows == 0 || rt.rows >= q * 32 + 32);
+      if (box_tma && p.row_dst != nullptr) {  // scattered rows (pit:m union rows): runs of 32 go by TMA
+        const int row0 = __shfl_sync(0xffffffffu, row, 0);
+        box_tma = rt.rows >= q * 32 + 32 && __all_sync(0xffffffffu, row == row0 + lane);
+      }
+      const int box_row0 = p.row_dst != nullptr ? __shfl_sync(0xffffffffu, row, 0) : rt.base + q * 32;
 #pragma unroll 1
-      for (int bx = 0; bx < Cfg::BN / 64; ++bx) {
+      for (int bx = bx0; bx < bx1; ++bx) {
         uint32_t v[64];
         const uint32_t ta = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * Cfg::BN + bx * 64);
         if (kb_first < kblocks) {
@@ -2200,6 +2323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 64; ++j) v[j] = 0u;
         }
+        if (box_tma && lane == 0) bulk_wait_read<0>();  // the previous box's store has read the staging
         __syncwarp();
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -2213,6 +2337,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           st_shared_v4(box + lane * 128 + ((static_cast<uint32_t>(j) ^ static_cast<uint32_t>(lane & 7)) << 4),
                        pack2(f[0], f[1], kBF16), pack2(f[2], f[3], kBF16), pack2(f[4], f[5], kBF16),
                        pack2(f[6], f[7], kBF16));
+        }
+        if (box_tma) {
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0 && n0 + bx * 64 < p.N) {
+            tma_store_2d(&tmC, box, n0 + bx * 64, box_row0);
+            bulk_commit();
+          }
+          continue;
         }
         __syncwarp();
         const int ch = lane & 7;
@@ -2232,15 +2365,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
+        __syncwarp();  // the staging box is rewritten by the next iteration
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader_te + acc * 8);
+      if (trace && q == 0 && half == 0 && lane == 0 && tu < 64) g_gk2_trace[640 + tu++] = gtimer();
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
   }
 
+  if (epi_warp && lane == 0 && c_tma) bulk_wait<0>();  // TMA stores complete before exit
   tc_fence_before();
   cluster_sync();
   if (warp == kAllocWarp) {
@@ -2779,6 +2915,22 @@ int run_rowgemm(const RowGemmParams& p, const void* B, int64_t ldb, int64_t grou
   return cuda_status();
 }
 
+int rg2_c_tma_enabled() {  // PIT_RG2_CTMA=0: rowgemm2 stores C by row segments only (A/B knob)
+  static int v = [] {
+    const char* e = getenv("PIT_RG2_CTMA");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
+int rg2_epi8_enabled() {  // PIT_RG2_EPI8=0: rowgemm2 drains TMEM with 4 warps only (A/B knob)
+  static int v = [] {
+    const char* e = getenv("PIT_RG2_EPI8");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 int rg2_enabled() {  // PIT_RG2=0: single-CTA rowgemm for the dense / contiguous-row cases too
   static int v = [] {
     const char* e = getenv("PIT_RG2");
@@ -2797,6 +2949,16 @@ int rg2_grouped() {  // PIT_RG2_GROUPED=0: grouped (MoE) GEMMs stay on single-CT
 
 // CTA-pair launch of the dense / contiguous-row rowgemm cases (see rowgemm2_kernel).
 
+// Clears the C rows whose bit in a single-group pit:m bitmap is 0 (a warp per row, 16-byte stores).
+__global__ void __launch_bounds__(256) zero_dead_rows_kernel(const uint32_t* __restrict__ occ, int64_t M,
+                                                             uint8_t* __restrict__ C, int64_t ld_bytes,
+                                                             int64_t row_bytes) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (row >= M || ((__ldg(occ + (row >> 5)) >> (row & 31)) & 1u)) return;
+  uint4* dst = reinterpret_cast<uint4*>(C + row * ld_bytes);
+  for (int64_t i = threadIdx.x & 31; i < row_bytes / 16; i += 32) dst[i] = make_uint4(0u, 0u, 0u, 0u);
+}
+
 template <bool kBF16>
 int run_rowgemm2(const RowGemmParams& p, const void* B, int64_t ldb, int64_t group_stride, cudaStream_t s) {
   using Cfg = Rg2Cfg;
@@ -2810,12 +2972,25 @@ int run_rowgemm2(const RowGemmParams& p, const void* B, int64_t ldb, int64_t gro
     return kErrCuda;
   RowGemmParams q = p;
   q.a_tma = 0;
+  q.epi8 = rg2_epi8_enabled();
   if (p.row_src == nullptr && (p.lda * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(p.A) & 15) == 0 &&
       a_tma_enabled() && (!p.masked || gm_mask_tma_enabled())) {
-    if (encode_tensor_map_2d(&tmA, dt, p.A, static_cast<uint64_t>(p.K), static_cast<uint64_t>(p.M),
+    if (encode_tensor_map_2d(&tmA, dt, p.A, static_cast<uint64_t>(p.K), static_cast<uint64_t>(p.a_rows ? p.a_rows : p.M),
                              static_cast<uint64_t>(p.lda) * 2, KS, 128, CU_TENSOR_MAP_SWIZZLE_128B) != CUDA_SUCCESS)
       return kErrCuda;
     q.a_tma = 1;
+  }
+  // C by TMA tile stores when the destination rows are consecutive (no scatter list, no groups)
+  CUtensorMap tmC;
+  memset(&tmC, 0, sizeof(tmC));
+  int c_tma = 0;
+  if (p.cnt == nullptr && (p.ldc * 2) % 16 == 0 &&
+      (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && rg2_c_tma_enabled()) {
+    const uint64_t crows = static_cast<uint64_t>(p.uniform_rows ? static_cast<int64_t>(p.G) * p.uniform_rows : p.M);
+    if (encode_tensor_map_2d(&tmC, dt, p.C, static_cast<uint64_t>(p.N), crows, static_cast<uint64_t>(p.ldc) * 2, 64,
+                             32, CU_TENSOR_MAP_SWIZZLE_128B) != CUDA_SUCCESS)
+      return kErrCuda;
+    c_tma = 1;
   }
   const int rows = p.uniform_rows ? p.uniform_rows : p.max_tiles * 128;
   // grouped: the device prefix decides; max_tiles (128-row tiles) bounds the pair tiles
@@ -2823,7 +2998,15 @@ int run_rowgemm2(const RowGemmParams& p, const void* B, int64_t ldb, int64_t gro
                                           : p.uniform_rows ? p.G * ceil_div(p.uniform_rows, 256) : ceil_div(rows, 256));
   const int n_tiles = static_cast<int>(ceil_div(p.N, Cfg::BN));
   const int64_t units = static_cast<int64_t>(pair_tiles) * n_tiles;
-  if (units == 0) return kOk;
+  if (units == 0) {
+    if (p.zero_occ != nullptr) {  // no live row: every row of C is a dead row
+      zero_dead_rows_kernel<<<static_cast<unsigned>(ceil_div(p.M, 8)), 256, 0, s>>>(
+          p.zero_occ, p.M, static_cast<uint8_t*>(p.C), p.ldc * 2, static_cast<int64_t>(p.N) * 2);
+      note_launch();
+      return cuda_status();
+    }
+    return kOk;
+  }
   if (units >= (1ll << 31)) return kErrShape;
   auto kern = rowgemm2_kernel<kBF16>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::SMEM));
@@ -2850,7 +3033,7 @@ int run_rowgemm2(const RowGemmParams& p, const void* B, int64_t ldb, int64_t gro
   }
   const int pairs = static_cast<int>(units < max_pairs ? units : max_pairs);
   cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
-  cudaLaunchKernelEx(&cfg, kern, tmB, tmA, q, n_tiles, pair_tiles);
+  cudaLaunchKernelEx(&cfg, kern, tmB, tmA, tmC, q, n_tiles, pair_tiles, c_tma);
   note_launch();
   return cuda_status();
 }
@@ -2875,6 +3058,11 @@ int rowgemm_dispatch(const RowGemmParams& p, const void* B, int64_t ldb, int ks,
   if (ks == 64 && p.N > 128 && p.occ == nullptr && (p.cnt == nullptr || (p.G <= kRg2MaxGroups && rg2_grouped())) &&
       (p.ldc % 8) == 0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 && rg2_enabled() && !small_single)
     return run_rowgemm2<kBF16>(p, B, ldb, group_stride, s);
+  if (p.zero_occ != nullptr) {  // the single-CTA kernels do not clear dead rows themselves
+    zero_dead_rows_kernel<<<static_cast<unsigned>(ceil_div(p.M, 8)), 256, 0, s>>>(
+        p.zero_occ, p.M, static_cast<uint8_t*>(p.C), p.ldc * 2, static_cast<int64_t>(p.N) * 2);
+    note_launch();
+  }
   if (p.N <= 64) {  // narrow products: 64-column units, no zero-filled B atoms or idle MMA columns
     if (ks == 64) return run_rowgemm<64, kBF16, 64>(p, B, ldb, group_stride, s);
     if (ks == 32) return run_rowgemm<32, kBF16, 64>(p, B, ldb, group_stride, s);
@@ -2885,16 +3073,6 @@ int rowgemm_dispatch(const RowGemmParams& p, const void* B, int64_t ldb, int ks,
   if (ks == 32) return run_rowgemm<32, kBF16, 256>(p, B, ldb, group_stride, s);
   if (ks == 16) return run_rowgemm<16, kBF16, 256>(p, B, ldb, group_stride, s);
   return kErrUnsupported;
-}
-
-// Clears the C rows whose bit in a single-group pit:m bitmap is 0 (a warp per row, 16-byte stores).
-__global__ void __launch_bounds__(256) zero_dead_rows_kernel(const uint32_t* __restrict__ occ, int64_t M,
-                                                             uint8_t* __restrict__ C, int64_t ld_bytes,
-                                                             int64_t row_bytes) {
-  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
-  if (row >= M || ((__ldg(occ + (row >> 5)) >> (row & 31)) & 1u)) return;
-  uint4* dst = reinterpret_cast<uint4*>(C + row * ld_bytes);
-  for (int64_t i = threadIdx.x & 31; i < row_bytes / 16; i += 32) dst[i] = make_uint4(0u, 0u, 0u, 0u);
 }
 
 // Clears C unless the union covers >= pct% of the rows (then the contiguous-tile kernel writes every
@@ -2909,6 +3087,43 @@ __global__ void __launch_bounds__(256) zero_unless_contig_kernel(const int32_t* 
     const int64_t r = i / chunks_per_row, c = i - r * chunks_per_row;
     reinterpret_cast<uint4*>(C + r * ld_bytes)[c] = make_uint4(0u, 0u, 0u, 0u);
   }
+}
+
+// One-K-group pit:m over gathered rows (BERT's padding removal): the live rows of A are copied
+// contiguous into caller scratch first (a warp per row, 16-byte copies, L2-resident right after
+// detection), so the CTA-pair GEMM loads A by TMA like a dense product. cp.async gathers of the
+// same rows held the pair mainloop at ~0.7 us per stage against 0.45 with TMA-fed A (the L2->SM
+// feed of 16-byte copies next to the TMA B tiles, scripts/rg2_trace.py).
+__global__ void __launch_bounds__(256) pack_rows_kernel(const uint8_t* __restrict__ A, int64_t lda_bytes,
+                                                        const int32_t* __restrict__ rows,
+                                                        const int32_t* __restrict__ n_rows, int64_t row_bytes,
+                                                        uint8_t* __restrict__ out) {
+  const int n = *n_rows;
+  const int lane = threadIdx.x & 31;
+  const int64_t chunks = row_bytes >> 4;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5); i < n;
+       i += static_cast<int64_t>(gridDim.x) * 8) {
+    const uint4* src = reinterpret_cast<const uint4*>(A + static_cast<int64_t>(__ldg(rows + i)) * lda_bytes);
+    uint4* dst = reinterpret_cast<uint4*>(out + i * row_bytes);
+    for (int64_t c = lane; c < chunks; c += 32) dst[c] = __ldg(src + c);
+  }
+}
+
+int gm_pack_enabled() {  // PIT_GM_PACK=0: one-K-group pit:m gathers its rows by cp.async (A/B knob)
+  static int v = [] {
+    const char* e = getenv("PIT_GM_PACK");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
+// bytes of scratch run_gm packs the live rows into (0: the case does not pack)
+int64_t gm_pack_bytes(const SpmmArgs& a) {
+  if (a.plan != kPlanPitM || ceil_div(a.K, a.t1) != 1 || a.rows == nullptr || a.n_rows == nullptr || a.N <= 128 ||
+      a.sak != 1 || (a.K * 2) % 16 != 0 || (a.sam * 2) % 16 != 0 || (reinterpret_cast<uintptr_t>(a.A) & 15) != 0 ||
+      !gm_pack_enabled() || !rg2_enabled())
+    return 0;
+  return a.n_rows_host * a.K * 2;
 }
 
 int gm_pairs_enabled() {  // PIT_GM_PAIRS=0: contiguous pit:m stays on the single-CTA rowgemm
@@ -2938,14 +3153,14 @@ bool gm_contig_capable(const SpmmArgs& a) {
 template <bool kBF16>
 int run_gm(const SpmmArgs& a, int ks, cudaStream_t s) {
   const int dense = a.plan == kPlanDense ? 1 : 0;
+  int zero_in_gemm = 0;
   if (!dense) {
     // rows named by no group stay exactly zero. One K-group (BERT's row-uniform micro-tiles): only
     // the dead rows are written (the union is that group's bitmap); otherwise all of C is cleared.
     if (ceil_div(a.K, a.t1) == 1 && a.occ != nullptr && (a.ldc % 8) == 0 && (a.N % 8) == 0 &&
         (reinterpret_cast<uintptr_t>(a.C) & 15) == 0) {
-      zero_dead_rows_kernel<<<static_cast<unsigned>(ceil_div(a.M, 8)), 256, 0, s>>>(
-          a.occ, a.M, static_cast<uint8_t*>(a.C), a.ldc * 2, a.N * 2);
-      note_launch();
+      zero_in_gemm = 1;  // rowgemm2 clears them beside its mainloop; rowgemm_dispatch launches the
+                         // clearing kernel itself when it picks another kernel
     } else if (gm_contig_capable(a) && (a.ldc % 8) == 0 && (a.N % 8) == 0 &&
                (reinterpret_cast<uintptr_t>(a.C) & 15) == 0) {
       // the contiguous-tile kernels write every row: clear C only if the union-row kernel runs
@@ -2977,6 +3192,19 @@ int run_gm(const SpmmArgs& a, int ks, cudaStream_t s) {
   p.WG = a.WG;
   p.t1 = dense ? 1 : a.t1;
   p.max_tiles = static_cast<int>(ceil_div(dense ? a.M : a.n_rows_host, 128));
+  p.zero_occ = zero_in_gemm ? a.occ : nullptr;
+  const int64_t pack_bytes = gm_pack_bytes(a);
+  if (pack_bytes > 0 && a.ws != nullptr && a.ws_bytes >= pack_bytes) {
+    const int64_t blocks = ceil_div(a.n_rows_host, 8);
+    const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
+    pack_rows_kernel<<<static_cast<unsigned>(blocks < cap ? blocks : cap), 256, 0, s>>>(
+        static_cast<const uint8_t*>(a.A), a.sam * 2, a.rows, a.n_rows, a.K * 2, static_cast<uint8_t*>(a.ws));
+    note_launch();
+    p.A = a.ws;
+    p.lda = a.K;
+    p.a_rows = static_cast<int>(a.n_rows_host);  // rows of the packed operand (bounds of its TMA map)
+    p.row_src = nullptr;                         // packed row i is union row i; C rows stay scattered
+  }
   // Scattered per-row K patterns (random (1,32) activation sparsity) make the union of live rows
   // (nearly) every row: union-row tiles then buy nothing and cost a per-row, per-K-block global
   // liveness lookup plus a block-wide vote per stage. The kernel switches (on the device, from the
@@ -3221,6 +3449,7 @@ int launch_rowgemm(const GroupedGemmArgs& g, cudaStream_t s) {
 }
 
 int64_t spmm_tc_workspace_bytes(const SpmmArgs& a) {
+  if (a.plan == kPlanPitM) return gm_pack_bytes(a);  // one-K-group pit:m: packed live rows
   // mirrors dispatch_tc: only the 128-row gathered-K kernel on 64-column units splits groups
   if (a.plan != kPlanPitK || a.t0 <= 64 || a.t0 > 128 || a.N > 64) return 0;
   const char* e = getenv("PIT_GK_NT");

@@ -21,3 +21,29 @@ def test_bench_gpus_flag_spawns_ranks():
     assert len(lines) == 1, r.stdout
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2
+
+
+def test_cpu_sections_one_and_all_cores():
+    """The CPU baselines beside each bench section: the reference path (pittile from baseline/_ref when
+    installed, else the oracle port) on one core and on every host core, CPU model stated."""
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--cpu-sections", "c1_1024,bert_ffn1",
+                        "--cpu-seconds", "0.05"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    for name in ("c1_1024", "bert_ffn1"):
+        s = d[name]
+        assert "error" not in s, s
+        assert s["value"] > 0 and s["unit"] == "TFLOP/s" and s["kind"] in ("reference", "port")
+        assert s["cores"] == len(os.sched_getaffinity(0)) and s["single_core"]["cores"] == 1
+        assert s["cpu_model"]
+
+
+def test_reference_arm_config_matches_ours():
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    w = dict(bench.WORKLOADS[bench.DEFAULT_WORKLOAD], name=bench.DEFAULT_WORKLOAD)
+    cfg = bench.base_config(w)
+    for key in ("M", "K", "N", "micro_tile", "pit_axis", "zero_ratio", "plan_tile", "workload"):
+        assert key in cfg
+    assert "bf16" in cfg["workload"] or "fp32" not in cfg["workload"]
