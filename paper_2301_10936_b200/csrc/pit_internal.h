@@ -133,6 +133,23 @@ bool spmm_tc_supported(const SpmmArgs& a);
 int64_t spmm_tc_workspace_bytes(const SpmmArgs& a);  // scratch the tcgen05 path can use (0: none)
 int gk2_trace_read(unsigned long long* host);  // diagnostic timeline (PIT_GK2_DIAG bit 4)
 
+// ----------------------------------------- K3s: pit:m at very high sparsity (pit_gm_sparse.cu)
+// The sparse path runs when live micro-tiles <= 1/kSparseDen of the (row, K-group) grid (decided on
+// the device from the index counts).
+constexpr int kSparseDen = 48;
+struct GmSparseWs {  // byte offsets into the caller's workspace
+  int64_t flag, cnt, off, U, pre, rows, X, part, bytes;
+};
+int64_t gm_sparse_bound_rows(int64_t M, int64_t nkg, int S);
+GmSparseWs gm_sparse_layout(int64_t M, int64_t N, int64_t WG, int S, int64_t bound_rows);
+int launch_gm_sparse_prep(const int32_t* counts, int nkg, int64_t M, int gps, int S, const uint32_t* occ, int64_t WG,
+                          uint8_t* ws, const GmSparseWs& w, cudaStream_t s);
+int launch_gm_sparse_pack(const int32_t* counts, int nkg, const void* A, int64_t lda_bytes, int S, int64_t M,
+                          const uint32_t* occ, int64_t WG, int t1, int64_t bound_rows, uint8_t* ws, const GmSparseWs& w,
+                          cudaStream_t s);
+int launch_gm_sparse_reduce(const int32_t* counts, int nkg, int dtype, int S, int64_t WG, int64_t N, void* C,
+                            int64_t ldc, int64_t M, uint8_t* ws, const GmSparseWs& w, cudaStream_t s);
+
 // Grouped gathered-row GEMM (MoE experts, batched per-slice plans): see rowgemm in pit_spmm_tc.cu.
 struct GroupedGemmArgs {
   int dtype;

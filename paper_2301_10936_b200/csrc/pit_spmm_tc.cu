@@ -1271,9 +1271,20 @@ struct RowGemmParams {
   int mask_tma;             // rowgemm, staged contiguous rows: A tiles by TMA + dead micro-tiles zeroed
   int a_rows;               // rows of A when it is not M (packed live rows); 0: M
   int epi8;                 // rowgemm2: 8 epilogue warps when the producer warps 4-7 are idle
+  int lagged;               // rowgemm2: per-warp cp.async arrivals kLag stages behind (A/B knob)
+  float* part;              // rowgemm2t: fp32 partial rows (row off[g] + token, pitch N) instead of C
+  int x_stride;             // rowgemm2t: packed token rows of group g start at g * x_stride (0: off[g])
+  const int* path_flag;     // device flag of the high-sparsity pit:m path (pit_gm_sparse.cu): the
+  int path_role;            // kernel runs only if the flag is set (1) / clear (2); 0: always
   const uint32_t* zero_occ; // rowgemm2, one-K-group pit:m: live-row bitmap; its dead C rows [0, M) are
                             // cleared by the otherwise idle warps 9 and 11 (no separate clearing launch)
 };
+
+// The high-sparsity pit:m path and the masked dense kernels are launched together; each leaves unless
+// the flag the sparse path's prep kernel wrote selects it.
+__device__ __forceinline__ bool path_skip(const RowGemmParams& p) {
+  return p.path_flag != nullptr && ((*p.path_flag != 0) != (p.path_role == 1));
+}
 
 template <int KS, int kBN = 256>
 struct GmCfg {
@@ -1362,6 +1373,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                       static_cast<int64_t>(*p.n_rows) * 100 >= static_cast<int64_t>(p.M) * (p.contig_pct % 1000);
   const bool diag_all_live = PIT_DIAG && p.contig_pct >= 1000;  // diagnostic builds: no zero-fill
   if (contig && p.exit_if_contig) return;  // rowgemm2 (masked) runs this product on CTA pairs
+  if (path_skip(p)) return;
   const int32_t* row_src = contig ? nullptr : p.row_src;
   const int32_t* row_dst = contig ? nullptr : p.row_dst;
   const int single_rows = p.cnt ? 0 : contig ? p.M : (p.n_rows ? *p.n_rows : p.M);
@@ -1900,6 +1912,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (p.masked && p.n_rows != nullptr &&
       static_cast<int64_t>(*p.n_rows) * 100 < static_cast<int64_t>(p.M) * p.contig_pct)
     return;
+  if (path_skip(p)) return;
   const int single_rows = p.masked ? p.M : (p.n_rows ? *p.n_rows : p.M);
   // pair row tiles that hold rows: one group of union rows from the device row count (the host sized
   // the grid for every row of A); grouped: from the device prefix, after the setup barrier
@@ -1935,9 +1948,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < Cfg::STAGES; ++i) {
-      // every operand by TMA (dense, packed rows): the issuing thread's arrival alone
-      // cp.async rows: one arrival per producer warp, kLag stages behind its copies (below)
-      mbar_init(&full_bar[i], mask_tma ? kMaskers : (p.a_tma ? 1 : kProdWarps + 1));
+      // every operand by TMA (dense, packed rows): the issuing thread's arrival alone; cp.async rows:
+      // one cp.async arrival per producer thread, or (lagged mode) one per warp kLag stages behind
+      mbar_init(&full_bar[i], mask_tma ? kMaskers : (p.a_tma ? 1 : (p.lagged ? kProdWarps : kProdThreads) + 1));
       mbar_init(&loaded_bar[i], 1);
       mbar_init(&pair_full[i], 2);
       mbar_init(&empty_bar[i], 1);
@@ -2186,10 +2199,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             cp_async_16(sA + swz<7>(static_cast<uint32_t>(row * 128 + ch * 16)), src, bytes);
           }
         }
-        if (!p.a_tma) {
-          // the warp's copies of this stage form one group; the group kLag stages older is waited
-          // for and signalled with one arrival per warp (256 per-thread cp.async arrivals on one
-          // barrier serialised the ring: 0.7 us per stage against 0.45 for TMA-fed A)
+        if (!p.a_tma && !p.lagged) cp_async_arrive_noinc(&full_bar[stage]);
+        if (!p.a_tma && p.lagged) {
+          // lagged mode (PIT_RG2_LAGGED=1, A/B knob): the warp's copies of this stage form one group;
+          // the group kLag stages older is waited for and signalled with one arrival per warp. Same
+          // speed as per-thread arrivals on the BERT product (0.7 us per stage either way: the
+          // cp.async feed, not the barrier, bounds it), so per-thread arrivals stay the default.
           cp_async_commit();
           if (++lagged > kLag) {
             cp_async_wait<kLag>();
@@ -2204,7 +2219,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    if (!p.a_tma && lagged > 0) {  // the last kLag stages
+    if (!p.a_tma && p.lagged && lagged > 0) {  // the last kLag stages
       cp_async_wait<0>();
       fence_proxy_async_smem();
       __syncwarp();
@@ -2400,7 +2415,7 @@ struct Rg2tCfg {
   static constexpr int W_BYTES = 2 * KS * 128;   // weights: the CTA's 128 features, 2 MN-major atoms
   static constexpr int X_BYTES = 128 * KS * 2;   // tokens: up to 128 K-major rows per CTA
   static constexpr int STAGE_BYTES = W_BYTES + X_BYTES;
-  static constexpr int STAGE_BUDGET = 232448 - 2048 - 4 * 1025 * 4;
+  static constexpr int STAGE_BUDGET = 232448 - 2048 - 8 * 1025 * 4 - 4 * 2048;  // static pto + soff, staging
   static constexpr int STAGES = STAGE_BUDGET / STAGE_BYTES > 8 ? 8 : STAGE_BUDGET / STAGE_BYTES;
   static constexpr int STG_BYTES = 4 * 2048;  // per epilogue warp: [32 tokens x 32 features] bf16
   static constexpr size_t SMEM = static_cast<size_t>(STAGES) * STAGE_BYTES + STG_BYTES + 2048;
@@ -2422,12 +2437,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   __shared__ int pto[kRg2MaxGroups + 1];  // prefix of 256-token tiles per group
+  // packed row offsets of the groups when the caller gave none (p.off == nullptr): prefix of cnt
+  __shared__ int soff[kRg2MaxGroups + 1];
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const int pair = static_cast<int>(blockIdx.x >> 1);
   const int npairs = static_cast<int>(gridDim.x >> 1);
+  if (path_skip(p)) return;  // both CTAs of the pair read the same flag
+  // fp32 partial rows from packed tokens (A by TMA from one thread; stores straight from registers):
+  // producer warps 4-7 take every other 32-token block of the epilogue beside warps 12-15
+  const bool epi8 = p.a_tma != 0 && p.part != nullptr;
+  const bool epi_warp = warp >= kEpiWarp0 || (epi8 && warp >= 4 && warp < kProdWarps);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < Cfg::STAGES; ++i) {
@@ -2437,7 +2459,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
-      mbar_init(&tempty_bar[i], 8);
+      mbar_init(&tempty_bar[i], epi8 ? 16 : 8);
     }
     fence_mbar_init();
     tma_prefetch_desc(&tmW);
@@ -2460,6 +2482,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       acc += (__ldg(p.cnt + g) + 255) >> 8;
     }
     if (lane == 31) pto[p.G] = incl;
+    if (p.off == nullptr) {
+      int trun = 0;
+      for (int g = g0; g < min(p.G, g0 + per); ++g) trun += __ldcg(p.cnt + g);
+      int tincl = trun;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, tincl, o);
+        if (lane >= o) tincl += y;
+      }
+      int tacc = tincl - trun;
+      for (int g = g0; g < min(p.G, g0 + per); ++g) {
+        soff[g] = tacc;
+        tacc += __ldcg(p.cnt + g);
+      }
+    }
   }
   tc_fence_before();
   cluster_sync();
@@ -2483,7 +2520,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     return TokTile{lo, start, ntok, (ntok + 15) & ~15};
   };
 
-  if (warp < kProdWarps) {
+  if (warp < kProdWarps && !epi_warp) {
     // ------------------------------------------------------------ producers
     constexpr int CPR = KS * 2 / 16;
     constexpr int RPT = 128 * CPR / kProdThreads;
@@ -2508,7 +2545,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           rid[j] = i < tcnt ? __ldg(p.row_src + static_cast<int64_t>(tt.g) * p.src_stride + t0 + i) : -1;
         }
       }
-      const int xbase = __ldg(p.off + tt.g) + t0;  // packed token rows (TMA path)
+      const int xbase = (p.x_stride ? tt.g * p.x_stride : p.off ? __ldg(p.off + tt.g) : soff[tt.g]) + t0;  // packed rows
       for (int kb = 0; kb < kblocks; ++kb) {
         const int k0 = kb * KS;
         mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -2595,27 +2632,38 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (acc == 0) acc_phase ^= 1;
       }
     }
-  } else if (warp >= kEpiWarp0) {
+  } else if (epi_warp) {
     // ------------------------------------------------------------ epilogue: lane = output feature
     using T = typename OutT<kBF16>::T;
     const int q = warp & 3;
+    const int half = warp < kProdWarps ? 1 : 0;  // epi8: warps 4-7 take the odd 32-token blocks
+    const int cstep = epi8 ? 64 : 32;
     const uint32_t leader_te = mapa_shared(smem_u32(tempty_bar), 0);
     T* C = static_cast<T*>(p.C);
-    const uint32_t stg_w = smem_u32(stg) + static_cast<uint32_t>(q * 2048);
+    const uint32_t stg_w = smem_u32(stg) + static_cast<uint32_t>(q * 2048);  // (bf16 path: 4 warps only)
     const bool vec_ok = (p.ldc % 8) == 0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = pair; u < units; u += npairs) {
       const TokTile tt = decode(u);
       const int ocw = (u % out_tiles) * 256 + 128 * static_cast<int>(rank) + q * 32;  // warp's features
-      const int gbase = __ldg(p.off + tt.g);
+      const int gbase = p.off ? __ldg(p.off + tt.g) : soff[tt.g];
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < tt.ntok; c += 32) {
+      for (int c = half * 32; c < tt.ntok; c += cstep) {
         uint32_t v[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * 256 + c), v);
         tmem_wait_ld();
+        if (p.part != nullptr) {
+          // fp32 partial rows: lane = feature, one coalesced 128-byte segment per token
+          const int f = ocw + lane;
+          float* prow = p.part + (static_cast<int64_t>(gbase) + tt.start + c) * p.N + f;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c + j < tt.ntok && f < p.N) prow[static_cast<int64_t>(j) * p.N] = __uint_as_float(v[j]);
+          continue;
+        }
         // destination row and scale of token c + lane
         const int within = tt.start + c + lane;
         int my_row = -1;
@@ -2973,6 +3021,11 @@ int run_rowgemm2(const RowGemmParams& p, const void* B, int64_t ldb, int64_t gro
   RowGemmParams q = p;
   q.a_tma = 0;
   q.epi8 = rg2_epi8_enabled();
+  static const int lagged_env = [] {
+    const char* e = getenv("PIT_RG2_LAGGED");
+    return e ? atoi(e) : 0;
+  }();
+  q.lagged = lagged_env;
   if (p.row_src == nullptr && (p.lda * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(p.A) & 15) == 0 &&
       a_tma_enabled() && (!p.masked || gm_mask_tma_enabled())) {
     if (encode_tensor_map_2d(&tmA, dt, p.A, static_cast<uint64_t>(p.K), static_cast<uint64_t>(p.a_rows ? p.a_rows : p.M),
@@ -3079,8 +3132,9 @@ int rowgemm_dispatch(const RowGemmParams& p, const void* B, int64_t ldb, int ks,
 // row itself): the decision is the kernels' own, read on the device.
 __global__ void __launch_bounds__(256) zero_unless_contig_kernel(const int32_t* __restrict__ n_rows, int pct,
                                                                  int64_t M, uint8_t* __restrict__ C, int64_t ld_bytes,
-                                                                 int64_t chunks_per_row) {
+                                                                 int64_t chunks_per_row, const int* __restrict__ sparse) {
   if (static_cast<int64_t>(*n_rows) * 100 >= M * pct) return;
+  if (sparse != nullptr && *sparse) return;  // the high-sparsity path writes every row of C
   const int64_t total = M * chunks_per_row;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -3126,6 +3180,32 @@ int64_t gm_pack_bytes(const SpmmArgs& a) {
   return a.n_rows_host * a.K * 2;
 }
 
+int gm_sparse_enabled() {  // PIT_GM_SPARSE=0: no high-sparsity pit:m path (A/B knob)
+  static int v = [] {
+    const char* e = getenv("PIT_GM_SPARSE");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
+// 2-D pit:m products the high-sparsity path (pit_gm_sparse.cu) can take: 16/32-wide micro-columns,
+// K in 256-column supergroups, 16-byte aligned row-major A and C
+bool gm_sparse_capable(const SpmmArgs& a) {
+  if (a.plan != kPlanPitM || a.occ == nullptr || a.counts == nullptr || !(a.t1 == 16 || a.t1 == 32) ||
+      a.K % 256 != 0 || ceil_div(a.K, a.t1) <= 1 || a.sak != 1 || (a.sam * 2) % 16 != 0 ||
+      (reinterpret_cast<uintptr_t>(a.A) & 15) != 0 || (a.ldc % 8) != 0 || (a.N % 8) != 0 ||
+      (reinterpret_cast<uintptr_t>(a.C) & 15) != 0 || a.M >= (1 << 24) || !gm_sparse_enabled() || !a_tma_enabled())
+    return false;
+  const int64_t S = a.K / 256;
+  return S <= kRg2MaxGroups && S * a.WG <= 8192;
+}
+
+int64_t gm_sparse_ws_bytes(const SpmmArgs& a) {
+  if (!gm_sparse_capable(a)) return 0;
+  const int S = static_cast<int>(a.K / 256);
+  return gm_sparse_layout(a.M, a.N, a.WG, S, gm_sparse_bound_rows(a.M, a.K / a.t1, S)).bytes;
+}
+
 int gm_pairs_enabled() {  // PIT_GM_PAIRS=0: contiguous pit:m stays on the single-CTA rowgemm
   static int v = [] {
     const char* e = getenv("PIT_GM_PAIRS");
@@ -3150,10 +3230,31 @@ bool gm_contig_capable(const SpmmArgs& a) {
          ceil_div(a.K, 64) <= GmCfg<64>::KB_MAX && gm_contig_pct() > 0;
 }
 
+}  // namespace
+template <bool kBF16>
+int run_rowgemm2t(const RowGemmParams& p, const void* B, int64_t ldb, cudaStream_t s);  // below
+namespace {
+
 template <bool kBF16>
 int run_gm(const SpmmArgs& a, int ks, cudaStream_t s) {
   const int dense = a.plan == kPlanDense ? 1 : 0;
   int zero_in_gemm = 0;
+  // high-sparsity path (pit_gm_sparse.cu): its prep kernel decides on the device and publishes the
+  // decision; the masked dense kernels below leave when it is set, the sparse kernels when it is not
+  const int* sparse_flag = nullptr;
+  GmSparseWs sw{};
+  int sp_S = 0;
+  int64_t sp_bound = 0;
+  if (!dense && gm_sparse_capable(a) && a.ws != nullptr && a.ws_bytes >= gm_sparse_ws_bytes(a)) {
+    sp_S = static_cast<int>(a.K / 256);
+    sp_bound = gm_sparse_bound_rows(a.M, a.K / a.t1, sp_S);
+    sw = gm_sparse_layout(a.M, a.N, a.WG, sp_S, sp_bound);
+    uint8_t* ws = static_cast<uint8_t*>(a.ws);
+    if (int st = launch_gm_sparse_prep(a.counts, static_cast<int>(ceil_div(a.K, a.t1)), a.M, 256 / a.t1, sp_S, a.occ,
+                                       a.WG, ws, sw, s))
+      return st;
+    sparse_flag = reinterpret_cast<const int*>(ws + sw.flag);
+  }
   if (!dense) {
     // rows named by no group stay exactly zero. One K-group (BERT's row-uniform micro-tiles): only
     // the dead rows are written (the union is that group's bitmap); otherwise all of C is cleared.
@@ -3168,7 +3269,7 @@ int run_gm(const SpmmArgs& a, int ks, cudaStream_t s) {
       const int64_t blocks = ceil_div(chunks, 256);
       const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
       zero_unless_contig_kernel<<<static_cast<unsigned>(blocks < cap ? blocks : cap), 256, 0, s>>>(
-          a.n_rows, gm_contig_pct(), a.M, static_cast<uint8_t*>(a.C), a.ldc * 2, a.N / 8);
+          a.n_rows, gm_contig_pct(), a.M, static_cast<uint8_t*>(a.C), a.ldc * 2, a.N / 8, sparse_flag);
       note_launch();
     } else if (cudaMemset2DAsync(a.C, a.ldc * 2, 0, a.N * 2, a.M, s) != cudaSuccess) {
       return cuda_status();
@@ -3193,6 +3294,32 @@ int run_gm(const SpmmArgs& a, int ks, cudaStream_t s) {
   p.t1 = dense ? 1 : a.t1;
   p.max_tiles = static_cast<int>(ceil_div(dense ? a.M : a.n_rows_host, 128));
   p.zero_occ = zero_in_gemm ? a.occ : nullptr;
+  if (sparse_flag != nullptr) {
+    // SRead into packed rows -> supergroup products (fp32 partial rows) -> ordered row sums into C
+    uint8_t* ws = static_cast<uint8_t*>(a.ws);
+    const int nkg = static_cast<int>(ceil_div(a.K, a.t1));
+    if (int st = launch_gm_sparse_pack(a.counts, nkg, a.A, a.sam * 2, sp_S, a.M, a.occ, a.WG, a.t1, sp_bound, ws, sw, s))
+      return st;
+    RowGemmParams q{};
+    q.A = ws + sw.X;
+    q.lda = 256;
+    q.M = static_cast<int>(sp_bound);  // packed rows (bounds of the TMA map)
+    q.C = a.C;
+    q.ldc = a.ldc;
+    q.N = static_cast<int>(a.N);
+    q.K = 256;
+    q.G = sp_S;
+    q.cnt = reinterpret_cast<const int32_t*>(ws + sw.cnt);
+    q.off = nullptr;  // the kernel derives the packed offsets from cnt
+    q.max_tiles = static_cast<int>(ceil_div(sp_bound, 256) + sp_S);
+    q.part = reinterpret_cast<float*>(ws + sw.part);
+    q.path_flag = sparse_flag;
+    q.path_role = 1;
+    if (int st = run_rowgemm2t<kBF16>(q, a.B, a.ldb, s)) return st;
+    if (int st = launch_gm_sparse_reduce(a.counts, nkg, a.dtype, sp_S, a.WG, a.N, a.C, a.ldc, a.M, ws, sw, s)) return st;
+    p.path_flag = sparse_flag;
+    p.path_role = 2;
+  }
   const int64_t pack_bytes = gm_pack_bytes(a);
   if (pack_bytes > 0 && a.ws != nullptr && a.ws_bytes >= pack_bytes) {
     const int64_t blocks = ceil_div(a.n_rows_host, 8);
@@ -3449,7 +3576,10 @@ int launch_rowgemm(const GroupedGemmArgs& g, cudaStream_t s) {
 }
 
 int64_t spmm_tc_workspace_bytes(const SpmmArgs& a) {
-  if (a.plan == kPlanPitM) return gm_pack_bytes(a);  // one-K-group pit:m: packed live rows
+  if (a.plan == kPlanPitM) {  // one-K-group pit:m: packed live rows; 2-D: the high-sparsity path
+    const int64_t pb = gm_pack_bytes(a), sb = gm_sparse_ws_bytes(a);
+    return pb > sb ? pb : sb;
+  }
   // mirrors dispatch_tc: only the 128-row gathered-K kernel on 64-column units splits groups
   if (a.plan != kPlanPitK || a.t0 <= 64 || a.t0 > 128 || a.N > 64) return 0;
   const char* e = getenv("PIT_GK_NT");

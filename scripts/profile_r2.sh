@@ -10,7 +10,8 @@ cap() {  # name kernel-regex skip command...
   local name=$1 rx=$2 skip=$3; shift 3
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$rx -s $skip -c 1 -o $OUT/prof_$name -f \
     "$@" > $OUT/ncu_$name.log 2>&1
-  python scripts/ncu_summary.py $OUT/prof_$name.ncu-rep > $OUT/ncu_full_$name.txt 2>&1
+  python scripts/ncu_summary.py $OUT/prof_$name.ncu-rep 12 > $OUT/ncu_full_$name.txt 2>&1
+  [ -n "$KEEP_REP" ] || rm -f $OUT/prof_$name.ncu-rep  # gpurun copies back at most 64 MiB
   echo "== $name"; grep -E "Kernel Name|gpu__time|utchmma.*pct|hmma_cycles|dram__bytes|lts__throughput" $OUT/ncu_full_$name.txt
 }
 if [ -z "$ARGS" ] || want bench; then
@@ -28,4 +29,4 @@ want bert $ARGS && cap bert_rg2 rowgemm2 2 python scripts/bert_probe.py --ncu
 want moe $ARGS && cap moe_rg2t rowgemm2t 1 python scripts/rowgemm_probe.py --ncu
 
 
-ls $OUT/*.ncu-rep | head -20
+ls $OUT/ncu_full_*.txt
