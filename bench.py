@@ -444,6 +444,37 @@ def pit_run(plan, A, B, w):
     return pit.run_matmul_with_index(plan, pit.DenseTensor(A), pit.DenseTensor(B), idx).array
 
 
+def _graph_ms(fn, flush, reps):
+    """Mean device time of fn() captured in a CUDA graph, L2 flushed before each replay (event
+    timestamps come in ~2 us quanta, so the mean, not the median, resolves below that)."""
+    import torch
+
+    stream = torch.cuda.current_stream()
+    side = torch.cuda.Stream()
+    side.wait_stream(stream)
+    with torch.cuda.stream(side):
+        for _ in range(2):
+            fn()
+    stream.wait_stream(side)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        fn()
+    for _ in range(3):
+        graph.replay()
+    ev = []
+    for _ in range(reps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        graph.replay()
+        e1.record(stream)
+        ev.append((e0, e1))
+    torch.cuda.synchronize()
+    del graph
+    return statistics.mean(a.elapsed_time(b) for a, b in ev)
+
+
 def bert_bench(args, dev, peaks):
     """C2 (BASELINE configs[1]): BERT-base FFN1 over a variable-length batch (32 sequences of
     U[16,128] tokens padded to 128), padding removed via pit:m with row-uniform (1, 768) micro-tiles:
@@ -451,6 +482,7 @@ def bert_bench(args, dev, peaks):
     Effective FLOPs = 2 * 3072 * live elements (padding excluded)."""
     import torch
 
+    import paper_2301_10936_b200 as pit
     from paper_2301_10936_b200.graph import CapturedSparseMatmul
 
     w = dict(WORKLOADS["bert_ffn1"], name="bert_ffn1")
@@ -473,8 +505,29 @@ def bert_bench(args, dev, peaks):
         ev.append((e0, e1))
     torch.cuda.synchronize()
     ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+    # context on the same box: the same product dense on the padded batch (cuBLAS and this package's
+    # dense plan), cuBLAS on the live rows alone (the floor for any padding removal), and the pit:m
+    # product with the index reused (what each further layer of a batch pays: PIT builds one index
+    # per batch)
+    rows = int(live // w["K"])
+    Al = torch.randn((rows, w["K"]), device=dev, dtype=torch.bfloat16)
+    ctx_reps = max(20, args.steps)
+    idx = pit.build_index_from_tensor(A, w["micro"], w["axis"])
+    reg = pit.register_builtin_kernels(include_b200_tiles=True)
+    dplan = pit.forced_plan(pit.bind_extents(pit.parse_expr("C[m,n] += A[m,k] * B[k,n]"),
+                                             dict(m=w["M"], k=w["K"], n=w["N"])), "dense", reg, tile_shape=(128, 64, 256))
+    context = {
+        "cublas_padded_ms": round(_graph_ms(lambda: torch.matmul(A, B), flush, ctx_reps), 4),
+        "cublas_live_rows_ms": round(_graph_ms(lambda: torch.matmul(Al, B), flush, ctx_reps), 4),
+        "pit_dense_padded_ms": round(_graph_ms(lambda: pit.run_matmul_with_index(
+            dplan, pit.DenseTensor(A), pit.DenseTensor(B), None), flush, ctx_reps), 4),
+        "pit_m_index_reused_ms": round(_graph_ms(lambda: pit.run_matmul_with_index(
+            plan, pit.DenseTensor(A), pit.DenseTensor(B), idx), flush, ctx_reps), 4),
+        "timing": "mean of CUDA-graph replays, L2 flushed before each",
+    }
     return {"workload": w["desc"], "value": round(eff / (ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s (effective)",
-            "ms_per_step": round(ms, 4), "live_rows": int(live // w["K"]), "rows": w["M"],
+            "ms_per_step": round(ms, 4), "step_mean_ms": round(statistics.mean(a.elapsed_time(b) for a, b in ev), 4),
+            "live_rows": rows, "rows": w["M"], "context": context,
             "frac_bf16_peak": round(eff / (ms * 1e-3) / 1e12 / peaks["bf16"], 4),
             "graph_replay_equals_eager": bool(torch.equal(captured.C, eager)),
             "execution": "CUDA graph: build_index_from_tensor (1, 768) + run_matmul_with_index (pit:m)"}
@@ -947,22 +1000,20 @@ def opt_bench(args, dev, peaks, tokens=4096, d_model=2048, d_ff=8192, zeros=(0.9
             ev.append((e0, e1))
         torch.cuda.synchronize()
         ms = statistics.median(a.elapsed_time(b) for a, b in ev)
-        # per-product split (eager, events around each call)
+        # per-product split: each product alone as a CUDA graph over the step's index, L2 flushed
         idx = pit.build_index_from_tensor(H, (1, 32), "m")
         split = []
         for plan, A, B, ix in ((plan_f, H, W2, idx), (plan_b, H.t(), dY, idx.transposed())):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            pit.run_matmul_with_index(plan, pit.DenseTensor(A), pit.DenseTensor(B), ix)
-            e0.record(stream)
-            pit.run_matmul_with_index(plan, pit.DenseTensor(A), pit.DenseTensor(B), ix)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            split.append(e0.elapsed_time(e1))
+            split.append(_graph_ms(lambda plan=plan, A=A, B=B, ix=ix: pit.run_matmul_with_index(
+                plan, pit.DenseTensor(A), pit.DenseTensor(B), ix), flush, max(args.steps, 10)))
         out["by_zero_ratio"][str(zr)] = {
             "value": round(eff / (ms * 1e-3) / 1e12, 2), "ms_per_step": round(ms, 4), "live_fraction": round(
                 live / (tokens * d_ff), 4),
             "fwd_pit_m_TFLOPs": round(eff / 2 / (split[0] * 1e-3) / 1e12, 1),
             "bwd_pit_k_TFLOPs": round(eff / 2 / (split[1] * 1e-3) / 1e12, 1),
+            "fwd_ms": round(split[0], 4), "bwd_ms": round(split[1], 4),
+            "fwd_path": "high-sparsity supergroup products + ordered partial-row reduction"
+                        if live * 48 <= tokens * d_ff else "masked dense tiles on CTA pairs",
             "max_rel_err_vs_f64": err,
             "graph_replay_equals_eager": bool(torch.equal(O_g[0], Y) and torch.equal(O_g[1], dW2))}
         del H, keep
