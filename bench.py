@@ -836,6 +836,13 @@ def attention_bench(args, dev, peaks, heads=12, seq=4096, hd=64):
     plan_k128 = pit.forced_plan(expr, "k", reg, tile_shape=tile128)
     variants["pit:k (128,1) column-major P"] = timed(
         lambda: pit.run_batched_matmul_with_index(plan_k128, A3k, V, pit.build_index(ann_dev, (128, 1), "k")))
+    # two 32-query block rows per group: half the union waste of (128,1), half its MMA width
+    tile64 = (64, 64, 256)
+    if reg.get("matmul", tile64) is None:
+        reg.register(pit.TileKernelDescriptor("matmul", tile64, "attn64"))
+    plan_k64 = pit.forced_plan(expr, "k", reg, tile_shape=tile64)
+    variants["pit:k (64,1) column-major P"] = timed(
+        lambda: pit.run_batched_matmul_with_index(plan_k64, A3k, V, pit.build_index(ann_dev, (64, 1), "k")))
     # online detection from the P values instead of the mask (K1 over the stacked 402 MB operand)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     pit.build_batched_index_from_tensor(A3k, (32, 1), "k")

@@ -223,11 +223,24 @@ __global__ void __launch_bounds__(256) gm_sparse_reduce_kernel(const int32_t* __
       const int i = static_cast<int>(e / (N >> 3));
       const int64_t c = (e - static_cast<int64_t>(i) * (N >> 3)) * 8;
       float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      for (int k = 0; k < nparts[i]; ++k) {
-        const float4 a = __ldcs(reinterpret_cast<const float4*>(part + prow[i][k] + c));
-        const float4 b = __ldcs(reinterpret_cast<const float4*>(part + prow[i][k] + c + 4));
-        acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
-        acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
+      const int np = nparts[i];
+      for (int k0 = 0; k0 < np; k0 += 4) {
+        // up to four partial rows' loads in flight before any is summed (ascending order kept)
+        float4 a[4], b[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (k0 + k < np) {
+            a[k] = __ldcs(reinterpret_cast<const float4*>(part + prow[i][k0 + k] + c));
+            b[k] = __ldcs(reinterpret_cast<const float4*>(part + prow[i][k0 + k] + c + 4));
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (k0 + k < np) {
+            acc[0] += a[k].x; acc[1] += a[k].y; acc[2] += a[k].z; acc[3] += a[k].w;
+            acc[4] += b[k].x; acc[5] += b[k].y; acc[6] += b[k].z; acc[7] += b[k].w;
+          }
+        }
       }
       T h[8];
 #pragma unroll
