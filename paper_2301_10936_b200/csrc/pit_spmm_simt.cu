@@ -16,11 +16,18 @@
 
 #include "pit_internal.h"
 
+#include <cstdlib>
+
 namespace pit {
 
 namespace {
 
 constexpr int BM = 64, BN = 64, BK = 16, TPB = 256;
+
+int getenv_int(const char* name, int dflt) {  // A/B knobs (PIT_SIMT_GK=0: the generic K7 kernel)
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
 
 template <typename T>
 __device__ __forceinline__ float to_acc(T v);
@@ -271,6 +278,123 @@ __global__ void reduce_rows_kernel(const T* __restrict__ A, int64_t P, int64_t L
   if (lane == 0) out[r] = from_acc<T, Acc>(acc);
 }
 
+// ---------------------------------------------------------------- pit:k fp32, pipelined (K7b)
+// The reference's own configuration (C1: 1024^3 fp32, 32x1 micro-tiles) on the CUDA cores with TF32
+// never used: CTA = (group g, 32-row chunk of it, 128-column tile); per stage 32 live k of the
+// group (stored order): the A^T strips (32 rows, 128 contiguous bytes of column-major A) and the 32
+// B rows (512 bytes each) by 16-byte cp.async into a 3-stage ring, then 16 FFMA per thread per k
+// (4 rows x 4 columns, float4 shared loads: A broadcast within the warp, B conflict-free). The
+// accumulation order per output is the stored k order, exactly as in spmm_simt_kernel (bitwise the
+// same results).
+constexpr int kGkBM = 32, kGkBN = 128, kGkBK = 32, kGkStages = 3, kGkThreads = 256;
+
+__device__ __forceinline__ void cp16(void* smem, const void* src, bool ok) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(ok ? 16 : 0) : "memory");
+}
+
+__global__ void __launch_bounds__(kGkThreads) gk_simt_f32_kernel(SpmmArgs a) {
+  extern __shared__ float4 gk_smem[];
+  float* As = reinterpret_cast<float*>(gk_smem);           // [stages][BK][BM]
+  float* Bs = As + kGkStages * kGkBK * kGkBM;               // [stages][BK][BN]
+  const float* A = static_cast<const float*>(a.A);
+  const float* B = static_cast<const float*>(a.B);
+  float* C = static_cast<float*>(a.C);
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  const int64_t n0 = static_cast<int64_t>(blockIdx.x) * kGkBN;
+  const int64_t chunks = (a.t0 + kGkBM - 1) / kGkBM;
+  const int64_t g = blockIdx.y / chunks;
+  const int64_t lr0 = (blockIdx.y % chunks) * kGkBM;  // first row of the chunk within the group
+  const int64_t m0 = g * a.t0 + lr0;
+  const int rows = static_cast<int>(min(static_cast<int64_t>(kGkBM), min(static_cast<int64_t>(a.t0) - lr0, a.M - m0)));
+  const int count = a.counts[g];
+  const int32_t* klist = a.slots + g * a.slot_stride;
+  const int nsteps = (count + kGkBK - 1) / kGkBK;
+
+  auto load_stage = [&](int step, int buf) {
+    const int kb = step * kGkBK;
+    {  // A: 32 k x 8 chunks (rows 4 at a time)
+      const int kk = tid >> 3, part = tid & 7;
+      const bool ok = kb + kk < count && part * 4 < rows;
+      const int k = ok ? __ldg(klist + kb + kk) : 0;
+      cp16(As + (buf * kGkBK + kk) * kGkBM + part * 4, A + (ok ? m0 + part * 4 + static_cast<int64_t>(k) * a.sak : 0), ok);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // B: 32 k x 32 chunks
+      const int c = tid + i * kGkThreads;
+      const int kk = c >> 5, part = c & 31;
+      const bool ok = kb + kk < count && n0 + part * 4 < a.N;
+      const int k = ok ? __ldg(klist + kb + kk) : 0;
+      cp16(Bs + (buf * kGkBK + kk) * kGkBN + part * 4, B + (ok ? static_cast<int64_t>(k) * a.ldb + n0 + part * 4 : 0), ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+
+#pragma unroll
+  for (int st = 0; st < kGkStages - 1; ++st) {
+    if (st < nsteps) load_stage(st, st);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int step = 0; step < nsteps; ++step) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(kGkStages - 2) : "memory");
+    __syncthreads();  // stage `step` landed for every thread; the buffer refilled below is free
+    const int nxt = step + kGkStages - 1;
+    if (nxt < nsteps) load_stage(nxt, nxt % kGkStages);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    const int buf = step % kGkStages;
+    const float* as = As + buf * kGkBK * kGkBM + ty * 4;
+    const float* bs = Bs + buf * kGkBK * kGkBN + tx * 4;
+    const int kn = min(kGkBK, count - step * kGkBK);
+    for (int kk = 0; kk < kn; ++kk) {
+      const float4 av = *reinterpret_cast<const float4*>(as + kk * kGkBM);
+      const float4 bv = *reinterpret_cast<const float4*>(bs + kk * kGkBN);
+      const float ar[4] = {av.x, av.y, av.z, av.w}, br[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(ar[i], br[j], acc[i][j]);
+    }
+  }
+  const int64_t n = n0 + tx * 4;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = ty * 4 + i;
+    if (r >= rows || n >= a.N) continue;
+    float* dst = C + (m0 + r) * a.ldc + n;
+    if (n + 4 <= a.N) *reinterpret_cast<float4*>(dst) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+    else for (int j = 0; j < 4 && n + j < a.N; ++j) dst[j] = acc[i][j];
+  }
+}
+
+bool gk_simt_f32_ok(const SpmmArgs& a) {
+  return a.plan == kPlanPitK && a.dtype == kDtypeF32 && a.batch <= 1 && a.sam == 1 && (a.sak % 4) == 0 &&
+         (a.ldb % 4) == 0 && (a.ldc % 4) == 0 && (a.N % 4) == 0 && (a.t0 % 4) == 0 &&
+         (reinterpret_cast<uintptr_t>(a.A) & 15) == 0 && (reinterpret_cast<uintptr_t>(a.B) & 15) == 0 &&
+         (reinterpret_cast<uintptr_t>(a.C) & 15) == 0 && getenv_int("PIT_SIMT_GK", 1) != 0;
+}
+
+int run_gk_simt_f32(const SpmmArgs& a, cudaStream_t s) {
+  const int64_t ytiles = a.n_groups * ceil_div(a.t0, kGkBM);
+  const int64_t xtiles = ceil_div(a.N, kGkBN);
+  if (ytiles == 0 || xtiles == 0) return kOk;
+  if (ytiles > 65535 || xtiles > (1ll << 31) - 1) return kErrShape;
+  constexpr int smem = kGkStages * kGkBK * (kGkBM + kGkBN) * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gk_simt_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  gk_simt_f32_kernel<<<dim3(static_cast<unsigned>(xtiles), static_cast<unsigned>(ytiles)), kGkThreads, smem, s>>>(a);
+  note_launch();
+  return cuda_status();
+}
+
 template <typename T, typename Acc>
 int run_simt(const SpmmArgs& a, cudaStream_t s) {
   int64_t ytiles;
@@ -295,7 +419,7 @@ int run_simt(const SpmmArgs& a, cudaStream_t s) {
 int launch_spmm_simt(const SpmmArgs& a, cudaStream_t s) {
   switch (a.dtype) {
     case kDtypeF32:
-      return run_simt<float, float>(a, s);
+      return gk_simt_f32_ok(a) ? run_gk_simt_f32(a, s) : run_simt<float, float>(a, s);
     case kDtypeF64:
       return run_simt<double, double>(a, s);
     case kDtypeBF16:
