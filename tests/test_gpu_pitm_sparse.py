@@ -43,17 +43,18 @@ def _case(tokens, d_ff, d_model, zero, t1=32, seed=0, dtype="bfloat16"):
     return pit, plan, idx, H, W, keep
 
 
-@pytest.mark.parametrize("tokens,d_ff,d_model,zero,t1", [
-    (4096, 8192, 2048, 0.99, 32),    # C4 at 99%: the sparse path
-    (4096, 8192, 2048, 0.985, 32),   # still under the switch
-    (1000, 2048, 384, 0.995, 32),    # ragged token count, narrow output
-    (2048, 4096, 512, 0.995, 16),    # 16-wide micro-columns
-    (4096, 8192, 2048, 0.9, 32),     # 90%: the masked dense path (flag clear)
+@pytest.mark.parametrize("tokens,d_ff,d_model,zero,t1,dtype", [
+    (4096, 8192, 2048, 0.99, 32, "bfloat16"),    # C4 at 99%: the sparse path
+    (4096, 8192, 2048, 0.985, 32, "bfloat16"),   # still under the switch
+    (1000, 2048, 384, 0.995, 32, "bfloat16"),    # ragged token count, narrow output
+    (2048, 4096, 512, 0.995, 16, "bfloat16"),    # 16-wide micro-columns
+    (2048, 4096, 1024, 0.99, 32, "float16"),     # fp16 operands
+    (4096, 8192, 2048, 0.9, 32, "bfloat16"),     # 90%: the masked dense path (flag clear)
 ])
-def test_pitm_high_sparsity_matches_f64(tokens, d_ff, d_model, zero, t1):
+def test_pitm_high_sparsity_matches_f64(tokens, d_ff, d_model, zero, t1, dtype):
     import torch
 
-    pit, plan, idx, H, W, keep = _case(tokens, d_ff, d_model, zero, t1, seed=tokens + d_model)
+    pit, plan, idx, H, W, keep = _case(tokens, d_ff, d_model, zero, t1, seed=tokens + d_model, dtype=dtype)
     poison = torch.full((tokens, d_model), float("nan"), dtype=H.dtype, device="cuda")
     del poison  # every row of C must be written (the allocator hands this block out next)
     C = pit.run_matmul_with_index(plan, pit.DenseTensor(H), pit.DenseTensor(W), idx).array

@@ -76,8 +76,9 @@ def test_bert_step_from_values_matches_f64(lengths_seed):
     assert np.all(got[~rows] == 0.0) and not np.isnan(got).any()
 
 
-@pytest.mark.parametrize("n_live", [0, 1, 37, 255, 256, 257, 2000])
-def test_row_uniform_live_counts_and_poisoned_output(n_live):
+@pytest.mark.parametrize("n_live,dtype", [(0, "bfloat16"), (1, "bfloat16"), (37, "bfloat16"), (255, "bfloat16"),
+                                          (256, "bfloat16"), (257, "bfloat16"), (2000, "bfloat16"), (1500, "float16")])
+def test_row_uniform_live_counts_and_poisoned_output(n_live, dtype):
     """Live-row counts around the 256-row pair tile and the 32-row store boxes; the output buffer is
     poisoned before the call and every row must come back finite (live) or exactly zero (dead)."""
     import torch
@@ -87,10 +88,11 @@ def test_row_uniform_live_counts_and_poisoned_output(n_live):
     rng = np.random.default_rng(n_live)
     live = np.zeros(m, dtype=bool)
     live[rng.choice(m, size=n_live, replace=False)] = True
-    A = torch.from_numpy(rng.standard_normal((m, k)).astype(np.float32) * live[:, None]).to(torch.bfloat16).cuda()
-    B = torch.from_numpy(rng.standard_normal((k, n)).astype(np.float32)).to(torch.bfloat16).cuda()
+    dt = getattr(torch, dtype)
+    A = torch.from_numpy(rng.standard_normal((m, k)).astype(np.float32) * live[:, None]).to(dt).cuda()
+    B = torch.from_numpy(rng.standard_normal((k, n)).astype(np.float32)).to(dt).cuda()
     idx = pit.build_index_from_tensor(A, (1, k), "m")
-    poison = torch.full((m, n), float("nan"), dtype=torch.bfloat16, device="cuda")
+    poison = torch.full((m, n), float("nan"), dtype=dt, device="cuda")
     del poison  # the caching allocator hands this block to the output next
     C = pit.run_matmul_with_index(_plan(m, k, n, tile=(128, k, 256)), pit.DenseTensor(A), pit.DenseTensor(B), idx)
     got = C.array.float().cpu().numpy()
