@@ -1,25 +1,26 @@
-// PIT sparse matmul on the 5th-gen tensor cores (tcgen05 + TMEM + TMA gather4), bf16/fp16 in,
-// fp32 accumulate, bf16/fp16 out.
+// PIT sparse matmul on the 5th-gen tensor cores (tcgen05 + TMEM, TMA tiles, cp.async gathers),
+// bf16/fp16 in, fp32 accumulate, bf16/fp16 out. Persistent, warp-specialised kernels (512 threads:
+// warps 0-7 producers, 8 MMA issuer, 9 TMEM allocator on single-CTA kernels, 10 relay (CTA pairs),
+// 11 TMA issuer in mask modes, 12-15 epilogue; CTA-pair kernels allocate TMEM from warp 0):
 //
-// Two persistent, warp-specialised kernels (warp 0 = TMA producer, warp 1 = MMA issuer,
-// warp 2 = TMEM allocator, warps 4..7 = epilogue):
-//
-//  * spmm_gk ("gathered K", PIT axis k; reference executor.py:386-423 `_matmul_pit_k`).
+//  * spmm_gk / spmm_gk2 ("gathered K", PIT axis k; reference executor.py:386-423 `_matmul_pit_k`).
 //    A group is an M-block of GW rows (micro-tile (GW,1)); its live k coordinates index rows of
-//    A^T (A is column-major, executor.py:318-325) and rows of B. Both operands are fetched with
-//    TMA tile::gather4 (four k rows per instruction) into MN-major swizzled shared memory and fed
-//    to tcgen05.mma in the transposed orientation D[n, m] += B^T[n, k] * A^T[k, m]:
-//    M_mma = 128 output columns (n), N_mma = GW output rows (m). That keeps the group width as
-//    the MMA's N, so 16..256-row micro-tiles all run as dense MMAs with no union waste.
-//    Each (group, n-tile) C block is owned by exactly one CTA and accumulated in TMEM.
+//    A^T (A is column-major, executor.py:318-325) and rows of B. Both are gathered with 16-byte
+//    cp.async into MN-major swizzled shared memory (TMA tile::gather4 measured at ~1/3 of the
+//    cp.async rate on this part, K2) and fed to tcgen05.mma: orientation T
+//    (D[n, m] += B^T A^T, group rows on the MMA's N side: 16..64-row micro-tiles run as dense MMAs
+//    with no union waste) or N (128-row groups); spmm_gk2 runs 256-row groups on CTA pairs. Split
+//    units balance few, unequal groups (C3's global query rows); TMA tile stores write C.
 //
-//  * spmm_gm ("gathered M", PIT axis m and the dense plan; executor.py:352-383 / :426-461).
-//    Output row tiles are 128 rows of the union of live rows (rows named by any K-block group).
-//    Per K-block stage the producer gathers those rows of A with gather4; a row that is not live
-//    in that K-block is pointed out of bounds, so TMA fills it with zeros. B K-blocks are plain 2-D
-//    TMA tiles. The C tile stays resident in TMEM across all K-blocks and is scattered to its rows
-//    once (SWrite fused in the epilogue). Rows outside the union are never written (C is zeroed
-//    up front), which keeps the reference's exact-zero guarantee (executor.py:8-9).
+//  * rowgemm / rowgemm2 / rowgemm2t ("gathered M", PIT axis m, dense, grouped; executor.py:352-383,
+//    :426-461). Output row tiles are union rows, consecutive slice rows or a group's rows; A rows by
+//    TMA tiles when consecutive (or packed first), by cp.async otherwise, with dead (row,
+//    micro-column) items zero-filled or zeroed in shared memory; B K-blocks are TMA tiles of the
+//    stacked [G, K, N] weights; K-blocks with no live row take no ring slot. The C tile stays in
+//    TMEM across K and is stored once (SWrite fused: TMA boxes for consecutive rows, 128-byte row
+//    segments for scattered ones). rowgemm2 runs 256x256 tiles on CTA pairs; rowgemm2t swaps the
+//    operand roles for small groups (MoE experts, the high-sparsity pit:m supergroups of
+//    pit_gm_sparse.cu, whose fp32 partial rows it writes).
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
