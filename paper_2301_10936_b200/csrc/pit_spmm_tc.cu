@@ -2658,19 +2658,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = half * 32; c < tt.ntok; c += cstep) {
+      if (p.part != nullptr) {
+        // fp32 partial rows: lane = feature, one coalesced 128-byte segment per token; two 32-token
+        // blocks of TMEM in flight per wait (the warp's blocks are 64 tokens apart with 8 warps)
+        const int f = ocw + lane;
+#pragma unroll 1
+        for (int c = half * 32; c < tt.ntok; c += 2 * cstep) {
+          uint32_t v[2][32];
+          const bool two = c + cstep < tt.ntok;
+          tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * 256 + c), v[0]);
+          if (two)
+            tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * 256 + c + cstep),
+                      v[1]);
+          tmem_wait_ld();
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            const int cb = c + b * cstep;
+            if (b == 1 && !two) break;
+            float* prow = static_cast<float*>(p.part) + (static_cast<int64_t>(gbase) + tt.start + cb) * p.N + f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (cb + j < tt.ntok && f < p.N) prow[static_cast<int64_t>(j) * p.N] = __uint_as_float(v[b][j]);
+          }
+        }
+      }
+#pragma unroll 1
+      for (int c = half * 32; p.part == nullptr && c < tt.ntok; c += cstep) {
         uint32_t v[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * 256 + c), v);
         tmem_wait_ld();
-        if (p.part != nullptr) {
-          // fp32 partial rows: lane = feature, one coalesced 128-byte segment per token
-          const int f = ocw + lane;
-          float* prow = p.part + (static_cast<int64_t>(gbase) + tt.start + c) * p.N + f;
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (c + j < tt.ntok && f < p.N) prow[static_cast<int64_t>(j) * p.N] = __uint_as_float(v[j]);
-          continue;
-        }
         // destination row and scale of token c + lane
         const int within = tt.start + c + lane;
         int my_row = -1;
