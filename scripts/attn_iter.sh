@@ -3,7 +3,7 @@
 OUT=gpurun_out; mkdir -p $OUT
 NB="--steps 10 --warmup 3 --no-e2e --no-cpu-baseline --no-index-bench --no-moe --no-opt --no-sweep --no-bert --no-c1"
 timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "attn or attention or batched or masked or pitm" 2>&1 | tail -3
-for v in "PIT_X=0" ${EXTRA_VARIANTS}; do
+for v in ${VARIANTS:-PIT_X=0}; do
   env $v timeout 600 python bench.py $NB > $OUT/attn_$v.json 2>$OUT/attn_$v.err
   python - "$OUT/attn_$v.json" "$v" <<'PY'
 import json, sys
