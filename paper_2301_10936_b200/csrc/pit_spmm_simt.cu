@@ -373,7 +373,9 @@ __global__ void __launch_bounds__(kGkThreads) gk_simt_f32_kernel(SpmmArgs a) {
 }
 
 bool gk_simt_f32_ok(const SpmmArgs& a) {
+  // whole 16-byte row quads only (M, t0 multiples of 4: a strip load never reads past A)
   return a.plan == kPlanPitK && a.dtype == kDtypeF32 && a.batch <= 1 && a.sam == 1 && (a.sak % 4) == 0 &&
+         (a.M % 4) == 0 &&
          (a.ldb % 4) == 0 && (a.ldc % 4) == 0 && (a.N % 4) == 0 && (a.t0 % 4) == 0 &&
          (reinterpret_cast<uintptr_t>(a.A) & 15) == 0 && (reinterpret_cast<uintptr_t>(a.B) & 15) == 0 &&
          (reinterpret_cast<uintptr_t>(a.C) & 15) == 0 && getenv_int("PIT_SIMT_GK", 1) != 0;
