@@ -1013,12 +1013,31 @@ def opt_bench(args, dev, peaks, tokens=4096, d_model=2048, d_ff=8192, zeros=(0.9
         for plan, A, B, ix in ((plan_f, H, W2, idx), (plan_b, H.t(), dY, idx.transposed())):
             split.append(_graph_ms(lambda plan=plan, A=A, B=B, ix=ix: pit.run_matmul_with_index(
                 plan, pit.DenseTensor(A), pit.DenseTensor(B), ix), flush, max(args.steps, 10)))
+        # the rest of FFN2's backward: dH = (dY . W2^T) * 1[H > 0] only inside H's live 1x32
+        # micro-tiles -- the output-sparse plan (SDDMM, K8) with the ReLU gate, annotation detected
+        # from H on the device each step; dense cuBLAS dY . W2^T (every element) beside it
+        from paper_2301_10936_b200.sddmm import run_sddmm_like
+
+        dH = torch.zeros_like(H)
+
+        def dh_step():
+            run_sddmm_like(dY, W2.t(), H, (1, 32), out=dH, gate=H)
+
+        dh_step()
+        dh_ms = _graph_ms(dh_step, flush, max(args.steps, 10))
+        dense_dh_ms = _graph_ms(lambda: torch.matmul(dY, W2.t()), flush, max(args.steps, 10))
+        refh = (dY[:256].double() @ W2.double().t()) * (H[:256] > 0)
+        errh = float((dH[:256].double() - refh).norm() / refh.norm().clamp_min(1e-30))
+        del dH
         out["by_zero_ratio"][str(zr)] = {
             "value": round(eff / (ms * 1e-3) / 1e12, 2), "ms_per_step": round(ms, 4), "live_fraction": round(
                 live / (tokens * d_ff), 4),
             "fwd_pit_m_TFLOPs": round(eff / 2 / (split[0] * 1e-3) / 1e12, 1),
             "bwd_pit_k_TFLOPs": round(eff / 2 / (split[1] * 1e-3) / 1e12, 1),
             "fwd_ms": round(split[0], 4), "bwd_ms": round(split[1], 4),
+            "dH_sddmm": {"ms": round(dh_ms, 4), "effective_TFLOPs": round(eff / 2 / (dh_ms * 1e-3) / 1e12, 1),
+                         "dense_cublas_ms": round(dense_dh_ms, 4), "rel_err_rows0_255_vs_f64": errh,
+                         "execution": "CUDA graph: run_sddmm_like(dY, W2^T, H, (1,32), gate=H): both output indexes detected from H on the device + the SDDMM"},
             "fwd_path": "high-sparsity supergroup products + ordered partial-row reduction"
                         if live * 48 <= tokens * d_ff else "masked dense tiles on CTA pairs",
             "max_rel_err_vs_f64": err,

@@ -188,6 +188,64 @@ __global__ void __launch_bounds__(kRaWarps * 32, 4) detect_rows_vec_kernel(const
 }
 
 // ---------------------------------------------------------------------------
+// Pass 1, coordinates along physical columns (pit_phys 1: groups = row bands of tr rows, bits over
+// micro-columns of tc columns), 16-byte aligned rows, micro-column = VPB 16-byte vectors (VPB a
+// power of two <= 32). A 256-thread block owns one band and 256 consecutive vectors of its rows:
+// thread = vector column, looping over the band's rows with 8 loads in flight and OR-ing liveness;
+// the VPB lanes of a micro-column OR by shuffles, the warp ballot packs its micro-columns' bits and
+// the block's (at most 8) words are stored whole. (The generic element path ran this case -- e.g. the
+// (128, 64) output-unit index of an SDDMM from values -- on a handful of CTAs: 6-15 ms for 64 MiB.)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) detect_cols_vec_kernel(const uint8_t* __restrict__ x, int64_t R,
+                                                              int64_t ld_bytes, int64_t nvec, int tr, int lg_vpb,
+                                                              int64_t GR, LiveMask lm, uint32_t* __restrict__ occ,
+                                                              int64_t WG) {
+  __shared__ uint32_t words[8];
+  const int64_t band = blockIdx.y;
+  const int64_t v = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;  // vector column
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 8) words[threadIdx.x] = 0u;
+  __syncthreads();
+  const int64_t r0 = band * tr;
+  const int64_t r1 = R - r0 < tr ? R : r0 + tr;
+  bool live = false;
+  if (v < nvec) {
+    const uint8_t* col = x + v * 16;
+    for (int64_t r = r0; r < r1 && !live; r += 8) {
+      uint4 q[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        q[u] = r + u < r1 ? __ldg(reinterpret_cast<const uint4*>(col + (r + u) * ld_bytes)) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) live |= ((q[u].x & lm.even) | (q[u].y & lm.odd) | (q[u].z & lm.even) | (q[u].w & lm.odd)) != 0;
+    }
+  }
+  // OR over the VPB vectors of each micro-column (aligned lane groups), then one bit per micro-column
+  uint32_t any = live ? 1u : 0u;
+  for (int o = 1; o < (1 << lg_vpb) && o < 32; o <<= 1) any |= __shfl_xor_sync(0xffffffffu, any, o);
+  const uint32_t ball = __ballot_sync(0xffffffffu, any != 0u);
+  if (lane == 0) {
+    // micro-columns covered by this warp: first = (blockIdx.x*256 + warp*32) >> lg_vpb
+    const int64_t mc0 = (static_cast<int64_t>(blockIdx.x) * 256 + (threadIdx.x & ~31)) >> lg_vpb;
+    const int per = lg_vpb >= 5 ? 1 : 32 >> lg_vpb;  // micro-columns per warp
+    uint32_t bits = 0;
+    for (int i = 0; i < per; ++i) bits |= ((ball >> (i << lg_vpb)) & 1u) << i;
+    const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * 256) >> lg_vpb >> 5;  // block's first word
+    const int64_t wi = (mc0 >> 5) - w0;
+    atomicOr(&words[wi], bits << (mc0 & 31));
+  }
+  __syncthreads();
+  const int64_t w0 = ((static_cast<int64_t>(blockIdx.x) * 256) >> lg_vpb) >> 5;
+  const int64_t wn = ((256 >> lg_vpb) + 31) >> 5;  // words this block covers (micro-columns / 32)
+  if (threadIdx.x < wn && w0 + threadIdx.x < WG) {
+    if (lg_vpb >= 4)
+      atomicOr(&occ[band * WG + w0 + threadIdx.x], words[threadIdx.x]);  // a word spans several blocks
+    else
+      occ[band * WG + w0 + threadIdx.x] = words[threadIdx.x];
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Pass 1, generic path: any micro-tile, any alignment, element loads.
 // Block covers 32 micro-row bands x TJ micro-columns; shared-memory bitmap tile in the
 // output's group-major orientation, then plain stores of whole words.
@@ -547,6 +605,17 @@ int launch_detect_values(const DetectValuesArgs& a, cudaStream_t s) {
     detect_rows_vec_kernel<<<static_cast<unsigned>(grid), kRaWarps * 32, 0, s>>>(
         static_cast<const uint8_t*>(a.x), a.R, row_bytes, ld_bytes, a.tr, static_cast<int>(vec_per_micro), GR, GC,
         live_mask_for(a.dtype), a.occ, WG, seg_groups, tiles);
+    note_launch();
+  } else if (a.pit_phys == 1 && aligned && (static_cast<int64_t>(a.tc) * eb) % 16 == 0 && vec_per_micro >= 1 &&
+             vec_per_micro <= 32 && (vec_per_micro & (vec_per_micro - 1)) == 0 && GR <= 65535) {
+    const int lg = __builtin_ctzll(static_cast<unsigned long long>(vec_per_micro));
+    const int64_t nvec = row_bytes / 16;
+    // a 32-bit word spans 32 micro-columns = 32 * VPB vectors: more than one block's 256 when VPB >= 16
+    if (lg >= 4 && cudaMemsetAsync(a.occ, 0, static_cast<size_t>(n_groups * WG) * sizeof(uint32_t), s) != cudaSuccess)
+      return cuda_status();
+    dim3 grid(static_cast<unsigned>(ceil_div(nvec, 256)), static_cast<unsigned>(GR));
+    detect_cols_vec_kernel<<<grid, 256, 0, s>>>(static_cast<const uint8_t*>(a.x), a.R, ld_bytes, nvec, a.tr, lg, GR,
+                                                live_mask_for(a.dtype), a.occ, WG);
     note_launch();
   } else {
     const int TJ = a.pit_phys == 0 ? 256 : (a.tc >= 8 ? 32 : 128);

@@ -42,6 +42,37 @@ def output_indexes(ann: SparsityAnnotation):
     return build_index(ann, UNIT_MICRO, "k"), build_occupancy(ann, ann.granularity, "k")
 
 
+def output_indexes_from_tensor(values, granularity):
+    """The two output indexes straight from the values of a tensor shaped like C (live micro-tile =
+    any element != 0): e.g. dH's mask is H's own (1, 32) activation pattern. Everything stays on the
+    device (K1 detection twice + compaction), so the call is CUDA-graph capturable -- unlike
+    ``from_mask`` on a CUDA tensor, which returns host bits."""
+    from .index import build_index_from_tensor
+
+    gran = (int(granularity[0]), int(granularity[1]))
+    fine = build_index_from_tensor(values, gran, "k")
+    return build_index_from_tensor(values, UNIT_MICRO, "k"), fine.occupancy_words()
+
+
+class _OutputSpec:
+    """Shape and micro-tile of C when its indexes come from values (no annotation object)."""
+
+    def __init__(self, shape, granularity):
+        self.tensor_shape = tuple(int(d) for d in shape)
+        self.granularity = tuple(int(g) for g in granularity)
+
+
+def run_sddmm_like(A, B, like, granularity, out=None, gate=None) -> DenseTensor:
+    """``run_sddmm`` with C's live micro-tiles detected on the device from ``like`` (a CUDA tensor
+    shaped like C): the ReLU-masked activation gradient dH = (dY . W2^T) * 1[H > 0] inside H's
+    live 1x32 micro-tiles is ``run_sddmm_like(dY, W2.t(), H, (1, 32), gate=H)``."""
+    like = _as_tensor(like)
+    if not (_is_torch(like) and like.is_cuda and like.dim() == 2):
+        raise ExecError("like must be a 2-D CUDA tensor shaped like the output")
+    spec = _OutputSpec(like.shape, granularity)
+    return run_sddmm(A, B, spec, out=out, gate=gate, indexes=output_indexes_from_tensor(like, granularity))
+
+
 def _launch(A2, Bt2, C2, M, N, K, batch, ann, gate, indexes):
     torch = __import__("torch")
     if A2.dtype not in (torch.bfloat16, torch.float16):

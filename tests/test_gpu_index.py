@@ -194,3 +194,20 @@ def test_whole_row_micro_tiles_match_oracle(dtype, shape, micro):
     idx = pit.build_index_from_tensor(t, micro, "m")
     counts, groups = orc.build_index_from_values(v, micro, "m")
     assert_same_index(idx, counts, groups)
+
+
+@pytest.mark.parametrize("dtype", ["bfloat16", "float32", "float16"])
+@pytest.mark.parametrize("shape,micro", [((512, 1024), (128, 64)), ((300, 2048), (1, 32)), ((257, 4096), (32, 16)),
+                                         ((1024, 520), (16, 8)), ((96, 8192), (8, 256)), ((70, 1000), (5, 8))])
+def test_columnwise_detection_vector_path_matches_oracle(dtype, shape, micro):
+    """PIT axis k over row-major values (groups = row bands, bits over micro-columns): the 16-byte
+    vector kernel (detect_cols_vec_kernel; micro-columns of 1-32 vectors, ragged band and column
+    tails, words shared by several blocks) is bit-exact against the oracle."""
+    pit = _pkg()
+    rng = np.random.default_rng(shape[0] * 7 + micro[1])
+    v = _values(shape, 0.001, rng)
+    v[:, rng.random(shape[1]) < 0.3] = 0.0
+    t = _torch_values(v, dtype, False)
+    idx = pit.build_index_from_tensor(t, micro, "k")
+    counts, groups = orc.build_index_from_values(t.float().cpu().numpy(), micro, "k")
+    assert_same_index(idx, counts, groups)

@@ -157,3 +157,43 @@ def test_batched_attention_scores(heads, seq):
         m = live[h]
         err = float((out[h].double()[m] - ref[m]).abs().max() / ref[m].abs().max())
         assert err <= 1e-2, (h, err)
+
+
+def test_sddmm_like_detects_the_output_mask_on_device_and_captures():
+    """dH = (dY . W2^T) * 1[H > 0] with the output indexes detected from H on the device: equal to the
+    annotation-driven call, and a CUDA-graph replay after H changes equals the eager call."""
+    import torch
+
+    import paper_2301_10936_b200 as pit
+    from paper_2301_10936_b200.sddmm import run_sddmm, run_sddmm_like
+
+    T, F, D = 1024, 2048, 256
+    rng = np.random.default_rng(8)
+    dY = _bf16(rng.standard_normal((T, D))).cuda()
+    W2 = _bf16(rng.standard_normal((F, D)) / 16).cuda()
+
+    def relu_masked(seed):
+        r = np.random.default_rng(seed)
+        keep = r.random((T, F // 32)) >= 0.95
+        return _bf16(np.maximum(r.standard_normal((T, F)), 0) * np.repeat(keep, 32, axis=1)).cuda()
+
+    H = relu_masked(1)
+    got = run_sddmm_like(dY, W2.t(), H, (1, 32), gate=H).array
+    ann = pit.from_mask(H.float().cpu().numpy() != 0, (1, 32)).on_device(torch.device("cuda"))
+    want = run_sddmm(dY, W2.t(), ann, gate=H).array
+    assert torch.equal(got, want)
+    out = torch.zeros_like(H)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        run_sddmm_like(dY, W2.t(), H, (1, 32), out=out, gate=H)
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        run_sddmm_like(dY, W2.t(), H, (1, 32), out=out, gate=H)
+    H.copy_(relu_masked(2))
+    out.zero_()
+    g.replay()
+    eager = run_sddmm_like(dY, W2.t(), H, (1, 32), gate=H).array
+    assert torch.equal(out, eager)
