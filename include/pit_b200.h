@@ -48,7 +48,7 @@ typedef enum { PIT_PLAN_DENSE = 0, PIT_PLAN_PIT_M = 1, PIT_PLAN_PIT_K = 2 } pit_
 PIT_API const char* pit_last_error(void);
 
 /* ABI version (major*100 + minor). */
-PIT_API int pit_abi_version(void); /* 103: pit_sddmm; 102: pit_grouped_gemm_args.rows_hint, pit_ep_* / pit_moe_dispatch */
+PIT_API int pit_abi_version(void); /* 104: pit_pack_groups; 103: pit_sddmm; 102: pit_grouped_gemm_args.rows_hint, pit_ep_* / pit_moe_dispatch */
 
 /* Number of kernels this library has launched in the process (monotonic; for launch accounting). */
 PIT_API long long pit_kernel_launches(void);
@@ -204,6 +204,13 @@ PIT_API int pit_moe_recv_plan(const int32_t* rc, int64_t W, int64_t El, int32_t*
 /* SRead of whole rows: dst row i = src row rows[i] (row_bytes each; pitches in bytes). */
 PIT_API int pit_gather_rows(const void* src, int64_t ld_src_bytes, const int32_t* rows, int64_t n, int64_t row_bytes,
                             void* dst, int64_t ld_dst_bytes, void* stream);
+
+/* Group-wise SRead with device counts (the MoE FFN1 input in expert order, so the grouped GEMM reads it by TMA):
+ * dst row offsets[g] + i = src row rows[g*stride + i] for i < counts[g], g < G; max_count bounds every count.
+ * 16-byte aligned rows and pitches (bytes). */
+PIT_API int pit_pack_groups(const void* src, int64_t ld_src_bytes, const int32_t* rows, int64_t stride,
+                            const int32_t* counts, const int32_t* offsets, int64_t G, int64_t max_count,
+                            int64_t row_bytes, void* dst, int64_t ld_dst_bytes, void* stream);
 
 /* SWrite of whole rows with a per-destination-row scale (MoE combine): dst[rows[i]] = scale[rows[i]] * src[i]. */
 PIT_API int pit_scatter_rows_scaled(const void* src, int dtype, int64_t ld_src, const int32_t* rows, int64_t n,

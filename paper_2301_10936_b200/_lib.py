@@ -55,6 +55,7 @@ EXPORTS = (
     "pit_moe_plan",
     "pit_moe_recv_plan",
     "pit_gather_rows",
+    "pit_pack_groups",
     "pit_scatter_rows_scaled",
     "pit_copy2d_async",
     "pit_reduce_rows",
@@ -207,6 +208,7 @@ def _declare(lib) -> None:
     lib.pit_moe_plan.argtypes = [vp, i64, vp, i64, vp, vp, vp, i64, vp]
     lib.pit_moe_recv_plan.argtypes = [vp, i64, i64, vp, i64, vp, vp]
     lib.pit_gather_rows.argtypes = [vp, i64, vp, i64, i64, vp, i64, vp]
+    lib.pit_pack_groups.argtypes = [vp, i64, vp, i64, vp, vp, i64, i64, i64, vp, i64, vp]
     lib.pit_scatter_rows_scaled.argtypes = [vp, i32, i64, vp, i64, i64, vp, vp, i64, vp]
     lib.pit_copy2d_async.argtypes = [vp, i64, vp, i64, i64, i64, vp]
     lib.pit_reduce_rows.argtypes = [vp, i32, i64, i64, i64, vp, i64, i32, i32, vp, vp]

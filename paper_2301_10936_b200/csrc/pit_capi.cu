@@ -117,7 +117,7 @@ extern "C" {
 
 const char* pit_last_error(void) { return g_err.c_str(); }
 
-int pit_abi_version(void) { return 103; }
+int pit_abi_version(void) { return 104; }
 
 // Diagnostic (not part of include/pit_b200.h): the CTA-pair gathered-K kernel's stage timeline.
 PIT_API int pit_debug_gk2_trace(unsigned long long* host_out_1024) { return pit::gk2_trace_read(host_out_1024); }
@@ -455,6 +455,16 @@ int pit_gather_rows(const void* src, int64_t ld_src_bytes, const int32_t* rows, 
   if (n < 0 || row_bytes < 0) return fail(kErrShape, "negative extent");
   if (n && (!src || !rows || !dst)) return fail(kErrArg, "null device pointer");
   return launch_gather_rows(src, ld_src_bytes, rows, n, row_bytes, dst, ld_dst_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int pit_pack_groups(const void* src, int64_t ld_src_bytes, const int32_t* rows, int64_t stride, const int32_t* counts,
+                    const int32_t* offsets, int64_t G, int64_t max_count, int64_t row_bytes, void* dst,
+                    int64_t ld_dst_bytes, void* stream) {
+  if (G < 0 || max_count < 0 || row_bytes < 0) return fail(kErrShape, "negative extent");
+  if (G && (!src || !rows || !counts || !offsets || !dst)) return fail(kErrArg, "null device pointer");
+  const int st = launch_pack_groups(src, ld_src_bytes, rows, stride, counts, offsets, G, max_count, row_bytes, dst,
+                                    ld_dst_bytes, static_cast<cudaStream_t>(stream));
+  return st == kErrUnsupported ? fail(st, "pit_pack_groups needs 16-byte aligned rows and pitches, G <= 65535") : st;
 }
 
 int pit_scatter_rows_scaled(const void* src, int dtype, int64_t ld_src, const int32_t* rows, int64_t n, int64_t width,

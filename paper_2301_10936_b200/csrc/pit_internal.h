@@ -183,6 +183,9 @@ int launch_moe_recv_plan(const int32_t* rc, int W, int El, int32_t* rows, int64_
                          cudaStream_t s);
 int launch_gather_rows(const void* src, int64_t ld_src_bytes, const int32_t* rows, int64_t n, int64_t row_bytes,
                        void* dst, int64_t ld_dst_bytes, cudaStream_t s);
+int launch_pack_groups(const void* src, int64_t ld_src_bytes, const int32_t* rows, int64_t stride,
+                       const int32_t* counts, const int32_t* offsets, int64_t G, int64_t max_count, int64_t row_bytes,
+                       void* dst, int64_t ld_dst_bytes, cudaStream_t s);
 int launch_scatter_rows_scaled(const void* src, int dtype, int64_t ld_src, const int32_t* rows, int64_t n,
                                int64_t width, const float* scale, void* dst, int64_t ld_dst, cudaStream_t s);
 

@@ -160,6 +160,25 @@ __global__ void gather_rows_kernel(const uint8_t* __restrict__ src, int64_t ld_s
   }
 }
 
+// Group-wise SRead with device counts: dst row offsets[g] + i = src row rows[g * stride + i] for
+// i < counts[g] (the grouped GEMM then reads its A rows by TMA instead of gathering them); a warp
+// per row, 16-byte vectors.
+__global__ void __launch_bounds__(256) pack_groups_kernel(const uint8_t* __restrict__ src, int64_t ld_src,
+                                                          const int32_t* __restrict__ rows, int64_t stride,
+                                                          const int32_t* __restrict__ counts,
+                                                          const int32_t* __restrict__ offsets, int64_t row_bytes,
+                                                          uint8_t* __restrict__ dst, int64_t ld_dst) {
+  const int g = blockIdx.y;
+  const int c = counts[g];
+  const int64_t o = offsets[g];
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5); i < c; i += static_cast<int64_t>(gridDim.x) * 8) {
+    const uint4* sr = reinterpret_cast<const uint4*>(src + static_cast<int64_t>(__ldg(rows + g * stride + i)) * ld_src);
+    uint4* dr = reinterpret_cast<uint4*>(dst + (o + i) * ld_dst);
+    for (int64_t v = lane; v < row_bytes / 16; v += 32) dr[v] = __ldg(sr + v);
+  }
+}
+
 // dst[rows[i]] = scale[rows[i]] * src[i] (SWrite with the router gate), bf16/fp16/fp32 rows.
 template <typename T>
 __global__ void scatter_rows_scaled_kernel(const T* __restrict__ src, int64_t ld_src, const int32_t* __restrict__ rows,
@@ -266,6 +285,21 @@ int launch_moe_recv_plan(const int32_t* rc, int W, int El, int32_t* rows, int64_
                                                                : 32),
             static_cast<unsigned>(El));
   recv_rows_kernel<<<grid, 256, 0, s>>>(rc, W, El, rows, stride);
+  note_launch();
+  return cuda_status();
+}
+
+int launch_pack_groups(const void* src, int64_t ld_src_bytes, const int32_t* rows, int64_t stride,
+                       const int32_t* counts, const int32_t* offsets, int64_t G, int64_t max_count, int64_t row_bytes,
+                       void* dst, int64_t ld_dst_bytes, cudaStream_t s) {
+  if (G == 0 || max_count == 0 || row_bytes == 0) return kOk;
+  if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) % 16 || ld_src_bytes % 16 ||
+      ld_dst_bytes % 16 || row_bytes % 16 || G > 65535)
+    return kErrUnsupported;
+  const int64_t bx = ceil_div(max_count, 8);
+  const dim3 grid(static_cast<unsigned>(bx < 16 ? bx : 16), static_cast<unsigned>(G));
+  pack_groups_kernel<<<grid, 256, 0, s>>>(static_cast<const uint8_t*>(src), ld_src_bytes, rows, stride, counts, offsets,
+                                          row_bytes, static_cast<uint8_t*>(dst), ld_dst_bytes);
   note_launch();
   return cuda_status();
 }

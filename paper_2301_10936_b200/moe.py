@@ -19,6 +19,8 @@ product; the NCCL-path exchange logic is backend-agnostic so it can be exercised
 
 from __future__ import annotations
 
+import os
+
 import ctypes as C
 from dataclasses import dataclass
 from typing import Optional
@@ -87,6 +89,16 @@ class CudaBackend:
                                                src.shape[1] * eb, out.data_ptr(), out.stride(0) * eb, self._stream()))
         return out
 
+    def pack_groups(self, src, rows, stride, counts, offsets, max_count, n_rows):
+        """Group-wise SRead: row offsets[g] + i of the result = src row rows[g * stride + i]."""
+        torch = _torch()
+        out = torch.empty((max(n_rows, 1), src.shape[1]), dtype=src.dtype, device=src.device)
+        eb = src.element_size()
+        _device.check(self.lib.pit_pack_groups(src.data_ptr(), src.stride(0) * eb, rows.data_ptr(), stride,
+                                               counts.data_ptr(), offsets.data_ptr(), counts.numel(), max_count,
+                                               src.shape[1] * eb, out.data_ptr(), out.stride(0) * eb, self._stream()))
+        return out
+
     def scatter_rows_scaled(self, src, rows, n, scale, out):
         _device.check(self.lib.pit_scatter_rows_scaled(src.data_ptr(), _device.dtype_code(src), src.stride(0),
                                                        rows.data_ptr(), n, src.shape[1],
@@ -128,6 +140,20 @@ def _raw_view(ptr: int, rows: int, cols: int, dtype, device):
 
     raw = torch.as_tensor(_CAI(), device=device)
     return raw.view(dtype)
+
+
+# FFN1's tokens are packed into expert order first (one group-wise SRead) when the experts' groups fill
+# the grouped GEMM's 256-row CTA-pair tiles (>= 256 tokens per expert on average, e.g. 16 experts per
+# rank at EP8): TMA-fed A rows instead of cp.async row gathers (EP8 per-rank proxy 0.221 -> 0.206 ms).
+# Small groups (~128 tokens per expert) run the swapped-role kernel, where packing measured slower.
+# PIT_MOE_PACK=0 / 1 forces it off / on (A/B knob).
+_PACK_ENV = os.environ.get("PIT_MOE_PACK")
+
+
+def _pack_ffn1(rows_hint: int, groups: int) -> bool:
+    if _PACK_ENV is not None:
+        return _PACK_ENV == "1"
+    return rows_hint >= 256 * groups
 
 
 class PeerExchange:
@@ -308,8 +334,12 @@ class SwitchMoE:
         R = self.world * ex.cap
         h = torch.empty((R, self.d_ff), dtype=x.dtype, device=x.device)
         max_tiles = -(-R // 128) + self.El
-        be.grouped_gemm(ex.recv, self.w1, lcounts, loff, ltiles, h, row_src=rows, src_stride=rows.shape[1], act=1,
-                        max_tiles=max_tiles, rows_hint=T)
+        if _pack_ffn1(T, self.El):  # the received tokens in local-expert order, read by TMA
+            xp = be.pack_groups(ex.recv, rows, rows.shape[1], lcounts, loff, rows.shape[1], R)
+            be.grouped_gemm(xp, self.w1, lcounts, loff, ltiles, h, act=1, max_tiles=max_tiles, rows_hint=T)
+        else:
+            be.grouped_gemm(ex.recv, self.w1, lcounts, loff, ltiles, h, row_src=rows, src_stride=rows.shape[1],
+                            act=1, max_tiles=max_tiles, rows_hint=T)
         be.grouped_gemm(h, self.w2, lcounts, loff, ltiles, ex.y, row_dst=rows, dst_stride=rows.shape[1],
                         max_tiles=max_tiles, rows_hint=T)
         ex.signal()                                         # y ready for the peers' pulls
@@ -325,9 +355,15 @@ class SwitchMoE:
         be = self.backend
         T = x.shape[0]
         expert, gate, counts, slots = be.route(logits)
-        offsets, tiles, _ = be.plan(counts)
         h = torch.empty((T, self.d_ff), dtype=x.dtype, device=x.device)
-        be.grouped_gemm(x, self.w1, counts, offsets, tiles, h, row_src=slots, src_stride=slots.shape[1], act=1)
+        if _pack_ffn1(T, self.E):
+            # SRead the tokens into expert order first: FFN1 then reads its A rows by TMA
+            offsets, tiles, _ = be.plan(counts)
+            xp = be.pack_groups(x, slots, slots.shape[1], counts, offsets, T, T)
+            be.grouped_gemm(xp, self.w1, counts, offsets, tiles, h, act=1)
+        else:
+            offsets, tiles, _ = be.plan(counts)
+            be.grouped_gemm(x, self.w1, counts, offsets, tiles, h, row_src=slots, src_stride=slots.shape[1], act=1)
         out = torch.empty((T, self.d_model), dtype=x.dtype, device=x.device)
         be.grouped_gemm(h, self.w2, counts, offsets, tiles, out, row_dst=slots, dst_stride=slots.shape[1],
                         row_scale=gate)

@@ -65,7 +65,7 @@ def test_geometry_and_validation_without_gpu(lib):
     args.sam, args.sak = 64, 1
     assert lib.pit_spmm(C.byref(args), None) == _lib.PIT_ERR_LAYOUT
     assert "col_major" in _lib.last_error()
-    assert lib.pit_abi_version() == 103
+    assert lib.pit_abi_version() == 104
     assert lib.pit_kernel_launches() == 0
 
 

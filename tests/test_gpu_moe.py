@@ -125,3 +125,37 @@ def test_grouped_gemm_batched_slices():
         ref = A[src[g, : counts[g]]].astype(np.float64) @ W[g].astype(np.float64)
         if counts[g]:
             assert orc.max_rel_error(got[o[g] : o[g + 1]], ref) <= 1e-2
+
+
+def test_ffn1_packing_is_bitwise_the_gathered_product():
+    """Large expert groups pack FFN1's tokens into expert order first (pit_pack_groups, TMA-fed A):
+    the same tiles in the same order as the cp.async row gathers, so bitwise the same layer output
+    (PIT_MOE_PACK=1 vs =0 in child processes)."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+from paper_2301_10936_b200.moe import SwitchMoE
+g = torch.Generator(device="cuda").manual_seed(7)
+T, E, d, F = 8192, 16, 512, 1024
+x = torch.randn((T, d), device="cuda", generator=g).to(torch.bfloat16)
+logits = torch.randn((T, E), device="cuda", generator=g)
+w1 = (torch.randn((E, d, F), device="cuda", generator=g) / 24).to(torch.bfloat16)
+w2 = (torch.randn((E, F, d), device="cuda", generator=g) / 32).to(torch.bfloat16)
+out = SwitchMoE(w1, w2, E)(x, logits)
+np.save(sys.argv[1], out.view(torch.int16).cpu().numpy())
+""" % str(root)
+    outs = []
+    for flag in ("1", "0"):
+        f = tempfile.mktemp(suffix=".npy")
+        r = subprocess.run([sys.executable, "-c", code, f], env=dict(os.environ, PIT_MOE_PACK=flag),
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(f))
+    assert np.array_equal(outs[0], outs[1])
