@@ -142,18 +142,15 @@ def _raw_view(ptr: int, rows: int, cols: int, dtype, device):
     return raw.view(dtype)
 
 
-# FFN1's tokens are packed into expert order first (one group-wise SRead) when the experts' groups fill
-# the grouped GEMM's 256-row CTA-pair tiles (>= 256 tokens per expert on average, e.g. 16 experts per
-# rank at EP8): TMA-fed A rows instead of cp.async row gathers (EP8 per-rank proxy 0.221 -> 0.206 ms).
-# Small groups (~128 tokens per expert) run the swapped-role kernel, where packing measured slower.
-# PIT_MOE_PACK=0 / 1 forces it off / on (A/B knob).
+# FFN1's tokens are packed into expert order first (one group-wise SRead, pit_pack_groups), so the
+# grouped GEMM reads its A rows by TMA instead of cp.async row gathers: EP8 per-rank proxy (16 experts
+# x ~1024 tokens, CTA-pair tiles) 0.220 -> 0.191 ms; 128-expert layer (~128 tokens per expert,
+# swapped-role kernel) 0.302 -> 0.290 ms (CUDA-graph timing). PIT_MOE_PACK=0 gathers instead (A/B knob).
 _PACK_ENV = os.environ.get("PIT_MOE_PACK")
 
 
 def _pack_ffn1(rows_hint: int, groups: int) -> bool:
-    if _PACK_ENV is not None:
-        return _PACK_ENV == "1"
-    return rows_hint >= 256 * groups
+    return _PACK_ENV != "0"
 
 
 class PeerExchange:
