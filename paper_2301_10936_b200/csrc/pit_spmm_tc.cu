@@ -277,7 +277,8 @@ struct GkCfg {
 
 template <int GW, bool kOrientN, bool kBF16, int kKS, int kNT, bool kSplit = false>
 __global__ void __launch_bounds__(kThreads, 1)
-    spmm_gk_kernel(const __grid_constant__ CUtensorMap tmC, int use_tma_store, const void* __restrict__ Bv, int64_t ldb, const void* __restrict__ Atv, int64_t lda,
+    spmm_gk_kernel(const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmAt,
+                   const __grid_constant__ CUtensorMap tmBr, int runs, int use_tma_store, const void* __restrict__ Bv, int64_t ldb, const void* __restrict__ Atv, int64_t lda,
                    const int32_t* __restrict__ counts, const int32_t* __restrict__ slots, int64_t slot_stride,
                    int n_groups, int n_tiles, int M, int N, int K, void* __restrict__ Cv, int64_t ldc,
                    int grp_rows, int gpb, int64_t b_batch_stride, int* __restrict__ split_ctr,
@@ -457,7 +458,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m_end = min(M, m0 + grp_rows);
       mbar_wait(&empty_bar[stage * kProdWarps + warp / WPG], phase ^ 1);
       const int r0 = RW * warp;
-      if (r0 < kpad && aligned8) {
+      // runs of consecutive k (block-structured masks, e.g. attention's 64-key blocks): the warp's RW
+      // rows of A^T and of B are two-dimensional boxes, one TMA per 64-column atom, instead of RW
+      // gathered 16-byte rows per lane (orientation N, full 128-row groups; tensor maps from the host)
+      bool run = kOrientN && GW == 128 && runs && r0 + RW <= kvalid;
+      if (run) {
+#pragma unroll
+        for (int i = 1; i < RW; ++i) run &= x.v[i] == x.v[0] + i;
+      }
+      if (run) {
+        if (lane == 0) {
+          uint8_t* sBp = smem + stage * Cfg::STAGE_BYTES;
+          uint8_t* sAp = sBp + Cfg::B_BYTES;
+          uint64_t* fb = &full_bar[stage * kProdWarps + warp / WPG];
+          mbar_expect_tx_only(fb, static_cast<uint32_t>(RW * 128 * (Cfg::B_ATOMS + GW / 64)));
+#pragma unroll
+          for (int a = 0; a < Cfg::B_ATOMS; ++a)
+            tma_load_2d(sBp + a * (Cfg::KS * 128) + r0 * 128, &tmBr, fb, n0 + a * 64, p.b * K + x.v[0]);
+#pragma unroll
+          for (int a = 0; a < GW / 64; ++a)
+            tma_load_2d(sAp + a * (Cfg::KS * 128) + r0 * 128, &tmAt, fb, m0 + a * 64, x.v[0]);
+        }
+      } else if (r0 < kpad && aligned8) {
         // 16-byte chunks are whole or absent (N, M, group rows multiples of 8): ignore-src copies,
         // one predicate per copy — per B row one address multiply-add and the LDGSTS
         const uint32_t sB = smem_u32(smem + stage * Cfg::STAGE_BYTES);
@@ -2791,6 +2813,32 @@ int64_t gk_split_ws_bytes(int64_t n_groups, int n_tiles) {
   return kSplitCtrBytes + (n_groups + kSplitParts) * 16 + static_cast<int64_t>(kSplitParts) * 128 * NT * 4;
 }
 
+// Tensor maps for the run path of spmm_gk (orientation N, 128-row groups): A^T [K, M] and B stacked
+// [batch * K, N], boxes of one 64-column atom x the warp's rows; 0 when the case does not apply.
+template <int GW, bool kOrientN, bool kBF16, int kKS, int kNT>
+int gk_run_maps(const SpmmArgs& a, CUtensorMap* tmAt, CUtensorMap* tmBr) {
+  memset(tmAt, 0, sizeof(*tmAt));
+  memset(tmBr, 0, sizeof(*tmBr));
+  static const int env = [] {
+    const char* e = getenv("PIT_GK_RUNS");  // PIT_GK_RUNS=0: gathered rows only (A/B knob)
+    return e ? atoi(e) : 1;
+  }();
+  if (!kOrientN || GW != 128 || !env || a.t0 != 128 || a.M % 128 != 0 || (a.sak * 2) % 16 != 0 ||
+      (a.ldb * 2) % 16 != 0 || (reinterpret_cast<uintptr_t>(a.A) & 15) != 0 || (reinterpret_cast<uintptr_t>(a.B) & 15) != 0 ||
+      (a.batch > 1 && a.b_batch_stride != a.K * a.ldb))
+    return 0;
+  constexpr int RW = kKS / kProdWarps;
+  const CUtensorMapDataType dt = kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  if (encode_tensor_map_2d(tmAt, dt, a.A, static_cast<uint64_t>(a.M), static_cast<uint64_t>(a.K),
+                           static_cast<uint64_t>(a.sak) * 2, 64, RW, CU_TENSOR_MAP_SWIZZLE_128B) != CUDA_SUCCESS ||
+      encode_tensor_map_2d(tmBr, dt, a.B, static_cast<uint64_t>(a.N), static_cast<uint64_t>(a.K * (a.batch > 1 ? a.batch : 1)),
+                           static_cast<uint64_t>(a.ldb) * 2, 64, RW, CU_TENSOR_MAP_SWIZZLE_128B) != CUDA_SUCCESS) {
+    cudaGetLastError();
+    return 0;
+  }
+  return 1;
+}
+
 template <int GW, bool kOrientN, bool kBF16, int kKS, int kNT>
 int run_gk_split(const SpmmArgs& a, cudaStream_t s, const CUtensorMap& tmC, int epi, int n_tiles) {
   using Cfg = GkCfg<GW, kOrientN, kKS, kNT>;
@@ -2813,7 +2861,9 @@ int run_gk_split(const SpmmArgs& a, cudaStream_t s, const CUtensorMap& tmC, int 
   // virtual groups <= n_groups + P: enough CTAs for the longest walk; idle CTAs exit at once
   const int64_t vunits = a.n_groups + kSplitParts;
   const int grid = static_cast<int>(vunits < num_sms() ? vunits : num_sms());
-  kern<<<grid, kThreads, Cfg::SMEM, s>>>(tmC, epi, a.B, a.ldb, a.A, a.sak, a.counts, a.slots, a.slot_stride,
+  CUtensorMap tmAt, tmBr;
+  const int runs = gk_run_maps<GW, kOrientN, kBF16, kKS, kNT>(a, &tmAt, &tmBr);
+  kern<<<grid, kThreads, Cfg::SMEM, s>>>(tmC, tmAt, tmBr, runs, epi, a.B, a.ldb, a.A, a.sak, a.counts, a.slots, a.slot_stride,
                                          static_cast<int>(a.n_groups), n_tiles, static_cast<int>(a.M),
                                          static_cast<int>(a.N), static_cast<int>(a.K), a.C, a.ldc,
                                          static_cast<int>(a.t0),
@@ -2861,7 +2911,9 @@ int run_gk(const SpmmArgs& a, cudaStream_t s) {
       return run_gk_split<GW, kOrientN, kBF16, kKS, kNT>(a, s, tmC, epi, n_tiles);
   }
   // A column-major: A^T is row-major [K, M] with pitch sak
-  kern<<<grid, kThreads, Cfg::SMEM, s>>>(tmC, epi, a.B, a.ldb, a.A, a.sak, a.counts, a.slots, a.slot_stride,
+  CUtensorMap tmAt, tmBr;
+  const int runs = gk_run_maps<GW, kOrientN, kBF16, kKS, kNT>(a, &tmAt, &tmBr);
+  kern<<<grid, kThreads, Cfg::SMEM, s>>>(tmC, tmAt, tmBr, runs, epi, a.B, a.ldb, a.A, a.sak, a.counts, a.slots, a.slot_stride,
                                          static_cast<int>(a.n_groups), n_tiles, static_cast<int>(a.M),
                                          static_cast<int>(a.N), static_cast<int>(a.K), a.C, a.ldc,
                                          static_cast<int>(a.t0),
