@@ -56,6 +56,9 @@ DEFAULT_WORKLOAD = "pitk_c1_8192"
 C1_1024 = dict(M=1024, K=1024, N=1024, micro=(32, 1), axis="k", zero=0.90, tile=(32, 64, 32),
                desc="BASELINE configs[0]: pit:k SpMM 1024^3 fp32, random 32x1 micro-tiles, 90% zero")
 FLUSH_BYTES = 256 << 20
+# CUDA event timestamps come in ~2 us quanta on this part (a 1-kernel graph replay reads 6.1 / 8.2 us,
+# nothing between): per-replay times are averaged (mean), which resolves below the quantum, rather
+# than taking a median that sits on the grid
 L2_GATHER_CEILING_GBPS = 11145.6  # best measured L2->SM cp.async gather rate (profiles/r1/copy_probe_l2_patterns.txt)
 
 
@@ -285,7 +288,7 @@ def run_ours(args, w):
             d1.record(stream)
             ev.append((d0, d1))
         torch.cuda.synchronize()
-        det_dev_ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+        det_dev_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
         del g_det
     except Exception:  # graph capture is an optimisation of the measurement, never a failure
         det_dev_ms = None
@@ -504,7 +507,7 @@ def bert_bench(args, dev, peaks):
         e1.record(stream)
         ev.append((e0, e1))
     torch.cuda.synchronize()
-    ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+    ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
     # context on the same box: the same product dense on the padded batch (cuBLAS and this package's
     # dense plan), cuBLAS on the live rows alone (the floor for any padding removal), and the pit:m
     # product with the index reused (what each further layer of a batch pays: PIT builds one index
@@ -550,7 +553,7 @@ def _time_layer(fn, steps, dev, world):
         e1.record(stream)
         ev.append((e0, e1))
     torch.cuda.synchronize()
-    ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+    ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
     if world > 1:
         ms = max_over_ranks(ms, dev)
     return ms
@@ -696,8 +699,8 @@ def sparsity_sweep_bench(args, dev, peaks, side=8192, micros=((32, 1), (128, 1),
                 e2.record(stream)
                 ev.append((e0, e1, e2))
             torch.cuda.synchronize()
-            det = statistics.median(a.elapsed_time(b) for a, b, _ in ev)
-            mm = statistics.median(b.elapsed_time(c) for _, b, c in ev)
+            det = statistics.mean(a.elapsed_time(b) for a, b, _ in ev)
+            mm = statistics.mean(b.elapsed_time(c) for _, b, c in ev)
             tf = flops / (mm * 1e-3) / 1e12
             kern = "spmm_gk2 (CTA pair)" if micro[0] > 128 else "spmm_gk"
             out[f"{micro[0]}x{micro[1]}@{zero}"] = {
@@ -738,7 +741,7 @@ def index_build_bench(dev, peaks, side=16384, reps=20):
         e1.record(stream)
         times.append((e0, e1))
     torch.cuda.synchronize()
-    ms = statistics.median(a.elapsed_time(b) for a, b in times)
+    ms = statistics.mean(a.elapsed_time(b) for a, b in times)
     nbytes = A.numel() * 2 + 4 * (idx.n_groups + total)
     gbps = nbytes / (ms * 1e-3) / 1e9
     del At, A
@@ -814,7 +817,7 @@ def attention_bench(args, dev, peaks, heads=12, seq=4096, hd=64):
             e1.record(stream)
             ev.append((e0, e1))
         torch.cuda.synchronize()
-        ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+        ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
         return {"ms_per_step": round(ms, 4), "value": round(eff / (ms * 1e-3) / 1e12, 2),
                 "max_rel_err_head0_vs_f64": err, "graph_replay_equals_eager": bool(torch.equal(O_g, O))}
 
@@ -922,7 +925,7 @@ def attention_scores_bench(args, dev, peaks, blocks, ann_dev, heads, seq, hd, fl
             e1.record(stream)
             ev.append((e0, e1))
         torch.cuda.synchronize()
-        return statistics.median(a.elapsed_time(b) for a, b in ev)
+        return statistics.mean(a.elapsed_time(b) for a, b in ev)
 
     for _ in range(3):
         graph.replay()
@@ -1006,7 +1009,7 @@ def opt_bench(args, dev, peaks, tokens=4096, d_model=2048, d_ff=8192, zeros=(0.9
             e1.record(stream)
             ev.append((e0, e1))
         torch.cuda.synchronize()
-        ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+        ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
         # per-product split: each product alone as a CUDA graph over the step's index, L2 flushed
         idx = pit.build_index_from_tensor(H, (1, 32), "m")
         split = []
@@ -1082,7 +1085,7 @@ def c1_fp32_bench(args, dev, peaks):
         e1.record(stream)
         ev.append((e0, e1))
     torch.cuda.synchronize()
-    ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+    ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
     return {"workload": w["desc"], "value": round(eff / (ms * 1e-3) / 1e12, 3), "unit": "TFLOP/s (effective)",
             "ms_per_step": round(ms, 4), "dtype": "f32", "kernel": "spmm_simt (K7 FFMA, fp32, no TF32)",
             "rel_err_normwise_vs_f64": err, "tolerance": 1e-5,
