@@ -2,11 +2,11 @@ timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --cache-co
 python - <<'PY'
 import csv, collections
 rows=[r for r in csv.reader(open("gpurun_out/moe_warm.csv")) if len(r) > 10]
-t=collections.defaultdict(list); b=collections.defaultdict(list)
+seq=[]
 for r in rows[1:]:
-    name=r[4].split("(")[0][-45:]
-    if r[-3]=="gpu__time_duration.sum": t[name].append(float(r[-1].replace(",","")))
-    if r[-3]=="dram__bytes_read.sum": b[name].append(float(r[-1].replace(",","")))
-for k in t:
-    print(f"{k:46s} n={len(t[k]):3d} last={t[k][-1]/1e3:8.1f} us  dram_read={b[k][-1]/1e6 if b[k] else 0:8.1f} MB")
+    if "pit::" not in r[4]: continue
+    if r[-3]=="gpu__time_duration.sum": seq.append([r[4].split("(")[0][-40:], float(r[-1].replace(",",""))/1e3, 0])
+    if r[-3]=="dram__bytes_read.sum" and seq: seq[-1][2]=float(r[-1].replace(",",""))/1e6
+for name,t,b in seq[-7:]:
+    print(f"{name:42s} {t:8.1f} us  dram {b:8.1f} MB")
 PY
