@@ -514,6 +514,8 @@ def bert_bench(args, dev, peaks):
     # per batch)
     rows = int(live // w["K"])
     Al = torch.randn((rows, w["K"]), device=dev, dtype=torch.bfloat16)
+    row_live = (A != 0).any(dim=1).cpu().numpy()  # the token rows the sequence lengths keep
+    ann_rows = pit.from_bits(row_live[:, None], (w["M"], w["K"]), (1, w["K"])).on_device(dev)
     ctx_reps = max(20, args.steps)
     idx = pit.build_index_from_tensor(A, w["micro"], w["axis"])
     reg = pit.register_builtin_kernels(include_b200_tiles=True)
@@ -526,6 +528,11 @@ def bert_bench(args, dev, peaks):
             dplan, pit.DenseTensor(A), pit.DenseTensor(B), None), flush, ctx_reps), 4),
         "pit_m_index_reused_ms": round(_graph_ms(lambda: pit.run_matmul_with_index(
             plan, pit.DenseTensor(A), pit.DenseTensor(B), idx), flush, ctx_reps), 4),
+        # the padding known from the sequence lengths instead of detected from the values: the
+        # annotation (1 bit per token row) on the device, index built from its bits
+        "pit_m_from_lengths_ms": round(_graph_ms(lambda: pit.run_matmul_with_index(
+            plan, pit.DenseTensor(A), pit.DenseTensor(B), pit.build_index(ann_rows, w["micro"], w["axis"])),
+            flush, ctx_reps), 4),
         "timing": "mean of CUDA-graph replays, L2 flushed before each",
     }
     return {"workload": w["desc"], "value": round(eff / (ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s (effective)",
