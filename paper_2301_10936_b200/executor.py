@@ -456,6 +456,14 @@ def run_matmul_with_index(
     host = not (A.is_device and B.is_device)
     if host and _pipelined_ok(A, B):
         Cres = _run_host_pipelined(plan, A, B, idx)
+    elif host and _stageable(B):
+        # large host B that is numpy or pageable (the reference's own contract): one copy into pinned
+        # memory, then the same pipelined path (B slab uploads, per-slab SpMM and C slab downloads
+        # overlap); C comes back as numpy when B came in as numpy (a view of the pinned result)
+        Bp = _torch().from_numpy(np.ascontiguousarray(B.array)) if not _is_torch(B.array) else B.array.contiguous()
+        Cres = _run_host_pipelined(plan, A, DenseTensor(Bp.pin_memory()), idx)
+        if not _is_torch(B.array):
+            Cres = Cres.numpy()
     else:
         Ad = _device.to_device(A.array)
         Bd = _device.to_device(B.array)
@@ -480,6 +488,20 @@ def _pipelined_ok(A: DenseTensor, B: DenseTensor) -> bool:
     b = B.array
     return (_is_torch(b) and not b.is_cuda and b.is_pinned() and _torch_layout(b) == ROW_MAJOR
             and b.numel() * b.element_size() >= _PIPE_MIN_BYTES and b.shape[1] >= 1024)
+
+
+def _stageable(B: DenseTensor) -> bool:
+    """Large row-major host B that is not pinned (numpy, pageable torch): worth one pinned copy."""
+    b = B.array
+    if _is_torch(b):
+        if b.is_cuda or b.is_pinned():
+            return False
+        n_bytes, layout, ndim = b.numel() * b.element_size(), _torch_layout(b), b.dim()
+    else:
+        b = np.asarray(b)
+        n_bytes, ndim = b.nbytes, b.ndim
+        layout = ROW_MAJOR if b.flags.c_contiguous else COL_MAJOR
+    return ndim == 2 and layout == ROW_MAJOR and n_bytes >= _PIPE_MIN_BYTES and b.shape[1] >= 1024
 
 
 def _run_host_pipelined(plan: SparseKernelPlan, A: DenseTensor, B: DenseTensor, idx):
