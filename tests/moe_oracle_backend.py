@@ -45,6 +45,14 @@ class OracleBackend:
     def gather_rows(self, src, rows, n):
         return src[rows[:n].long()].clone()
 
+    def pack_groups(self, src, rows, stride, counts, offsets, max_count, n_rows):
+        """csrc pack_groups_kernel: out[offsets[g] + i] = src[rows[g, i]] for i < counts[g]."""
+        out = src.new_zeros((max(n_rows, 1), src.shape[1]))
+        for g in range(counts.numel()):
+            c, o = int(counts[g]), int(offsets[g])
+            out[o:o + c] = src[rows.view(-1, stride)[g, :c].long()]
+        return out
+
     def scatter_rows_scaled(self, src, rows, n, scale, out):
         r = rows[:n].long()
         out[r] = (src[:n].double() * scale[r].double()[:, None]).to(out.dtype)
