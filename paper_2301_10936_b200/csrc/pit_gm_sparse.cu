@@ -20,6 +20,7 @@
 //
 // Work: the tensor pipe executes union-row products (~8% of dense at 1% density); the traffic is
 // the weights once, the packed rows, and the fp32 partials (~2.5 per output row at 1%).
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -141,7 +142,7 @@ __global__ void __launch_bounds__(256) gm_sparse_pack_kernel(const int32_t* __re
                                                              const int* __restrict__ cnt, int S,
                                                              const int32_t* __restrict__ rows, int64_t M,
                                                              const uint32_t* __restrict__ occ, int64_t WG, int lg_t1,
-                                                             uint8_t* __restrict__ X, int64_t bound_rows) {
+                                                             uint8_t* __restrict__ X, int64_t bound_rows, int sg) {
   extern __shared__ int soff[];  // [S + 1] packed offsets
   __shared__ int red[16];
   if (!sparse_verdict(counts, nkg, M, red)) return;
@@ -156,12 +157,14 @@ __global__ void __launch_bounds__(256) gm_sparse_pack_kernel(const int32_t* __re
       if (soff[mid] <= j) lo = mid; else hi = mid;
     }
     const int r = __ldcg(rows + lo * M + (j - soff[lo]));
-    const int64_t col = static_cast<int64_t>(lo) * 256 + lane * 8;  // element column
-    const int64_t kg = col >> lg_t1;
-    const bool live = (__ldg(occ + kg * WG + (r >> 5)) >> (r & 31)) & 1u;
-    uint4 v = make_uint4(0u, 0u, 0u, 0u);
-    if (live) v = __ldg(reinterpret_cast<const uint4*>(A + static_cast<int64_t>(r) * lda_bytes + col * 2));
-    reinterpret_cast<uint4*>(X + j * 512)[lane] = v;
+    for (int c0 = 0; c0 < sg; c0 += 256) {  // 256 columns (32 lanes x 8) per pass
+      const int64_t col = static_cast<int64_t>(lo) * sg + c0 + lane * 8;  // element column
+      const int64_t kg = col >> lg_t1;
+      const bool live = (__ldg(occ + kg * WG + (r >> 5)) >> (r & 31)) & 1u;
+      uint4 v = make_uint4(0u, 0u, 0u, 0u);
+      if (live) v = __ldg(reinterpret_cast<const uint4*>(A + static_cast<int64_t>(r) * lda_bytes + col * 2));
+      reinterpret_cast<uint4*>(X + j * (sg * 2) + c0 * 2)[lane] = v;
+    }
   }
 }
 
@@ -255,6 +258,14 @@ __global__ void __launch_bounds__(256) gm_sparse_reduce_kernel(const int32_t* __
 
 int64_t gm_sparse_bound_rows(int64_t M, int64_t nkg, int S) { return ceil_div(M * nkg, kSparseDen) + S; }
 
+int gm_sg() {  // columns per supergroup: 256, or PIT_GM_SG=512 (A/B knob)
+  static const int v = [] {
+    const char* e = getenv("PIT_GM_SG");
+    return e && atoi(e) == 512 ? 512 : 256;
+  }();
+  return v;
+}
+
 GmSparseWs gm_sparse_layout(int64_t M, int64_t N, int64_t WG, int S, int64_t bound_rows) {
   GmSparseWs w{};
   int64_t o = 0;
@@ -269,7 +280,7 @@ GmSparseWs gm_sparse_layout(int64_t M, int64_t N, int64_t WG, int S, int64_t bou
   w.U = take(4 * S * WG);
   w.pre = take(4 * S * WG);
   w.rows = take(4 * S * M);
-  w.X = take(bound_rows * 512);
+  w.X = take(bound_rows * gm_sg() * 2);
   w.part = take(bound_rows * N * 4);
   w.bytes = o;
   return w;
@@ -291,7 +302,8 @@ int launch_gm_sparse_pack(const int32_t* counts, int nkg, const void* A, int64_t
   const int64_t cap = static_cast<int64_t>(n_sms()) * 8;
   gm_sparse_pack_kernel<<<static_cast<unsigned>(blocks < cap ? blocks : cap), 256, (S + 1) * sizeof(int), s>>>(
       counts, nkg, static_cast<const uint8_t*>(A), lda_bytes, reinterpret_cast<const int*>(ws + w.cnt), S,
-      reinterpret_cast<const int32_t*>(ws + w.rows), M, occ, WG, t1 == 16 ? 4 : t1 == 32 ? 5 : 6, ws + w.X, bound_rows);
+      reinterpret_cast<const int32_t*>(ws + w.rows), M, occ, WG, t1 == 16 ? 4 : t1 == 32 ? 5 : 6, ws + w.X, bound_rows,
+      gm_sg());
   note_launch();
   return cuda_status();
 }

@@ -141,6 +141,7 @@ struct GmSparseWs {  // byte offsets into the caller's workspace
   int64_t flag, cnt, off, U, pre, rows, X, part, bytes;
 };
 int64_t gm_sparse_bound_rows(int64_t M, int64_t nkg, int S);
+int gm_sg();  // columns per supergroup (256; PIT_GM_SG=512)
 GmSparseWs gm_sparse_layout(int64_t M, int64_t N, int64_t WG, int S, int64_t bound_rows);
 int launch_gm_sparse_prep(const int32_t* counts, int nkg, int64_t M, int gps, int S, const uint32_t* occ, int64_t WG,
                           uint8_t* ws, const GmSparseWs& w, cudaStream_t s);

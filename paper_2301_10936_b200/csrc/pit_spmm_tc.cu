@@ -3267,17 +3267,17 @@ int gm_sparse_enabled() {  // PIT_GM_SPARSE=0: no high-sparsity pit:m path (A/B 
 // K in 256-column supergroups, 16-byte aligned row-major A and C
 bool gm_sparse_capable(const SpmmArgs& a) {
   if (a.plan != kPlanPitM || a.occ == nullptr || a.counts == nullptr || !(a.t1 == 16 || a.t1 == 32) ||
-      a.K % 256 != 0 || ceil_div(a.K, a.t1) <= 1 || a.sak != 1 || (a.sam * 2) % 16 != 0 ||
+      a.K % gm_sg() != 0 || ceil_div(a.K, a.t1) <= 1 || a.sak != 1 || (a.sam * 2) % 16 != 0 ||
       (reinterpret_cast<uintptr_t>(a.A) & 15) != 0 || (a.ldc % 8) != 0 || (a.N % 8) != 0 ||
       (reinterpret_cast<uintptr_t>(a.C) & 15) != 0 || a.M >= (1 << 24) || !gm_sparse_enabled() || !a_tma_enabled())
     return false;
-  const int64_t S = a.K / 256;
+  const int64_t S = a.K / gm_sg();
   return S <= kRg2MaxGroups && S * a.WG <= 8192;
 }
 
 int64_t gm_sparse_ws_bytes(const SpmmArgs& a) {
   if (!gm_sparse_capable(a)) return 0;
-  const int S = static_cast<int>(a.K / 256);
+  const int S = static_cast<int>(a.K / gm_sg());
   return gm_sparse_layout(a.M, a.N, a.WG, S, gm_sparse_bound_rows(a.M, a.K / a.t1, S)).bytes;
 }
 
@@ -3321,11 +3321,11 @@ int run_gm(const SpmmArgs& a, int ks, cudaStream_t s) {
   int sp_S = 0;
   int64_t sp_bound = 0;
   if (!dense && gm_sparse_capable(a) && a.ws != nullptr && a.ws_bytes >= gm_sparse_ws_bytes(a)) {
-    sp_S = static_cast<int>(a.K / 256);
+    sp_S = static_cast<int>(a.K / gm_sg());
     sp_bound = gm_sparse_bound_rows(a.M, a.K / a.t1, sp_S);
     sw = gm_sparse_layout(a.M, a.N, a.WG, sp_S, sp_bound);
     uint8_t* ws = static_cast<uint8_t*>(a.ws);
-    if (int st = launch_gm_sparse_prep(a.counts, static_cast<int>(ceil_div(a.K, a.t1)), a.M, 256 / a.t1, sp_S, a.occ,
+    if (int st = launch_gm_sparse_prep(a.counts, static_cast<int>(ceil_div(a.K, a.t1)), a.M, gm_sg() / a.t1, sp_S, a.occ,
                                        a.WG, ws, sw, s))
       return st;
     sparse_flag = reinterpret_cast<const int*>(ws + sw.flag);
@@ -3377,12 +3377,12 @@ int run_gm(const SpmmArgs& a, int ks, cudaStream_t s) {
       return st;
     RowGemmParams q{};
     q.A = ws + sw.X;
-    q.lda = 256;
+    q.lda = gm_sg();
     q.M = static_cast<int>(sp_bound);  // packed rows (bounds of the TMA map)
     q.C = a.C;
     q.ldc = a.ldc;
     q.N = static_cast<int>(a.N);
-    q.K = 256;
+    q.K = gm_sg();
     q.G = sp_S;
     q.cnt = reinterpret_cast<const int32_t*>(ws + sw.cnt);
     q.off = nullptr;  // the kernel derives the packed offsets from cnt
