@@ -134,3 +134,17 @@ def test_device_ops_fail_loudly_without_gpu():
     ann = pit.random_annotation((8, 8), (1, 1), 0.5, seed=0)
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         pit.build_index(ann, (1, 4), "m")
+
+
+def test_host_pipeline_slab_schedule_tiles_columns():
+    """The B / C column slabs of the pinned-host pipeline (executor._slab_schedule) tile [0, N)
+    exactly, in order, with no empty slab, small slabs at both ends for wide N."""
+    from paper_2301_10936_b200.executor import _slab_schedule
+
+    for N in (1024, 1500, 2048, 3000, 4096, 5000, 8192, 8200, 16384, 65536):
+        sched = _slab_schedule(N)
+        assert [j0 for j0, _ in sched] == [sum(w for _, w in sched[:i]) for i in range(len(sched))]
+        assert sum(w for _, w in sched) == N and all(w > 0 for _, w in sched)
+        if N >= 4096:
+            widths = [w for _, w in sched]
+            assert widths[0] < max(widths) and widths[-1] < max(widths)
