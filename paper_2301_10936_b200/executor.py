@@ -817,6 +817,12 @@ def run_batched_matmul_with_index(plan: SparseKernelPlan, A3, B3, idx: Optional[
             keep.append(occ)
             a.occ = occ.data_ptr()
             a.words_per_group = occ.shape[1]
+            if batch == 1:  # a single slice runs the 2-D pit:m kernels: union rows + per-group counts
+                rows, n_rows = idx.union_coords()
+                a.counts, _, alive = idx.device_ptrs()
+                keep += [rows, n_rows, *alive]
+                a.rows, a.n_rows = rows.data_ptr(), n_rows.data_ptr()
+                a.n_rows_bound = M
     _attach_workspace(a, keep)
     _device.check(_lib.load().pit_spmm(C.byref(a), _device.stream_ptr()), ExecError)
     if stats is not None:
@@ -838,7 +844,7 @@ def run_sparse_batched_matmul(plan: SparseKernelPlan, A3, B3, anns, stats: Optio
     """Batched run_sparse_matmul: per-slice annotations -> stacked index -> one launch. pit:m slices
     the tensor-core path cannot take in one launch (fp32, or B rows not 16-byte aligned) run slice
     by slice through run_matmul_with_index, each with its own index."""
-    if plan.pit_axis == "m" and not _batched_pit_m_ok(B3):
+    if plan.pit_axis == "m" and not _batched_pit_m_ok(A3, B3):
         torch = _torch()
         outs = []
         for b, ann in enumerate(anns):
@@ -849,10 +855,12 @@ def run_sparse_batched_matmul(plan: SparseKernelPlan, A3, B3, anns, stats: Optio
     return run_batched_matmul_with_index(plan, A3, B3, idx, stats=stats)
 
 
-def _batched_pit_m_ok(B3) -> bool:
-    if not _is_torch(B3):
+def _batched_pit_m_ok(A3, B3) -> bool:
+    """One tensor-core launch takes the stacked pit:m product: bf16 / fp16, A and B rows 16-byte
+    aligned (TMA pitches)."""
+    if not (_is_torch(B3) and _is_torch(A3)):
         return False
     torch = _torch()
     es = B3.element_size()
     return B3.dtype in (torch.bfloat16, torch.float16) and (B3.shape[2] * es) % 16 == 0 and \
-        (B3.stride(0) * es) % 16 == 0
+        (B3.stride(0) * es) % 16 == 0 and A3.dim() == 3 and (A3.stride(1) * A3.element_size()) % 16 == 0
