@@ -242,3 +242,36 @@ def test_random_sread_swrite_case_matches_oracle(cid):
         assert pit.swrite(tile, dst, idx, g, start=start, accumulate=acc) == \
             orc.swrite(want_tile, want, groups, micro, d, g, start=start, accumulate=acc)
         np.testing.assert_array_equal(dst, want)
+
+
+@pytest.mark.parametrize("cid", range(32 * SCALE))
+def test_random_detection_special_values(cid):
+    """K1 value-route detection (index.py:164-173) on random shapes, micro-tiles, dtypes and layouts
+    with the special values of Appendix A.4 planted: -0.0 is zero; NaN, +-inf and subnormals are
+    live. Canonical dump equal to the oracle's."""
+    import torch
+
+    import paper_2301_10936_b200 as pit
+
+    rng = np.random.default_rng(7900 + cid)
+    r, c = int(rng.integers(1, 700)), int(rng.integers(1, 700))
+    dt = rng.choice([torch.float32, torch.float64, torch.bfloat16, torch.float16])
+    axis = rng.choice(["m", "k"])
+    t = int(rng.choice([1, 2, 3, 8, 16, 32, 64, 128, 256]))
+    micro = (1, t) if axis == "m" else (t, 1)
+    if rng.random() < 0.3:
+        micro = (int(rng.choice([2, 4, 8])), t) if axis == "m" else (t, int(rng.choice([2, 4, 8])))
+    x = np.zeros((r, c), np.float64)
+    live = rng.random((r, c)) < float(rng.choice([0.0, 0.001, 0.02, 0.3]))
+    x[live] = rng.standard_normal(int(live.sum()))
+    tiny = {torch.float32: 1e-45, torch.float64: 5e-324, torch.bfloat16: 1e-40, torch.float16: 6e-8}[dt]
+    for val in (-0.0, np.nan, np.inf, -np.inf, tiny, -tiny):
+        n = int(rng.integers(0, 4))
+        x[rng.integers(0, r, n), rng.integers(0, c, n)] = val
+    xd = torch.from_numpy(x).to(dt).cuda()
+    if rng.random() < 0.5:
+        xd = xd.t().contiguous().t()  # column-major storage
+    xr = xd.double().cpu().numpy()  # the values as stored (rounding / flush of the narrow types)
+    idx = pit.build_index_from_tensor(xd, micro, axis)
+    counts, groups = orc.build_index_from_values(xr, micro, axis)
+    assert pit.dump_index(idx) == orc.dump_index(micro, axis, counts, groups), (cid, r, c, dt, micro, axis)
