@@ -535,13 +535,34 @@ __global__ void __launch_bounds__(kCompactThreads) compact_kernel(const uint32_t
 }
 
 // OR of all group rows: the union of live coordinates (used by pit:m union-row tiles).
-__global__ void union_kernel(const uint32_t* __restrict__ occ, int64_t n_groups, int64_t WG,
-                             uint32_t* __restrict__ uni) {
-  const int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (w >= WG) return;
+// Union of every group's occupancy words: block = 32 consecutive words (lane = word, coalesced
+// 128-byte rows) x 32 warps striding the groups with four independent loads in flight; the warps'
+// partial ORs meet in shared memory. (A thread per word looping over all groups took 19 us for
+// 256 groups x 128 words: one CTA, one dependent load chain per thread.)
+constexpr int kUnionWarps = 32;
+__global__ void __launch_bounds__(kUnionWarps * 32) union_kernel(const uint32_t* __restrict__ occ, int64_t n_groups,
+                                                                 int64_t WG, uint32_t* __restrict__ uni) {
+  __shared__ uint32_t part[kUnionWarps][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t w = static_cast<int64_t>(blockIdx.x) * 32 + lane;
   uint32_t acc = 0;
-  for (int64_t g = 0; g < n_groups; ++g) acc |= occ[g * WG + w];
-  uni[w] = acc;
+  if (w < WG) {
+    int64_t g = warp;
+    for (; g + 3 * kUnionWarps < n_groups; g += 4 * kUnionWarps) {
+      const uint32_t a = __ldg(occ + g * WG + w), b = __ldg(occ + (g + kUnionWarps) * WG + w);
+      const uint32_t c = __ldg(occ + (g + 2 * kUnionWarps) * WG + w), d = __ldg(occ + (g + 3 * kUnionWarps) * WG + w);
+      acc |= (a | b) | (c | d);
+    }
+    for (; g < n_groups; g += kUnionWarps) acc |= __ldg(occ + g * WG + w);
+  }
+  part[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t u = 0;
+#pragma unroll
+    for (int i = 0; i < kUnionWarps; ++i) u |= part[i][lane];
+    if (w < WG) uni[w] = u;
+  }
 }
 
 // Rebuild the occupancy bitmap from (possibly reordered) slots: lets kernels that need
@@ -726,7 +747,8 @@ int launch_occ_counts(const uint32_t* occ, int64_t n_groups, int64_t WG, int32_t
 
 int launch_union(const uint32_t* occ, int64_t n_groups, int64_t WG, uint32_t* uni, cudaStream_t s) {
   if (WG == 0) return 0;
-  union_kernel<<<static_cast<unsigned>(ceil_div(WG, 256)), 256, 0, s>>>(occ, n_groups, WG, uni);
+  if (ceil_div(WG, 32) > 0x7fffffffll) return kErrShape;
+  union_kernel<<<static_cast<unsigned>(ceil_div(WG, 32)), kUnionWarps * 32, 0, s>>>(occ, n_groups, WG, uni);
   note_launch();
   return cuda_status();
 }
