@@ -275,3 +275,36 @@ def test_random_detection_special_values(cid):
     idx = pit.build_index_from_tensor(xd, micro, axis)
     counts, groups = orc.build_index_from_values(xr, micro, axis)
     assert pit.dump_index(idx) == orc.dump_index(micro, axis, counts, groups), (cid, r, c, dt, micro, axis)
+
+
+@pytest.mark.parametrize("cid", range(16 * SCALE))
+def test_random_numpy_case_matches_oracle(cid):
+    """The reference's own contract, numpy in / numpy out (f32 / f64), through run_sparse_matmul and
+    build_index_from_tensor + run_matmul_with_index on host arrays; every fourth case has a B large
+    enough (>= 32 MiB) for the pinned, slab-pipelined host path."""
+    import paper_2301_10936_b200 as pit
+
+    rng = np.random.default_rng(8100 + cid)
+    dt = rng.choice([np.float32, np.float64])
+    axis = rng.choice(["m", "k"])
+    if cid % 4 == 3:
+        m, k, n = int(rng.choice([64, 200])), 2048, 4096 if dt == np.float32 else 2048
+    else:
+        m, k, n = (int(rng.integers(1, 400)) for _ in range(3))
+    tile = (32, 64, 32) if axis == "k" else (16, 32, 128)
+    reg = pit.register_builtin_kernels()
+    expr = pit.bind_extents(pit.parse_expr(MATMUL), dict(m=m, k=k, n=n))
+    plan = pit.forced_plan(expr, str(axis), reg, tile_shape=tile)
+    ann = pit.random_annotation((m, k), (int(rng.choice([1, 4, 32])), int(rng.choice([1, 4, 32]))),
+                                float(rng.choice([0.0, 0.5, 0.9, 1.0])), seed=int(rng.integers(1 << 30)))
+    A = (rng.standard_normal((m, k)) * ann.materialize(np.float64)).astype(dt)
+    B = rng.standard_normal((k, n)).astype(dt)
+    At = pit.DenseTensor.from_array(A, layout=plan.sparse_layout)
+    if rng.random() < 0.5:
+        C = pit.run_sparse_matmul(plan, At, pit.DenseTensor(B), ann).array
+    else:
+        idx = pit.build_index_from_tensor(At.array, plan.micro_tile, str(axis))
+        C = pit.run_matmul_with_index(plan, At, pit.DenseTensor(B), idx).array
+    assert isinstance(C, np.ndarray) and C.dtype == dt and C.shape == (m, n), cid
+    ref = orc.dense_reference_f64(A.astype(np.float64), B.astype(np.float64))
+    assert orc.verify_close(C.astype(np.float64), ref), (cid, orc.max_rel_error(C, ref))
