@@ -245,6 +245,79 @@ __global__ void __launch_bounds__(256) detect_cols_vec_kernel(const uint8_t* __r
   }
 }
 
+// PIT axis along the contiguous columns (pit_phys == 1), 16-byte aligned rows, VPB = 2^lg vectors per
+// micro-column (lg <= 5) and bands that tile 32-row slabs (tr divides 32 or 32 divides tr). Block =
+// one 32-row slab x 256 vector columns; thread = one vector column, its 32 rows loaded 8 at a time
+// (a warp instruction reads one 512-byte segment of a row), liveness kept as a 32-bit row mask.
+// Per band of the slab one ballot over the warp's lanes; lane b compresses band b's ballot into
+// micro-column bits; shared-memory words; plain stores when the block owns whole words and whole
+// bands, atomicOr into a cleared bitmap otherwise (tall bands, or words wider than the block).
+// detect_cols_vec_kernel (one band per block row, one thread per vector column) put too few bytes
+// in flight: 36-50 us for 64 MiB at (1, 32) and (128, 64).
+__global__ void __launch_bounds__(256) detect_cols_slab_kernel(const uint8_t* __restrict__ x, int64_t R,
+                                                               int64_t ld_bytes, int64_t nvec, int tr, int lg,
+                                                               int64_t GR, LiveMask lm, uint32_t* __restrict__ occ,
+                                                               int64_t WG, int atomic_out) {
+  __shared__ uint32_t words[32][8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t v = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 32;
+  reinterpret_cast<uint32_t*>(words)[threadIdx.x] = 0u;
+  __syncthreads();
+  uint32_t lb = 0;
+  if (v < nvec) {
+    const uint8_t* col = x + v * 16;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint4 q[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t r = r0 + c * 8 + u;
+        q[u] = r < R ? __ldg(reinterpret_cast<const uint4*>(col + r * ld_bytes)) : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const bool live = ((q[u].x & lm.even) | (q[u].y & lm.odd) | (q[u].z & lm.even) | (q[u].w & lm.odd)) != 0;
+        lb |= static_cast<uint32_t>(live) << (c * 8 + u);
+      }
+    }
+  }
+  const int nb = tr >= 32 ? 1 : 32 / tr;  // bands in the slab
+  const uint32_t band_rows = tr >= 32 ? 0xffffffffu : (1u << tr) - 1u;
+  uint32_t mine = 0;  // lane b: the warp's ballot of band b
+  for (int b = 0; b < nb; ++b) {
+    const uint32_t ball = __ballot_sync(0xffffffffu, (lb & (band_rows << (tr >= 32 ? 0 : b * tr))) != 0u);
+    if (lane == b) mine = ball;
+  }
+  if (lane < nb && mine) {
+    const int per = lg >= 5 ? 1 : 32 >> lg;  // micro-columns per warp
+    uint32_t bits = mine;
+    if (lg > 0) {
+      const uint32_t vmask = lg >= 5 ? 0xffffffffu : (1u << (1 << lg)) - 1u;
+      bits = 0;
+      for (int i = 0; i < per; ++i) bits |= ((mine >> (i << lg)) & vmask) ? (1u << i) : 0u;
+    }
+    const int64_t mc0 = (static_cast<int64_t>(blockIdx.x) * 256 + warp * 32) >> lg;
+    const int64_t w0 = ((static_cast<int64_t>(blockIdx.x) * 256) >> lg) >> 5;
+    atomicOr(&words[lane][(mc0 >> 5) - w0], bits << (mc0 & 31));
+  }
+  __syncthreads();
+  const int wn = ((256 >> lg) + 31) >> 5;  // words the block touches per band
+  const int64_t w0 = ((static_cast<int64_t>(blockIdx.x) * 256) >> lg) >> 5;
+  const int64_t band0 = r0 / tr;
+  if (threadIdx.x < nb * wn) {
+    const int b = threadIdx.x / wn, w = threadIdx.x % wn;
+    const int64_t band = band0 + b;
+    if (band < GR && w0 + w < WG) {
+      const uint32_t val = words[b][w];
+      if (!atomic_out)
+        occ[band * WG + w0 + w] = val;
+      else if (val)
+        atomicOr(&occ[band * WG + w0 + w], val);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Pass 1, generic path: any micro-tile, any alignment, element loads.
 // Block covers 32 micro-row bands x TJ micro-columns; shared-memory bitmap tile in the
@@ -589,6 +662,15 @@ __global__ void slots_to_occ_kernel(const int32_t* __restrict__ counts, const in
 // ---------------------------------------------------------------------------- launchers
 static bool R_fits_grid(int64_t GR) { return GR / 32 + 1 < (1ll << 31); }
 
+// PIT_COLS_SLAB=0: column-axis detection on the one-band-per-block kernel (A/B knob)
+static bool cols_slab_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("PIT_COLS_SLAB");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+
 int launch_detect_values(const DetectValuesArgs& a, cudaStream_t s) {
   const int eb = dtype_bytes(a.dtype);
   const int64_t GR = ceil_div(a.R, a.tr), GC = ceil_div(a.C, a.tc);
@@ -626,6 +708,19 @@ int launch_detect_values(const DetectValuesArgs& a, cudaStream_t s) {
     detect_rows_vec_kernel<<<static_cast<unsigned>(grid), kRaWarps * 32, 0, s>>>(
         static_cast<const uint8_t*>(a.x), a.R, row_bytes, ld_bytes, a.tr, static_cast<int>(vec_per_micro), GR, GC,
         live_mask_for(a.dtype), a.occ, WG, seg_groups, tiles);
+    note_launch();
+  } else if (a.pit_phys == 1 && aligned && (static_cast<int64_t>(a.tc) * eb) % 16 == 0 && vec_per_micro >= 1 &&
+             vec_per_micro <= 32 && (vec_per_micro & (vec_per_micro - 1)) == 0 &&
+             (a.tr % 32 == 0 || 32 % a.tr == 0) && ceil_div(a.R, 32) <= 65535 && cols_slab_enabled()) {
+    const int lg = __builtin_ctzll(static_cast<unsigned long long>(vec_per_micro));
+    const int64_t nvec = row_bytes / 16;
+    const int atomic_out = a.tr > 32 || lg >= 4;  // several blocks share a band's word
+    if (atomic_out &&
+        cudaMemsetAsync(a.occ, 0, static_cast<size_t>(n_groups * WG) * sizeof(uint32_t), s) != cudaSuccess)
+      return cuda_status();
+    dim3 grid(static_cast<unsigned>(ceil_div(nvec, 256)), static_cast<unsigned>(ceil_div(a.R, 32)));
+    detect_cols_slab_kernel<<<grid, 256, 0, s>>>(static_cast<const uint8_t*>(a.x), a.R, ld_bytes, nvec, a.tr, lg, GR,
+                                                 live_mask_for(a.dtype), a.occ, WG, atomic_out);
     note_launch();
   } else if (a.pit_phys == 1 && aligned && (static_cast<int64_t>(a.tc) * eb) % 16 == 0 && vec_per_micro >= 1 &&
              vec_per_micro <= 32 && (vec_per_micro & (vec_per_micro - 1)) == 0 && GR <= 65535) {
