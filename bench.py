@@ -279,6 +279,8 @@ def run_ours(args, w):
         g_det = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g_det):
             pit.build_index_from_tensor(A, micro, axis)
+        for _ in range(3):
+            g_det.replay()
         ev = []
         for _ in range(args.steps):
             flush.zero_()
@@ -544,7 +546,7 @@ def bert_bench(args, dev, peaks):
 
 
 def _time_layer(fn, steps, dev, world):
-    """Median per-call device time of fn() (CUDA events on the current stream), max over ranks."""
+    """Mean per-call device time of fn() (CUDA events on the current stream), max over ranks."""
     import torch
     import torch.distributed as dist
 
@@ -923,6 +925,8 @@ def attention_scores_bench(args, dev, peaks, blocks, ann_dev, heads, seq, hd, fl
         step()
 
     def timed(fn, reps):
+        for _ in range(3):  # warm-up: the first eager cuBLAS call carries its one-time setup
+            fn()
         ev = []
         for _ in range(reps):
             flush.zero_()
