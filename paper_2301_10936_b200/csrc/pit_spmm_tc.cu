@@ -41,6 +41,11 @@ namespace {
 // split each stage's copies), 8 MMA issuer, 9 TMEM allocator, 12..15 epilogue (one per TMEM lane
 // quarter).
 constexpr int kProdWarps = 8;
+#ifndef PIT_GK_IDX_DEPTH
+#define PIT_GK_IDX_DEPTH 3
+#endif
+constexpr int kGkIdxDepth = PIT_GK_IDX_DEPTH;  // spmm_gk producers: stages of slot indices in flight + 1
+static_assert(kGkIdxDepth >= 3, "the rotation needs at least three slot sets");
 constexpr int kProdThreads = kProdWarps * 32;
 constexpr int kMmaWarp = 8;
 constexpr int kAllocWarp = 9;
@@ -584,22 +589,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         phase ^= 1;
       }
     };
-    Pos P0 = cur, P1 = advance(P0), P2;
-    Idx X0 = load_idx(P0), X1 = load_idx(P1), X2;
+    // D-way rotation: the slot indices of stage s + D - 1 load while stage s issues (fixed registers
+    // per slot set; a register move of an index whose load is still pending would stall the warp).
+    // This form (arrays, one unrolled loop) measured 342 -> 360 TFLOP/s on C1 32x1 against the
+    // hand-rotated three-way code it replaced, same box; D = 4 / 5 / 6: 354 / 349 / 338
+    // (scripts/gk_deep_ab.sh with PIT_GK_IDX_DEPTH builds).
+    constexpr int D = kGkIdxDepth;
+    Pos P[D];
+    Idx X[D];
+    P[0] = cur;
+#pragma unroll
+    for (int i = 1; i < D - 1; ++i) P[i] = advance(P[i - 1]);
+#pragma unroll
+    for (int i = 0; i < D - 1; ++i) X[i] = load_idx(P[i]);
     while (true) {
-      if (P0.u >= units) break;
-      P2 = advance(P1);
-      X2 = load_idx(P2);
-      issue(P0, X0);
-      if (P1.u >= units) break;
-      P0 = advance(P2);
-      X0 = load_idx(P0);
-      issue(P1, X1);
-      if (P2.u >= units) break;
-      P1 = advance(P0);
-      X1 = load_idx(P1);
-      issue(P2, X2);
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        if (P[j].u >= units) goto producers_done;
+        const int n = (j + D - 1) % D, pv = (j + D - 2) % D;
+        P[n] = advance(P[pv]);
+        X[n] = load_idx(P[n]);
+        issue(P[j], X[j]);
+      }
     }
+  producers_done:;
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idesc = kOrientN ? idesc_f16(128, Cfg::N_TILE, kBF16, true, true)
@@ -1088,6 +1101,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     // Three stages in flight with fixed register roles (no loop-carried copies: a register move of
     // an index whose load is still pending would stall the warp on it, defeating the prefetch).
+#ifdef PIT_GK2_HAND
     Pos P0 = cur, P1 = advance(P0), P2;
     Idx X0 = load_idx(P0), X1 = load_idx(P1), X2;
     while (true) {
@@ -1104,6 +1118,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       X1 = load_idx(P1);
       issue(P2, X2);
     }
+#else
+    constexpr int D = kGkIdxDepth;  // the spmm_gk rotation (arrays, one unrolled loop)
+    Pos P[D];
+    Idx X[D];
+    P[0] = cur;
+#pragma unroll
+    for (int i = 1; i < D - 1; ++i) P[i] = advance(P[i - 1]);
+#pragma unroll
+    for (int i = 0; i < D - 1; ++i) X[i] = load_idx(P[i]);
+    while (true) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        if (P[j].u >= units) goto producers_done;
+        const int n = (j + D - 1) % D, pv = (j + D - 2) % D;
+        P[n] = advance(P[pv]);
+        X[n] = load_idx(P[n]);
+        issue(P[j], X[j]);
+      }
+    }
+  producers_done:;
+#endif
   } else if (warp == kRelayWarp) {
     // ------------------------------------------------------------ relay: local full -> pair full
     if (lane == 0) {
