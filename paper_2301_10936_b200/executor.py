@@ -842,8 +842,8 @@ def run_batched_matmul_with_index(plan: SparseKernelPlan, A3, B3, idx: Optional[
 
 def run_sparse_batched_matmul(plan: SparseKernelPlan, A3, B3, anns, stats: Optional[ExecStats] = None):
     """Batched run_sparse_matmul: per-slice annotations -> stacked index -> one launch. pit:m slices
-    the tensor-core path cannot take in one launch (fp32, or B rows not 16-byte aligned) run slice
-    by slice through run_matmul_with_index, each with its own index."""
+    the tensor-core path cannot take in one launch (fp32, or A / B rows not 16-byte aligned) run
+    slice by slice through run_sparse_matmul, each with its own index."""
     if plan.pit_axis == "m" and not _batched_pit_m_ok(A3, B3):
         torch = _torch()
         outs = []
