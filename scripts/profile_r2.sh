@@ -27,6 +27,10 @@ want gk2 $ARGS && cap gk2 spmm_gk2 3 python bench.py --workload pitk_256_8192 --
 want gm32 $ARGS && cap gm32 rowgemm2 3 python bench.py --workload pitm_32_8192 --steps 1 --warmup 3 $NB
 want bert $ARGS && cap bert_rg2 rowgemm2 2 python scripts/bert_probe.py --ncu
 want moe $ARGS && cap moe_rg2t rowgemm2t 1 python scripts/rowgemm_probe.py --ncu
+want attn $ARGS && cap attn_gk spmm_gk_kernel 2 python scripts/attn_warm.py
+want sddmm $ARGS && cap sddmm_c3 sddmm_kernel 2 python scripts/sddmm_probe.py
+want c4 $ARGS && cap c4_k3s_product rowgemm2t 1 python scripts/c4_probe.py 0.99 --ncu
+want cols $ARGS && cap detect_cols detect_cols_slab 2 python scripts/dh_probe.py
 
 
 ls $OUT/ncu_full_*.txt
