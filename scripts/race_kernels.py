@@ -35,6 +35,19 @@ H = (torch.relu(torch.randn((1024, 2048), device=dev)) * keep.repeat_interleave(
 W = torch.randn((2048, 384), device=dev, dtype=torch.bfloat16)
 pit.run_matmul_with_index(plan(1024, 2048, 384, "m", (16, 32, 128)), pit.DenseTensor(H), pit.DenseTensor(W),
                           pit.build_index_from_tensor(H, (1, 32), "m"))
+# column-axis detection (slab kernel, plain-store and atomic modes), the occupancy union, the 32x1
+# gathered-K kernel (slot-index rotation) and the SDDMM with its two output indexes
+from paper_2301_10936_b200.sddmm import run_sddmm_like  # noqa: E402
+
+for micro in ((1, 32), (128, 64), (4, 8), (1, 256)):
+    pit.build_index_from_tensor(H, micro, "k")
+pit.build_index_from_tensor(H, (1, 32), "m").union_coords()
+A32 = (torch.randn((512, 1024), device=dev, dtype=torch.bfloat16) * (torch.rand((512 // 32, 1024), device=dev) > 0.9)
+       .repeat_interleave(32, dim=0).to(torch.bfloat16)).t().contiguous().t()
+pit.run_matmul_with_index(plan(512, 1024, 1024, "k", (32, 64, 32)), pit.DenseTensor(A32),
+                          pit.DenseTensor(torch.randn((1024, 1024), device=dev, dtype=torch.bfloat16)),
+                          pit.build_index_from_tensor(A32, (32, 1), "k"))
+run_sddmm_like(torch.randn((1024, 384), device=dev, dtype=torch.bfloat16), W.t(), H, (1, 32), gate=H)
 w1 = torch.randn((8, 256, 512), device=dev, dtype=torch.bfloat16) * 0.05
 w2 = torch.randn((8, 512, 256), device=dev, dtype=torch.bfloat16) * 0.05
 moe = SwitchMoE(w1, w2, 8)
