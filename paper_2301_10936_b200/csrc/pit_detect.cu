@@ -704,7 +704,10 @@ int launch_detect_values(const DetectValuesArgs& a, cudaStream_t s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, detect_rows_vec_kernel, kRaWarps * 32, 0);
     if (per_sm < 1) per_sm = 1;
     const int64_t resident = static_cast<int64_t>(per_sm) * sms;  // one wave of persistent CTAs
-    const int64_t grid = tiles < resident ? tiles : resident;
+    // every CTA takes the same number of tiles (C1's 1024 tiles: 512 CTAs x 2 instead of 592 CTAs
+    // with a 27%-idle second pass; 34.3 -> 33.9 us per graph)
+    const int64_t per_cta = ceil_div(tiles, resident);
+    const int64_t grid = ceil_div(tiles, per_cta);
     detect_rows_vec_kernel<<<static_cast<unsigned>(grid), kRaWarps * 32, 0, s>>>(
         static_cast<const uint8_t*>(a.x), a.R, row_bytes, ld_bytes, a.tr, static_cast<int>(vec_per_micro), GR, GC,
         live_mask_for(a.dtype), a.occ, WG, seg_groups, tiles);

@@ -211,3 +211,51 @@ def test_columnwise_detection_vector_path_matches_oracle(dtype, shape, micro):
     idx = pit.build_index_from_tensor(t, micro, "k")
     counts, groups = orc.build_index_from_values(t.float().cpu().numpy(), micro, "k")
     assert_same_index(idx, counts, groups)
+
+
+@pytest.mark.parametrize("shape,micro,axis,col_major",
+                         [((8192, 1024), (32, 1), "k", True), ((1000, 777), (1, 16), "m", False),
+                          ((4096, 768), (1, 768), "m", False), ((96, 3000), (16, 1), "k", True)])
+def test_index_build_repeats_across_calls_streams_and_graph_replays(shape, micro, axis, col_major):
+    """K1 called repeatedly: eager calls on two streams, then a captured build replayed over
+    changing values (the serving pattern of graph.py) -- every index equals the oracle's, so no
+    state survives from one build into the next."""
+    import torch
+
+    pit = _pkg()
+    rng = np.random.default_rng(sum(shape) + micro[0])
+    dev_vals = []
+    for density in (0.02, 0.3, 0.0005):
+        v = _values(shape, density, rng)
+        dev_vals.append((v, _torch_values(v, "bfloat16", col_major)))
+    side = torch.cuda.Stream()
+    for rep in range(2):
+        for v, t in dev_vals:
+            stream = side if rep else torch.cuda.current_stream()
+            stream.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(stream):
+                idx = pit.build_index_from_tensor(t, micro, axis)
+            torch.cuda.current_stream().wait_stream(stream)
+            counts, groups = orc.build_index_from_values(v.astype(np.float32), micro, axis)
+            assert_same_index(idx, counts, groups)
+    buf = dev_vals[0][1].clone()
+    s2 = torch.cuda.Stream()
+    s2.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s2):
+        pit.build_index_from_tensor(buf, micro, axis)  # warm-up outside the capture
+    torch.cuda.current_stream().wait_stream(s2)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        gidx = pit.build_index_from_tensor(buf, micro, axis)
+    for _ in range(2):
+        for v, t in dev_vals:
+            buf.copy_(t)
+            g.replay()
+            torch.cuda.synchronize()
+            counts, groups = orc.build_index_from_values(v.astype(np.float32), micro, axis)
+            c_dev, s_dev = gidx.device_arrays()  # the host view caches: read the replayed buffers
+            c_h, s_h = c_dev.cpu().numpy(), s_dev.cpu().numpy()
+            np.testing.assert_array_equal(c_h, counts)
+            for grp in range(len(groups)):
+                np.testing.assert_array_equal(s_h[grp, : c_h[grp]], groups[grp], err_msg=f"group {grp}")
