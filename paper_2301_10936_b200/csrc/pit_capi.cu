@@ -174,9 +174,8 @@ int pit_build_index(const uint8_t* packed, int64_t s0, int64_t s1, int g0, int g
   if (!packed || !occ || (!counts) != (!slots)) return fail(kErrArg, "null device pointer");
   DetectBitsArgs a{packed, s0, s1, g0, g1, t0, t1, pit_dim, occ};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (int st = launch_detect_bits(a, s)) return st;
-  if (!counts) return kOk;  // occupancy bitmap only
-  return launch_compact(occ, ng, wg, counts, slots, pg, s);
+  if (!counts) return launch_detect_bits(a, s);  // occupancy bitmap only
+  return launch_index_from_bits(a, counts, slots, pg, s);
 }
 
 int pit_cover_counts(const uint8_t* packed, int64_t s0, int64_t s1, int g0, int g1, int n_candidates,

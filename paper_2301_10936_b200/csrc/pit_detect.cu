@@ -384,58 +384,46 @@ __device__ __forceinline__ uint32_t range_mask(int a, int b) {
   return hi & ~((1u << a) - 1u);
 }
 
+// Bitmap word w of group g when a coordinate block spans >= 32 coordinates (lcg >= lct + 5, e.g.
+// 64-key blocks under (t0, 1) micro-tiles): the word's 32 coordinates fall in at most two blocks,
+// so each block is tested once (OR over the group's blocks) and its coordinates set by mask.
+template <typename I>
+__device__ __forceinline__ uint32_t bits_word_pow2(const uint8_t* __restrict__ packed, I s0, I s1, int lg0, int lg1,
+                                                   int lt0, int lt1, int pit_dim, I pit_grid, I g, I w) {
+  const I bg1 = (s1 + (I(1) << lg1) - 1) >> lg1;
+  const I gs = pit_dim == 0 ? s1 : s0;
+  const int lgt = pit_dim == 0 ? lt1 : lt0, lgg = pit_dim == 0 ? lg1 : lg0;
+  const int lct = pit_dim == 0 ? lt0 : lt1, lcg = pit_dim == 0 ? lg0 : lg1;
+  const I glo = (g << lgt) >> lgg;
+  const I ghi = (min((g + 1) << lgt, gs) + (I(1) << lgg) - 1) >> lgg;
+  const I c_end = min(w * 32 + 32, pit_grid);
+  const int sh = lcg - lct;  // log2(coordinates per block)
+  uint32_t word = 0;
+  for (I cb = (w * 32) >> sh; cb <= (c_end - 1) >> sh; ++cb) {
+    bool live = false;
+    for (I gb = glo; gb < ghi && !live; ++gb) {
+      const I f = pit_dim == 0 ? cb * bg1 + gb : gb * bg1 + cb;
+      live = (__ldg(packed + (f >> 3)) >> (7 - (f & 7))) & 1;
+    }
+    if (live) {
+      const I lo = max(cb << sh, w * 32), hi = min((cb + 1) << sh, c_end);
+      word |= range_mask(static_cast<int>(lo - w * 32), static_cast<int>(hi - w * 32));
+    }
+  }
+  return word;
+}
+
+// A thread per (group, word), coordinate blocks >= 32 coordinates wide (the launcher sends the
+// narrower-block geometry to detect_bits_pow2_lane_kernel).
 template <typename I>
 __global__ void detect_bits_pow2_kernel(const uint8_t* __restrict__ packed, I s0, I s1, int lg0, int lg1, int lt0,
                                         int lt1, int pit_dim, I n_groups, I pit_grid, I WG,
                                         uint32_t* __restrict__ occ) {
-  const I bg1 = (s1 + (I(1) << lg1) - 1) >> lg1;
-  // group axis (warp-uniform-ish) and coordinate axis parameters
-  const I gs = pit_dim == 0 ? s1 : s0, cs = pit_dim == 0 ? s0 : s1;
-  const int lgt = pit_dim == 0 ? lt1 : lt0, lgg = pit_dim == 0 ? lg1 : lg0;
-  const int lct = pit_dim == 0 ? lt0 : lt1, lcg = pit_dim == 0 ? lg0 : lg1;
   const I n_items = n_groups * WG;
   for (I item = static_cast<I>(blockIdx.x) * blockDim.x + threadIdx.x; item < n_items;
        item += static_cast<I>(gridDim.x) * blockDim.x) {
     const I g = item / WG, w = item - g * WG;
-    const I glo = (g << lgt) >> lgg;
-    const I ghi = (min((g + 1) << lgt, gs) + (I(1) << lgg) - 1) >> lgg;
-    uint32_t word = 0;
-    const I c_end = min(w * 32 + 32, pit_grid);
-    if (lcg >= lct + 5) {
-      // a coordinate block spans >= 32 coordinates (e.g. 64-key blocks, (t0,1) micro-tiles): the
-      // word's 32 coordinates fall in at most two blocks, so test each block once (OR over the
-      // group's blocks) and set its coordinates by mask — not 32 x (group blocks) bit loads
-      const int sh = lcg - lct;  // log2(coordinates per block)
-      for (I cb = (w * 32) >> sh; cb <= (c_end - 1) >> sh; ++cb) {
-        bool live = false;
-        for (I gb = glo; gb < ghi && !live; ++gb) {
-          const I f = pit_dim == 0 ? cb * bg1 + gb : gb * bg1 + cb;
-          live = (__ldg(packed + (f >> 3)) >> (7 - (f & 7))) & 1;
-        }
-        if (live) {
-          const I lo = max(cb << sh, w * 32), hi = min((cb + 1) << sh, c_end);
-          word |= range_mask(static_cast<int>(lo - w * 32), static_cast<int>(hi - w * 32));
-        }
-      }
-      occ[static_cast<int64_t>(g) * WG + w] = word;
-      continue;
-    }
-    for (I c = w * 32; c < c_end; ++c) {
-      const I clo = (c << lct) >> lcg;
-      const I chi = (min((c + 1) << lct, cs) + (I(1) << lcg) - 1) >> lcg;
-      bool live = false;
-      for (I gb = glo; gb < ghi && !live; ++gb) {
-        for (I cb = clo; cb < chi; ++cb) {
-          const I f = pit_dim == 0 ? cb * bg1 + gb : gb * bg1 + cb;
-          if ((__ldg(packed + (f >> 3)) >> (7 - (f & 7))) & 1) {
-            live = true;
-            break;
-          }
-        }
-      }
-      word |= static_cast<uint32_t>(live) << (c - w * 32);
-    }
-    occ[static_cast<int64_t>(g) * WG + w] = word;
+    occ[static_cast<int64_t>(g) * WG + w] = bits_word_pow2<I>(packed, s0, s1, lg0, lg1, lt0, lt1, pit_dim, pit_grid, g, w);
   }
 }
 
@@ -540,21 +528,20 @@ constexpr int kCompactThreads = 256;
 // Few long groups (e.g. pit:m over tall operands): blockIdx.y splits a group's words into ranges of
 // words_per_split; a split first counts the live coordinates before its range (re-reading those
 // words, cheap next to the scan) so every split writes its slots independently.
-__global__ void __launch_bounds__(kCompactThreads) compact_kernel(const uint32_t* __restrict__ occ, int64_t n_groups,
-                                                                  int64_t WG, int32_t* __restrict__ counts,
-                                                                  int32_t* __restrict__ slots, int64_t slot_stride,
-                                                                  int64_t words_per_split) {
-  __shared__ int warp_tot[kCompactThreads / 32];
-  const int64_t g = blockIdx.x;
+// word_at(w, own): bitmap word w of group g; own = the word lies in this block's range (a fused
+// source stores it to the bitmap then; words before the range are only counted).
+template <class WordAt>
+__device__ __forceinline__ void compact_group(WordAt word_at, int64_t g, int64_t WG, int32_t* __restrict__ counts,
+                                              int32_t* __restrict__ slots, int64_t slot_stride,
+                                              int64_t words_per_split, int* warp_tot) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t* row = occ + g * WG;
   int32_t* out = slots + g * slot_stride;
   const int64_t w_begin = static_cast<int64_t>(blockIdx.y) * words_per_split;
   const int64_t w_end = w_begin + words_per_split < WG ? w_begin + words_per_split : WG;
   int base = 0;
   if (w_begin > 0) {
     int pre = 0;
-    for (int64_t w = threadIdx.x; w < w_begin; w += kCompactThreads) pre += __popc(__ldg(row + w));
+    for (int64_t w = threadIdx.x; w < w_begin; w += kCompactThreads) pre += __popc(word_at(w, false));
 #pragma unroll
     for (int o = 16; o; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
     if (lane == 0) warp_tot[warp] = pre;
@@ -565,7 +552,7 @@ __global__ void __launch_bounds__(kCompactThreads) compact_kernel(const uint32_t
   }
   for (int64_t w0 = w_begin; w0 < w_end; w0 += kCompactThreads) {
     const int64_t w = w0 + threadIdx.x;
-    uint32_t word = w < w_end ? __ldg(row + w) : 0u;
+    uint32_t word = w < w_end ? word_at(w, true) : 0u;
     const int c = __popc(word);
     int incl = c;
 #pragma unroll
@@ -605,6 +592,38 @@ __global__ void __launch_bounds__(kCompactThreads) compact_kernel(const uint32_t
     __syncthreads();
   }
   if (threadIdx.x == 0 && blockIdx.y == gridDim.y - 1) counts[g] = base;
+}
+
+__global__ void __launch_bounds__(kCompactThreads) compact_kernel(const uint32_t* __restrict__ occ, int64_t n_groups,
+                                                                  int64_t WG, int32_t* __restrict__ counts,
+                                                                  int32_t* __restrict__ slots, int64_t slot_stride,
+                                                                  int64_t words_per_split) {
+  __shared__ int warp_tot[kCompactThreads / 32];
+  const int64_t g = blockIdx.x;
+  const uint32_t* row = occ + g * WG;
+  compact_group([row](int64_t w, bool) { return __ldg(row + w); }, g, WG, counts, slots, slot_stride,
+                words_per_split, warp_tot);
+}
+
+// Annotation route, index in one launch: power-of-two geometry with coordinate blocks >= 32
+// coordinates wide (e.g. the (128, 1) key index of a 32x64 attention block mask) -- a word's 32
+// coordinates fall in at most two blocks, so a compaction thread derives its bitmap word from the
+// packed bits itself (the same few byte loads detect_bits_pow2_kernel makes), stores it and
+// compacts; no bitmap round trip through a second launch.
+__global__ void __launch_bounds__(kCompactThreads) bits_compact_pow2_kernel(
+    const uint8_t* __restrict__ packed, int32_t s0, int32_t s1, int lg0, int lg1, int lt0, int lt1, int pit_dim,
+    int32_t pit_grid, int64_t WG, uint32_t* __restrict__ occ, int32_t* __restrict__ counts,
+    int32_t* __restrict__ slots, int64_t slot_stride, int64_t words_per_split) {
+  __shared__ int warp_tot[kCompactThreads / 32];
+  const int32_t g = static_cast<int32_t>(blockIdx.x);
+  uint32_t* row = occ + static_cast<int64_t>(g) * WG;
+  auto word_at = [&](int64_t w, bool own) {
+    const uint32_t word = bits_word_pow2<int32_t>(packed, s0, s1, lg0, lg1, lt0, lt1, pit_dim, pit_grid, g,
+                                                  static_cast<int32_t>(w));
+    if (own) row[w] = word;
+    return word;
+  };
+  compact_group(word_at, g, WG, counts, slots, slot_stride, words_per_split, warp_tot);
 }
 
 // OR of all group rows: the union of live coordinates (used by pit:m union-row tiles).
@@ -800,11 +819,8 @@ int launch_detect_bits(const DetectBitsArgs& a, cudaStream_t s) {
   return cuda_status();
 }
 
-int launch_compact(const uint32_t* occ, int64_t n_groups, int64_t WG, int32_t* counts, int32_t* slots,
-                   int64_t slot_stride, cudaStream_t s) {
-  if (n_groups == 0) return 0;
-  if (n_groups >= (1ll << 31)) return kErrShape;
-  // split long groups when there are too few groups to fill the GPU
+// split long groups over blockIdx.y when there are too few groups to fill the GPU
+static void compact_splits(int64_t n_groups, int64_t WG, int64_t* splits_out, int64_t* wps_out) {
   int64_t splits = 1, wps = WG;
   const int64_t target = 2 * static_cast<int64_t>(sm_count());
   if (n_groups < target && WG > 4 * kCompactThreads) {
@@ -815,8 +831,57 @@ int launch_compact(const uint32_t* occ, int64_t n_groups, int64_t WG, int32_t* c
     wps = ceil_div(ceil_div(WG, splits), kCompactThreads) * kCompactThreads;
     splits = ceil_div(WG, wps);
   }
+  *splits_out = splits;
+  *wps_out = wps;
+}
+
+int launch_compact(const uint32_t* occ, int64_t n_groups, int64_t WG, int32_t* counts, int32_t* slots,
+                   int64_t slot_stride, cudaStream_t s) {
+  if (n_groups == 0) return 0;
+  if (n_groups >= (1ll << 31)) return kErrShape;
+  int64_t splits, wps;
+  compact_splits(n_groups, WG, &splits, &wps);
   dim3 grid(static_cast<unsigned>(n_groups), static_cast<unsigned>(splits));
   compact_kernel<<<grid, kCompactThreads, 0, s>>>(occ, n_groups, WG, counts, slots, slot_stride, wps);
+  note_launch();
+  return cuda_status();
+}
+
+// PIT_BITS_FUSE=0: annotation-route index as detect_bits + compact (two launches; A/B knob)
+static bool bits_fuse_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("PIT_BITS_FUSE");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+
+int launch_index_from_bits(const DetectBitsArgs& a, int32_t* counts, int32_t* slots, int64_t slot_stride,
+                           cudaStream_t s) {
+  const int64_t G0 = ceil_div(a.s0, a.t0), G1 = ceil_div(a.s1, a.t1);
+  const int64_t n_groups = a.pit_dim == 0 ? G1 : G0;
+  const int64_t pit_grid = a.pit_dim == 0 ? G0 : G1;
+  const int64_t WG = ceil_div(pit_grid, 32);
+  if (n_groups == 0 || pit_grid == 0) return 0;
+  const int64_t G0b = ceil_div(a.s0, a.g0), G1b = ceil_div(a.s1, a.g1);
+  const bool fits32 = n_groups * WG * 32 < (1ll << 31) && G0b * G1b < (1ll << 31) &&
+                      (a.s0 + a.t0) * 2 < (1ll << 31) && (a.s1 + a.t1) * 2 < (1ll << 31) && n_groups < 65536ll * 32768;
+  auto p2 = [](int v) { return v > 0 && (v & (v - 1)) == 0; };
+  const bool all_pow2 = p2(a.t0) && p2(a.t1) && p2(a.g0) && p2(a.g1);
+  const int ct = a.pit_dim == 0 ? a.t0 : a.t1, cg = a.pit_dim == 0 ? a.g0 : a.g1;
+  if (!(fits32 && all_pow2 && bits_fuse_enabled()) ||
+      __builtin_ctz(static_cast<unsigned>(cg)) < __builtin_ctz(static_cast<unsigned>(ct)) + 5) {
+    if (int st = launch_detect_bits(a, s)) return st;
+    return launch_compact(a.occ, n_groups, WG, counts, slots, slot_stride, s);
+  }
+  int64_t splits, wps;
+  compact_splits(n_groups, WG, &splits, &wps);
+  dim3 grid(static_cast<unsigned>(n_groups), static_cast<unsigned>(splits));
+  bits_compact_pow2_kernel<<<grid, kCompactThreads, 0, s>>>(
+      a.packed, static_cast<int32_t>(a.s0), static_cast<int32_t>(a.s1), __builtin_ctz(static_cast<unsigned>(a.g0)),
+      __builtin_ctz(static_cast<unsigned>(a.g1)), __builtin_ctz(static_cast<unsigned>(a.t0)),
+      __builtin_ctz(static_cast<unsigned>(a.t1)), a.pit_dim, static_cast<int32_t>(pit_grid), WG, a.occ, counts,
+      slots, slot_stride, wps);
   note_launch();
   return cuda_status();
 }

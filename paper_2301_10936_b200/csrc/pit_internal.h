@@ -68,6 +68,10 @@ struct DetectBitsArgs {
 
 int launch_detect_values(const DetectValuesArgs& a, cudaStream_t s);
 int launch_detect_bits(const DetectBitsArgs& a, cudaStream_t s);
+// detect_bits + compact; one launch when the geometry allows (power-of-two, coordinate blocks >= 32
+// coordinates wide)
+int launch_index_from_bits(const DetectBitsArgs& a, int32_t* counts, int32_t* slots, int64_t slot_stride,
+                           cudaStream_t s);
 int launch_compact(const uint32_t* occ, int64_t n_groups, int64_t WG, int32_t* counts, int32_t* slots,
                    int64_t slot_stride, cudaStream_t s);
 int launch_union(const uint32_t* occ, int64_t n_groups, int64_t WG, uint32_t* uni, cudaStream_t s);

@@ -66,6 +66,53 @@ def test_build_index_sweep_matches_oracle():
         assert_same_index(idx, counts, groups)
 
 
+FUSED_BITS_CASES = [
+    # power-of-two geometry with coordinate blocks >= 32 coordinates wide: bitmap words derived from
+    # the packed bits inside the compaction launch (bits_compact_pow2_kernel)
+    ((4096, 4096), (32, 64), (128, 1), "k", 0.8),   # C3's key index of a 32x64 block mask
+    ((4096, 4096), (32, 64), (32, 1), "k", 0.8),
+    ((1000, 3000), (32, 64), (64, 2), "k", 0.7),    # ragged extents, t1 = 2
+    ((2048, 1024), (64, 32), (1, 1), "m", 0.5),
+    ((777, 333), (128, 4), (4, 8), "m", 0.3),
+    ((256, 131072), (32, 64), (128, 1), "k", 0.9),  # two long groups: split over blockIdx.y
+    ((96, 65536), (32, 128), (32, 4), "k", 0.0),    # fully live
+    ((96, 65536), (32, 128), (32, 4), "k", 1.0),    # fully dead
+]
+
+
+@pytest.mark.parametrize("shape,gran,micro,axis,ratio", FUSED_BITS_CASES)
+def test_build_index_fused_bits_route_matches_oracle(shape, gran, micro, axis, ratio):
+    pit = _pkg()
+    ann = pit.random_annotation(shape, gran, ratio, seed=shape[0] * 3 + shape[1])
+    idx = pit.build_index(ann, micro, axis)
+    counts, groups = orc.build_index(ann.tensor_shape, ann.granularity, ann.packed, micro, axis)
+    assert_same_index(idx, counts, groups)
+    # the bitmap the fused launch stores is the one the two-launch route writes
+    occ = idx.occupancy_words().cpu().numpy().view(np.uint32)
+    ref_occ = np.zeros(occ.shape, np.uint32)
+    for g, grp in enumerate(groups):
+        grp = np.asarray(grp, dtype=np.int64)
+        np.bitwise_or.at(ref_occ[g], grp // 32, (np.uint32(1) << (grp % 32).astype(np.uint32)))
+    np.testing.assert_array_equal(occ, ref_occ)
+
+
+def test_build_index_fused_bits_sweep_matches_oracle():
+    pit = _pkg()
+    rng = np.random.default_rng(11)
+    for trial in range(60):
+        axis = "m" if rng.integers(2) else "k"
+        cg = int(rng.choice([32, 64, 128]))           # coordinate-axis granularity
+        ct = int(rng.choice([1, 2, 4]))
+        ct = min(ct, cg // 32)                         # coordinate blocks >= 32 coordinates
+        gg, gt = int(rng.choice([1, 2, 8, 32])), int(rng.choice([1, 4, 16, 128]))
+        cs, gs = int(rng.integers(1, 5000)), int(rng.integers(1, 600))
+        shape, gran, micro = ((cs, gs), (cg, gg), (ct, gt)) if axis == "m" else ((gs, cs), (gg, cg), (gt, ct))
+        ann = pit.random_annotation(shape, gran, float(rng.choice([0.0, 0.5, 0.9, 1.0])), seed=100 + trial)
+        idx = pit.build_index(ann, micro, axis)
+        counts, groups = orc.build_index(ann.tensor_shape, ann.granularity, ann.packed, micro, axis)
+        assert_same_index(idx, counts, groups)
+
+
 DTYPES = ["float32", "float64", "bfloat16", "float16", "uint8", "bool"]
 
 
