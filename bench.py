@@ -599,24 +599,34 @@ def moe_bench(args, world, rank, dev, peaks, tokens_per_gpu=16384, n_experts=128
     for _ in range(max(3, args.warmup)):
         eager = layer(x, logits)
     torch.cuda.synchronize()
-    # the layer as a served model runs it: one CUDA graph (no host round trip on either path)
-    side = torch.cuda.Stream()
-    side.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(side):
-        layer(x, logits)
-    torch.cuda.current_stream().wait_stream(side)
-    torch.cuda.synchronize()
+    graphable = layer.exchange != "nccl"  # the all-to-all-v fallback reads split sizes on the host
     if world > 1:
         dist.barrier()
-    graph = torch.cuda.CUDAGraph()
-    launches0 = _lib.kernel_launches()
-    with torch.cuda.graph(graph):
-        out_g = layer(x, logits)
-    launches_per_layer = _lib.kernel_launches() - launches0
-    for _ in range(max(3, args.warmup)):
-        graph.replay()
-    ms = _time_layer(graph.replay, steps, dev, world)
-    replay_ok = bool(torch.equal(out_g, eager))
+    if graphable:
+        # the layer as a served model runs it: one CUDA graph (no host round trip on either path)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            layer(x, logits)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        graph = torch.cuda.CUDAGraph()
+        launches0 = _lib.kernel_launches()
+        with torch.cuda.graph(graph):
+            out_g = layer(x, logits)
+        launches_per_layer = _lib.kernel_launches() - launches0
+        for _ in range(max(3, args.warmup)):
+            graph.replay()
+        ms = _time_layer(graph.replay, steps, dev, world)
+        replay_ok = bool(torch.equal(out_g, eager))
+    else:
+        launches0 = _lib.kernel_launches()
+        layer(x, logits)
+        launches_per_layer = _lib.kernel_launches() - launches0
+        ms = _time_layer(lambda: layer(x, logits), steps, dev, world)
+        replay_ok = None
     ep_error = layer._peer.error() if layer._peer is not None else 0
     baseline = None
     if world > 1 and dist.get_backend() == "nccl":
@@ -664,7 +674,8 @@ def moe_bench(args, world, rank, dev, peaks, tokens_per_gpu=16384, n_experts=128
            "config": {"experts": E, "experts_per_gpu": El, "d_model": d_model, "d_ff": d_ff,
                       "tokens_per_gpu": tokens_per_gpu, "routing": "top-1 argmax, Gaussian logits, dropless",
                       "parallelism": f"ep{world}" if world > 1 else "single GPU", "received_rank0": received,
-                      "exchange": layer.exchange, "execution": "CUDA graph of the whole layer"},
+                      "exchange": layer.exchange, "peer_fallback": layer.fallback_reason,
+                      "execution": "CUDA graph of the whole layer" if graphable else "eager (all-to-all-v fallback)"},
            "gpu_launches_per_layer": int(launches_per_layer), "graph_replay_equals_eager": replay_ok,
            "exchange_timeouts": int(ep_error)}
     if world > 1:

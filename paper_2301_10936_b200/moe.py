@@ -153,6 +153,11 @@ def _pack_ffn1(rows_hint: int, groups: int) -> bool:
     return _PACK_ENV != "0"
 
 
+class PeerUnavailable(RuntimeError):
+    """Some rank of the group cannot map the others' exchange regions (no CUDA IPC / peer access).
+    Raised on every rank together."""
+
+
 class PeerExchange:
     """One exchange region per rank, mapped into every other rank through CUDA IPC (pit_ep_* in the C
     ABI). `dispatch` / `recv_plan` / `signal` / `combine` are stream-ordered device calls with no host
@@ -182,17 +187,36 @@ class PeerExchange:
         peers = [0] * self.world
         peers[self.rank] = self.region
         if self.world > 1:
+            # every rank learns whether every rank mapped every peer: a rank whose IPC open fails must
+            # not leave the others waiting in the barrier below (they all raise PeerUnavailable)
+            err = ""
             h = (C.c_char * 64)()
-            _device.check(self.lib.pit_ep_ipc_handle(self.region, h))
+            if self.lib.pit_ep_ipc_handle(self.region, h) != 0:
+                err = _lib.last_error()
             handles = [None] * self.world
-            dist.all_gather_object(handles, bytes(h), group=group)
+            dist.all_gather_object(handles, bytes(h) if not err else None, group=group)
             for r in range(self.world):
-                if r == self.rank:
+                if r == self.rank or err:
                     continue
+                if handles[r] is None:
+                    err = f"rank {r} could not export its region"
+                    break
                 p = C.c_void_p()
-                _device.check(self.lib.pit_ep_ipc_open(C.create_string_buffer(handles[r], 64), C.byref(p)))
+                if self.lib.pit_ep_ipc_open(C.create_string_buffer(handles[r], 64), C.byref(p)) != 0:
+                    err = f"opening rank {r}'s region: {_lib.last_error()}"
+                    break
                 self._opened.append(p.value)
                 peers[r] = p.value
+            errs = [None] * self.world
+            dist.all_gather_object(errs, err, group=group)
+            bad = [(r, e) for r, e in enumerate(errs) if e]
+            if bad:
+                for q in self._opened:
+                    self.lib.pit_ep_ipc_close(q)
+                self._opened = []
+                self.lib.pit_ep_region_free(self.region)
+                self.region = None
+                raise PeerUnavailable(f"peer-memory exchange unavailable (rank {bad[0][0]}: {bad[0][1]})")
         self.peers_dev = torch.tensor(peers, dtype=torch.int64, device=self.device)
         self.args = _lib.EpArgs(self.rank, self.world, self.El, self.cap, self.row_bytes, self.region,
                                 self.peers_dev.data_ptr())
@@ -292,6 +316,8 @@ class SwitchMoE:
         # "peer": device-driven exchange over NVLink (default with W > 1); "nccl": all-to-all-v baseline;
         # "local": single-GPU path (W == 1). "peer" at W == 1 runs the exchange kernels against itself.
         self.exchange = exchange or ("local" if self.world == 1 else "peer")
+        self._exchange_requested = exchange is not None
+        self.fallback_reason = None
         if self.exchange not in ("local", "peer", "nccl"):
             raise ValueError(f"unknown exchange {self.exchange!r}")
         if self.exchange == "local" and self.world > 1:
@@ -319,7 +345,15 @@ class SwitchMoE:
         T = x.shape[0]
         if self._peer is None:  # collective: the first call of every rank creates the regions
             cap = self.capacity if self.capacity is not None else T
-            self._peer = self._peer_factory(self.group, self.El, cap, self.d_model, x.dtype, x.device)
+            try:
+                self._peer = self._peer_factory(self.group, self.El, cap, self.d_model, x.dtype, x.device)
+            except PeerUnavailable as e:
+                if self._exchange_requested:
+                    raise
+                # default exchange on a box without peer mappings: every rank switches to the NCCL
+                # all-to-all-v exchange together (the error was raised on all of them)
+                self.exchange, self.fallback_reason = "nccl", str(e)
+                return self._forward_ep(x, logits)
         ex = self._peer
         if T > ex.cap:
             raise ValueError(f"{T} tokens exceed the exchange capacity {ex.cap}")

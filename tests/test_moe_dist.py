@@ -1,6 +1,7 @@
 """CPU, world size 2 over gloo: the expert-parallel exchanges of SwitchMoE equal the single-process
-oracle. "nccl": counts all-to-all, token all-to-all-v, receive plan, reverse all-to-all, gate-scaled
-combine. "peer": the peer-memory protocol of csrc/pit_ep.cu (region positions, receive plan, pull
+oracle. "default" on a group whose ranks cannot map each other's regions: every rank falls back to
+the all-to-all-v exchange together. "nccl": counts all-to-all, token all-to-all-v, receive plan,
+reverse all-to-all, gate-scaled combine. "peer": the peer-memory protocol of csrc/pit_ep.cu (region positions, receive plan, pull
 combine) restated on CPU (tests/moe_oracle_backend.EmulatedPeerExchange). Compute runs in the
 test-only oracle backend."""
 
@@ -33,6 +34,18 @@ def _problem(T, E, d, F, seed):
     return x, logits, w1, w2
 
 
+def _unmappable_peers(group, *args):
+    """A PeerExchange whose IPC open fails on rank 1 only: like PeerExchange, the ranks share their
+    errors and all raise PeerUnavailable together."""
+    from paper_2301_10936_b200.moe import PeerUnavailable
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    errs = [None] * world
+    dist.all_gather_object(errs, "cudaIpcOpenMemHandle: peer access unsupported" if rank == 1 else "", group=group)
+    bad = [(r, e) for r, e in enumerate(errs) if e]
+    raise PeerUnavailable(f"peer-memory exchange unavailable (rank {bad[0][0]}: {bad[0][1]})")
+
+
 def _worker(rank, world, port, T, E, d, F, q, exchange="nccl"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -44,12 +57,17 @@ def _worker(rank, world, port, T, E, d, F, q, exchange="nccl"):
         x, logits, w1, w2 = _problem(T, E, d, F, seed=5)
         El = E // world
         sl = slice(rank * T, (rank + 1) * T)
+        factory = EmulatedPeerExchange if exchange == "peer" else _unmappable_peers if exchange == "default" else None
         layer = SwitchMoE(torch.from_numpy(w1[rank * El : (rank + 1) * El]).double(),
                           torch.from_numpy(w2[rank * El : (rank + 1) * El]).double(), E, group=dist.group.WORLD,
-                          backend=OracleBackend(), exchange=exchange,
-                          exchange_factory=EmulatedPeerExchange if exchange == "peer" else None)
+                          backend=OracleBackend(), exchange=None if exchange == "default" else exchange,
+                          exchange_factory=factory)
         out = layer(torch.from_numpy(x[sl]).double(), torch.from_numpy(logits[sl]))
         received = layer.stats.received
+        if exchange == "default":  # no peer mappings: every rank fell back to the all-to-all-v exchange
+            assert layer.exchange == "nccl" and "rank 1" in layer.fallback_reason
+            out2 = layer(torch.from_numpy(x[sl]).double(), torch.from_numpy(logits[sl]))
+            assert torch.equal(out, out2)
         if exchange == "peer":
             received = int(layer._peer.lcounts.sum())
             out2 = layer(torch.from_numpy(x[sl]).double(), torch.from_numpy(logits[sl]))  # regions reused
@@ -59,7 +77,7 @@ def _worker(rank, world, port, T, E, d, F, q, exchange="nccl"):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("exchange", ["nccl", "peer"])
+@pytest.mark.parametrize("exchange", ["nccl", "peer", "default"])
 @pytest.mark.parametrize("E", [4, 8])
 def test_expert_parallel_exchange_matches_single_process(E, exchange):
     T, d, F, world = 37, 16, 24, 2
