@@ -379,10 +379,9 @@ def run_ours(args, w):
         "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {**base_config(w), "parallelism": f"replica x{world} (per-GPU work fixed)",
-                   "l2": "flushed (256 MiB write) before every step; inputs also exceed L2",
-                   "execution": "CUDA graph of detect+SpMM (paper_2301_10936_b200.graph)" if not args.no_graph
-                   else "eager API calls"},
+        "config": base_config(w, world),
+        "execution": "CUDA graph of detect+SpMM (paper_2301_10936_b200.graph)" if not args.no_graph
+                     else "eager API calls",
         "roofline": roofline, "detection": detection,
         "clocks": clocks.summary(), "gpu_launches": int(launches),
         "graph_replay_equals_eager": replay_ok,
@@ -1398,10 +1397,12 @@ def cpu_sections_subprocess(names, target_s: float, timeout: float = 600) -> dic
         return {n: {"error": (r.stderr or "no output")[-300:]} for n in names}
 
 
-def base_config(w: dict) -> dict:
-    return {"workload": w["desc"], "name": w["name"], "M": w["M"], "K": w["K"], "N": w["N"],
+def base_config(w: dict, world: int = 1) -> dict:
+    """The workload both arms run (identical dicts; each arm's dtype and execution are top-level)."""
+    return {"workload": w["desc"].replace(" bf16", ""), "name": w["name"], "M": w["M"], "K": w["K"], "N": w["N"],
             "micro_tile": list(w["micro"]), "pit_axis": w["axis"], "zero_ratio": w["zero"],
-            "plan_tile": list(w["tile"])}
+            "plan_tile": list(w["tile"]), "parallelism": f"replica x{world} (per-GPU work fixed)",
+            "l2": "inputs exceed L2; the GPU arm also flushes L2 (256 MiB write) before every step"}
 
 
 def run_reference(args, w):
@@ -1419,14 +1420,15 @@ def run_reference(args, w):
     value = statistics.mean(vals)
     # one step = the full workload (every M-block group); its expected effective FLOPs / the rate
     step_flops = 2.0 * w["M"] * w["K"] * w["N"] * (1.0 - (w["zero"] or 0.0))
-    cfg = dict(base_config(w), workload=w["desc"].replace("bf16", "fp32 (the reference has no bf16)"), execution=f"reference CPU path, {cores} processes x 1 thread, fp32 "
-                                         "(the reference has no bf16, executor.py:40-41)")
+    cfg = base_config(w, world)
     return {
         "impl": "reference", "metric": "PIT sparse matmul effective TFLOP/s (online detection + SpMM)",
         "value": round(value, 6), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(step_flops / (value * 1e12) * 1e3, 1) if value > 0 else None,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": cfg,
+        "execution": f"reference CPU path ({base['implementation']}), {cores} processes x 1 thread, fp32 "
+                     "(the reference has no bf16, executor.py:40-41)",
         "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample", "implementation",
                                                "cpu_model")} | {"value": round(value, 6)},
         "e2e": {"value": round(value, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
